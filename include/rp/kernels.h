@@ -1,0 +1,95 @@
+/* roundpipe-b200 kernel C-ABI: the sm_100a kernels of one RoundPipe stage.
+ * Device pointers + a cudaStream_t passed as void*; return codes as in
+ * include/rp/cabi.h. Callable from the C++ runtime and, for tests, through
+ * ctypes with torch-allocated buffers. Layouts are row-major; "ld" is the
+ * row pitch in elements.
+ */
+#ifndef RP_KERNELS_H_
+#define RP_KERNELS_H_
+#include <stdint.h>
+#include "rp/cabi.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* D[M,N] (+)= A[M,K] . B[N,K]^T  (bf16 in, fp32 accumulate in TMEM).
+ * a_mn_major=0: A stored [M,K] (lda >= K);  1: A stored [K,M] (lda >= M).
+ * b_mn_major=0: B stored [N,K] (ldb >= K);  1: B stored [K,N] (ldb >= N).
+ * out_f32=0: D bf16 = acc (+ R, a bf16 [M,N] residual, optional);
+ * out_f32=1: D fp32 = acc, or D += acc when accumulate=1. */
+typedef struct {
+  int32_t M, N, K;
+  const void* A; int64_t lda; int32_t a_mn_major;
+  const void* B; int64_t ldb; int32_t b_mn_major;
+  void* D; int64_t ldd; int32_t out_f32; int32_t accumulate;
+  const void* R; int64_t ldr;
+} rp_gemm_args_t;
+int rp_gemm_bf16(const rp_gemm_args_t* args, void* stream);
+
+/* AdamW hyper-parameters (decoupled weight decay), fp32. */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay, grad_scale;
+} rp_adam_hparams_t;
+
+/* RMSNorm over rows of h (h % 8 == 0): y = bf16(w * x * rstd). */
+int rp_rmsnorm_fwd(const void* x, int64_t ldx, const void* w, void* y, int64_t ldy,
+                   float* rstd, int32_t rows, int32_t h, float eps, void* stream);
+/* dx = rstd*(dy*w - xhat*mean(dy*w*xhat)) [+ dres]; dx32 (fp32) and/or dx16
+ * (bf16) outputs; dw[h] += sum_rows dy*xhat (fp32, atomics). Rows dense. */
+int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
+                   const float* dres, float* dx32, void* dx16, float* dw, int32_t rows,
+                   int32_t h, void* stream);
+/* Per-head RMSNorm of q and k slots of the fused qkv row + RoPE (rotate_half,
+ * cos_sin = float2 (cos, sin) table [seq, head_dim/2]); position = t % seq. */
+int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t nk,
+                        int32_t head_dim, const void* qw, const void* kw,
+                        const float* cos_sin, int32_t seq, void* q_out, void* k_out,
+                        float* rstd_q, float* rstd_k, int32_t T, float eps, void* stream);
+int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, int64_t ld,
+                        int32_t nq, int32_t nk, int32_t head_dim, const void* qw,
+                        const void* kw, const float* rstd_q, const float* rstd_k,
+                        const float* cos_sin, int32_t seq, void* dqkv, int64_t ldd,
+                        float* dqw, float* dkw, int32_t T, void* stream);
+/* gu rows = [gate | up] (2m); act = silu(gate) * up. */
+int rp_swiglu_fwd(const void* gu, void* act, int64_t T, int32_t m, void* stream);
+int rp_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t T, int32_t m,
+                  void* stream);
+/* out[t] = table[ids[t]] (table: device or host-mapped pinned memory). */
+int rp_embed_fwd(const int32_t* ids, const void* table, void* out, int32_t T, int32_t h,
+                 void* stream);
+/* dE[ids[t]] += dx[t] (fp32). */
+int rp_embed_bwd(const int32_t* ids, const float* dx, float* dE, int32_t T, int32_t h,
+                 void* stream);
+/* Cross-entropy over a bf16 logits chunk [rows, V]: loss_sum += lse - z[label]
+ * (label < 0 ignored), logits overwritten IN PLACE by (softmax - onehot) *
+ * grad_scale; row_lse optional. */
+int rp_ce_fwd_bwd(void* logits, int64_t ld, const int32_t* labels, int32_t rows, int32_t V,
+                  float grad_scale, float* loss_sum, float* row_lse, void* stream);
+/* AdamW on one fp32 state chunk (in place); w16 (optional) receives bf16
+ * weights. step >= 1 is the bias-correction step. */
+int rp_adamw(float* master, float* m, float* v, const float* grad, void* w16, int64_t n,
+             const rp_adam_hparams_t* hp, int32_t step, void* stream);
+int rp_f32_to_bf16(const float* a, void* b, int64_t n, void* stream);
+int rp_bf16_to_f32(const void* a, float* b, int64_t n, void* stream);
+int rp_add_f32(float* a, const float* b, int64_t n, void* stream);
+
+/* Causal GQA flash attention, head_dim 64 or 128, bf16 in/out.
+ * q [T, nq, hd] (row pitch ldq), k/v [T, nk, hd] (pitch ldk/ldv), o [T, nq, hd];
+ * lse [nq, T] fp32 (natural log). Sequences are packed: T = batch * seq and
+ * attention never crosses a seq boundary. */
+int rp_attn_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
+                int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
+/* Backward: dq/dk/dv bf16 (same layouts as q/k/v, own pitches). Needs
+ * workspace: dq_acc fp32 [T, nq, hd] and delta fp32 [nq, T]. */
+int rp_attn_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+                const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                int64_t lddv, float* dq_acc, float* delta, int32_t T, int32_t seq, int32_t nq,
+                int32_t nk, int32_t head_dim, float scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RP_KERNELS_H_ */

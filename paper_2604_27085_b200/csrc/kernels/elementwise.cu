@@ -1,0 +1,631 @@
+// HBM-bound kernels of one Qwen3 decoder stage (sm_100a):
+//   RMSNorm fwd/bwd, fused per-head QK-RMSNorm + RoPE fwd/bwd, SwiGLU fwd/bwd,
+//   embedding gather / scatter-add, LM-head cross-entropy (in-place dlogits),
+//   fused AdamW on a streamed fp32 state chunk, and small utilities.
+// All are 16-byte vectorised, fp32 internally; reductions of parameter grads
+// go registers -> shared memory -> one atomicAdd per column per block.
+// Math follows transformers' Qwen3 (modeling_qwen3.py: RMSNorm :50-67,
+// rotate_half / apply_rotary_pos_emb :151-182, MLP :70-83) in fp32.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rp/kernels.h"
+
+namespace rp {
+namespace {
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ __nv_bfloat16 f2bf(float v) { return __float2bfloat16_rn(v); }
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&f)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = bf2f(b[i]);
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = f2bf(f[i]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int THREADS>
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < THREADS / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// y = bf16(w * x * rstd), rstd = 1/sqrt(mean(x^2) + eps). One block per row.
+template <int THREADS>
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
+                                   const __nv_bfloat16* __restrict__ w,
+                                   __nv_bfloat16* __restrict__ y, long long ldy,
+                                   float* __restrict__ rstd, int h, float eps) {
+  __shared__ float red[THREADS / 32];
+  const long long row = blockIdx.x;
+  const __nv_bfloat16* xr = x + row * ldx;
+  float ss = 0.f;
+  for (int c = threadIdx.x * 8; c < h; c += THREADS * 8) {
+    float f[8];
+    load8(xr + c, f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+  }
+  const float r = rsqrtf(block_sum<THREADS>(ss, red) / h + eps);
+  if (threadIdx.x == 0 && rstd) rstd[row] = r;
+  for (int c = threadIdx.x * 8; c < h; c += THREADS * 8) {
+    float f[8], g[8];
+    load8(xr + c, f);
+    load8(w + c, g);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = g[i] * (f[i] * r);
+    store8(y + row * ldy + c, f);
+  }
+}
+
+// dx = rstd * (g - xhat * mean(g * xhat)),  g = dy * w,  xhat = x * rstd
+// dx_total = dx + dres (optional fp32 residual grad); written fp32 and/or bf16.
+// dw[c] += sum_rows dy * xhat. Each block walks a contiguous row range.
+template <int THREADS, int MAXC>
+__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                   const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ w,
+                                   const float* __restrict__ rstd,
+                                   const float* __restrict__ dres, float* __restrict__ dx32,
+                                   __nv_bfloat16* __restrict__ dx16, float* __restrict__ dw,
+                                   int rows, int h) {
+  __shared__ float red[THREADS / 32];
+  float dw_acc[MAXC][8];
+#pragma unroll
+  for (int j = 0; j < MAXC; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dw_acc[j][i] = 0.f;
+  const int per = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  for (int row = r0; row < r1; ++row) {
+    const long long off = (long long)row * h;
+    const float r = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 8;
+      if (c < h) {
+        float a[8], b[8], g[8];
+        load8(dy + off + c, a);
+        load8(x + off + c, b);
+        load8(w + c, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot += a[i] * g[i] * b[i] * r;
+      }
+    }
+    const float mean = block_sum<THREADS>(dot, red) / h;
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 8;
+      if (c < h) {
+        float a[8], b[8], g[8], o[8];
+        load8(dy + off + c, a);
+        load8(x + off + c, b);
+        load8(w + c, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float xh = b[i] * r;
+          o[i] = r * (a[i] * g[i] - xh * mean);
+          dw_acc[j][i] += a[i] * xh;
+        }
+        if (dres) {
+          const float4 d0 = *reinterpret_cast<const float4*>(dres + off + c);
+          const float4 d1 = *reinterpret_cast<const float4*>(dres + off + c + 4);
+          o[0] += d0.x; o[1] += d0.y; o[2] += d0.z; o[3] += d0.w;
+          o[4] += d1.x; o[5] += d1.y; o[6] += d1.z; o[7] += d1.w;
+        }
+        if (dx32) {
+          *reinterpret_cast<float4*>(dx32 + off + c) = make_float4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<float4*>(dx32 + off + c + 4) = make_float4(o[4], o[5], o[6], o[7]);
+        }
+        if (dx16) store8(dx16 + off + c, o);
+      }
+    }
+  }
+  if (dw && r1 > r0) {
+#pragma unroll
+    for (int j = 0; j < MAXC; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 8;
+      if (c < h)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicAdd(dw + c + i, dw_acc[j][i]);
+    }
+  }
+}
+
+// ------------------------------------------------------- QK-norm + RoPE
+// One warp per (token, head); lane l holds E = hd/32 consecutive elements,
+// its rotate_half partner lives in lane l ^ 16.
+template <int E>
+__global__ void qk_norm_rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld,
+                                        int nq, int nk, const __nv_bfloat16* __restrict__ qw,
+                                        const __nv_bfloat16* __restrict__ kw,
+                                        const float2* __restrict__ cs, int seq,
+                                        __nv_bfloat16* __restrict__ qo,
+                                        __nv_bfloat16* __restrict__ ko,
+                                        float* __restrict__ rstd_q, float* __restrict__ rstd_k,
+                                        int T, float eps) {
+  constexpr int HD = 32 * E, HALF = HD / 2;
+  const int lane = threadIdx.x % 32;
+  const long long warp_id = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int heads = nq + nk;
+  if (warp_id >= (long long)T * heads) return;
+  const int t = (int)(warp_id / heads), hh = (int)(warp_id % heads);
+  const bool is_q = hh < nq;
+  const __nv_bfloat16* src = qkv + (long long)t * ld + (long long)hh * HD + lane * E;
+  const __nv_bfloat16* wgt = (is_q ? qw : kw) + lane * E;
+  float v[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i] = bf2f(src[i]);
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < E; ++i) ss += v[i] * v[i];
+  const float r = rsqrtf(warp_sum(ss) / HD + eps);
+  float n[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) n[i] = bf2f(f2bf(bf2f(wgt[i]) * (v[i] * r)));
+  const int pos = t % seq;
+  const bool lo = lane < 16;
+  __nv_bfloat16 out[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const float partner = __shfl_xor_sync(0xffffffffu, n[i], 16);
+    const int j = (lane * E + i) % HALF;
+    const float2 c = cs[(long long)pos * HALF + j];  // (cos, sin)
+    out[i] = f2bf(lo ? n[i] * c.x - partner * c.y : n[i] * c.x + partner * c.y);
+  }
+  __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD + lane * E
+                            : ko + ((long long)t * nk + (hh - nq)) * HD + lane * E;
+#pragma unroll
+  for (int i = 0; i < E; ++i) dst[i] = out[i];
+  if (lane == 0) {
+    if (is_q) rstd_q[(long long)t * nq + hh] = r;
+    else rstd_k[(long long)t * nk + (hh - nq)] = r;
+  }
+}
+
+// Backward: undo the rotation (R^T), then per-head RMSNorm backward.
+// dqkv[:, q/k slots] = dx; dqw/dkw[hd] += sum(dn * xhat).
+template <int E>
+__global__ void qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq,
+                                        const __nv_bfloat16* __restrict__ dk,
+                                        const __nv_bfloat16* __restrict__ qkv, long long ld,
+                                        int nq, int nk, const __nv_bfloat16* __restrict__ qw,
+                                        const __nv_bfloat16* __restrict__ kw,
+                                        const float* __restrict__ rstd_q,
+                                        const float* __restrict__ rstd_k,
+                                        const float2* __restrict__ cs, int seq,
+                                        __nv_bfloat16* __restrict__ dqkv, long long ldd,
+                                        float* __restrict__ dqw, float* __restrict__ dkw, int T) {
+  constexpr int HD = 32 * E, HALF = HD / 2;
+  __shared__ float sq[HD], sk[HD];
+  for (int i = threadIdx.x; i < HD; i += blockDim.x) sq[i] = sk[i] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x % 32;
+  const int heads = nq + nk;
+  float accq[E], acck[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) accq[i] = acck[i] = 0.f;
+  const long long total = (long long)T * heads;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x / 32);
+  for (long long wid = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; wid < total;
+       wid += nwarps) {
+    const int t = (int)(wid / heads), hh = (int)(wid % heads);
+    const bool is_q = hh < nq;
+    const __nv_bfloat16* g = is_q ? dq + ((long long)t * nq + hh) * HD
+                                  : dk + ((long long)t * nk + (hh - nq)) * HD;
+    const float r = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
+    const __nv_bfloat16* src = qkv + (long long)t * ld + (long long)hh * HD + lane * E;
+    const __nv_bfloat16* wgt = (is_q ? qw : kw) + lane * E;
+    const int pos = t % seq;
+    const bool lo = lane < 16;
+    float dn[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const float gi = bf2f(g[lane * E + i]);
+      const float partner = __shfl_xor_sync(0xffffffffu, gi, 16);
+      const int j = (lane * E + i) % HALF;
+      const float2 c = cs[(long long)pos * HALF + j];
+      dn[i] = lo ? gi * c.x + partner * c.y : gi * c.x - partner * c.y;
+    }
+    float xh[E], gx[E], dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      xh[i] = bf2f(src[i]) * r;
+      gx[i] = dn[i] * bf2f(wgt[i]);
+      dot += gx[i] * xh[i];
+      if (is_q) accq[i] += dn[i] * xh[i]; else acck[i] += dn[i] * xh[i];
+    }
+    const float mean = warp_sum(dot) / HD;
+    __nv_bfloat16* dst = dqkv + (long long)t * ldd + (long long)hh * HD + lane * E;
+#pragma unroll
+    for (int i = 0; i < E; ++i) dst[i] = f2bf(r * (gx[i] - xh[i] * mean));
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    atomicAdd(&sq[lane * E + i], accq[i]);
+    atomicAdd(&sk[lane * E + i], acck[i]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HD; i += blockDim.x) {
+    atomicAdd(dqw + i, sq[i]);
+    atomicAdd(dkw + i, sk[i]);
+  }
+}
+
+// ------------------------------------------------------------------ SwiGLU
+// gu row = [gate(0..m) | up(0..m)];  act = silu(g) * u
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ act, long long T, int m) {
+  const long long n8 = T * m / 8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8, t = e / m;
+    const int c = (int)(e % m);
+    float g[8], u[8], o[8];
+    load8(gu + t * 2 * m + c, g);
+    load8(gu + t * 2 * m + m + c, u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.f + __expf(-g[k])) * u[k];
+    store8(act + e, o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact,
+                                  const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ dgu, long long T, int m) {
+  const long long n8 = T * m / 8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 8, t = e / m;
+    const int c = (int)(e % m);
+    float d[8], g[8], u[8], dg[8], du[8];
+    load8(dact + e, d);
+    load8(gu + t * 2 * m + c, g);
+    load8(gu + t * 2 * m + m + c, u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float s = 1.f / (1.f + __expf(-g[k]));
+      du[k] = d[k] * g[k] * s;
+      dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
+    }
+    store8(dgu + t * 2 * m + c, dg);
+    store8(dgu + t * 2 * m + m + c, du);
+  }
+}
+
+// --------------------------------------------------------------- embedding
+// out[t] = table[ids[t]]; table may be device memory or host-mapped pinned
+// memory (zero-copy gather over PCIe: only the T used rows cross the link).
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ ids,
+                                 const __nv_bfloat16* __restrict__ table,
+                                 __nv_bfloat16* __restrict__ out, int T, int h) {
+  const int t = blockIdx.x;
+  const long long row = ids[t];
+  const uint4* src = reinterpret_cast<const uint4*>(table + row * h);
+  uint4* dst = reinterpret_cast<uint4*>(out + (long long)t * h);
+  for (int i = threadIdx.x; i < h / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// dE[ids[t]] += dx[t]  (fp32 accumulate; repeated ids handled by atomics)
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ ids, const float* __restrict__ dx,
+                                 float* __restrict__ dE, int T, int h) {
+  const int t = blockIdx.x;
+  const long long row = ids[t];
+  for (int i = threadIdx.x; i < h; i += blockDim.x)
+    atomicAdd(dE + row * h + i, dx[(long long)t * h + i]);
+}
+
+// ---------------------------------------------------------- cross-entropy
+// Per row of a bf16 logits chunk: lse, loss = lse - z[label] (label < 0 =>
+// ignored), and in place dz = (softmax(z) - onehot) * grad_scale.
+template <int THREADS>
+__global__ void ce_fwd_bwd_kernel(__nv_bfloat16* __restrict__ z, long long ldz,
+                                  const int32_t* __restrict__ labels, int V, float grad_scale,
+                                  float* __restrict__ loss_sum, float* __restrict__ row_lse) {
+  __shared__ float red[THREADS / 32];
+  __shared__ float smax[THREADS / 32];
+  const long long row = blockIdx.x;
+  __nv_bfloat16* zr = z + row * ldz;
+  const int label = labels[row];
+  const bool vec = (V % 8 == 0) && (ldz % 8 == 0);
+  // pass 1: running max + rescaled sum (online softmax per thread)
+  float mx = -INFINITY, sum = 0.f;
+  if (vec) {
+    for (int c = threadIdx.x * 8; c < V; c += THREADS * 8) {
+      float f[8];
+      load8(zr + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (f[i] > mx) { sum *= __expf(mx - f[i]); mx = f[i]; }
+        sum += __expf(f[i] - mx);
+      }
+    }
+  } else {
+    for (int c = threadIdx.x; c < V; c += THREADS) {
+      const float f = bf2f(zr[c]);
+      if (f > mx) { sum *= __expf(mx - f); mx = f; }
+      sum += __expf(f - mx);
+    }
+  }
+  // block max
+  float m = mx;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x % 32 == 0) smax[threadIdx.x / 32] = m;
+  __syncthreads();
+  float gmax = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < THREADS / 32; ++i) gmax = fmaxf(gmax, smax[i]);
+  const float part = mx == -INFINITY ? 0.f : sum * __expf(mx - gmax);
+  const float total = block_sum<THREADS>(part, red);
+  const float lse = gmax + __logf(total);
+  const float zl = label >= 0 ? bf2f(zr[label]) : 0.f;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (row_lse) row_lse[row] = lse;
+    if (label >= 0 && loss_sum) atomicAdd(loss_sum, lse - zl);
+  }
+  // pass 2: dz in place
+  const float s = label >= 0 ? grad_scale : 0.f;
+  if (vec) {
+    for (int c = threadIdx.x * 8; c < V; c += THREADS * 8) {
+      float f[8];
+      load8(zr + c, f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = (__expf(f[i] - lse) - (c + i == label ? 1.f : 0.f)) * s;
+      store8(zr + c, f);
+    }
+  } else {
+    for (int c = threadIdx.x; c < V; c += THREADS) {
+      const float f = bf2f(zr[c]);
+      zr[c] = f2bf((__expf(f - lse) - (c == label ? 1.f : 0.f)) * s);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- AdamW
+// One streamed chunk of fp32 (master, m, v) in device memory, updated in
+// place from the fp32 grad; writes the new bf16 weights. Decoupled weight
+// decay (AdamW): p -= lr * (mhat / (sqrt(vhat) + eps) + wd * p).
+__global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, __nv_bfloat16* __restrict__ w16,
+                             long long n, float lr, float b1, float b2, float eps, float wd,
+                             float bc1, float bc2, float gscale) {
+  const long long n4 = n / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float* P = &pp.x;
+    float* Mm = &mm.x;
+    float* Vv = &vv.x;
+    const float* G = &gg.x;
+    __nv_bfloat16 o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gk = G[k] * gscale;
+      Mm[k] = b1 * Mm[k] + (1.f - b1) * gk;
+      Vv[k] = b2 * Vv[k] + (1.f - b2) * gk * gk;
+      const float upd = (Mm[k] / bc1) / (sqrtf(Vv[k] / bc2) + eps) + wd * P[k];
+      P[k] -= lr * upd;
+      o[k] = f2bf(P[k]);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    if (w16) {
+      uint2 u;
+      __nv_bfloat162 lo2 = __halves2bfloat162(o[0], o[1]);
+      __nv_bfloat162 hi2 = __halves2bfloat162(o[2], o[3]);
+      u.x = *reinterpret_cast<uint32_t*>(&lo2);
+      u.y = *reinterpret_cast<uint32_t*>(&hi2);
+      reinterpret_cast<uint2*>(w16)[i] = u;
+    }
+  }
+  // tail
+  const long long tail0 = n4 * 4;
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid < n - tail0) {
+    const long long k = tail0 + tid;
+    const float gk = g[k] * gscale;
+    m[k] = b1 * m[k] + (1.f - b1) * gk;
+    v[k] = b2 * v[k] + (1.f - b2) * gk * gk;
+    p[k] -= lr * ((m[k] / bc1) / (sqrtf(v[k] / bc2) + eps) + wd * p[k]);
+    if (w16) w16[k] = f2bf(p[k]);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ a, __nv_bfloat16* __restrict__ b,
+                                   long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    b[i] = f2bf(a[i]);
+}
+
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ a, float* __restrict__ b,
+                                   long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    b[i] = bf2f(a[i]);
+}
+
+__global__ void add_f32_kernel(float* __restrict__ a, const float* __restrict__ b, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] += b[i];
+}
+
+int grid_for(long long work, int threads, int max_blocks = 148 * 8) {
+  long long b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (int)(b < max_blocks ? b : max_blocks);
+}
+
+int status() { return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA; }
+
+}  // namespace
+}  // namespace rp
+
+using namespace rp;
+#define RP_API extern "C" __attribute__((visibility("default")))
+
+RP_API int rp_rmsnorm_fwd(const void* x, int64_t ldx, const void* w, void* y, int64_t ldy,
+                          float* rstd, int32_t rows, int32_t h, float eps, void* stream) {
+  if (h % 8 || ldx % 8 || ldy % 8 || rows <= 0) return RP_E_INPUT;
+  rmsnorm_fwd_kernel<256><<<rows, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)x, ldx, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, ldy, rstd, h, eps);
+  return status();
+}
+
+RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
+                          const float* dres, float* dx32, void* dx16, float* dw, int32_t rows,
+                          int32_t h, void* stream) {
+  if (h % 8 || rows <= 0 || h > 256 * 8 * 4) return RP_E_INPUT;
+  const int grid = rows < 148 * 4 ? rows : 148 * 4;
+  if (h <= 256 * 8)
+    rmsnorm_bwd_kernel<256, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd, dres,
+        dx32, (__nv_bfloat16*)dx16, dw, rows, h);
+  else
+    rmsnorm_bwd_kernel<256, 4><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd, dres,
+        dx32, (__nv_bfloat16*)dx16, dw, rows, h);
+  return status();
+}
+
+RP_API int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t nk,
+                               int32_t head_dim, const void* qw, const void* kw,
+                               const float* cos_sin, int32_t seq, void* q_out, void* k_out,
+                               float* rstd_q, float* rstd_k, int32_t T, float eps,
+                               void* stream) {
+  const long long warps = (long long)T * (nq + nk);
+  const int grid = (int)((warps + 7) / 8);
+  auto s = (cudaStream_t)stream;
+  if (head_dim == 128)
+    qk_norm_rope_fwd_kernel<4><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
+        (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
+        T, eps);
+  else if (head_dim == 64)
+    qk_norm_rope_fwd_kernel<2><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
+        (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
+        T, eps);
+  else
+    return RP_E_INPUT;
+  return status();
+}
+
+RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, int64_t ld,
+                               int32_t nq, int32_t nk, int32_t head_dim, const void* qw,
+                               const void* kw, const float* rstd_q, const float* rstd_k,
+                               const float* cos_sin, int32_t seq, void* dqkv, int64_t ldd,
+                               float* dqw, float* dkw, int32_t T, void* stream) {
+  auto s = (cudaStream_t)stream;
+  const int grid = 148 * 2;
+  if (head_dim == 128)
+    qk_norm_rope_bwd_kernel<4><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
+        (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
+        seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
+  else if (head_dim == 64)
+    qk_norm_rope_bwd_kernel<2><<<grid, 256, 0, s>>>(
+        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
+        (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
+        seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
+  else
+    return RP_E_INPUT;
+  return status();
+}
+
+RP_API int rp_swiglu_fwd(const void* gu, void* act, int64_t T, int32_t m, void* stream) {
+  if (m % 8) return RP_E_INPUT;
+  swiglu_fwd_kernel<<<grid_for(T * m / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, T, m);
+  return status();
+}
+
+RP_API int rp_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t T, int32_t m,
+                         void* stream) {
+  if (m % 8) return RP_E_INPUT;
+  swiglu_bwd_kernel<<<grid_for(T * m / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, T, m);
+  return status();
+}
+
+RP_API int rp_embed_fwd(const int32_t* ids, const void* table, void* out, int32_t T, int32_t h,
+                        void* stream) {
+  if (h % 8) return RP_E_INPUT;
+  embed_fwd_kernel<<<T, 128, 0, (cudaStream_t)stream>>>(ids, (const __nv_bfloat16*)table,
+                                                        (__nv_bfloat16*)out, T, h);
+  return status();
+}
+
+RP_API int rp_embed_bwd(const int32_t* ids, const float* dx, float* dE, int32_t T, int32_t h,
+                        void* stream) {
+  embed_bwd_kernel<<<T, 256, 0, (cudaStream_t)stream>>>(ids, dx, dE, T, h);
+  return status();
+}
+
+RP_API int rp_ce_fwd_bwd(void* logits, int64_t ld, const int32_t* labels, int32_t rows,
+                         int32_t V, float grad_scale, float* loss_sum, float* row_lse,
+                         void* stream) {
+  if (rows <= 0) return RP_OK;
+  ce_fwd_bwd_kernel<512><<<rows, 512, 0, (cudaStream_t)stream>>>(
+      (__nv_bfloat16*)logits, ld, labels, V, grad_scale, loss_sum, row_lse);
+  return status();
+}
+
+RP_API int rp_adamw(float* master, float* m, float* v, const float* grad, void* w16, int64_t n,
+                    const rp_adam_hparams_t* hp, int32_t step, void* stream) {
+  if (!hp || step < 1 || (reinterpret_cast<uintptr_t>(master) & 15) ||
+      (reinterpret_cast<uintptr_t>(m) & 15) || (reinterpret_cast<uintptr_t>(v) & 15) ||
+      (reinterpret_cast<uintptr_t>(grad) & 15) || (w16 && (reinterpret_cast<uintptr_t>(w16) & 7)))
+    return RP_E_INPUT;
+  const float bc1 = 1.f - powf(hp->beta1, (float)step);
+  const float bc2 = 1.f - powf(hp->beta2, (float)step);
+  adamw_kernel<<<grid_for(n / 4 + 4, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      master, m, v, grad, (__nv_bfloat16*)w16, n, hp->lr, hp->beta1, hp->beta2, hp->eps,
+      hp->weight_decay, bc1, bc2, hp->grad_scale);
+  return status();
+}
+
+RP_API int rp_f32_to_bf16(const float* a, void* b, int64_t n, void* stream) {
+  f32_to_bf16_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(a, (__nv_bfloat16*)b, n);
+  return status();
+}
+
+RP_API int rp_bf16_to_f32(const void* a, float* b, int64_t n, void* stream) {
+  bf16_to_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)a,
+                                                                          b, n);
+  return status();
+}
+
+RP_API int rp_add_f32(float* a, const float* b, int64_t n, void* stream) {
+  add_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(a, b, n);
+  return status();
+}

@@ -1,0 +1,331 @@
+// Persistent warp-specialised bf16 GEMM for sm_100a (tcgen05 + TMEM + TMA).
+//
+//   D[M,N] (+)= A[M,K] . B[N,K]^T      bf16 inputs, fp32 accumulation in TMEM
+//
+// Each operand is K-major (row-major with K contiguous) or MN-major (K rows
+// with M/N contiguous), so one kernel family covers the three GEMMs of every
+// linear layer without materialised transposes:
+//   forward  Y  = X  . W^T   A=X  K-major,  B=W  K-major
+//   dgrad    dX = dY . W     A=dY K-major,  B=W  N-major
+//   wgrad    dW += dY^T . X  A=dY M-major,  B=X  N-major   (fp32 accumulate)
+//
+// Tile 128x256x64, 4-stage TMA->smem ring (SWIZZLE_128B), one elected thread
+// issues tcgen05.mma (M=128, N=256, K=16) into a double-buffered 2x256-column
+// TMEM accumulator; 4 epilogue warps drain TMEM (tcgen05.ld 32x32b) while the
+// next tile's MMAs run. Grid = min(tiles, #SMs), static round-robin tiles with
+// M fastest so consecutive CTAs share the B panel in L2.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels/sm100.cuh"
+#include "rp/kernels.h"
+
+namespace rp {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int NUM_THREADS = 256;             // w0 TMA, w1 MMA, w2 TMEM, w4-7 epilogue
+constexpr int TMEM_COLS = 512;               // 2 x 256-column accumulators
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+enum Epi : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2 };
+
+struct Params {
+  int M, N, K;
+  void* D;
+  long long ldd;
+  const __nv_bfloat16* R;  // optional bf16 residual for EPI_BF16
+  long long ldr;
+  int vec;                 // 16-byte vector stores/loads legal for D (and R)
+};
+
+template <int A_MN, int B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
+                const __grid_constant__ CUtensorMap tma_b, Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;   // [2]
+  uint64_t* acc_empty = acc_full + 2;    // [2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * STAGE_BYTES;
+        uint8_t* sb = sa + A_STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (A_MN) {
+          tma_load_2d(sa, &tma_a, &full[stage], m0, k0);
+          tma_load_2d(sa + 8192, &tma_a, &full[stage], m0 + 64, k0);
+        } else {
+          tma_load_2d(sa, &tma_a, &full[stage], k0, m0);
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+        } else {
+          tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+        const uint32_t b_addr = a_addr + A_STAGE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                   : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+          const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                   : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+          umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      umma_commit(&acc_full[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+        tmem_ld_wait();
+        const int col0 = n0 + c;
+        if (row_ok && col0 < p.N) {
+        const bool full_chunk = p.vec && col0 + 32 <= p.N;
+        if (EPI == EPI_BF16) {
+          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col0;
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          if (p.R) {
+            const __nv_bfloat16* r = p.R + (long long)row * p.ldr + col0;
+            if (full_chunk) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                uint4 rv = *reinterpret_cast<const uint4*>(r + i);
+                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[i + j] += __bfloat162float(rb[j]);
+              }
+            } else {
+              for (int i = 0; i < 32 && col0 + i < p.N; ++i) f[i] += __bfloat162float(r[i]);
+            }
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 o;
+              o.x = pack_bf16x2(f[i], f[i + 1]);
+              o.y = pack_bf16x2(f[i + 2], f[i + 3]);
+              o.z = pack_bf16x2(f[i + 4], f[i + 5]);
+              o.w = pack_bf16x2(f[i + 6], f[i + 7]);
+              *reinterpret_cast<uint4*>(d + i) = o;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) d[i] = __float2bfloat16_rn(f[i]);
+          }
+        } else {
+          float* d = reinterpret_cast<float*>(p.D) + (long long)row * p.ldd + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                     __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+              if (EPI == EPI_F32_ACC) {
+                const float4 old = *reinterpret_cast<const float4*>(d + i);
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              *reinterpret_cast<float4*>(d + i) = o;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+              d[i] = (EPI == EPI_F32_ACC ? d[i] : 0.f) + __uint_as_float(v[i]);
+          }
+        }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---- host side: tensor maps ------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+    return reinterpret_cast<EncodeFn>(ptr);
+  }();
+  return fn;
+}
+
+// 2-D bf16 map over a row-major [rows, cols] matrix (cols contiguous, row
+// pitch ld elements) with a {box_cols, box_rows} SWIZZLE_128B box.
+bool make_map(CUtensorMap* map, const void* base, long long rows, long long cols, long long ld,
+              int box_cols, int box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t elem[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+            box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+template <int A_MN, int B_MN, int EPI>
+cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                   cudaStream_t stream) {
+  auto kern = gemm_kernel<A_MN, B_MN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
+template <int A_MN, int B_MN>
+cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
+                         cudaStream_t s) {
+  switch (epi) {
+    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, p, s);
+    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, p, s);
+    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, p, s);
+  }
+}
+
+}  // namespace
+}  // namespace rp
+
+using namespace rp;
+
+extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm_args_t* g,
+                                                                   void* stream) {
+  if (!g || g->M <= 0 || g->N <= 0 || g->K <= 0 || !g->A || !g->B || !g->D) return RP_E_INPUT;
+  if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
+      (reinterpret_cast<uintptr_t>(g->B) & 15))
+    return RP_E_INPUT;
+  CUtensorMap ta, tb;
+  bool ok = g->a_mn_major ? make_map(&ta, g->A, g->K, g->M, g->lda, 64, 64)
+                          : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
+  ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
+                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64, BN));
+  if (!ok) return RP_E_CUDA;
+  const int esz = g->out_f32 ? 4 : 2;
+  const bool vec = (g->ldd * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
+                   (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0));
+  Params p{g->M, g->N, g->K, g->D, g->ldd, reinterpret_cast<const __nv_bfloat16*>(g->R), g->ldr,
+           vec ? 1 : 0};
+  const int epi = g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
+  if (g->out_f32 && g->R) return RP_E_INPUT;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (g->a_mn_major)
+    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, p, s) : dispatch_epi<1, 0>(epi, ta, tb, p, s);
+  else
+    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, p, s) : dispatch_epi<0, 0>(epi, ta, tb, p, s);
+  return e == cudaSuccess ? RP_OK : RP_E_CUDA;
+}

@@ -1,0 +1,172 @@
+"""Thin torch-tensor front-end to the sm_100a kernel C-ABI (include/rp/kernels.h).
+
+Torch is only the allocator and stream provider here: every call goes
+straight to libroundpipe_b200.so; there is no eager fallback. Used by the GPU
+parity tests, smoke() and micro-benchmarks. The runtime (C++) calls the same
+entry points directly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native
+
+I32, I64, VP = C.c_int32, C.c_int64, C.c_void_p
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [("M", I32), ("N", I32), ("K", I32),
+                ("A", VP), ("lda", I64), ("a_mn_major", I32),
+                ("B", VP), ("ldb", I64), ("b_mn_major", I32),
+                ("D", VP), ("ldd", I64), ("out_f32", I32), ("accumulate", I32),
+                ("R", VP), ("ldr", I64)]
+
+
+def _lib():
+    return _native.load()
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return VP(s.cuda_stream)
+
+
+def _ptr(t):
+    return VP(t.data_ptr()) if t is not None else VP(0)
+
+
+def _check(code):
+    return _native.check(_lib(), "rp_", code)
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, D: torch.Tensor, *, a_mn_major=False,
+         b_mn_major=False, accumulate=False, residual: torch.Tensor | None = None,
+         stream=None):
+    """D[M,N] (+)= op(A)[M,K] . op(B)[N,K]^T.
+
+    A is [M,K] (a_mn_major=False) or [K,M] (True); B is [N,K] or [K,N].
+    D bf16 (optionally + residual) or fp32 (optionally accumulated).
+    """
+    assert A.dtype == torch.bfloat16 and B.dtype == torch.bfloat16
+    M = A.shape[1] if a_mn_major else A.shape[0]
+    K = A.shape[0] if a_mn_major else A.shape[1]
+    N = B.shape[1] if b_mn_major else B.shape[0]
+    Kb = B.shape[0] if b_mn_major else B.shape[1]
+    assert K == Kb and tuple(D.shape) == (M, N)
+    assert D.dtype in (torch.bfloat16, torch.float32)
+    for t in (A, B, D) + ((residual,) if residual is not None else ()):
+        assert t.is_cuda and t.stride(1) == 1
+    args = GemmArgs(M, N, K, _ptr(A), A.stride(0), int(a_mn_major),
+                    _ptr(B), B.stride(0), int(b_mn_major),
+                    _ptr(D), D.stride(0), int(D.dtype == torch.float32), int(accumulate),
+                    _ptr(residual), residual.stride(0) if residual is not None else 0)
+    f = _lib().rp_gemm_bf16
+    f.restype = C.c_int
+    _check(f(C.byref(args), _stream(stream)))
+    return D
+
+
+class AdamHParams(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("eps", C.c_float), ("weight_decay", C.c_float), ("grad_scale", C.c_float)]
+
+
+def _call(name, *args):
+    f = getattr(_lib(), name)
+    f.restype = C.c_int
+    return _check(f(*args))
+
+
+F = C.c_float
+
+
+def rmsnorm_fwd(x, w, y, rstd, eps=1e-6, stream=None):
+    rows, h = x.shape
+    _call("rp_rmsnorm_fwd", _ptr(x), I64(x.stride(0)), _ptr(w), _ptr(y), I64(y.stride(0)),
+          _ptr(rstd), I32(rows), I32(h), F(eps), _stream(stream))
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dx32=None, dx16=None, dw=None, dres=None, stream=None):
+    rows, h = x.shape
+    _call("rp_rmsnorm_bwd", _ptr(dy), _ptr(x), _ptr(w), _ptr(rstd), _ptr(dres), _ptr(dx32),
+          _ptr(dx16), _ptr(dw), I32(rows), I32(h), _stream(stream))
+
+
+def qk_norm_rope_fwd(qkv, nq, nk, hd, qw, kw, cos_sin, seq, q_out, k_out, rstd_q, rstd_k,
+                     eps=1e-6, stream=None):
+    T = qkv.shape[0]
+    _call("rp_qk_norm_rope_fwd", _ptr(qkv), I64(qkv.stride(0)), I32(nq), I32(nk), I32(hd),
+          _ptr(qw), _ptr(kw), _ptr(cos_sin), I32(seq), _ptr(q_out), _ptr(k_out), _ptr(rstd_q),
+          _ptr(rstd_k), I32(T), F(eps), _stream(stream))
+
+
+def qk_norm_rope_bwd(dq, dk, qkv, nq, nk, hd, qw, kw, rstd_q, rstd_k, cos_sin, seq, dqkv,
+                     dqw, dkw, stream=None):
+    T = qkv.shape[0]
+    _call("rp_qk_norm_rope_bwd", _ptr(dq), _ptr(dk), _ptr(qkv), I64(qkv.stride(0)), I32(nq),
+          I32(nk), I32(hd), _ptr(qw), _ptr(kw), _ptr(rstd_q), _ptr(rstd_k), _ptr(cos_sin),
+          I32(seq), _ptr(dqkv), I64(dqkv.stride(0)), _ptr(dqw), _ptr(dkw), I32(T),
+          _stream(stream))
+
+
+def swiglu_fwd(gu, act, stream=None):
+    T, m = act.shape
+    _call("rp_swiglu_fwd", _ptr(gu), _ptr(act), I64(T), I32(m), _stream(stream))
+
+
+def swiglu_bwd(dact, gu, dgu, stream=None):
+    T, m = dact.shape
+    _call("rp_swiglu_bwd", _ptr(dact), _ptr(gu), _ptr(dgu), I64(T), I32(m), _stream(stream))
+
+
+def embed_fwd(ids, table, out, stream=None):
+    T, h = out.shape
+    _call("rp_embed_fwd", _ptr(ids), _ptr(table), _ptr(out), I32(T), I32(h), _stream(stream))
+
+
+def embed_bwd(ids, dx, dE, stream=None):
+    T, h = dx.shape
+    _call("rp_embed_bwd", _ptr(ids), _ptr(dx), _ptr(dE), I32(T), I32(h), _stream(stream))
+
+
+def ce_fwd_bwd(logits, labels, grad_scale, loss_sum, row_lse=None, stream=None):
+    rows, V = logits.shape
+    _call("rp_ce_fwd_bwd", _ptr(logits), I64(logits.stride(0)), _ptr(labels), I32(rows), I32(V),
+          F(grad_scale), _ptr(loss_sum), _ptr(row_lse), _stream(stream))
+
+
+def adamw(master, m, v, grad, w16, step, lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-8,
+          weight_decay=0.0, grad_scale=1.0, stream=None):
+    hp = AdamHParams(lr, beta1, beta2, eps, weight_decay, grad_scale)
+    _call("rp_adamw", _ptr(master), _ptr(m), _ptr(v), _ptr(grad), _ptr(w16),
+          I64(master.numel()), C.byref(hp), I32(step), _stream(stream))
+
+
+def attn_fwd(q, k, v, o, lse, seq, nq, nk, hd, scale=None, stream=None):
+    T = q.shape[0]
+    scale = scale if scale is not None else hd ** -0.5
+    _call("rp_attn_fwd", _ptr(q), I64(q.stride(0)), _ptr(k), I64(k.stride(0)), _ptr(v),
+          I64(v.stride(0)), _ptr(o), I64(o.stride(0)), _ptr(lse), I32(T), I32(seq), I32(nq),
+          I32(nk), I32(hd), F(scale), _stream(stream))
+
+
+def attn_bwd(q, k, v, o, do, lse, dq, dk, dv, dq_acc, delta, seq, nq, nk, hd, scale=None,
+             stream=None):
+    T = q.shape[0]
+    scale = scale if scale is not None else hd ** -0.5
+    _call("rp_attn_bwd", _ptr(q), I64(q.stride(0)), _ptr(k), I64(k.stride(0)), _ptr(v),
+          I64(v.stride(0)), _ptr(o), I64(o.stride(0)), _ptr(do), I64(do.stride(0)), _ptr(lse),
+          _ptr(dq), I64(dq.stride(0)), _ptr(dk), I64(dk.stride(0)), _ptr(dv), I64(dv.stride(0)),
+          _ptr(dq_acc), _ptr(delta), I32(T), I32(seq), I32(nq), I32(nk), I32(hd), F(scale),
+          _stream(stream))
+
+
+def rope_table(seq, hd, theta=1e6):
+    """float2 (cos, sin) table [seq, hd/2], computed in float64 then rounded."""
+    import numpy as np
+    inv = 1.0 / (theta ** (np.arange(0, hd, 2, dtype=np.float64) / hd))
+    ang = np.arange(seq, dtype=np.float64)[:, None] * inv[None, :]
+    tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+    return torch.from_numpy(np.ascontiguousarray(tab))
