@@ -1,0 +1,106 @@
+/* roundpipe-b200 runtime C-ABI: the B200 executor of the RoundPipe step.
+ *
+ * Mirrors the paper's runtime interface:
+ *   rp_forward_backward()  — micro-batches the step, plans (reference
+ *       partitioner + dispatcher, cached), walks the dispatch list on the
+ *       GPUs and returns as soon as the loss is known (early return);
+ *   rp_step()              — queues the optimizer (fused AdamW on streamed
+ *       fp32 state chunks, written back to pinned host memory); returns
+ *       immediately. Sync mode applies it before the next iteration's
+ *       uploads, async mode is the staleness-1 hand-off of the paper;
+ *   rp_sync()              — drains everything.
+ * Host buffers are plain pointers; no torch types cross this ABI.
+ */
+#ifndef RP_RUNTIME_H_
+#define RP_RUNTIME_H_
+#include <stdint.h>
+
+#include "rp/cabi.h"
+#include "rp/kernels.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rp_runtime rp_runtime_t;
+
+enum {
+  RP_RT_SKIP_INIT = 1,      /* do not randomise weights (caller loads them) */
+  RP_RT_RECORD_TIMELINE = 2 /* record per-task CUDA events (measured bubble) */
+};
+
+typedef struct {
+  const char* model;           /* configs/models name or JSON path */
+  int32_t seq_len;             /* s */
+  int32_t micro_batch;         /* b: sequences per micro-batch */
+  int32_t micro_batches;       /* M per iteration */
+  int32_t round_micro_batches; /* M_R; 0 = M (single round per iteration) */
+  int32_t num_gpus;            /* N devices (0..N-1) driven by this process */
+  int32_t async_optimizer;     /* 1 = RoundPipe (staleness-1), 0 = RoundPipe-sync */
+  int64_t mem_limit_bytes;     /* partitioner memory limit; 0 = 90% of HBM */
+  double residency_factor;     /* partitioner residency (reference default 2.0) */
+  const rp_layer_cost_t* costs;/* optional cost table, L+1 rows (NULL = cost model) */
+  int32_t n_costs;
+  rp_adam_hparams_t adam;
+  uint64_t init_seed;
+  float init_std;
+  int32_t flags;               /* RP_RT_* */
+} rp_runtime_config_t;
+
+typedef struct {
+  int32_t num_layers;          /* L decoder layers; pseudo-layer L is the head */
+  int32_t num_slots;           /* S of the plan */
+  int64_t params_total;
+  int64_t host_bytes_pinned;
+  int64_t device_bytes[8];
+  int64_t h2d_bytes, d2h_bytes, p2p_bytes; /* cumulative */
+  int32_t iterations_done;
+  int32_t kernels_launched;    /* cumulative count of this library's kernel launches */
+} rp_runtime_stats_t;
+
+int rp_runtime_create(const rp_runtime_config_t* cfg, rp_runtime_t** out);
+int rp_runtime_destroy(rp_runtime_t* rt);
+
+/* The stage plan and per-slot durations the executor runs. */
+int rp_runtime_plan(rp_runtime_t* rt, rp_stage_plan_t* plan, int64_t* slot_durs,
+                    int32_t cap, int32_t* n_slots);
+
+/* Parameter groups: -1 = embedding, 0..L-1 decoder layers, L = head.
+ * Values are fp32 in the flat order of include/rp/layout. */
+int rp_param_count(rp_runtime_t* rt, int32_t group, int64_t* n);
+int rp_set_params(rp_runtime_t* rt, int32_t group, const float* values, int64_t n);
+/* which: 0 fp32 master, 1 bf16 master (as fp32), 2 last iteration's grads,
+ *        3 Adam m, 4 Adam v */
+int rp_get_params(rp_runtime_t* rt, int32_t group, int32_t which, float* out, int64_t n);
+
+/* tokens/labels: host int32 [M, b, s]; labels < 0 are ignored. *loss = mean
+ * token cross-entropy of the step (returned as soon as it is known). */
+int rp_forward_backward(rp_runtime_t* rt, const int32_t* tokens, const int32_t* labels,
+                        float* loss);
+int rp_step(rp_runtime_t* rt);
+int rp_sync(rp_runtime_t* rt);
+
+/* Measured per-task compute intervals (ns on a common clock), emission
+ * order of the dispatch list; feed to rp_interior_bubble / rp_idle_in_window. */
+int rp_timeline(rp_runtime_t* rt, rp_timed_event_t* out, int64_t cap, int64_t* n);
+int rp_runtime_stats(rp_runtime_t* rt, rp_runtime_stats_t* stats);
+int rp_timeline_clear(rp_runtime_t* rt);
+/* The cost table the plan was built from (L+1 rows). */
+int rp_runtime_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
+/* Flat layout of a group: (offset, rows, cols) per tensor, order
+ * embedding: [table]; layer: in_norm qkv q_norm k_norm o post_norm gate_up down;
+ * head: final_norm lm_head. */
+int rp_param_layout(rp_runtime_t* rt, int32_t group, int64_t* offs, int64_t* rows,
+                    int64_t* cols, int32_t cap, int32_t* n);
+const char* rp_runtime_last_error(void);
+/* Kernel profiling of the following steps (CUDA events around each launch on
+ * its own stream). Read: per category 0 GEMM (FLOPs), 1 attention (FLOPs),
+ * 2 HBM-bound stage kernels (bytes), 3 AdamW (bytes): summed kernel ms,
+ * algorithmic work and launch count. */
+int rp_runtime_profile(rp_runtime_t* rt, int32_t enable);
+int rp_runtime_profile_read(rp_runtime_t* rt, double* time_ms, double* work, int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RP_RUNTIME_H_ */

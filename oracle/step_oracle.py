@@ -1,0 +1,243 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY — the CPU restatement of one RoundPipe
+training step. Never imported by the product; only tests/, smoke() and
+bench.py's cpu_baseline / --impl reference legs use it, as the checker.
+
+The reference repository has no data-plane code: no
+file computes a loss, gradient or optimizer update. This module restates,
+in fp32 PyTorch on the CPU:
+  * the Qwen3 decoder math of transformers 5.5.0 (third-party, pinned in
+    this image): RMSNorm modeling_qwen3.py:50-67, MLP/SwiGLU :70-83, rotary
+    :86-182, GQA eager attention :184-220, per-head q/k-norm :248-264,
+    decoder layer :294-336, Qwen3ForCausalLM :442+ (untied LM head);
+  * the RoundPipe mixed-precision model: fp32
+    optimizer copy, bf16 master copy used for compute (here: bf16-rounded
+    weights computed in fp32);
+  * the optimizer hand-off (consistency.hpp:98-109):
+      sync  — iteration t+1 sees grads of t;
+      async — step(t+1) applies grads of t, first visible to iteration t+2
+              (staleness 1);
+  * loss = sum of token CE over the step / number of valid labels; AdamW =
+    torch.optim.AdamW (decoupled weight decay).
+Pinning: tests/golden/make_step_golden.py checks this module's loss and
+gradients against transformers' Qwen3ForCausalLM on identical weights and
+commits the numbers (tests/golden/step_golden.json).
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@dataclass
+class Shape:
+    hidden: int
+    heads: int
+    kv_heads: int
+    head_dim: int
+    inter: int
+    layers: int
+    vocab: int
+    rope_theta: float = 1e6
+    eps: float = 1e-6
+
+    @staticmethod
+    def from_config(name: str) -> "Shape":
+        path = name if name.endswith(".json") else os.path.join(
+            ROOT, "configs", "models", name + ".json")
+        with open(path) as f:
+            j = json.load(f)
+        return Shape(int(j["hidden_dim"]), j["num_heads"], j["num_kv_heads"],
+                     j.get("head_dim", int(j["hidden_dim"]) // j["num_heads"]),
+                     int(j["intermediate_dim"]), j["num_layers"], j["vocab_size"],
+                     j.get("rope_theta", 1e6), j.get("rms_norm_eps", 1e-6))
+
+
+# parameter names and shapes, in the flat per-layer order the runtime uses
+def layer_param_shapes(s: Shape):
+    qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
+    return [("input_norm", (s.hidden,)), ("qkv", (qd + 2 * kd, s.hidden)),
+            ("q_norm", (s.head_dim,)), ("k_norm", (s.head_dim,)),
+            ("o", (s.hidden, qd)), ("post_norm", (s.hidden,)),
+            ("gate_up", (2 * s.inter, s.hidden)), ("down", (s.hidden, s.inter))]
+
+
+def head_param_shapes(s: Shape):
+    return [("final_norm", (s.hidden,)), ("lm_head", (s.vocab, s.hidden))]
+
+
+def init_params(s: Shape, seed: int = 0, std: float = 0.02):
+    """Deterministic init: N(0, std) matrices, ones for norms; values are
+    rounded to bf16 so the fp32 oracle and the bf16 GPU copy start equal."""
+    g = torch.Generator().manual_seed(seed)
+
+    def mk(name, shape):
+        if len(shape) == 1:
+            return torch.ones(shape)
+        return (torch.randn(shape, generator=g) * std).to(torch.bfloat16).float()
+    params = {"embed": (torch.randn(s.vocab, s.hidden, generator=g) * std)
+              .to(torch.bfloat16).float()}
+    for l in range(s.layers):
+        for n, sh in layer_param_shapes(s):
+            params[f"layers.{l}.{n}"] = mk(n, sh)
+    for n, sh in head_param_shapes(s):
+        params[f"head.{n}"] = mk(n, sh)
+    return params
+
+
+def rms(x, w, eps):
+    return w * (x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps))
+
+
+def rope_cos_sin(seq, hd, theta):
+    inv = 1.0 / (theta ** (torch.arange(0, hd, 2, dtype=torch.float64) / hd))
+    ang = torch.arange(seq, dtype=torch.float64)[:, None] * inv[None, :]
+    cos, sin = ang.cos().float(), ang.sin().float()
+    return torch.cat([cos, cos], -1), torch.cat([sin, sin], -1)
+
+
+def rotate_half(x):
+    h = x.shape[-1] // 2
+    return torch.cat([-x[..., h:], x[..., :h]], -1)
+
+
+def decoder_layer(x, p, pre, s: Shape, cos, sin):
+    """x [b, S, h] fp32 -> [b, S, h]; p(name) gives the fp32 weight."""
+    b, S, _ = x.shape
+    qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
+    h1 = rms(x, p(pre + "input_norm"), s.eps)
+    qkv = h1 @ p(pre + "qkv").t()
+    q = qkv[..., :qd].view(b, S, s.heads, s.head_dim)
+    k = qkv[..., qd:qd + kd].view(b, S, s.kv_heads, s.head_dim)
+    v = qkv[..., qd + kd:].view(b, S, s.kv_heads, s.head_dim)
+    q = rms(q, p(pre + "q_norm"), s.eps).transpose(1, 2)
+    k = rms(k, p(pre + "k_norm"), s.eps).transpose(1, 2)
+    v = v.transpose(1, 2)
+    q = q * cos + rotate_half(q) * sin
+    k = k * cos + rotate_half(k) * sin
+    rep = s.heads // s.kv_heads
+    k = k.repeat_interleave(rep, 1)
+    v = v.repeat_interleave(rep, 1)
+    att = (q @ k.transpose(-1, -2)) * (s.head_dim ** -0.5)
+    mask = torch.ones(S, S, dtype=torch.bool).triu(1)
+    att = att.masked_fill(mask, float("-inf")).softmax(-1)
+    o = (att @ v).transpose(1, 2).reshape(b, S, qd)
+    x2 = x + o @ p(pre + "o").t()
+    h2 = rms(x2, p(pre + "post_norm"), s.eps)
+    gu = h2 @ p(pre + "gate_up").t()
+    act = torch.nn.functional.silu(gu[..., :s.inter]) * gu[..., s.inter:]
+    return x2 + act @ p(pre + "down").t()
+
+
+def forward_loss_sum(params, tokens, labels, s: Shape):
+    """Sum of token cross-entropy (labels < 0 ignored) for tokens [b, S]."""
+    b, S = tokens.shape
+    cos, sin = rope_cos_sin(S, s.head_dim, s.rope_theta)
+
+    def p(name):
+        return params[name]
+    x = params["embed"][tokens]
+    for l in range(s.layers):
+        x = decoder_layer(x, p, f"layers.{l}.", s, cos, sin)
+    x = rms(x, p("head.final_norm"), s.eps)
+    logits = x @ p("head.lm_head").t()
+    return torch.nn.functional.cross_entropy(
+        logits.view(-1, s.vocab), labels.reshape(-1).long(), ignore_index=-100,
+        reduction="sum")
+
+
+def bf16_round(t):
+    return t.to(torch.bfloat16).float()
+
+
+class StepOracle:
+    """fp32 CPU RoundPipe step: M micro-batches of [b, S] tokens per
+    iteration, grads accumulated over the step, AdamW on an fp32 copy,
+    compute on bf16-rounded weights, sync or async (staleness-1) hand-off."""
+
+    def __init__(self, s: Shape, params: dict, lr=1e-3, betas=(0.9, 0.95), eps=1e-8,
+                 weight_decay=0.0, mode="sync", threads: int | None = None):
+        assert mode in ("sync", "async")
+        if threads:
+            torch.set_num_threads(threads)
+        self.s = s
+        self.mode = mode
+        self.master = {k: v.clone().float().requires_grad_(False) for k, v in params.items()}
+        self.opt_params = {k: torch.nn.Parameter(v.clone()) for k, v in self.master.items()}
+        self.opt = torch.optim.AdamW(list(self.opt_params.values()), lr=lr, betas=betas, eps=eps,
+                                     weight_decay=weight_decay)
+        # weights the next iteration computes with (bf16 master copy)
+        self.used = {k: bf16_round(v) for k, v in self.master.items()}
+        self.pending = None  # async: result of the last optimizer step
+        self.last_grads = None
+
+    def _fwd_bwd(self, tokens, labels):
+        w = {k: v.clone().requires_grad_(True) for k, v in self.used.items()}
+        n_valid = int((labels >= 0).sum())
+        total = 0.0
+        for mb in range(tokens.shape[0]):
+            loss = forward_loss_sum(w, tokens[mb], labels[mb], self.s) / n_valid
+            loss.backward()
+            total += loss.item()
+        return total, {k: v.grad if v.grad is not None else torch.zeros_like(v)
+                       for k, v in w.items()}
+
+    def _apply(self, grads):
+        for k, prm in self.opt_params.items():
+            prm.grad = grads[k].clone()
+        self.opt.step()
+        self.opt.zero_grad(set_to_none=True)
+        return {k: bf16_round(p.detach()) for k, p in self.opt_params.items()}
+
+    def step(self, tokens, labels):
+        """tokens, labels: [M, b, S] int. Returns the step's mean loss."""
+        loss, grads = self._fwd_bwd(tokens, labels)
+        self.last_grads = grads
+        if self.mode == "sync":
+            self.used = self._apply(grads)
+        else:
+            # step(t+1) applies grads of t; its result is uploaded at t+2
+            if self.pending is not None:
+                self.used = self.pending
+            self.pending = self._apply(grads)
+        return loss
+
+    def master_fp32(self):
+        return {k: p.detach().clone() for k, p in self.opt_params.items()}
+
+
+def synthetic_batch(s: Shape, M: int, b: int, S: int, seed: int = 1234):
+    """Token ids ~ U{0..V-1} (seeded), labels = ids shifted by one, last
+    position of each sequence ignored (-100)."""
+    g = torch.Generator().manual_seed(seed)
+    ids = torch.randint(0, s.vocab, (M, b, S + 1), generator=g)
+    tokens = ids[..., :S].contiguous()
+    labels = ids[..., 1:].contiguous()
+    return tokens.int(), labels.int()
+
+
+def _cli():
+    import argparse
+    import time
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="tiny")
+    ap.add_argument("--seq", type=int, default=256)
+    ap.add_argument("--M", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--mode", default="sync")
+    a = ap.parse_args()
+    s = Shape.from_config(a.model)
+    o = StepOracle(s, init_params(s), mode=a.mode)
+    tok, lab = synthetic_batch(s, a.M, 1, a.seq)
+    for i in range(a.steps):
+        t0 = time.time()
+        print(i, o.step(tok, lab), f"{time.time() - t0:.2f}s")
+
+
+if __name__ == "__main__":
+    _cli()

@@ -629,3 +629,50 @@ RP_API int rp_add_f32(float* a, const float* b, int64_t n, void* stream) {
   add_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(a, b, n);
   return status();
 }
+
+// ---------------------------------------------------------------- init
+namespace rp {
+namespace {
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdULL; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ULL; x ^= x >> 33;
+  return static_cast<uint32_t>(x);
+}
+// Deterministic N(0, std) (Box-Muller on a counter hash), rounded to bf16;
+// writes the bf16 value and (optionally) its exact fp32 widening.
+__global__ void init_normal_kernel(float* __restrict__ f32, uint16_t* __restrict__ b16,
+                                   long long n, unsigned long long seed, float std) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t a = mix32(seed * 0x9E3779B97F4A7C15ULL + 2 * (unsigned long long)i);
+    const uint32_t b = mix32(seed * 0x9E3779B97F4A7C15ULL + 2 * (unsigned long long)i + 1);
+    const float u1 = (a + 1.0f) * 2.3283064e-10f, u2 = b * 2.3283064e-10f;
+    const float z = sqrtf(-2.f * __logf(u1)) * __cosf(6.2831853f * u2) * std;
+    const __nv_bfloat16 hb = __float2bfloat16_rn(z);
+    if (f32) f32[i] = __bfloat162float(hb);
+    b16[i] = *reinterpret_cast<const uint16_t*>(&hb);
+  }
+}
+__global__ void fill_kernel(float* __restrict__ f32, uint16_t* __restrict__ b16, long long n,
+                            float value) {
+  const __nv_bfloat16 hb = __float2bfloat16_rn(value);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (f32) f32[i] = value;
+    b16[i] = *reinterpret_cast<const uint16_t*>(&hb);
+  }
+}
+}  // namespace
+}  // namespace rp
+
+RP_API int rp_init_normal(float* f32, void* b16, int64_t n, uint64_t seed, float std,
+                          void* stream) {
+  init_normal_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+      f32, (uint16_t*)b16, n, seed, std);
+  return status();
+}
+
+RP_API int rp_fill(float* f32, void* b16, int64_t n, float value, void* stream) {
+  fill_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(f32, (uint16_t*)b16, n,
+                                                                           value);
+  return status();
+}

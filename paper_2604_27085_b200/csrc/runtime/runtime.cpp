@@ -1,0 +1,1297 @@
+// roundpipe-b200 executor: runs the RoundPipe training step on B200s.
+//
+// Control plane: the planner API of this repo (include/roundpipe, the
+// reference's API) — optimal_partition -> slot_table_from_plan ->
+// synthesize (round-robin dispatch list, reference scheduler.hpp:120-144).
+// The controller walks Schedule.tasks in emission order; every (round, slot)
+// runs the slot's layers for M_R micro-batches on worker task.gpu, so the
+// stage->GPU assignment and execution order are the reference's by
+// construction (tests compare the measured timeline's task list with the
+// reference dispatcher's).
+//
+// Data plane, per worker, all asynchronous on CUDA streams; ONE controller
+// thread enqueues everything (the paper's single controller,
+// PAPER.md:352-361) in a topological order of the dependency graph:
+//   compute  (high priority)  stage kernels: tcgen05 GEMMs, flash attention,
+//                             fused norm/rope/swiglu, chunked LM-head + CE
+//   act      (high priority)  activation/gradient hand-off, checkpoints
+//   w_h2d    (low priority)   weight uploads from the pinned bf16 master
+//   opt_h2d / opt_comp / opt_d2h (low priority)  AdamW on streamed fp32
+//                             (master, m, v) chunks, written back to host
+// The optimizer hand-off is the reference's EventPerLayer protocol
+// (consistency.hpp:122-135), per layer l and iteration t:
+//   (1) upload(l,t)    -> p_copy(l,t)     (2) p_copy(l,t) -> upload(l,t+1)
+//   (3) GradWrite(l,t) -> g_copy(l,t)     (4) g_copy(l,t) -> GradWrite(l,t+1)
+// with one cudaEvent per (action, group). g_copy(l,t) is the AdamW pass that
+// consumes grad[t%2]; its bf16 result waits in `pend` until p_copy(l,t+1)
+// (async, staleness 1) or is copied back at once (sync).
+#include <cuda_runtime.h>
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "runtime/runtime_internal.h"
+
+namespace rp {
+namespace rt {
+
+using roundpipe::LayerRange;
+using roundpipe::StageKind;
+
+static int64_t align128(int64_t x) { return (x + 127) / 128 * 128; }
+
+LayerLayout make_layer_layout(const Shape& s) {
+  LayerLayout L;
+  int64_t off = 0;
+  auto put = [&](Tensor& t, int64_t rows, int64_t cols) {
+    t.off = off;
+    t.rows = rows;
+    t.cols = cols;
+    off = align128(off + rows * cols);
+  };
+  put(L.in_norm, s.h, 1);
+  put(L.qkv, s.qkvd(), s.h);
+  put(L.q_norm, s.hd, 1);
+  put(L.k_norm, s.hd, 1);
+  put(L.o, s.h, s.qd());
+  put(L.post_norm, s.h, 1);
+  put(L.gate_up, 2LL * s.m, s.h);
+  put(L.down, s.h, s.m);
+  L.total = off;
+  return L;
+}
+
+HeadLayout make_head_layout(const Shape& s) {
+  HeadLayout H;
+  H.final_norm = Tensor{0, s.h, 1};
+  H.lm_head = Tensor{align128(s.h), s.V, s.h};
+  H.total = align128(H.lm_head.off + (int64_t)s.V * s.h);
+  return H;
+}
+
+// ---- pinned host arena -------------------------------------------------------------
+// One anonymous mapping, first-touched and registered with CUDA in parallel
+// 1 GiB pieces (pinning 100+ GB from one thread costs about a minute).
+class HostArena {
+ public:
+  void reserve(std::size_t bytes) {
+    size_ = (bytes + (2u << 20) - 1) & ~std::size_t((2u << 20) - 1);
+    base_ = static_cast<uint8_t*>(
+        mmap(nullptr, size_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0));
+    if (base_ == MAP_FAILED) {
+      base_ = nullptr;
+      throw RtError(RP_E_INTERNAL, "mmap failed for host arena");
+    }
+    madvise(base_, size_, MADV_HUGEPAGE);
+    const std::size_t piece = std::size_t(1) << 30;
+    const std::size_t pieces = (size_ + piece - 1) / piece;
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::atomic<std::size_t> next{0};
+    std::atomic<int> err{0};
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (std::size_t i; (i = next++) < pieces;) {
+          const std::size_t off = i * piece, len = std::min(piece, size_ - off);
+          std::memset(base_ + off, 0, len);
+          if (cudaHostRegister(base_ + off, len, cudaHostRegisterPortable) != cudaSuccess)
+            err = 1;
+        }
+      });
+    for (auto& t : th) t.join();
+    registered_ = true;
+    if (err) throw RtError(RP_E_CUDA, "cudaHostRegister failed");
+  }
+  void* take(std::size_t bytes) {
+    used_ = (used_ + 255) & ~std::size_t(255);
+    if (used_ + bytes > size_) throw RtError(RP_E_INTERNAL, "host arena exhausted");
+    void* p = base_ + used_;
+    used_ += bytes;
+    return p;
+  }
+  std::size_t size() const { return size_; }
+  ~HostArena() {
+    if (!base_) return;
+    if (registered_) {
+      const std::size_t piece = std::size_t(1) << 30;
+      for (std::size_t off = 0; off < size_; off += piece) cudaHostUnregister(base_ + off);
+    }
+    munmap(base_, size_);
+  }
+
+ private:
+  uint8_t* base_ = nullptr;
+  std::size_t size_ = 0, used_ = 0;
+  bool registered_ = false;
+};
+
+// ---- the runtime --------------------------------------------------------------------
+struct Runtime {
+  rp_runtime_config_t cfg{};
+  std::string model;
+  Shape s;
+  LayerLayout LL;
+  HeadLayout HL;
+  int T = 0, M = 0, MR = 0, N = 1, R = 1, S = 1, ndev = 1;
+  std::vector<roundpipe::LayerCost> costs;
+  roundpipe::StagePlan plan;
+  std::vector<roundpipe::StageSlot> slots;
+  std::vector<int> bwd_slot_of;  // decoder layer -> slot index recomputing it
+  roundpipe::Schedule sched;
+  int horizon = 0;
+  HostArena arena;
+  std::vector<HostGroup> host;       // g = group + 1
+  std::vector<Gpu> gpus;             // logical workers
+  std::vector<int> loaded_iter;      // [worker * G + g] iteration whose weights are loaded
+  std::vector<int> grad_owner;       // g -> worker holding this iteration's grads
+  std::vector<int> pend_owner;       // g -> worker holding pending AdamW output (-1 none)
+  std::vector<cudaEvent_t> pcopy_ev; // g -> event of the latest p_copy (publication)
+  std::vector<cudaEvent_t> state_ev; // g -> event of the latest fp32 state write-back
+  std::vector<std::vector<int>> uploaders;  // g -> workers that uploaded this version
+  std::vector<char> fused_worker;    // worker ran a fused task this iteration
+  int iter = 0, last_iter = -1;
+  bool grads_pending = false;
+  float* loss_host = nullptr;        // pinned [N]
+  std::vector<cudaEvent_t> ev_loss;  // per worker, after its last fused task
+  std::vector<TaskRecord> records;
+  std::vector<cudaEvent_t> event_pool;
+  int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, kernels = 0;
+  int64_t chunk_elems = 32ll << 20;  // optimizer chunk (elements)
+  int logits_rows = 1024;            // LM-head chunk rows
+  int parities = 1;                  // hand-off / checkpoint buffer sets
+  // kernel profiling (one step at a time): per category CUDA-event pairs
+  // around each launch on its own stream, with the launch's algorithmic work
+  struct ProfRec {
+    int cat;
+    cudaEvent_t a, b;
+    double work;
+  };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_pool;
+  std::size_t prof_next = 0;
+  cudaEvent_t prof_event() {
+    if (prof_next == prof_pool.size()) prof_pool.push_back(new_event(true));
+    return prof_pool[prof_next++];
+  }
+  int prof_begin(cudaStream_t st) {
+    if (!prof_on) return -1;
+    ProfRec r{0, prof_event(), prof_event(), 0.0};
+    RP_CUDA(cudaEventRecord(r.a, st));
+    prof.push_back(r);
+    return (int)prof.size() - 1;
+  }
+  void prof_end(int idx, cudaStream_t st, int cat, double work) {
+    if (idx < 0) return;
+    prof[idx].cat = cat;
+    prof[idx].work = work;
+    RP_CUDA(cudaEventRecord(prof[idx].b, st));
+  }
+
+  int ngroups() const { return s.L + 2; }
+  int64_t group_numel(int g) const {
+    if (g == 0) return (int64_t)s.V * s.h;
+    if (g == s.L + 1) return HL.total;
+    return LL.total;
+  }
+  int worker_of(int round, int slot) const { return (int)(((int64_t)round * S + slot) % N); }
+
+  void init(const rp_runtime_config_t& c);
+  void build_plan();
+  void ensure_horizon(int it);
+  void alloc_worker(Gpu& G, int id);
+  void init_weights();
+  cudaEvent_t new_event(bool timing);
+  void set_dev(const Gpu& G) { RP_CUDA(cudaSetDevice(G.dev)); }
+  void d2d(void* dst, const Gpu& Gd, const void* src, const Gpu& Gs, std::size_t bytes,
+           cudaStream_t st);
+
+  void forward_backward(const int32_t* tokens, const int32_t* labels, float* loss);
+  void run_slot(Gpu& G, int it, int round, int slot, int first_round, float grad_scale);
+  void upload(Gpu& G, int g, int it, bool last_use);
+  void p_copy(int g);
+  void layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out);
+  void layer_bwd(Gpu& G, int l, LayerActs& A, bool first);
+  void head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale);
+  void step();
+  void adam_group(Gpu& G, int g, int parity);
+  void sync_all();
+  void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
+            bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_, int N_, int K_,
+            const void* Rz = nullptr, int64_t ldr = 0);
+  ~Runtime();
+};
+
+cudaEvent_t Runtime::new_event(bool timing) {
+  cudaEvent_t e;
+  RP_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  event_pool.push_back(e);
+  return e;
+}
+
+void Runtime::d2d(void* dst, const Gpu& Gd, const void* src, const Gpu& Gs, std::size_t bytes,
+                  cudaStream_t st) {
+  if (Gd.dev == Gs.dev) {
+    RP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  } else {  // NVLink peer copy through NVSwitch
+    RP_CUDA(cudaMemcpyPeerAsync(dst, Gd.dev, src, Gs.dev, bytes, st));
+    p2p_bytes += (int64_t)bytes;
+  }
+}
+
+void Runtime::gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B,
+                   int64_t ldb, bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_,
+                   int N_, int K_, const void* Rz, int64_t ldr) {
+  rp_gemm_args_t a{};
+  a.M = M_;
+  a.N = N_;
+  a.K = K_;
+  a.A = A;
+  a.lda = lda;
+  a.a_mn_major = a_mn;
+  a.B = B;
+  a.ldb = ldb;
+  a.b_mn_major = b_mn;
+  a.D = D;
+  a.ldd = ldd;
+  a.out_f32 = f32;
+  a.accumulate = acc;
+  a.R = Rz;
+  a.ldr = ldr;
+  const int pi = prof_begin(st);
+  RP_K(rp_gemm_bf16(&a, st));
+  prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)K_);
+  ++kernels;
+}
+
+void Runtime::init(const rp_runtime_config_t& c) {
+  cfg = c;
+  model = c.model ? c.model : "qwen3-8b";
+  cfg.model = nullptr;
+  const auto shape = roundpipe::config_io::load_shape(model);
+  s.h = (int)shape.cfg.hidden_dim;
+  s.nq = shape.cfg.num_heads;
+  s.nk = shape.cfg.num_kv_heads;
+  s.hd = shape.head_dim;
+  s.m = (int)shape.cfg.intermediate_dim;
+  s.L = shape.cfg.num_layers;
+  s.V = shape.vocab_size;
+  s.theta = shape.rope_theta;
+  s.eps = shape.rms_norm_eps;
+  if (shape.cfg.total_experts != 1)
+    throw RtError(RP_E_INPUT, "MoE models are not supported by the executor yet");
+  if (c.seq_len < 128 || c.seq_len % 128 || c.micro_batch < 1 || c.micro_batches < 1 ||
+      c.num_gpus < 1)
+    throw RtError(RP_E_INPUT, "need seq_len % 128 == 0, b >= 1, M >= 1, N >= 1");
+  if (s.h % 64 || s.m % 64 || (s.hd != 64 && s.hd != 128) || s.V % 8 || s.nq % s.nk)
+    throw RtError(RP_E_INPUT, "unsupported model dims");
+  T = c.seq_len * c.micro_batch;
+  M = c.micro_batches;
+  N = c.num_gpus;
+  RP_CUDA(cudaGetDeviceCount(&ndev));
+  if (ndev < 1) throw RtError(RP_E_CUDA, "no CUDA device");
+  ndev = std::min(ndev, N);
+  for (int a = 0; a < ndev; ++a)  // NVLink P2P for hand-offs between workers
+    for (int b = 0; b < ndev; ++b) {
+      int ok = 0;
+      if (a == b || cudaDeviceCanAccessPeer(&ok, a, b) != cudaSuccess || !ok) continue;
+      RP_CUDA(cudaSetDevice(a));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) RP_CUDA(e);
+      cudaGetLastError();
+    }
+  LL = make_layer_layout(s);
+  HL = make_head_layout(s);
+  if (!(cfg.residency_factor > 0)) cfg.residency_factor = 2.0;
+  if (cfg.adam.lr == 0.f && cfg.adam.beta1 == 0.f) {
+    cfg.adam = rp_adam_hparams_t{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f, 1.0f};
+  }
+  if (cfg.adam.grad_scale == 0.f) cfg.adam.grad_scale = 1.f;
+  build_plan();
+  MR = c.round_micro_batches ? c.round_micro_batches : M;
+  R = M / MR;
+  if (R > 1 && N > 1)
+    throw RtError(RP_E_INPUT, "multi-round iterations need N == 1 (host grad merge not built)");
+  parities = N > 1 ? 2 : 1;
+
+  std::size_t bytes = 0;
+  for (int g = 0; g < ngroups(); ++g) bytes += (std::size_t)group_numel(g) * 14 + 4 * 256;
+  arena.reserve(bytes);
+  host.resize(ngroups());
+  for (int g = 0; g < ngroups(); ++g) {
+    HostGroup& H = host[g];
+    H.n = group_numel(g);
+    H.w16 = static_cast<uint16_t*>(arena.take(H.n * 2));
+    H.master = static_cast<float*>(arena.take(H.n * 4));
+    H.m = static_cast<float*>(arena.take(H.n * 4));
+    H.v = static_cast<float*>(arena.take(H.n * 4));
+  }
+  grad_owner.assign(ngroups(), 0);
+  pend_owner.assign(ngroups(), -1);
+  pcopy_ev.assign(ngroups(), nullptr);
+  state_ev.assign(ngroups(), nullptr);
+  uploaders.assign(ngroups(), {});
+  loaded_iter.assign((std::size_t)N * ngroups(), -1);
+  RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N));
+  gpus.resize(N);
+  for (int w = 0; w < N; ++w) alloc_worker(gpus[w], w);
+  ev_loss.resize(N);
+  for (int w = 0; w < N; ++w) {
+    set_dev(gpus[w]);
+    ev_loss[w] = new_event(false);
+  }
+  if (!(cfg.flags & RP_RT_SKIP_INIT)) init_weights();
+  sync_all();
+}
+
+void Runtime::build_plan() {
+  if (cfg.costs && cfg.n_costs > 0) {
+    if (cfg.n_costs != s.L + 1) throw RtError(RP_E_INPUT, "cost table must have L+1 rows");
+    for (int i = 0; i < cfg.n_costs; ++i) {
+      roundpipe::LayerCost lc;
+      lc.t_fwd_ns = cfg.costs[i].t_fwd_ns;
+      lc.t_bwd_ns = cfg.costs[i].t_bwd_ns;
+      lc.param_bytes = cfg.costs[i].param_bytes;
+      lc.act_ckpt_bytes = cfg.costs[i].act_ckpt_bytes;
+      lc.act_full_bytes = cfg.costs[i].act_full_bytes;
+      costs.push_back(lc);
+    }
+    cfg.costs = nullptr;
+  } else {
+    const auto mc = roundpipe::config_io::load_model(model);
+    const auto gpu = roundpipe::config_io::load_gpu("b200");
+    costs = roundpipe::cost_model::layer_costs(
+        mc, roundpipe::Workload{cfg.seq_len, cfg.micro_batch}, gpu, true);
+  }
+  roundpipe::PartitionProblem p;
+  p.costs = costs;
+  p.num_gpus = cfg.num_gpus;
+  p.micro_batches = cfg.micro_batches;
+  p.residency_factor = cfg.residency_factor;
+  if (cfg.mem_limit_bytes > 0) {
+    p.mem_limit_bytes = cfg.mem_limit_bytes;
+  } else {
+    cudaDeviceProp prop;
+    RP_CUDA(cudaGetDeviceProperties(&prop, 0));
+    p.mem_limit_bytes = (int64_t)(0.9 * (double)prop.totalGlobalMem);
+  }
+  plan = roundpipe::partitioner::optimal_partition(p);
+  slots = roundpipe::scheduler::slot_table_from_plan(plan, costs);
+  S = (int)slots.size();
+  bwd_slot_of.assign(s.L, -1);
+  for (const auto& sl : slots)
+    if (sl.kind == StageKind::Backward)
+      for (int l = sl.layers.first; l <= sl.layers.last; ++l) bwd_slot_of[l] = sl.index;
+  ensure_horizon(8);
+}
+
+void Runtime::ensure_horizon(int it) {
+  if (it < horizon) return;
+  int h = std::max(8, horizon);
+  while (h <= it) h *= 2;
+  roundpipe::ScheduleSpec spec;
+  spec.kind = cfg.async_optimizer ? roundpipe::ScheduleKind::RoundPipe
+                                  : roundpipe::ScheduleKind::RoundPipeSync;
+  spec.num_gpus = cfg.num_gpus;
+  spec.micro_batches = cfg.micro_batches;
+  spec.round_micro_batches = cfg.round_micro_batches ? cfg.round_micro_batches : cfg.micro_batches;
+  spec.iterations = h;
+  for (const auto& sl : slots) spec.slot_durs.push_back(sl.dur_ns);
+  sched = roundpipe::scheduler::synthesize(spec);
+  if (auto err = roundpipe::scheduler::validate(sched))
+    throw RtError(RP_E_INTERNAL, "dispatch list invalid: " + *err);
+  horizon = h;
+}
+
+void Runtime::alloc_worker(Gpu& G, int id) {
+  G.id = id;
+  G.dev = id % ndev;
+  set_dev(G);
+  int lo = 0, hi = 0;
+  RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // lo = least, hi = greatest
+  auto mk = [&](cudaStream_t* st, int prio) {
+    RP_CUDA(cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, prio));
+  };
+  mk(&G.compute, hi);
+  mk(&G.act, hi);
+  mk(&G.w_h2d, lo);
+  mk(&G.opt_h2d, lo);
+  mk(&G.opt_d2h, lo);
+  mk(&G.opt_comp, lo);
+  G.allocated.assign(8, 0);
+  auto dalloc = [&](std::size_t bytes, int cat) -> void* {
+    void* p = nullptr;
+    RP_CUDA(cudaMalloc(&p, std::max<std::size_t>(bytes, 256)));
+    G.allocated[cat] += bytes;
+    return p;
+  };
+  const int64_t Th = (int64_t)T * s.h;
+  G.groups.resize(ngroups());
+  for (int g = 0; g < ngroups(); ++g) {
+    DevGroup& D = G.groups[g];
+    const int64_t n = group_numel(g);
+    D.w = static_cast<uint16_t*>(dalloc(n * 2, 0));
+    D.grad[0] = static_cast<float*>(dalloc(n * 4, 1));
+    D.grad[1] = static_cast<float*>(dalloc(n * 4, 1));
+    D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
+    D.ev_upload = new_event(false);
+    D.ev_lastuse = new_event(false);
+    D.ev_gradwrite = new_event(false);
+    D.ev_adam[0] = new_event(false);
+    D.ev_adam[1] = new_event(false);
+    D.ev_pcopy = new_event(false);
+  }
+  const int nsets = std::max(1, s.L - plan.fused_stage.first);
+  G.acts.resize(nsets);
+  for (auto& A : G.acts) {
+    A.x = static_cast<uint16_t*>(dalloc(Th * 2, 3));
+    A.h1 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
+    A.qkv = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 3));
+    A.q = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 3));
+    A.k = static_cast<uint16_t*>(dalloc((int64_t)T * s.kd() * 2, 3));
+    A.o = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 3));
+    A.x2 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
+    A.h2 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
+    A.gu = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 3));
+    A.act = static_cast<uint16_t*>(dalloc((int64_t)T * s.m * 2, 3));
+    A.rstd1 = static_cast<float*>(dalloc((std::size_t)T * 4, 3));
+    A.rstd2 = static_cast<float*>(dalloc((std::size_t)T * 4, 3));
+    A.rstd_q = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
+    A.rstd_k = static_cast<float*>(dalloc((int64_t)T * s.nk * 4, 3));
+    A.lse = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
+  }
+  G.dx32[0] = static_cast<float*>(dalloc(Th * 4, 4));
+  G.dx32[1] = static_cast<float*>(dalloc(Th * 4, 4));
+  G.dx16 = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  G.dh = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  G.dact = static_cast<uint16_t*>(dalloc((int64_t)T * s.m * 2, 4));
+  G.dgu = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
+  G.dattn = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 4));
+  G.dqkv = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 4));
+  G.dq_t = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 4));
+  G.dk_t = static_cast<uint16_t*>(dalloc((int64_t)T * s.kd() * 2, 4));
+  G.dq_acc = static_cast<float*>(dalloc((int64_t)T * s.qd() * 4, 4));
+  G.delta = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 4));
+  G.xbuf[0] = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  G.xbuf[1] = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  G.hN = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  G.rstdN = static_cast<float*>(dalloc((std::size_t)T * 4, 4));
+  G.logits = static_cast<uint16_t*>(dalloc((int64_t)std::min(T, logits_rows) * s.V * 2, 4));
+  G.loss_dev = static_cast<float*>(dalloc(64, 4));
+  G.tokens_dev = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
+  G.labels_dev = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
+  G.ev_tokens = new_event(false);
+  {  // RoPE (cos, sin) table: float64 on the host, rounded (as the oracle)
+    const int half = s.hd / 2;
+    std::vector<float> tab((std::size_t)cfg.seq_len * half * 2);
+    for (int p = 0; p < cfg.seq_len; ++p)
+      for (int j = 0; j < half; ++j) {
+        const double inv = 1.0 / std::pow(s.theta, (2.0 * j) / s.hd);
+        tab[((std::size_t)p * half + j) * 2] = (float)std::cos(p * inv);
+        tab[((std::size_t)p * half + j) * 2 + 1] = (float)std::sin(p * inv);
+      }
+    G.cos_sin = static_cast<float*>(dalloc(tab.size() * 4, 4));
+    RP_CUDA(cudaMemcpy(G.cos_sin, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  }
+  if (S > 1) {  // hand-off and checkpoint buffers
+    auto mkbuf = [&](std::size_t bytes, int cat) {
+      Slotbuf b;
+      b.p = dalloc(bytes, cat);
+      b.ready = new_event(false);
+      b.read = new_event(false);
+      return b;
+    };
+    for (int p = 0; p < parities; ++p)
+      for (int mb = 0; mb < MR; ++mb) {
+        G.hand_act.push_back(mkbuf(Th * 2, 5));
+        G.hand_grad.push_back(mkbuf(Th * 4, 5));
+      }
+    G.ckpt.resize((std::size_t)parities * s.L * MR);
+    for (int p = 0; p < parities; ++p)
+      for (int l = 0; l < plan.fused_stage.first && l < s.L; ++l)
+        for (int mb = 0; mb < MR; ++mb)
+          G.ckpt[((std::size_t)p * s.L + l) * MR + mb] = mkbuf(Th * 2, 5);
+  }
+  for (int b = 0; b < 2; ++b)
+    for (int j = 0; j < 3; ++j)
+      G.opt_buf[b][j] = static_cast<float*>(dalloc((std::size_t)chunk_elems * 4, 6));
+  G.opt_free[0] = new_event(false);
+  G.opt_free[1] = new_event(false);
+  G.anchor = new_event(true);
+  RP_CUDA(cudaEventRecord(G.anchor, G.compute));
+}
+
+// ---- weight init (bench path; tests load weights through rp_set_params) ----------
+void Runtime::init_weights() {
+  Gpu& G = gpus[0];
+  set_dev(G);
+  const float std_ = cfg.init_std > 0 ? cfg.init_std : 0.02f;
+  for (int g = 0; g < ngroups(); ++g) {
+    HostGroup& H = host[g];
+    DevGroup& D = G.groups[g];
+    float* f32 = D.grad[0];  // scratch
+    RP_K(rp_init_normal(f32, D.w, H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_, G.compute));
+    std::vector<std::pair<int64_t, int64_t>> ones;
+    if (g >= 1 && g <= s.L)
+      ones = {{LL.in_norm.off, s.h}, {LL.q_norm.off, s.hd}, {LL.k_norm.off, s.hd},
+              {LL.post_norm.off, s.h}};
+    else if (g == s.L + 1)
+      ones = {{HL.final_norm.off, s.h}};
+    for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, D.w + off, n, 1.0f, G.compute));
+    RP_CUDA(cudaMemcpyAsync(H.master, f32, H.n * 4, cudaMemcpyDeviceToHost, G.compute));
+    RP_CUDA(cudaMemcpyAsync(H.w16, D.w, H.n * 2, cudaMemcpyDeviceToHost, G.compute));
+    RP_CUDA(cudaStreamSynchronize(G.compute));
+  }
+}
+
+// ---- GPU lane: weight upload ----------------------------------------------------------
+// upload(l, t): bf16 master (pinned host) -> worker weights, on the
+// low-priority H2D stream, after p_copy(l, t-1) (edge 2) and after the last
+// compute read of the previous version (WAR). A worker that already holds
+// this iteration's version skips the copy. After the LAST upload of the
+// group in the iteration, the pending AdamW result may be published
+// (p_copy, edge 1) — async mode only.
+void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
+  DevGroup& D = G.groups[g];
+  HostGroup& H = host[g];
+  int& have = loaded_iter[(std::size_t)G.id * ngroups() + g];
+  if (have != it) {
+    if (pcopy_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.w_h2d, pcopy_ev[g], 0));  // edge (2)
+    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse, 0));
+    RP_CUDA(cudaMemcpyAsync(D.w, H.w16, H.n * 2, cudaMemcpyHostToDevice, G.w_h2d));
+    h2d_bytes += H.n * 2;
+    RP_CUDA(cudaEventRecord(D.ev_upload, G.w_h2d));
+    have = it;
+    uploaders[g].push_back(G.id);
+  }
+  if (last_use && cfg.async_optimizer && pend_owner[g] >= 0) p_copy(g);
+  set_dev(G);
+}
+
+// p_copy: pending AdamW result (device) -> bf16 master (pinned host), after
+// every upload of the current version (edge 1).
+void Runtime::p_copy(int g) {
+  Gpu& O = gpus[pend_owner[g]];
+  set_dev(O);
+  DevGroup& D = O.groups[g];
+  HostGroup& H = host[g];
+  for (int w : uploaders[g])
+    RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, gpus[w].groups[g].ev_upload, 0));
+  uploaders[g].clear();
+  RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[0], 0));
+  RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[1], 0));
+  RP_CUDA(cudaMemcpyAsync(H.w16, D.pend, H.n * 2, cudaMemcpyDeviceToHost, O.opt_d2h));
+  d2h_bytes += H.n * 2;
+  RP_CUDA(cudaEventRecord(D.ev_pcopy, O.opt_d2h));
+  pcopy_ev[g] = D.ev_pcopy;
+  pend_owner[g] = -1;
+}
+
+// ---- decoder layer -------------------------------------------------------------------
+void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out) {
+  const uint16_t* W = G.groups[l + 1].w;
+  cudaStream_t st = G.compute;
+  const int h = s.h, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
+  A.xin = x;
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_rmsnorm_fwd(x, h, W + LL.in_norm.off, A.h1, h, A.rstd1, T, h, (float)s.eps, st));
+    prof_end(pi_, st, 2, 4.0 * T * h);
+  }
+  gemm(st, A.h1, h, false, W + LL.qkv.off, h, false, A.qkv, qkvd, false, false, T, qkvd, h);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_qk_norm_rope_fwd(A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off, W + LL.k_norm.off,
+                           G.cos_sin, cfg.seq_len, A.q, A.k, A.rstd_q, A.rstd_k, T, (float)s.eps,
+                           st));
+    prof_end(pi_, st, 2, 4.0 * T * (s.nq + s.nk) * s.hd);
+  }
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_attn_fwd(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, A.lse, T, cfg.seq_len, s.nq,
+                   s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
+    prof_end(pi_, st, 1, 2.0 * s.nq * s.hd * (double)T * cfg.seq_len);
+  }
+  gemm(st, A.o, qd, false, W + LL.o.off, qd, false, A.x2, h, false, false, T, h, qd, x, h);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
+    prof_end(pi_, st, 2, 4.0 * T * h);
+  }
+  gemm(st, A.h2, h, false, W + LL.gate_up.off, h, false, A.gu, 2 * s.m, false, false, T, 2 * s.m,
+       h);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_swiglu_fwd(A.gu, A.act, T, s.m, st));
+    prof_end(pi_, st, 2, 6.0 * T * s.m);
+  }
+  gemm(st, A.act, s.m, false, W + LL.down.off, s.m, false, x_out, h, false, false, T, h, s.m,
+       A.x2, h);
+  kernels += 5;
+}
+
+// Backward of decoder layer l. In: G.dx32[0] (fp32) / G.dx16 (bf16) =
+// dL/d(layer output). Out: the same buffers = dL/d(layer input). Weight grads
+// go to grad[t%2]: the first micro-batch overwrites, later ones accumulate.
+void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
+  DevGroup& D = G.groups[l + 1];
+  const uint16_t* W = D.w;
+  float* dW = D.grad[last_iter & 1];
+  cudaStream_t st = G.compute;
+  const int h = s.h, m = s.m, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
+  if (first)
+    for (const Tensor* t : {&LL.in_norm, &LL.q_norm, &LL.k_norm, &LL.post_norm})
+      RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
+  // MLP:  x3 = x2 + act(gu(h2)) Wd^T
+  gemm(st, G.dx16, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
+  gemm(st, G.dx16, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_swiglu_bwd(G.dact, A.gu, G.dgu, T, m, st));
+    prof_end(pi_, st, 2, 10.0 * T * m);
+  }
+  gemm(st, G.dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
+  gemm(st, G.dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_rmsnorm_bwd(G.dh, A.x2, W + LL.post_norm.off, A.rstd2, G.dx32[0], G.dx32[1], G.dx16,
+                      dW + LL.post_norm.off, T, h, st));
+    prof_end(pi_, st, 2, 14.0 * T * h);
+  }
+  // attention:  x2 = x + attn(qkv(h1)) Wo^T
+  gemm(st, G.dx16, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
+  gemm(st, G.dx16, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_attn_bwd(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, G.dattn, qd, A.lse, G.dq_t,
+                   qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.dq_acc, G.delta, T, cfg.seq_len,
+                   s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
+    prof_end(pi_, st, 1, 5.0 * s.nq * s.hd * (double)T * cfg.seq_len);
+  }
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_qk_norm_rope_bwd(G.dq_t, G.dk_t, A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off,
+                           W + LL.k_norm.off, A.rstd_q, A.rstd_k, G.cos_sin, cfg.seq_len, G.dqkv,
+                           qkvd, dW + LL.q_norm.off, dW + LL.k_norm.off, T, st));
+    prof_end(pi_, st, 2, 8.0 * T * (s.nq + s.nk) * s.hd);
+  }
+  gemm(st, G.dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
+  gemm(st, G.dqkv, qkvd, true, A.h1, h, true, dW + LL.qkv.off, h, true, !first, qkvd, h, T);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_rmsnorm_bwd(G.dh, A.xin, W + LL.in_norm.off, A.rstd1, G.dx32[1], G.dx32[0], G.dx16,
+                      dW + LL.in_norm.off, T, h, st));
+    prof_end(pi_, st, 2, 14.0 * T * h);
+  }
+  kernels += 8;
+}
+
+// Head pseudo-layer: final RMSNorm + LM head + CE forward and backward,
+// chunked over token rows: only a [rows, V] logits chunk ever exists, and the
+// CE kernel overwrites it in place with dlogits.
+void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale) {
+  DevGroup& D = G.groups[s.L + 1];
+  const uint16_t* W = D.w;
+  float* dW = D.grad[last_iter & 1];
+  cudaStream_t st = G.compute;
+  const int h = s.h, V = s.V;
+  if (first) RP_CUDA(cudaMemsetAsync(dW + HL.final_norm.off, 0, (size_t)h * 4, st));
+  RP_K(rp_rmsnorm_fwd(x, h, W + HL.final_norm.off, G.hN, h, G.rstdN, T, h, (float)s.eps, st));
+  const int rows = std::min(T, logits_rows);
+  for (int r0 = 0; r0 < T; r0 += rows) {
+    const int nr = std::min(rows, T - r0);
+    gemm(st, G.hN + (int64_t)r0 * h, h, false, W + HL.lm_head.off, h, false, G.logits, V, false,
+         false, nr, V, h);
+    {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_ce_fwd_bwd(G.logits, V, G.labels_dev + (int64_t)gmb * T + r0, nr, V, grad_scale,
+                       G.loss_dev, nullptr, st));
+    prof_end(pi_, st, 2, 6.0 * nr * (double)V);
+  }
+    gemm(st, G.logits, V, false, W + HL.lm_head.off, h, true, G.dh + (int64_t)r0 * h, h, false,
+         false, nr, h, V);
+    gemm(st, G.logits, V, true, G.hN + (int64_t)r0 * h, h, true, dW + HL.lm_head.off, h, true,
+         !(first && r0 == 0), V, h, nr);
+    kernels += 1;
+  }
+  RP_K(rp_rmsnorm_bwd(G.dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.dx32[0], G.dx16,
+                      dW + HL.final_norm.off, T, h, st));
+  kernels += 2;
+}
+
+// ---- one (round, slot) on one worker ----------------------------------------------------
+void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, float grad_scale) {
+  const roundpipe::StageSlot& ss = slots[slot];
+  const int a = ss.layers.first, b = ss.layers.last;
+  const int rin = round - first_round;
+  const int par = round % parities;
+  const bool has_grads = ss.kind != StageKind::Forward;
+  cudaStream_t st = G.compute;
+  Gpu* next = slot + 1 < S ? &gpus[worker_of(round, slot + 1)] : nullptr;
+
+  // ---- uploads, in the order compute needs the layers
+  auto needs_embed = ss.kind != StageKind::Backward && a == 0;
+  std::vector<int> gs;  // groups used by this slot
+  if (needs_embed) gs.push_back(0);
+  if (ss.kind == StageKind::Backward)
+    for (int l = b; l >= a; --l) gs.push_back(l + 1);
+  else
+    for (int l = a; l <= b; ++l) gs.push_back(l + 1);
+  for (int g : gs) {
+    const bool last_use = rin == R - 1 && (g == 0 ? ss.kind != StageKind::Backward
+                                                  : ss.kind != StageKind::Forward);
+    upload(G, g, it, last_use);
+  }
+  auto wait_group = [&](int g) { RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_upload, 0)); };
+  // groups whose grads this slot produces
+  std::vector<int> grad_groups;
+  if (has_grads) {
+    for (int l = a; l <= std::min(b, s.L - 1); ++l) grad_groups.push_back(l + 1);
+    if (b == s.L) grad_groups.push_back(s.L + 1);
+    if (a == 0) grad_groups.push_back(0);
+    // grad[t%2] may be overwritten once AdamW consumed it (edge 4, parity form)
+    for (int g : grad_groups) RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_adam[it & 1], 0));
+  }
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_tokens, 0));
+  const bool want_tl = cfg.flags & RP_RT_RECORD_TIMELINE;
+  const std::size_t Th2 = (std::size_t)T * s.h * 2, Th4 = (std::size_t)T * s.h * 4;
+
+  for (int mb = 0; mb < MR; ++mb) {
+    const int gmb = rin * MR + mb;
+    const bool first = rin == 0 && mb == 0;
+    const int hb = par * MR + mb;  // hand-off buffer index
+    TaskRecord rec{};
+    if (want_tl) {
+      rec.task = roundpipe::Task{it, round, slot, mb, G.id, ss.dur_ns};
+      rec.worker = G.id;
+      rec.start = new_event(true);
+      rec.end = new_event(true);
+      RP_CUDA(cudaEventRecord(rec.start, st));
+    }
+    const int32_t* ids = G.tokens_dev + (int64_t)gmb * T;
+    // input activation of the slot (fwd / fused)
+    const uint16_t* x_in = nullptr;
+    Slotbuf* in_buf = nullptr;
+    if (ss.kind != StageKind::Backward) {
+      if (a == 0) {
+        wait_group(0);
+        uint16_t* dst = ss.kind == StageKind::Fused && a < s.L ? G.acts[0].x : G.xbuf[0];
+        RP_K(rp_embed_fwd(ids, G.groups[0].w, dst, T, s.h, st));
+        ++kernels;
+        x_in = dst;
+      } else {
+        in_buf = &G.hand_act[hb];
+        RP_CUDA(cudaStreamWaitEvent(st, in_buf->ready, 0));
+        x_in = static_cast<const uint16_t*>(in_buf->p);
+      }
+    }
+    if (ss.kind == StageKind::Forward) {
+      const uint16_t* x = x_in;
+      for (int l = a; l <= b; ++l) {
+        // checkpoint x_l for the backward slot that recomputes layer l
+        Gpu& O = gpus[worker_of(round, bwd_slot_of[l])];
+        Slotbuf& ck = O.ckpt[((std::size_t)par * s.L + l) * MR + mb];
+        cudaEvent_t xr = new_event(false);
+        RP_CUDA(cudaEventRecord(xr, st));
+        RP_CUDA(cudaStreamWaitEvent(G.act, xr, 0));
+        RP_CUDA(cudaStreamWaitEvent(G.act, ck.read, 0));
+        d2d(ck.p, O, x, G, Th2, G.act);
+        RP_CUDA(cudaEventRecord(ck.ready, G.act));
+        wait_group(l + 1);
+        uint16_t* out = x == G.xbuf[0] ? G.xbuf[1] : G.xbuf[0];
+        RP_CUDA(cudaStreamWaitEvent(st, ck.ready, 0));  // x_l is overwritten next layer
+        layer_fwd(G, l, x, G.acts[0], out);
+        x = out;
+      }
+      if (in_buf) RP_CUDA(cudaEventRecord(in_buf->read, st));
+      // hand x_{b+1} to the next slot
+      Slotbuf& nb = next->hand_act[hb];
+      cudaEvent_t xr = new_event(false);
+      RP_CUDA(cudaEventRecord(xr, st));
+      RP_CUDA(cudaStreamWaitEvent(G.act, xr, 0));
+      RP_CUDA(cudaStreamWaitEvent(G.act, nb.read, 0));
+      d2d(nb.p, *next, x, G, Th2, G.act);
+      RP_CUDA(cudaEventRecord(nb.ready, G.act));
+      RP_CUDA(cudaStreamWaitEvent(st, nb.ready, 0));  // xbuf reuse
+    } else if (ss.kind == StageKind::Fused) {
+      const int nl = s.L - a;  // decoder layers inside the fused stage
+      const uint16_t* x = x_in;
+      for (int i = 0; i < nl; ++i) {
+        const int l = a + i;
+        wait_group(l + 1);
+        uint16_t* out = (i + 1 < nl) ? G.acts[i + 1].x : G.xbuf[1];
+        layer_fwd(G, l, x, G.acts[i], out);
+        x = out;
+      }
+      wait_group(s.L + 1);
+      head_fwd_bwd(G, x, gmb, first, grad_scale);
+      for (int i = nl - 1; i >= 0; --i) layer_bwd(G, a + i, G.acts[i], first);
+      if (in_buf) RP_CUDA(cudaEventRecord(in_buf->read, st));
+    } else {  // Backward: incoming dL/dx_{b+1} from the previous slot
+      Slotbuf& gi = G.hand_grad[hb];
+      RP_CUDA(cudaStreamWaitEvent(st, gi.ready, 0));
+      RP_CUDA(cudaMemcpyAsync(G.dx32[0], gi.p, Th4, cudaMemcpyDeviceToDevice, st));
+      RP_K(rp_f32_to_bf16(G.dx32[0], G.dx16, (int64_t)T * s.h, st));
+      ++kernels;
+      RP_CUDA(cudaEventRecord(gi.read, st));
+      for (int l = b; l >= a; --l) {
+        Slotbuf& ck = G.ckpt[((std::size_t)par * s.L + l) * MR + mb];
+        RP_CUDA(cudaStreamWaitEvent(st, ck.ready, 0));
+        wait_group(l + 1);
+        LayerActs& A = G.acts[0];
+        layer_fwd(G, l, static_cast<const uint16_t*>(ck.p), A, G.xbuf[1]);  // recompute
+        layer_bwd(G, l, A, first);
+        RP_CUDA(cudaEventRecord(ck.read, st));
+      }
+    }
+    if (has_grads) {
+      if (a == 0) {  // embedding gradient (scatter-add of dL/dx_0)
+        float* dE = G.groups[0].grad[it & 1];
+        if (first) RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+        RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
+        ++kernels;
+      } else {  // hand dL/dx_a to the next (backward) slot
+        Slotbuf& nb = next->hand_grad[hb];
+        cudaEvent_t gr = new_event(false);
+        RP_CUDA(cudaEventRecord(gr, st));
+        RP_CUDA(cudaStreamWaitEvent(G.act, gr, 0));
+        RP_CUDA(cudaStreamWaitEvent(G.act, nb.read, 0));
+        d2d(nb.p, *next, G.dx32[0], G, Th4, G.act);
+        RP_CUDA(cudaEventRecord(nb.ready, G.act));
+        RP_CUDA(cudaStreamWaitEvent(st, nb.ready, 0));  // dx32 reuse
+      }
+    }
+    if (want_tl) {
+      RP_CUDA(cudaEventRecord(rec.end, st));
+      records.push_back(rec);
+    }
+  }
+  // last compute read of the slot's weights; grads complete (GradWrite)
+  for (int g : gs) RP_CUDA(cudaEventRecord(G.groups[g].ev_lastuse, st));
+  if (has_grads && rin == R - 1)
+    for (int g : grad_groups) {
+      RP_CUDA(cudaEventRecord(G.groups[g].ev_gradwrite, st));
+      grad_owner[g] = G.id;
+    }
+  if (ss.kind == StageKind::Fused) {
+    RP_CUDA(cudaEventRecord(ev_loss[G.id], st));
+    fused_worker[G.id] = 1;
+  }
+}
+
+void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, float* loss) {
+  const int it = iter++;
+  last_iter = it;
+  ensure_horizon(it);
+  int64_t n_valid = 0;
+  for (int64_t i = 0; i < (int64_t)M * T; ++i) n_valid += labels[i] >= 0;
+  const float grad_scale = n_valid > 0 ? 1.0f / (float)n_valid : 0.f;
+  fused_worker.assign(N, 0);
+  for (Gpu& G : gpus) {
+    set_dev(G);
+    RP_CUDA(cudaMemcpyAsync(G.tokens_dev, tokens, (size_t)M * T * 4, cudaMemcpyHostToDevice,
+                            G.act));
+    RP_CUDA(cudaMemcpyAsync(G.labels_dev, labels, (size_t)M * T * 4, cudaMemcpyHostToDevice,
+                            G.act));
+    RP_CUDA(cudaMemsetAsync(G.loss_dev, 0, 4, G.act));
+    RP_CUDA(cudaEventRecord(G.ev_tokens, G.act));
+    h2d_bytes += (int64_t)M * T * 8;
+  }
+  // walk the dispatch list of this iteration in emission order
+  int first_round = -1;
+  for (std::size_t i = 0; i < sched.tasks.size();) {
+    const roundpipe::Task& t = sched.tasks[i];
+    if (t.iteration < it) {
+      ++i;
+      continue;
+    }
+    if (t.iteration > it) break;
+    if (first_round < 0) first_round = t.round;
+    Gpu& G = gpus[t.gpu];
+    set_dev(G);
+    run_slot(G, it, t.round, t.slot, first_round, grad_scale);
+    i += MR;  // a (round, slot) is MR consecutive tasks on one worker
+  }
+  // early return: the loss is known once the fused slots are done
+  double total = 0.0;
+  for (Gpu& G : gpus) {
+    if (!fused_worker[G.id]) continue;
+    set_dev(G);
+    RP_CUDA(cudaStreamWaitEvent(G.act, ev_loss[G.id], 0));
+    RP_CUDA(cudaMemcpyAsync(loss_host + G.id, G.loss_dev, 4, cudaMemcpyDeviceToHost, G.act));
+    RP_CUDA(cudaStreamSynchronize(G.act));
+    total += loss_host[G.id];
+  }
+  if (loss) *loss = (float)(total * grad_scale);
+  grads_pending = true;
+}
+
+// ---- optimizer lane -------------------------------------------------------------------
+// AdamW for one parameter group over fp32 state chunks streamed from pinned
+// host memory: H2D (opt_h2d) -> kernel (opt_comp) -> D2H (opt_d2h), two chunk
+// slots in flight. Consumes grad[parity] (g_copy) and leaves the new bf16
+// weights in `pend` for p_copy.
+void Runtime::adam_group(Gpu& G, int g, int parity) {
+  DevGroup& D = G.groups[g];
+  HostGroup& H = host[g];
+  const int step_no = ++H.step;
+  RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_gradwrite, 0));  // edge (3)
+  RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_pcopy, 0));      // pend free again
+  if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
+  for (int64_t off = 0; off < H.n; off += chunk_elems) {
+    const int64_t n = std::min<int64_t>(chunk_elems, H.n - off);
+    const int sl = G.opt_slot;
+    G.opt_slot ^= 1;
+    float** buf = G.opt_buf[sl];
+    RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, G.opt_free[sl], 0));
+    RP_CUDA(cudaMemcpyAsync(buf[0], H.master + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
+    RP_CUDA(cudaMemcpyAsync(buf[1], H.m + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
+    RP_CUDA(cudaMemcpyAsync(buf[2], H.v + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
+    h2d_bytes += n * 12;
+    cudaEvent_t ev_in = new_event(false);
+    RP_CUDA(cudaEventRecord(ev_in, G.opt_h2d));
+    RP_CUDA(cudaStreamWaitEvent(G.opt_comp, ev_in, 0));
+    const int pi_ = prof_begin(G.opt_comp);
+    RP_K(rp_adamw(buf[0], buf[1], buf[2], D.grad[parity] + off, D.pend + off, n, &cfg.adam,
+                  step_no, G.opt_comp));
+    prof_end(pi_, G.opt_comp, 3, 30.0 * n);
+    ++kernels;
+    cudaEvent_t ev_out = new_event(false);
+    RP_CUDA(cudaEventRecord(ev_out, G.opt_comp));
+    RP_CUDA(cudaStreamWaitEvent(G.opt_d2h, ev_out, 0));
+    RP_CUDA(cudaMemcpyAsync(H.master + off, buf[0], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
+    RP_CUDA(cudaMemcpyAsync(H.m + off, buf[1], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
+    RP_CUDA(cudaMemcpyAsync(H.v + off, buf[2], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
+    d2h_bytes += n * 12;
+    RP_CUDA(cudaEventRecord(G.opt_free[sl], G.opt_d2h));
+  }
+  RP_CUDA(cudaEventRecord(D.ev_adam[parity], G.opt_comp));  // g_copy(l, t) complete
+  if (!D.ev_state) D.ev_state = new_event(false);
+  RP_CUDA(cudaEventRecord(D.ev_state, G.opt_d2h));
+  state_ev[g] = D.ev_state;
+  pend_owner[g] = G.id;
+  if (!cfg.async_optimizer) p_copy(g);  // sync: iteration t+1 sees grads of t
+}
+
+void Runtime::step() {
+  if (!grads_pending) return;
+  grads_pending = false;
+  const int parity = last_iter & 1;
+  // optimizer lane order = GradWrite order: head first, then layers L-1..0
+  for (int l = s.L; l >= 0; --l) {
+    std::vector<int> gs = l == 0 ? std::vector<int>{1, 0} : std::vector<int>{l + 1};
+    for (int g : gs) {
+      Gpu& G = gpus[grad_owner[g]];
+      set_dev(G);
+      adam_group(G, g, parity);
+    }
+  }
+  if (event_pool.size() > 500000) sync_all();
+}
+
+void Runtime::sync_all() {
+  for (Gpu& G : gpus) {
+    set_dev(G);
+    RP_CUDA(cudaDeviceSynchronize());
+  }
+}
+
+Runtime::~Runtime() {
+  for (Gpu& G : gpus) {
+    cudaSetDevice(G.dev);
+    cudaDeviceSynchronize();
+  }
+  for (auto e : event_pool) cudaEventDestroy(e);
+  for (Gpu& G : gpus) {
+    cudaSetDevice(G.dev);
+    for (cudaStream_t st : {G.compute, G.act, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp})
+      if (st) cudaStreamDestroy(st);
+  }
+  if (loss_host) cudaFreeHost(loss_host);
+}
+
+}  // namespace rt
+}  // namespace rp
+
+// ======================================================================== C-ABI
+namespace {
+using rp::rt::RtError;
+using rp::rt::Runtime;
+thread_local std::string g_rt_error;
+
+template <class F>
+int rt_guard(F&& f) {
+  try {
+    g_rt_error.clear();
+    f();
+    return RP_OK;
+  } catch (const RtError& e) {
+    g_rt_error = e.what();
+    return e.code;
+  } catch (const roundpipe::InfeasibleError& e) {
+    g_rt_error = e.what();
+    return RP_E_INFEASIBLE;
+  } catch (const roundpipe::ConfigError& e) {
+    g_rt_error = e.what();
+    return RP_E_INPUT;
+  } catch (const std::invalid_argument& e) {
+    g_rt_error = e.what();
+    return RP_E_INPUT;
+  } catch (const std::exception& e) {
+    g_rt_error = e.what();
+    return RP_E_INTERNAL;
+  }
+}
+
+uint16_t f32_to_bf16_host(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+float bf16_to_f32_host(uint16_t b) {
+  const uint32_t u = (uint32_t)b << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+Runtime* R(rp_runtime_t* p) { return reinterpret_cast<Runtime*>(p); }
+int gidx(Runtime* rt, int32_t group) {
+  if (group < -1 || group > rt->s.L) throw RtError(RP_E_INPUT, "parameter group out of range");
+  return group + 1;
+}
+}  // namespace
+
+#define RP_API extern "C" __attribute__((visibility("default")))
+
+RP_API const char* rp_runtime_last_error(void) { return g_rt_error.c_str(); }
+
+RP_API int rp_runtime_create(const rp_runtime_config_t* cfg, rp_runtime_t** out) {
+  return rt_guard([&] {
+    if (!cfg || !out) throw RtError(RP_E_INPUT, "null argument");
+    auto rt = std::make_unique<Runtime>();
+    rt->init(*cfg);
+    *out = reinterpret_cast<rp_runtime_t*>(rt.release());
+  });
+}
+
+RP_API int rp_runtime_destroy(rp_runtime_t* rt) {
+  return rt_guard([&] { delete R(rt); });
+}
+
+RP_API int rp_runtime_plan(rp_runtime_t* p, rp_stage_plan_t* plan, int64_t* slot_durs,
+                           int32_t cap, int32_t* n_slots) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    const auto& pl = rt->plan;
+    if (plan) {
+      plan->num_fwd = (int32_t)pl.fwd_stages.size();
+      plan->num_bwd = (int32_t)pl.bwd_stages.size();
+      plan->fused = rp_layer_range_t{pl.fused_stage.first, pl.fused_stage.last};
+      plan->t_max_ns = pl.t_max_ns;
+      plan->objective = pl.objective;
+      if (plan->num_fwd > plan->cap || plan->num_bwd > plan->cap)
+        throw RtError(RP_E_TOOSMALL, "plan capacity");
+      for (int i = 0; i < plan->num_fwd; ++i)
+        plan->fwd[i] = rp_layer_range_t{pl.fwd_stages[i].first, pl.fwd_stages[i].last};
+      for (int i = 0; i < plan->num_bwd; ++i)
+        plan->bwd[i] = rp_layer_range_t{pl.bwd_stages[i].first, pl.bwd_stages[i].last};
+    }
+    if (n_slots) *n_slots = (int32_t)rt->slots.size();
+    if (slot_durs) {
+      if ((int32_t)rt->slots.size() > cap) throw RtError(RP_E_TOOSMALL, "slot capacity");
+      for (std::size_t i = 0; i < rt->slots.size(); ++i) slot_durs[i] = rt->slots[i].dur_ns;
+    }
+  });
+}
+
+RP_API int rp_runtime_costs(rp_runtime_t* p, rp_layer_cost_t* out, int32_t cap, int32_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    *n = (int32_t)rt->costs.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "cost capacity");
+    for (int i = 0; i < *n; ++i)
+      out[i] = rp_layer_cost_t{rt->costs[i].t_fwd_ns, rt->costs[i].t_bwd_ns,
+                               rt->costs[i].param_bytes, rt->costs[i].act_ckpt_bytes,
+                               rt->costs[i].act_full_bytes};
+  });
+}
+
+RP_API int rp_param_count(rp_runtime_t* p, int32_t group, int64_t* n) {
+  return rt_guard([&] { *n = R(p)->group_numel(gidx(R(p), group)); });
+}
+
+// Flat layout of a group: (offset, rows, cols) per tensor, in the order
+// embed | in_norm qkv q_norm k_norm o post_norm gate_up down | final_norm lm_head.
+RP_API int rp_param_layout(rp_runtime_t* p, int32_t group, int64_t* offs, int64_t* rows,
+                           int64_t* cols, int32_t cap, int32_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    const int g = gidx(rt, group);
+    std::vector<rp::rt::Tensor> ts;
+    if (g == 0) ts = {rp::rt::Tensor{0, rt->s.V, rt->s.h}};
+    else if (g == rt->s.L + 1) ts = {rt->HL.final_norm, rt->HL.lm_head};
+    else {
+      const auto& L = rt->LL;
+      ts = {L.in_norm, L.qkv, L.q_norm, L.k_norm, L.o, L.post_norm, L.gate_up, L.down};
+    }
+    *n = (int32_t)ts.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "layout capacity");
+    for (int i = 0; i < *n; ++i) {
+      offs[i] = ts[i].off;
+      rows[i] = ts[i].rows;
+      cols[i] = ts[i].cols;
+    }
+  });
+}
+
+RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, int64_t n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    const int g = gidx(rt, group);
+    rp::rt::HostGroup& H = rt->host[g];
+    if (n != H.n || !values) throw RtError(RP_E_INPUT, "size mismatch");
+    rt->sync_all();
+    for (int64_t i = 0; i < n; ++i) {
+      H.master[i] = values[i];
+      H.w16[i] = f32_to_bf16_host(values[i]);
+      H.m[i] = 0.f;
+      H.v[i] = 0.f;
+    }
+    H.step = 0;
+    for (int w = 0; w < rt->N; ++w) rt->loaded_iter[(std::size_t)w * rt->ngroups() + g] = -1;
+  });
+}
+
+RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* out, int64_t n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    const int g = gidx(rt, group);
+    rp::rt::HostGroup& H = rt->host[g];
+    if (n != H.n || !out) throw RtError(RP_E_INPUT, "size mismatch");
+    rt->sync_all();
+    switch (which) {
+      case 0: std::memcpy(out, H.master, n * 4); break;
+      case 1:
+        for (int64_t i = 0; i < n; ++i) out[i] = bf16_to_f32_host(H.w16[i]);
+        break;
+      case 2: {
+        if (rt->last_iter < 0) throw RtError(RP_E_INPUT, "no iteration has run");
+        rp::rt::Gpu& G = rt->gpus[rt->grad_owner[g]];
+        rt->set_dev(G);
+        RP_CUDA(cudaMemcpy(out, G.groups[g].grad[rt->last_iter & 1], n * 4,
+                           cudaMemcpyDeviceToHost));
+        break;
+      }
+      case 3: std::memcpy(out, H.m, n * 4); break;
+      case 4: std::memcpy(out, H.v, n * 4); break;
+      default: throw RtError(RP_E_INPUT, "bad selector");
+    }
+  });
+}
+
+RP_API int rp_forward_backward(rp_runtime_t* p, const int32_t* tokens, const int32_t* labels,
+                               float* loss) {
+  return rt_guard([&] {
+    if (!tokens || !labels) throw RtError(RP_E_INPUT, "null tokens/labels");
+    R(p)->forward_backward(tokens, labels, loss);
+  });
+}
+
+RP_API int rp_step(rp_runtime_t* p) {
+  return rt_guard([&] { R(p)->step(); });
+}
+
+RP_API int rp_sync(rp_runtime_t* p) {
+  return rt_guard([&] { R(p)->sync_all(); });
+}
+
+RP_API int rp_timeline(rp_runtime_t* p, rp_timed_event_t* out, int64_t cap, int64_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    *n = (int64_t)rt->records.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "timeline capacity");
+    // one clock per physical device: the anchor of its lowest worker
+    std::vector<cudaEvent_t> anchor(rt->ndev, nullptr);
+    for (auto& G : rt->gpus)
+      if (!anchor[G.dev]) anchor[G.dev] = G.anchor;
+    for (int64_t i = 0; i < *n; ++i) {
+      const auto& r = rt->records[(std::size_t)i];
+      const int dev = rt->gpus[r.worker].dev;
+      float a = 0.f, b = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&a, anchor[dev], r.start));
+      RP_CUDA(cudaEventElapsedTime(&b, anchor[dev], r.end));
+      rp_timed_event_t e{};
+      e.task.iteration = r.task.iteration;
+      e.task.round = r.task.round;
+      e.task.slot = r.task.slot;
+      e.task.mb = r.task.mb;
+      e.task.gpu = r.task.gpu;
+      e.start_ns = (int64_t)std::llround((double)a * 1e6);
+      e.end_ns = (int64_t)std::llround((double)b * 1e6);
+      e.task.dur_ns = e.end_ns - e.start_ns;
+      out[i] = e;
+    }
+  });
+}
+
+RP_API int rp_timeline_clear(rp_runtime_t* p) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    rt->records.clear();
+  });
+}
+
+RP_API int rp_runtime_stats(rp_runtime_t* p, rp_runtime_stats_t* st) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    std::memset(st, 0, sizeof(*st));
+    st->num_layers = rt->s.L;
+    st->num_slots = (int32_t)rt->slots.size();
+    for (int g = 0; g < rt->ngroups(); ++g) st->params_total += rt->host[g].n;
+    st->host_bytes_pinned = (int64_t)rt->arena.size();
+    for (auto& G : rt->gpus)
+      for (int c = 0; c < 8 && c < (int)G.allocated.size(); ++c)
+        st->device_bytes[c] += (int64_t)G.allocated[c];
+    st->h2d_bytes = rt->h2d_bytes;
+    st->d2h_bytes = rt->d2h_bytes;
+    st->p2p_bytes = rt->p2p_bytes;
+    st->iterations_done = rt->iter;
+    st->kernels_launched = (int32_t)rt->kernels;
+  });
+}
+
+RP_API int rp_runtime_profile(rp_runtime_t* p, int32_t enable) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    rt->prof_on = enable != 0;
+    rt->prof.clear();
+    rt->prof_next = 0;
+  });
+}
+
+// Per category (0 GEMM, 1 attention, 2 HBM-bound stage kernels, 3 AdamW):
+// summed kernel time (ms), algorithmic work (FLOPs or bytes), launch count.
+RP_API int rp_runtime_profile_read(rp_runtime_t* p, double* time_ms, double* work,
+                                   int64_t* launches) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    for (int c = 0; c < 4; ++c) time_ms[c] = work[c] = 0.0, launches[c] = 0;
+    for (const auto& r : rt->prof) {
+      float ms = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      time_ms[r.cat] += ms;
+      work[r.cat] += r.work;
+      launches[r.cat] += 1;
+    }
+  });
+}

@@ -1,0 +1,139 @@
+// Internal structures of the roundpipe-b200 executor (see runtime.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "roundpipe/roundpipe.hpp"
+#include "rp/kernels.h"
+#include "rp/runtime.h"
+
+namespace rp {
+namespace rt {
+
+struct RtError : std::runtime_error {
+  int code;
+  RtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define RP_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::rp::rt::RtError(RP_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_) + \
+                                             " @" + __FILE__ + ":" + std::to_string(__LINE__)); \
+  } while (0)
+#define RP_K(expr)                                                                     \
+  do {                                                                                 \
+    int c_ = (expr);                                                                   \
+    if (c_ != RP_OK)                                                                   \
+      throw ::rp::rt::RtError(c_, std::string("kernel failed: ") + #expr + " -> " +    \
+                                      cudaGetErrorString(cudaGetLastError()));          \
+  } while (0)
+
+// Decoder shape (Qwen3 family).
+struct Shape {
+  int h = 0, nq = 0, nk = 0, hd = 0, m = 0, L = 0, V = 0;
+  double theta = 1e6, eps = 1e-6;
+  int qd() const { return nq * hd; }
+  int kd() const { return nk * hd; }
+  int qkvd() const { return qd() + 2 * kd(); }
+};
+
+// Flat parameter layout of one group; every tensor starts on a 128-element
+// (256-byte) boundary so TMA/vector loads are aligned.
+struct Tensor {
+  int64_t off = 0, rows = 0, cols = 1;
+  int64_t numel() const { return rows * cols; }
+};
+struct LayerLayout {
+  Tensor in_norm, qkv, q_norm, k_norm, o, post_norm, gate_up, down;
+  int64_t total = 0;
+};
+struct HeadLayout {
+  Tensor final_norm, lm_head;
+  int64_t total = 0;
+};
+LayerLayout make_layer_layout(const Shape& s);
+HeadLayout make_head_layout(const Shape& s);
+
+// Pinned host state of one parameter group: fp32 optimizer copy (master,
+// m, v) and the bf16 master copy the GPUs upload.
+struct HostGroup {
+  int64_t n = 0;
+  uint16_t* w16 = nullptr;
+  float* master = nullptr;
+  float* m = nullptr;
+  float* v = nullptr;
+  int step = 0;
+};
+
+// Device-side state of one parameter group on one worker.
+struct DevGroup {
+  uint16_t* w = nullptr;                  // bf16 weights of the current upload
+  float* grad[2] = {nullptr, nullptr};    // fp32 accumulators by iteration parity
+  uint16_t* pend = nullptr;               // AdamW output awaiting p_copy
+  cudaEvent_t ev_upload = nullptr;        // upload(l, t)              GPU lane
+  cudaEvent_t ev_lastuse = nullptr;       // last compute read of w (WAR)
+  cudaEvent_t ev_gradwrite = nullptr;     // GradWrite(l, t)           GPU lane
+  cudaEvent_t ev_adam[2] = {nullptr, nullptr};  // g_copy: AdamW consumed grad[p]
+  cudaEvent_t ev_pcopy = nullptr;         // p_copy(l, t)              optimizer lane
+  cudaEvent_t ev_state = nullptr;         // fp32 state written back to host
+};
+
+// Activations of one decoder layer for one micro-batch.
+struct LayerActs {
+  uint16_t *x, *h1, *qkv, *q, *k, *o, *x2, *h2, *gu, *act;
+  float *rstd1, *rstd_q, *rstd_k, *lse, *rstd2;
+  const uint16_t* xin = nullptr;  // the input actually used by layer_fwd
+};
+
+// A hand-off / checkpoint buffer with its producer and consumer events.
+struct Slotbuf {
+  void* p = nullptr;
+  cudaEvent_t ready = nullptr;  // recorded by the producer after the write
+  cudaEvent_t read = nullptr;   // recorded by the consumer after the last read
+};
+
+// One logical RoundPipe worker ("stateless GPU"). Workers map onto physical
+// devices (worker % device_count); N workers on one B200 exercise the full
+// N-way dispatch in tests.
+struct Gpu {
+  int id = 0, dev = 0;
+  cudaStream_t compute = nullptr, act = nullptr, w_h2d = nullptr;
+  cudaStream_t opt_h2d = nullptr, opt_d2h = nullptr, opt_comp = nullptr;
+  std::vector<DevGroup> groups;           // index g = group + 1 (0 = embedding)
+  std::vector<LayerActs> acts;            // per decoder layer of the fused stage
+  float* dx32[2] = {nullptr, nullptr};
+  uint16_t *dx16 = nullptr, *dh = nullptr, *dact = nullptr, *dgu = nullptr, *dattn = nullptr;
+  uint16_t *dqkv = nullptr, *dq_t = nullptr, *dk_t = nullptr;
+  float *dq_acc = nullptr, *delta = nullptr;
+  uint16_t* xbuf[2] = {nullptr, nullptr};
+  uint16_t *hN = nullptr, *logits = nullptr;
+  float *rstdN = nullptr, *loss_dev = nullptr;
+  int32_t *tokens_dev = nullptr, *labels_dev = nullptr;
+  float* cos_sin = nullptr;
+  float* opt_buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  cudaEvent_t opt_free[2] = {nullptr, nullptr};
+  int opt_slot = 0;
+  // hand-offs by round parity and micro-batch: activations (bf16) into a
+  // forward/fused slot, gradients (fp32) into a backward slot
+  std::vector<Slotbuf> hand_act, hand_grad;   // [parity * MR + mb]
+  std::vector<Slotbuf> ckpt;                  // [(parity * L + l) * MR + mb]
+  cudaEvent_t anchor = nullptr;
+  cudaEvent_t ev_tokens = nullptr;
+  std::vector<std::size_t> allocated;
+};
+
+struct TaskRecord {
+  roundpipe::Task task;
+  int worker;
+  cudaEvent_t start, end;
+};
+
+}  // namespace rt
+}  // namespace rp
