@@ -74,12 +74,15 @@ HeadLayout make_head_layout(const Shape& s) {
 }
 
 // ---- pinned host arena -------------------------------------------------------------
-// One anonymous mapping, first-touched and registered with CUDA in parallel
-// 1 GiB pieces (pinning 100+ GB from one thread costs about a minute).
+// One anonymous mapping carved into 2 MiB-aligned buffers; commit() first-
+// touches the pages and registers every buffer with CUDA from a pool of
+// threads (pinning 100+ GB from one thread costs about a minute). Each
+// buffer is its own registration, so no transfer spans two of them.
 class HostArena {
  public:
+  static constexpr std::size_t kAlign = std::size_t(2) << 20;
   void reserve(std::size_t bytes) {
-    size_ = (bytes + (2u << 20) - 1) & ~std::size_t((2u << 20) - 1);
+    size_ = (bytes + kAlign - 1) & ~(kAlign - 1);
     base_ = static_cast<uint8_t*>(
         mmap(nullptr, size_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0));
     if (base_ == MAP_FAILED) {
@@ -87,18 +90,28 @@ class HostArena {
       throw RtError(RP_E_INTERNAL, "mmap failed for host arena");
     }
     madvise(base_, size_, MADV_HUGEPAGE);
-    const std::size_t piece = std::size_t(1) << 30;
-    const std::size_t pieces = (size_ + piece - 1) / piece;
+  }
+  void* take(std::size_t bytes) {
+    used_ = (used_ + kAlign - 1) & ~(kAlign - 1);
+    const std::size_t len = (bytes + kAlign - 1) & ~(kAlign - 1);
+    if (used_ + len > size_) throw RtError(RP_E_INTERNAL, "host arena exhausted");
+    void* p = base_ + used_;
+    bufs_.push_back({used_, len});
+    used_ += len;
+    return p;
+  }
+  void commit() {
+    // split big buffers' first-touch across threads, register each buffer once
     const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::atomic<std::size_t> next{0};
     std::atomic<int> err{0};
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nt; ++t)
       th.emplace_back([&] {
-        for (std::size_t i; (i = next++) < pieces;) {
-          const std::size_t off = i * piece, len = std::min(piece, size_ - off);
-          std::memset(base_ + off, 0, len);
-          if (cudaHostRegister(base_ + off, len, cudaHostRegisterPortable) != cudaSuccess)
+        for (std::size_t i; (i = next++) < bufs_.size();) {
+          std::memset(base_ + bufs_[i].first, 0, bufs_[i].second);
+          if (cudaHostRegister(base_ + bufs_[i].first, bufs_[i].second,
+                               cudaHostRegisterPortable) != cudaSuccess)
             err = 1;
         }
       });
@@ -106,26 +119,18 @@ class HostArena {
     registered_ = true;
     if (err) throw RtError(RP_E_CUDA, "cudaHostRegister failed");
   }
-  void* take(std::size_t bytes) {
-    used_ = (used_ + 255) & ~std::size_t(255);
-    if (used_ + bytes > size_) throw RtError(RP_E_INTERNAL, "host arena exhausted");
-    void* p = base_ + used_;
-    used_ += bytes;
-    return p;
-  }
   std::size_t size() const { return size_; }
   ~HostArena() {
     if (!base_) return;
-    if (registered_) {
-      const std::size_t piece = std::size_t(1) << 30;
-      for (std::size_t off = 0; off < size_; off += piece) cudaHostUnregister(base_ + off);
-    }
+    if (registered_)
+      for (const auto& b : bufs_) cudaHostUnregister(base_ + b.first);
     munmap(base_, size_);
   }
 
  private:
   uint8_t* base_ = nullptr;
   std::size_t size_ = 0, used_ = 0;
+  std::vector<std::pair<std::size_t, std::size_t>> bufs_;
   bool registered_ = false;
 };
 
@@ -319,7 +324,8 @@ void Runtime::init(const rp_runtime_config_t& c) {
   parities = N > 1 ? 2 : 1;
 
   std::size_t bytes = 0;
-  for (int g = 0; g < ngroups(); ++g) bytes += (std::size_t)group_numel(g) * 14 + 4 * 256;
+  for (int g = 0; g < ngroups(); ++g)
+    bytes += (std::size_t)group_numel(g) * 14 + 4 * HostArena::kAlign;
   arena.reserve(bytes);
   host.resize(ngroups());
   for (int g = 0; g < ngroups(); ++g) {
@@ -330,6 +336,7 @@ void Runtime::init(const rp_runtime_config_t& c) {
     H.m = static_cast<float*>(arena.take(H.n * 4));
     H.v = static_cast<float*>(arena.take(H.n * 4));
   }
+  arena.commit();
   grad_owner.assign(ngroups(), 0);
   pend_owner.assign(ngroups(), -1);
   pcopy_ev.assign(ngroups(), nullptr);

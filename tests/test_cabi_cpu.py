@@ -1,0 +1,74 @@
+"""CPU-side checks (no GPU needed): the C-ABI library loads, exports every
+entry point declared in include/rp/*.h, the planner works through it, the
+data-plane oracle reproduces its pinned golden numbers, and the runtime's
+layout / cost conventions match the oracle's."""
+import json
+import os
+import re
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for h in ("cabi.h", "kernels.h", "runtime.h"):
+        text = open(os.path.join(ROOT, "include", "rp", h)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        syms |= set(re.findall(r"\b(rp_[a-z0-9_]+)\s*\(", text))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    from paper_2604_27085_b200 import _native
+    lib = _native.load()
+    missing = [s for s in sorted(declared_symbols()) if not hasattr(lib, s)]
+    assert not missing, missing
+    v = lib.rp_version
+    v.restype = ctypes.c_char_p
+    assert b"sm_100a" in v()
+
+
+def test_no_gpu_needed_for_planning(product):
+    plan = product.optimal_partition([(5, 15, 1), (5, 15, 1), (9, 27, 1)], 2, 4)
+    assert plan.num_slots() >= 1
+
+
+def test_oracle_reproduces_golden_first_step():
+    import torch
+    from oracle import step_oracle as O
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "step_golden.json")))
+    s = O.Shape.from_config("tiny")
+    o = O.StepOracle(s, O.init_params(s, seed=0), mode="sync", lr=gold["hparams"]["lr"],
+                     betas=tuple(gold["hparams"]["betas"]), eps=gold["hparams"]["eps"],
+                     weight_decay=gold["hparams"]["weight_decay"])
+    tok, lab = O.synthetic_batch(s, gold["M"], 1, gold["seq"])
+    loss = o.step(tok, lab)
+    assert abs(loss - gold["sync"]["losses"][0]) < 1e-5 * abs(loss)
+    for k, n in gold["sync"]["grad_norms_step0"].items():
+        assert abs(o.last_grads[k].norm().item() - n) <= 1e-4 * max(n, 1e-12) + 1e-12, k
+    assert gold["hf_check"]["worst_grad_rel_l2"] < 1e-4
+    del torch
+
+
+def test_layout_matches_oracle_parameter_shapes():
+    """include/rp layout order == oracle/step_oracle.layer_param_shapes."""
+    from oracle import step_oracle as O
+    from paper_2604_27085_b200.runtime import HEAD_TENSORS, LAYER_TENSORS
+    s = O.Shape.from_config("qwen3-8b")
+    assert [n for n, _ in O.layer_param_shapes(s)] == LAYER_TENSORS
+    assert [n for n, _ in O.head_param_shapes(s)] == HEAD_TENSORS
+    total = sum(int(np.prod(sh)) for _, sh in O.layer_param_shapes(s))
+    # 8B layer: linear 4096 x (6144 + 4096 + 3 x 12288) + 2 hidden norms + q/k norms
+    assert total == 4096 * (6144 + 4096 + 3 * 12288) + 4096 * 2 + 128 * 2
+
+
+def test_bench_flop_model_matches_survey():
+    """bench.py's executed-FLOP model: 262.7 TFLOP per 8B micro-batch with
+    recompute of every layer."""
+    import bench
+    d = bench.MODEL_DIMS["qwen3-8b"]
+    f = bench.step_flops(d, 4096, 4096, recompute_layers=36)
+    assert abs(f / 1e12 - 262.7) / 262.7 < 0.01, f / 1e12
