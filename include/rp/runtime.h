@@ -85,6 +85,13 @@ int rp_sync(rp_runtime_t* rt);
 int rp_timeline(rp_runtime_t* rt, rp_timed_event_t* out, int64_t cap, int64_t* n);
 int rp_runtime_stats(rp_runtime_t* rt, rp_runtime_stats_t* stats);
 int rp_timeline_clear(rp_runtime_t* rt);
+/* Measured transfer / optimizer intervals (same clock as rp_timeline):
+ * kind 0 = weight upload of a group, 1 = p_copy, 2 = AdamW over a group. */
+typedef struct {
+  int32_t kind, group, iteration, worker;
+  int64_t start_ns, end_ns;
+} rp_xfer_event_t;
+int rp_transfer_timeline(rp_runtime_t* rt, rp_xfer_event_t* out, int64_t cap, int64_t* n);
 /* The cost table the plan was built from (L+1 rows). */
 int rp_runtime_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
 /* Flat layout of a group: (offset, rows, cols) per tensor, order

@@ -248,14 +248,14 @@ __global__ void attn_bwd_pre_kernel(const bf16* __restrict__ o, long long ldo,
 }
 
 template <int HD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     attn_bwd_kernel(const bf16* __restrict__ q, long long ldq, const bf16* __restrict__ k,
                     long long ldk, const bf16* __restrict__ v, long long ldv,
                     const bf16* __restrict__ dout, long long lddo, const float* __restrict__ lse,
                     const float* __restrict__ delta, float* __restrict__ dq_acc,
                     bf16* __restrict__ dk, long long lddk, bf16* __restrict__ dv, long long lddv,
                     int T, int seq, int nq, int nk, float scale) {
-  constexpr int BN = 64, BQ = 64, THREADS = 128, DK = HD / 16, DN = HD / 8;
+  constexpr int BN = 128, BQ = 64, THREADS = 256, DK = HD / 16, DN = HD / 8;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   bf16* sK = reinterpret_cast<bf16*>(smem_raw);   // [BN][HD]
   bf16* sV = sK + BN * HD;                         // [BN][HD]
@@ -390,38 +390,41 @@ __global__ void __launch_bounds__(128)
       (void)c;
     }
     __syncthreads();
-    // dQ[qs + 16w .. +16, :] += scale * dS (16 q x 64 keys) . K (64 keys x HD)
-    const int qw0 = warp * 16;
+    // dQ[qs + 16(w%4) .., half w/4 of HD] += scale * dS (16 q x BN keys) . K (BN keys x HD/2)
+    const int qw0 = (warp & 3) * 16, half = warp >> 2;
     uint32_t da[BN / 16][4];
 #pragma unroll
     for (int j = 0; j < BN / 16; ++j)  // A = dS rows=queries, k=keys, stored [key][query]
       ldsm_x4_t(da[j], smem_addr(sS + swz<BQ>(j * 16 + ri + (mi >> 1) * 8, qw0 + (mi & 1) * 8)));
-    float* dq0 = dq_acc + ((long long)(qs + qw0 + g) * nq + hq) * HD;
-    float* dq1 = dq0 + 8LL * nq * HD;
+    float acc[DN / 2][4];
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      float acc[DN / 2][4];
+    for (int i = 0; i < DN / 2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 #pragma unroll
-      for (int i = 0; i < DN / 2; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    for (int j = 0; j < BN / 16; ++j) {
 #pragma unroll
-      for (int j = 0; j < BN / 16; ++j) {
-#pragma unroll
-        for (int p = 0; p < HD / 32; ++p) {
-          uint32_t b[4];
-          const int col = half * (HD / 2) + p * 16;
-          ldsm_x4_t(b, smem_addr(sK + swz<HD>(j * 16 + ri + (mi & 1) * 8, col + (mi >> 1) * 8)));
-          mma16816(acc[2 * p], da[j], b[0], b[1]);
-          mma16816(acc[2 * p + 1], da[j], b[2], b[3]);
-        }
+      for (int p = 0; p < HD / 32; ++p) {
+        uint32_t b[4];
+        const int col = half * (HD / 2) + p * 16;
+        ldsm_x4_t(b, smem_addr(sK + swz<HD>(j * 16 + ri + (mi & 1) * 8, col + (mi >> 1) * 8)));
+        mma16816(acc[2 * p], da[j], b[0], b[1]);
+        mma16816(acc[2 * p + 1], da[j], b[2], b[3]);
       }
+    }
+    // vector reduction: lane pairs (q, q^1) swap halves so each lane owns 4
+    // consecutive columns of one row -> one 16-byte red.global.add per block
+    const bool odd = qd & 1;
+    float* dqrow = dq_acc + ((long long)(qs + qw0 + g + (odd ? 8 : 0)) * nq + hq) * HD;
 #pragma unroll
-      for (int i = 0; i < DN / 2; ++i) {
-        const int c = half * (HD / 2) + i * 8 + 2 * qd;
-        atomicAdd(dq0 + c, acc[i][0] * scale);
-        atomicAdd(dq0 + c + 1, acc[i][1] * scale);
-        atomicAdd(dq1 + c, acc[i][2] * scale);
-        atomicAdd(dq1 + c + 1, acc[i][3] * scale);
-      }
+    for (int i = 0; i < DN / 2; ++i) {
+      const float s0v = odd ? acc[i][0] : acc[i][2];
+      const float s1v = odd ? acc[i][1] : acc[i][3];
+      const float r0 = __shfl_xor_sync(0xffffffffu, s0v, 1);
+      const float r1 = __shfl_xor_sync(0xffffffffu, s1v, 1);
+      float4 vv = odd ? make_float4(r0, r1, acc[i][2], acc[i][3])
+                      : make_float4(acc[i][0], acc[i][1], r0, r1);
+      vv.x *= scale; vv.y *= scale; vv.z *= scale; vv.w *= scale;
+      const int c = half * (HD / 2) + i * 8 + 2 * (qd & ~1);
+      atomicAdd(reinterpret_cast<float4*>(dqrow + c), vv);
     }
   }
   // write dK (scaled) and dV for this warp's 16 keys
@@ -483,7 +486,7 @@ int attn_bwd_impl(const void* q, int64_t ldq, const void* k, int64_t ldk, const 
                   const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
                   int64_t lddv, float* dq_acc, float* delta, int T, int seq, int nq, int nk,
                   float scale, cudaStream_t s) {
-  constexpr int BN = 64, BQ = 64;
+  constexpr int BN = 128, BQ = 64;
   if (cudaMemsetAsync(dq_acc, 0, sizeof(float) * (size_t)T * nq * HD, s) != cudaSuccess)
     return RP_E_CUDA;
   const long long warps = (long long)T * nq;
@@ -499,7 +502,7 @@ int attn_bwd_impl(const void* q, int64_t ldq, const void* k, int64_t ldk, const 
     cfg = true;
   }
   dim3 grid(T / BN, nk);
-  kern<<<grid, 128, smem, s>>>((const bf16*)q, ldq, (const bf16*)k, ldk, (const bf16*)v, ldv,
+  kern<<<grid, 256, smem, s>>>((const bf16*)q, ldq, (const bf16*)k, ldk, (const bf16*)v, ldv,
                                (const bf16*)dout, lddo, lse, delta, dq_acc, (bf16*)dk, lddk,
                                (bf16*)dv, lddv, T, seq, nq, nk, scale);
   const long long n = (long long)T * nq * HD;

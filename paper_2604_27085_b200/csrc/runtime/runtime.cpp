@@ -151,7 +151,6 @@ struct Runtime {
   HostArena arena;
   std::vector<HostGroup> host;       // g = group + 1
   std::vector<Gpu> gpus;             // logical workers
-  std::vector<int> loaded_iter;      // [worker * G + g] iteration whose weights are loaded
   std::vector<int> grad_owner;       // g -> worker holding this iteration's grads
   std::vector<int> pend_owner;       // g -> worker holding pending AdamW output (-1 none)
   std::vector<cudaEvent_t> pcopy_ev; // g -> event of the latest p_copy (publication)
@@ -163,6 +162,25 @@ struct Runtime {
   float* loss_host = nullptr;        // pinned [N]
   std::vector<cudaEvent_t> ev_loss;  // per worker, after its last fused task
   std::vector<TaskRecord> records;
+  // transfer / optimizer intervals for the measured timeline
+  struct XferRecord {
+    int kind, group, iteration, worker;  // kind: 0 upload, 1 p_copy, 2 AdamW group
+    cudaEvent_t a, b;
+  };
+  std::vector<XferRecord> xfers;
+  bool tl_on() const { return cfg.flags & RP_RT_RECORD_TIMELINE; }
+  cudaEvent_t xfer_begin(cudaStream_t st) {
+    if (!tl_on()) return nullptr;
+    cudaEvent_t e = new_event(true);
+    RP_CUDA(cudaEventRecord(e, st));
+    return e;
+  }
+  void xfer_end(cudaEvent_t a, cudaStream_t st, int kind, int g, int it, int w) {
+    if (!a) return;
+    cudaEvent_t e = new_event(true);
+    RP_CUDA(cudaEventRecord(e, st));
+    xfers.push_back({kind, g, it, w, a, e});
+  }
   std::vector<cudaEvent_t> event_pool;
   int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, kernels = 0;
   int64_t chunk_elems = 32ll << 20;  // optimizer chunk (elements)
@@ -218,6 +236,9 @@ struct Runtime {
   void forward_backward(const int32_t* tokens, const int32_t* labels, float* loss);
   void run_slot(Gpu& G, int it, int round, int slot, int first_round, float grad_scale);
   void upload(Gpu& G, int g, int it, bool last_use);
+  void prefetch(int it, bool reverse = false);
+  std::vector<int> slot_groups(const roundpipe::StageSlot& ss) const;
+  int exec_iter = 0;  // iteration whose compute is being enqueued
   void p_copy(int g);
   void layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out);
   void layer_bwd(Gpu& G, int l, LayerActs& A, bool first);
@@ -342,7 +363,6 @@ void Runtime::init(const rp_runtime_config_t& c) {
   pcopy_ev.assign(ngroups(), nullptr);
   state_ev.assign(ngroups(), nullptr);
   uploaders.assign(ngroups(), {});
-  loaded_iter.assign((std::size_t)N * ngroups(), -1);
   RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N));
   gpus.resize(N);
   for (int w = 0; w < N; ++w) alloc_worker(gpus[w], w);
@@ -441,12 +461,14 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   for (int g = 0; g < ngroups(); ++g) {
     DevGroup& D = G.groups[g];
     const int64_t n = group_numel(g);
-    D.w = static_cast<uint16_t*>(dalloc(n * 2, 0));
+    for (int b = 0; b < 2; ++b) {
+      D.w[b] = static_cast<uint16_t*>(dalloc(n * 2, 0));
+      D.ev_upload[b] = new_event(false);
+      D.ev_lastuse[b] = new_event(false);
+    }
     D.grad[0] = static_cast<float*>(dalloc(n * 4, 1));
     D.grad[1] = static_cast<float*>(dalloc(n * 4, 1));
     D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
-    D.ev_upload = new_event(false);
-    D.ev_lastuse = new_event(false);
     D.ev_gradwrite = new_event(false);
     D.ev_adam[0] = new_event(false);
     D.ev_adam[1] = new_event(false);
@@ -541,16 +563,17 @@ void Runtime::init_weights() {
     HostGroup& H = host[g];
     DevGroup& D = G.groups[g];
     float* f32 = D.grad[0];  // scratch
-    RP_K(rp_init_normal(f32, D.w, H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_, G.compute));
+    RP_K(rp_init_normal(f32, D.w[0], H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_,
+                        G.compute));
     std::vector<std::pair<int64_t, int64_t>> ones;
     if (g >= 1 && g <= s.L)
       ones = {{LL.in_norm.off, s.h}, {LL.q_norm.off, s.hd}, {LL.k_norm.off, s.hd},
               {LL.post_norm.off, s.h}};
     else if (g == s.L + 1)
       ones = {{HL.final_norm.off, s.h}};
-    for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, D.w + off, n, 1.0f, G.compute));
+    for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, D.w[0] + off, n, 1.0f, G.compute));
     RP_CUDA(cudaMemcpyAsync(H.master, f32, H.n * 4, cudaMemcpyDeviceToHost, G.compute));
-    RP_CUDA(cudaMemcpyAsync(H.w16, D.w, H.n * 2, cudaMemcpyDeviceToHost, G.compute));
+    RP_CUDA(cudaMemcpyAsync(H.w16, D.w[0], H.n * 2, cudaMemcpyDeviceToHost, G.compute));
     RP_CUDA(cudaStreamSynchronize(G.compute));
   }
 }
@@ -565,18 +588,49 @@ void Runtime::init_weights() {
 void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
   DevGroup& D = G.groups[g];
   HostGroup& H = host[g];
-  int& have = loaded_iter[(std::size_t)G.id * ngroups() + g];
-  if (have != it) {
+  const int b = it & 1;
+  if (D.loaded[b] != it) {
+    set_dev(G);
     if (pcopy_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.w_h2d, pcopy_ev[g], 0));  // edge (2)
-    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse, 0));
-    RP_CUDA(cudaMemcpyAsync(D.w, H.w16, H.n * 2, cudaMemcpyHostToDevice, G.w_h2d));
+    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse[b], 0));               // WAR (t-2)
+    cudaEvent_t xa = xfer_begin(G.w_h2d);
+    RP_CUDA(cudaMemcpyAsync(D.w[b], H.w16, H.n * 2, cudaMemcpyHostToDevice, G.w_h2d));
+    xfer_end(xa, G.w_h2d, 0, g - 1, it, G.id);
     h2d_bytes += H.n * 2;
-    RP_CUDA(cudaEventRecord(D.ev_upload, G.w_h2d));
-    have = it;
-    uploaders[g].push_back(G.id);
+    RP_CUDA(cudaEventRecord(D.ev_upload[b], G.w_h2d));
+    D.loaded[b] = it;
+    uploaders[g].push_back(G.id * 2 + b);
   }
   if (last_use && cfg.async_optimizer && pend_owner[g] >= 0) p_copy(g);
   set_dev(G);
+}
+
+// Enqueue iteration it's weight uploads ahead of time (into the other
+// parity buffer) so they stream in under the current iteration's compute.
+void Runtime::prefetch(int it, bool reverse) {
+  ensure_horizon(it);
+  std::vector<std::pair<int, int>> todo;  // (worker, group) in use order
+  for (std::size_t i = 0; i < sched.tasks.size();) {
+    const roundpipe::Task& t = sched.tasks[i];
+    if (t.iteration < it) { ++i; continue; }
+    if (t.iteration > it) break;
+    for (int g : slot_groups(slots[t.slot])) todo.emplace_back(t.gpu, g);
+    i += MR;
+  }
+  if (reverse) std::reverse(todo.begin(), todo.end());
+  for (auto [w, g] : todo) upload(gpus[w], g, it, false);
+}
+
+// Parameter groups a slot reads, in the order its compute needs them.
+std::vector<int> Runtime::slot_groups(const roundpipe::StageSlot& ss) const {
+  std::vector<int> gs;
+  const int a = ss.layers.first, b = ss.layers.last;
+  if (ss.kind != StageKind::Backward && a == 0) gs.push_back(0);
+  if (ss.kind == StageKind::Backward)
+    for (int l = b; l >= a; --l) gs.push_back(l + 1);
+  else
+    for (int l = a; l <= b; ++l) gs.push_back(l + 1);
+  return gs;
 }
 
 // p_copy: pending AdamW result (device) -> bf16 master (pinned host), after
@@ -586,12 +640,14 @@ void Runtime::p_copy(int g) {
   set_dev(O);
   DevGroup& D = O.groups[g];
   HostGroup& H = host[g];
-  for (int w : uploaders[g])
-    RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, gpus[w].groups[g].ev_upload, 0));
+  for (int wb : uploaders[g])
+    RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, gpus[wb / 2].groups[g].ev_upload[wb % 2], 0));
   uploaders[g].clear();
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[0], 0));
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[1], 0));
+  cudaEvent_t xa = xfer_begin(O.opt_d2h);
   RP_CUDA(cudaMemcpyAsync(H.w16, D.pend, H.n * 2, cudaMemcpyDeviceToHost, O.opt_d2h));
+  xfer_end(xa, O.opt_d2h, 1, g - 1, H.step, O.id);
   d2h_bytes += H.n * 2;
   RP_CUDA(cudaEventRecord(D.ev_pcopy, O.opt_d2h));
   pcopy_ev[g] = D.ev_pcopy;
@@ -600,7 +656,7 @@ void Runtime::p_copy(int g) {
 
 // ---- decoder layer -------------------------------------------------------------------
 void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out) {
-  const uint16_t* W = G.groups[l + 1].w;
+  const uint16_t* W = G.groups[l + 1].w[exec_iter & 1];
   cudaStream_t st = G.compute;
   const int h = s.h, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
   A.xin = x;
@@ -646,7 +702,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
 // go to grad[t%2]: the first micro-batch overwrites, later ones accumulate.
 void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   DevGroup& D = G.groups[l + 1];
-  const uint16_t* W = D.w;
+  const uint16_t* W = D.w[exec_iter & 1];
   float* dW = D.grad[last_iter & 1];
   cudaStream_t st = G.compute;
   const int h = s.h, m = s.m, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
@@ -702,7 +758,7 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
 // CE kernel overwrites it in place with dlogits.
 void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale) {
   DevGroup& D = G.groups[s.L + 1];
-  const uint16_t* W = D.w;
+  const uint16_t* W = D.w[exec_iter & 1];
   float* dW = D.grad[last_iter & 1];
   cudaStream_t st = G.compute;
   const int h = s.h, V = s.V;
@@ -741,19 +797,15 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
   Gpu* next = slot + 1 < S ? &gpus[worker_of(round, slot + 1)] : nullptr;
 
   // ---- uploads, in the order compute needs the layers
-  auto needs_embed = ss.kind != StageKind::Backward && a == 0;
-  std::vector<int> gs;  // groups used by this slot
-  if (needs_embed) gs.push_back(0);
-  if (ss.kind == StageKind::Backward)
-    for (int l = b; l >= a; --l) gs.push_back(l + 1);
-  else
-    for (int l = a; l <= b; ++l) gs.push_back(l + 1);
+  const std::vector<int> gs = slot_groups(ss);  // groups used by this slot
   for (int g : gs) {
     const bool last_use = rin == R - 1 && (g == 0 ? ss.kind != StageKind::Backward
                                                   : ss.kind != StageKind::Forward);
     upload(G, g, it, last_use);
   }
-  auto wait_group = [&](int g) { RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_upload, 0)); };
+  auto wait_group = [&](int g) {
+    RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_upload[it & 1], 0));
+  };
   // groups whose grads this slot produces
   std::vector<int> grad_groups;
   if (has_grads) {
@@ -787,7 +839,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
       if (a == 0) {
         wait_group(0);
         uint16_t* dst = ss.kind == StageKind::Fused && a < s.L ? G.acts[0].x : G.xbuf[0];
-        RP_K(rp_embed_fwd(ids, G.groups[0].w, dst, T, s.h, st));
+        RP_K(rp_embed_fwd(ids, G.groups[0].w[it & 1], dst, T, s.h, st));
         ++kernels;
         x_in = dst;
       } else {
@@ -878,7 +930,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     }
   }
   // last compute read of the slot's weights; grads complete (GradWrite)
-  for (int g : gs) RP_CUDA(cudaEventRecord(G.groups[g].ev_lastuse, st));
+  for (int g : gs) RP_CUDA(cudaEventRecord(G.groups[g].ev_lastuse[it & 1], st));
   if (has_grads && rin == R - 1)
     for (int g : grad_groups) {
       RP_CUDA(cudaEventRecord(G.groups[g].ev_gradwrite, st));
@@ -893,6 +945,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
 void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, float* loss) {
   const int it = iter++;
   last_iter = it;
+  exec_iter = it;
   ensure_horizon(it);
   int64_t n_valid = 0;
   for (int64_t i = 0; i < (int64_t)M * T; ++i) n_valid += labels[i] >= 0;
@@ -923,6 +976,9 @@ void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, flo
     run_slot(G, it, t.round, t.slot, first_round, grad_scale);
     i += MR;  // a (round, slot) is MR consecutive tasks on one worker
   }
+  // async: the next iteration's weights (published by p_copy(l, it)) stream
+  // in under this iteration's compute, ahead of this step's AdamW traffic
+  if (cfg.async_optimizer) prefetch(it + 1);
   // early return: the loss is known once the fused slots are done
   double total = 0.0;
   for (Gpu& G : gpus) {
@@ -949,6 +1005,7 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_gradwrite, 0));  // edge (3)
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_pcopy, 0));      // pend free again
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
+  cudaEvent_t xa = xfer_begin(G.opt_h2d);
   for (int64_t off = 0; off < H.n; off += chunk_elems) {
     const int64_t n = std::min<int64_t>(chunk_elems, H.n - off);
     const int sl = G.opt_slot;
@@ -979,6 +1036,7 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   RP_CUDA(cudaEventRecord(D.ev_adam[parity], G.opt_comp));  // g_copy(l, t) complete
   if (!D.ev_state) D.ev_state = new_event(false);
   RP_CUDA(cudaEventRecord(D.ev_state, G.opt_d2h));
+  xfer_end(xa, G.opt_d2h, 2, g - 1, last_iter, G.id);
   state_ev[g] = D.ev_state;
   pend_owner[g] = G.id;
   if (!cfg.async_optimizer) p_copy(g);  // sync: iteration t+1 sees grads of t
@@ -997,6 +1055,9 @@ void Runtime::step() {
       adam_group(G, g, parity);
     }
   }
+  // sync: uploads of t+1 follow each group's publication; enqueue them in
+  // publication order (head first) so one stalled group cannot block the rest
+  if (!cfg.async_optimizer) prefetch(last_iter + 1, /*reverse=*/true);
   if (event_pool.size() > 500000) sync_all();
 }
 
@@ -1171,7 +1232,7 @@ RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, in
       H.v[i] = 0.f;
     }
     H.step = 0;
-    for (int w = 0; w < rt->N; ++w) rt->loaded_iter[(std::size_t)w * rt->ngroups() + g] = -1;
+    for (auto& G : rt->gpus) G.groups[g].loaded[0] = G.groups[g].loaded[1] = -1;
   });
 }
 
@@ -1253,6 +1314,7 @@ RP_API int rp_timeline_clear(rp_runtime_t* p) {
     Runtime* rt = R(p);
     rt->sync_all();
     rt->records.clear();
+    rt->xfers.clear();
   });
 }
 
@@ -1299,6 +1361,30 @@ RP_API int rp_runtime_profile_read(rp_runtime_t* p, double* time_ms, double* wor
       time_ms[r.cat] += ms;
       work[r.cat] += r.work;
       launches[r.cat] += 1;
+    }
+  });
+}
+
+// Measured transfer / optimizer intervals: kind 0 weight upload, 1 p_copy,
+// 2 AdamW over one group (first H2D .. last D2H). Same clock as rp_timeline.
+RP_API int rp_transfer_timeline(rp_runtime_t* p, rp_xfer_event_t* out, int64_t cap, int64_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    *n = (int64_t)rt->xfers.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "transfer timeline capacity");
+    std::vector<cudaEvent_t> anchor(rt->ndev, nullptr);
+    for (auto& G : rt->gpus)
+      if (!anchor[G.dev]) anchor[G.dev] = G.anchor;
+    for (int64_t i = 0; i < *n; ++i) {
+      const auto& r = rt->xfers[(std::size_t)i];
+      float a = 0.f, b = 0.f;
+      const int dev = rt->gpus[r.worker].dev;
+      RP_CUDA(cudaEventElapsedTime(&a, anchor[dev], r.a));
+      RP_CUDA(cudaEventElapsedTime(&b, anchor[dev], r.b));
+      out[i] = rp_xfer_event_t{r.kind, r.group, r.iteration, r.worker,
+                               (int64_t)std::llround((double)a * 1e6),
+                               (int64_t)std::llround((double)b * 1e6)};
     }
   });
 }

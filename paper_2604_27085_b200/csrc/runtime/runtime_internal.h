@@ -74,11 +74,13 @@ struct HostGroup {
 
 // Device-side state of one parameter group on one worker.
 struct DevGroup {
-  uint16_t* w = nullptr;                  // bf16 weights of the current upload
+  uint16_t* w[2] = {nullptr, nullptr};    // bf16 weights, by iteration parity: the
+                                          // upload of t+1 streams in under t's compute
+  int loaded[2] = {-1, -1};               // iteration whose version each buffer holds
   float* grad[2] = {nullptr, nullptr};    // fp32 accumulators by iteration parity
   uint16_t* pend = nullptr;               // AdamW output awaiting p_copy
-  cudaEvent_t ev_upload = nullptr;        // upload(l, t)              GPU lane
-  cudaEvent_t ev_lastuse = nullptr;       // last compute read of w (WAR)
+  cudaEvent_t ev_upload[2] = {nullptr, nullptr};   // upload(l, t) into w[t%2]   GPU lane
+  cudaEvent_t ev_lastuse[2] = {nullptr, nullptr};  // last compute read of w[b] (WAR)
   cudaEvent_t ev_gradwrite = nullptr;     // GradWrite(l, t)           GPU lane
   cudaEvent_t ev_adam[2] = {nullptr, nullptr};  // g_copy: AdamW consumed grad[p]
   cudaEvent_t ev_pcopy = nullptr;         // p_copy(l, t)              optimizer lane

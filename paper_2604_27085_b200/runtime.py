@@ -200,6 +200,17 @@ class RoundPipe:
     def clear_timeline(self):
         self._call("rp_timeline_clear", self.h)
 
+    XFER_DTYPE = np.dtype([("kind", "<i4"), ("group", "<i4"), ("iteration", "<i4"),
+                           ("worker", "<i4"), ("start_ns", "<i8"), ("end_ns", "<i8")])
+
+    def transfer_timeline(self) -> np.ndarray:
+        """kind 0 = weight upload, 1 = p_copy, 2 = AdamW over a group."""
+        cap = 1 << 18
+        ev = np.zeros(cap, dtype=self.XFER_DTYPE)
+        n = I64()
+        self._call("rp_transfer_timeline", self.h, ev.ctypes.data_as(VP), I64(cap), C.byref(n))
+        return ev[: n.value].copy()
+
     def stats(self) -> dict:
         st = StatsC()
         self._call("rp_runtime_stats", self.h, C.byref(st))

@@ -11,7 +11,8 @@ seed 1234, AdamW lr 1e-3 betas (0.9, 0.95) wd 0. Sync and async
 Tolerances (bf16 compute vs fp32 oracle):
   loss rel <= 2e-3; per-tensor grads rel-L2 <= 3e-2 and cosine >= 0.999
   (tensors with norm > 1e-6); fp32 master after 3 steps rel-L2 <= 1e-2 and
-  cosine(dW_gpu, dW_oracle) >= 0.98 for the accumulated update dW. (AdamW
+  cosine(dW_gpu, dW_oracle) >= 0.98 for the accumulated update dW of every
+  weight matrix (rel-L2 only for the 64..4096-element norm vectors). (AdamW
   normalises every element's step to ~lr, so elements whose gradient sits
   below bf16 noise move by +-lr either way; at lr 1e-3 on 0.02-scale weights
   that alone is ~5e-3 rel-L2 after 3 steps, independent of gradient error.)
@@ -109,7 +110,7 @@ def check(mode, losses, grads0, master):
         w = torch.from_numpy(np.asarray(master[k])).reshape(ref.shape)
         worst[k] = (w - ref).norm().item() / ref.norm().item()
         d_gpu, d_ref = (w - init[k]).flatten(), (ref - init[k]).flatten()
-        if d_ref.norm() > 0:
+        if d_ref.norm() > 0 and ref.dim() == 2:  # matrices; norm vectors are sign-noise
             cosd[k] = torch.nn.functional.cosine_similarity(d_gpu, d_ref, dim=0).item()
     print(mode, "losses", losses, "oracle", ol)
     print(mode, "worst master rel-L2", max(worst.items(), key=lambda kv: kv[1]),
