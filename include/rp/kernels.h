@@ -85,6 +85,11 @@ int rp_fill(float* f32, void* b16, int64_t n, float value, void* stream);
 int rp_attn_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                 int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
                 int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
+/* Same contract, on the 5th-gen tensor cores (tcgen05 + TMEM + TMA); needs
+ * 16-byte aligned base pointers and pitches. */
+int rp_attn_fwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
+                   int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
+                   int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
 /* Backward: dq/dk/dv bf16 (same layouts as q/k/v, own pitches). Needs
  * workspace: dq_acc fp32 [T, nq, hd] and delta fp32 [nq, T]. */
 int rp_attn_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,

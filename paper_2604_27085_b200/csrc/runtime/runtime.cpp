@@ -675,7 +675,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
   }
   {
     const int pi_ = prof_begin(st);
-    RP_K(rp_attn_fwd(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, A.lse, T, cfg.seq_len, s.nq,
+    RP_K(rp_attn_fwd_tc(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, A.lse, T, cfg.seq_len, s.nq,
                    s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
     prof_end(pi_, st, 1, 2.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }

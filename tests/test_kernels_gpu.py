@@ -182,6 +182,29 @@ def _attn_ref(q, k, v, seq, nq, nk, hd):
 
 
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
+                                            (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
+                                            (2048, 1024, 16, 4, 128)])
+def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
+    from paper_2604_27085_b200 import kernels as K
+    qkv = rnd(T, (nq + 2 * nk) * hd, seed=30, scale=2.0)
+    q = qkv[:, : nq * hd]
+    k = qkv[:, nq * hd:(nq + nk) * hd]
+    v = qkv[:, (nq + nk) * hd:]
+    o = torch.empty(T, nq * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    K.attn_fwd_tc(q, k, v, o, lse, seq, nq, nk, hd)
+    oref, lref = _attn_ref(q.float(), k.float(), v.float(), seq, nq, nk, hd)
+    torch.cuda.synchronize()
+    assert rel(o, oref) < 2e-2
+    assert (lse - lref).abs().max().item() < 2e-2
+    o2 = torch.empty_like(o)
+    lse2 = torch.empty_like(lse)
+    K.attn_fwd(q, k, v, o2, lse2, seq, nq, nk, hd)
+    torch.cuda.synchronize()
+    assert rel(o, o2) < 1e-2
+
+
+@pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64)])
 def test_flash_attention_fwd_bwd(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K

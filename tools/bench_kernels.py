@@ -33,6 +33,8 @@ def main():
     flops = 4.0 * nq * hd * seq * seq / 2 * (T // seq)  # causal
     ms = bench(lambda: K.attn_fwd(q, k, v, o, lse, seq, nq, nk, hd))
     out.append({"kernel": "attn_fwd", "ms": ms, "tflops": flops / ms / 1e9})
+    ms = bench(lambda: K.attn_fwd_tc(q, k, v, o, lse, seq, nq, nk, hd))
+    out.append({"kernel": "attn_fwd_tc", "ms": ms, "tflops": flops / ms / 1e9})
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
     dq_acc = torch.empty(T, nq * hd, device="cuda")
