@@ -1,0 +1,569 @@
+// Causal GQA flash-attention BACKWARD on the 5th-gen tensor cores (sm_100a),
+// as two deterministic kernels (no atomics):
+//
+//  (A) dK/dV, key-major. CTA = 128 keys x 1 KV head; loops over the G query
+//      heads of the group and every query tile (64 queries) at or after the
+//      diagonal. Per tile: S^T = K Q^T and dP^T = V dO^T (tcgen05, M128 N64)
+//      into double-buffered TMEM; 4 softmax warps (thread = key row) form
+//      P^T = exp2(S^T*scale*log2e - lse*log2e) and dS^T = P^T (dP^T - delta)
+//      in bf16 smem; then dV += P^T dO and dK += dS^T Q (M128 N=hd K64)
+//      accumulate in TMEM for the whole loop. Epilogue: dK*scale, dV -> bf16.
+//  (B) dQ, query-major. CTA = 128 queries x 1 head; loops over key tiles
+//      (128 keys) up to the diagonal: S = Q K^T and dP = dO V^T (M128 N128)
+//      -> softmax warps (thread = query row) write dS to smem -> dQ += dS K
+//      (M128 N=hd K128, K as an MN-major operand). Epilogue: dQ*scale -> bf16.
+// (B) recomputes S and dP instead of reducing dQ partials through atomics.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels/sm100.cuh"
+#include "rp/kernels.h"
+
+namespace rp {
+namespace {
+
+using namespace sm100;
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float ex2b(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ====================================================================== (A) dK / dV
+constexpr int A_BK = 128;                 // keys per CTA
+constexpr int A_BQ = 64;                  // queries per tile
+constexpr int SUB128 = 128 * 128;         // 128 rows x 64 bf16 (16 KB)
+constexpr int SUB64 = 64 * 128;           // 64 rows x 64 bf16 (8 KB)
+
+template <int HD>
+struct DkvSmem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int K = 0;
+  static constexpr int V = K + NSUB * SUB128;
+  static constexpr int Q0 = V + NSUB * SUB128;        // stage s: Q at Q0 + s*STAGE
+  static constexpr int STAGE = 2 * NSUB * SUB64;      // Q + dO of one query tile
+  static constexpr int DO_OFF = NSUB * SUB64;         // dO after Q inside a stage
+  static constexpr int PS = Q0 + 2 * STAGE;           // buffer b: P^T at PS + b*2*SUB128/2
+  static constexpr int PS_BUF = 2 * (A_BK * A_BQ * 2);  // P^T + dS^T (16 KB each)
+  static constexpr int BAR = PS + 2 * PS_BUF;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v,
+                        const __grid_constant__ CUtensorMap tm_q,
+                        const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                        const float* __restrict__ delta, bf16* __restrict__ dk, long long lddk,
+                        bf16* __restrict__ dv, long long lddv, int T, int seq, int nq, int nk,
+                        float scale) {
+  using L = DkvSmem<HD>;
+  constexpr int NSUB = L::NSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2]
+  uint64_t* sd_full = bar + 5;   // [2]
+  uint64_t* sd_free = bar + 7;   // [2]
+  uint64_t* ps_full = bar + 9;   // [2]
+  uint64_t* ps_empty = bar + 11; // [2]
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kb = blockIdx.x, kvh = blockIdx.y;
+  const int k0 = kb * A_BK;
+  const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
+  const int G = nq / nk;
+  const int nqt = (s_end - k0) / A_BQ;  // query tiles at/after the diagonal
+  const int iters = G * nqt;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_free[i], 4);
+      mbar_init(&ps_full[i], 4);
+      mbar_init(&ps_empty[i], 1);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S^T[b] at b*128 (64 cols), dP^T[b] at b*128+64, dV at 256, dK at 384
+  const uint32_t TM_DV = 256, TM_DK = 384;
+
+  if (warp == 0 && lane == 0) {
+    mbar_arrive_expect_tx(kv_full, 2 * NSUB * SUB128);
+    for (int sub = 0; sub < NSUB; ++sub) {
+      tma_load_2d(sm + L::K + sub * SUB128, &tm_k, kv_full, kvh * HD + 64 * sub, k0);
+      tma_load_2d(sm + L::V + sub * SUB128, &tm_v, kv_full, kvh * HD + 64 * sub, k0);
+    }
+    for (int it = 0; it < iters; ++it) {
+      const int s = it & 1;
+      mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+      const int hq = kvh * G + it / nqt;
+      const int qs = k0 + (it % nqt) * A_BQ;
+      uint8_t* qd = sm + L::Q0 + s * L::STAGE;
+      mbar_arrive_expect_tx(&q_full[s], L::STAGE);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(qd + sub * SUB64, &tm_q, &q_full[s], hq * HD + 64 * sub, qs);
+        tma_load_2d(qd + L::DO_OFF + sub * SUB64, &tm_do, &q_full[s], hq * HD + 64 * sub, qs);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A_BQ, 0, 0);   // K-major x K-major
+    constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);     // K-major x MN-major
+    const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
+    auto issue_grads = [&](int it) {
+      const int s = it & 1, b = it & 1;
+      mbar_wait(&ps_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t q_addr = smem_u32(sm + L::Q0 + s * L::STAGE);
+      const uint32_t do_addr = q_addr + L::DO_OFF;
+      const uint32_t p_addr = smem_u32(sm + L::PS + b * L::PS_BUF);
+      const uint32_t ds_addr = p_addr + A_BK * A_BQ * 2;
+#pragma unroll
+      for (int kk = 0; kk < A_BQ / 16; ++kk) {
+        const uint64_t pa = umma_desc_sw128(p_addr + kk * 32, 16, 1024);
+        const uint64_t da = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
+        const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
+        const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
+        umma_f16(tmem + TM_DV, pa, ob, idesc_g, (it | kk) != 0);
+        umma_f16(tmem + TM_DK, da, qb, idesc_g, (it | kk) != 0);
+      }
+      umma_commit(&ps_empty[b]);
+      umma_commit(&q_empty[s]);
+    };
+    mbar_wait(kv_full, 0);
+    for (int it = 0; it < iters; ++it) {
+      const int s = it & 1, b = it & 1;
+      mbar_wait(&q_full[s], (it >> 1) & 1);
+      if (it >= 2) mbar_wait(&sd_free[b], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t q_addr = smem_u32(sm + L::Q0 + s * L::STAGE);
+      const uint32_t do_addr = q_addr + L::DO_OFF;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
+        const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
+        umma_f16(tmem + b * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
+                 umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
+        umma_f16(tmem + b * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
+                 umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(&sd_full[b]);
+      if (it >= 1) issue_grads(it - 1);
+    }
+    issue_grads(iters - 1);
+    umma_commit(acc_done);
+  } else if (warp >= 2) {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // key row within the tile
+    const int key = k0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    for (int it = 0; it < iters; ++it) {
+      const int b = it & 1;
+      const int hq = kvh * G + it / nqt;
+      const int qs = k0 + (it % nqt) * A_BQ;
+      const float* lse_t = lse + (long long)hq * T + qs;
+      const float* del_t = delta + (long long)hq * T + qs;
+      mbar_wait(&sd_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[64], dpv[64];
+      tmem_ld_32x32b_x32(lane_base + b * 128, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld_32x32b_x32(lane_base + b * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+      tmem_ld_32x32b_x32(lane_base + b * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(dpv));
+      tmem_ld_32x32b_x32(lane_base + b * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(dpv + 32));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sd_free[b]);
+      uint32_t pk[32], dk2[32];
+      const bool diag = qs < key + 1 && qs + A_BQ > k0;  // tile crosses this key block
+#pragma unroll
+      for (int c = 0; c < A_BQ; c += 2) {
+        float p0 = ex2b(fmaf(__uint_as_float(sv[c]), sl2, -lse_t[c] * kLog2e));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[c + 1]), sl2, -lse_t[c + 1] * kLog2e));
+        if (diag) {
+          if (qs + c < key) p0 = 0.f;
+          if (qs + c + 1 < key) p1 = 0.f;
+        }
+        const float d0 = p0 * (__uint_as_float(dpv[c]) - del_t[c]);
+        const float d1 = p1 * (__uint_as_float(dpv[c + 1]) - del_t[c + 1]);
+        pk[c / 2] = pack_bf16x2(p0, p1);
+        dk2[c / 2] = pack_bf16x2(d0, d1);
+      }
+      if (it >= 2) {
+        mbar_wait(&ps_empty[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+      }
+      uint8_t* prow = sm + L::PS + b * L::PS_BUF + (r >> 3) * 1024 + (r & 7) * 128;
+      uint8_t* drow = prow + A_BK * A_BQ * 2;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const int off = (ch ^ (r & 7)) << 4;
+        *reinterpret_cast<uint4*>(prow + off) =
+            make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        *reinterpret_cast<uint4*>(drow + off) =
+            make_uint4(dk2[ch * 4], dk2[ch * 4 + 1], dk2[ch * 4 + 2], dk2[ch * 4 + 3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps_full[b]);
+    }
+    // epilogue: dK (scaled) and dV rows -> bf16
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    bf16* dkr = dk + (long long)key * lddk + (long long)kvh * HD;
+    bf16* dvr = dv + (long long)key * lddv + (long long)kvh * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t a[32], v[32];
+      tmem_ld_32x32b_x32(lane_base + TM_DK + c, a);
+      tmem_ld_32x32b_x32(lane_base + TM_DV + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 u, w;
+        u.x = pack_bf16x2(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale);
+        u.y = pack_bf16x2(__uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale);
+        u.z = pack_bf16x2(__uint_as_float(a[i + 4]) * scale, __uint_as_float(a[i + 5]) * scale);
+        u.w = pack_bf16x2(__uint_as_float(a[i + 6]) * scale, __uint_as_float(a[i + 7]) * scale);
+        w.x = pack_bf16x2(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        w.y = pack_bf16x2(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        w.z = pack_bf16x2(__uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+        w.w = pack_bf16x2(__uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+        *reinterpret_cast<uint4*>(dkr + c + i) = u;
+        *reinterpret_cast<uint4*>(dvr + c + i) = w;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ======================================================================== (B) dQ
+constexpr int B_T = 128;  // queries per CTA and keys per tile
+
+template <int HD>
+struct DqSmem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int Q = 0;
+  static constexpr int DO = Q + NSUB * SUB128;
+  static constexpr int KV0 = DO + NSUB * SUB128;     // stage s: K at KV0 + s*STAGE, V after
+  static constexpr int STAGE = 2 * NSUB * SUB128;
+  static constexpr int DS = KV0 + 2 * STAGE;         // dS [128 q][128 keys], 2 sub-tiles
+  static constexpr int BAR = DS + 2 * SUB128;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ lse,
+                       const float* __restrict__ delta, bf16* __restrict__ dq, long long lddq,
+                       int T, int seq, int nq, int nk, float scale) {
+  using L = DqSmem<HD>;
+  constexpr int NSUB = L::NSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* sd_full = bar + 5;
+  uint64_t* sd_free = bar + 6;
+  uint64_t* ds_full = bar + 7;
+  uint64_t* dq_done = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qblocks = T / B_T;
+  const int qb = qblocks - 1 - blockIdx.x;
+  const int h = blockIdx.y, kvh = h / (nq / nk);
+  const int q0 = qb * B_T;
+  const int s0 = (q0 / seq) * seq;
+  const int ntiles = (q0 - s0) / B_T + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(sd_full, 1);
+    mbar_init(sd_free, 4);
+    mbar_init(ds_full, 4);
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
+
+  if (warp == 0 && lane == 0) {
+    mbar_arrive_expect_tx(q_full, 2 * NSUB * SUB128);
+    for (int sub = 0; sub < NSUB; ++sub) {
+      tma_load_2d(sm + L::Q + sub * SUB128, &tm_q, q_full, h * HD + 64 * sub, q0);
+      tma_load_2d(sm + L::DO + sub * SUB128, &tm_do, q_full, h * HD + 64 * sub, q0);
+    }
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+      const int k0 = s0 + j * B_T;
+      uint8_t* kd = sm + L::KV0 + st * L::STAGE;
+      mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(kd + sub * SUB128, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
+        tma_load_2d(kd + NSUB * SUB128 + sub * SUB128, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
+                    k0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(B_T, B_T, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(B_T, HD, 0, 1);
+    const uint32_t q_addr = smem_u32(sm + L::Q), do_addr = smem_u32(sm + L::DO);
+    const uint32_t ds_addr = smem_u32(sm + L::DS);
+    mbar_wait(q_full, 0);
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&kv_full[st], (j >> 1) & 1);
+      if (j >= 1) mbar_wait(sd_free, (j - 1) & 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + st * L::STAGE);
+      const uint32_t v_addr = k_addr + NSUB * SUB128;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t o = (kk >> 2) * SUB128 + (kk & 3) * 32;
+        umma_f16(tmem + TM_S, umma_desc_sw128(q_addr + o, 16, 1024),
+                 umma_desc_sw128(k_addr + o, 16, 1024), idesc_s, kk != 0);
+        umma_f16(tmem + TM_DP, umma_desc_sw128(do_addr + o, 16, 1024),
+                 umma_desc_sw128(v_addr + o, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(sd_full);
+      mbar_wait(ds_full, j & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < B_T / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(ds_addr + (kk >> 2) * SUB128 + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB128, 1024);
+        umma_f16(tmem + TM_DQ, ad, bd, idesc_q, (j | kk) != 0);
+      }
+      umma_commit(dq_done);
+      umma_commit(&kv_empty[st]);
+    }
+  } else if (warp >= 2) {
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // query row
+    const int qrow = q0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
+    const float dl = delta[(long long)h * T + qrow];
+    uint8_t* ds_row = sm + L::DS + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int j = 0; j < ntiles; ++j) {
+      mbar_wait(sd_full, j & 1);
+      tc_fence_after();
+      if (j >= 1) mbar_wait(dq_done, (j - 1) & 1);  // previous dQ MMA done reading dS
+      const bool diag = j == ntiles - 1;
+#pragma unroll 1
+      for (int c = 0; c < B_T; c += 32) {
+        uint32_t sv[32], dpv[32];
+        tmem_ld_32x32b_x32(lane_base + TM_S + c, sv);
+        tmem_ld_32x32b_x32(lane_base + TM_DP + c, dpv);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
+          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
+          if (diag) {
+            if (c + i > r) p0 = 0.f;
+            if (c + i + 1 > r) p1 = 0.f;
+          }
+          pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
+                                  p1 * (__uint_as_float(dpv[i + 1]) - dl));
+        }
+        const int sub = c >> 6;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int ch = ((c & 63) >> 3) + q4;
+          *reinterpret_cast<uint4*>(ds_row + sub * SUB128 + ((ch ^ (r & 7)) << 4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sd_free);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+    }
+    mbar_wait(dq_done, (ntiles - 1) & 1);
+    tc_fence_after();
+    bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(lane_base + TM_DQ + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
+        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
+        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
+        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
+        *reinterpret_cast<uint4*>(dqr + c + i) = u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// delta[h, t] = sum_d dO[t,h,d] * O[t,h,d]; one warp per (t, h), 16-byte loads
+template <int HD>
+__global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf16* __restrict__ d,
+                             long long lddo, float* __restrict__ delta, int T, int nq) {
+  const long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (w >= (long long)T * nq) return;
+  const int t = (int)(w / nq), h = (int)(w % nq);
+  float acc = 0.f;
+  for (int c = lane * 8; c < HD; c += 256) {
+    const uint4 a = *reinterpret_cast<const uint4*>(o + (long long)t * ldo + h * HD + c);
+    const uint4 b = *reinterpret_cast<const uint4*>(d + (long long)t * lddo + h * HD + c);
+    const bf16* pa = reinterpret_cast<const bf16*>(&a);
+    const bf16* pb = reinterpret_cast<const bf16*>(&b);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += __bfloat162float(pa[i]) * __bfloat162float(pb[i]);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) delta[(long long)h * T + t] = acc;
+}
+
+// ---- host ------------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+    return reinterpret_cast<EncodeFn>(ptr);
+  }();
+  return fn;
+}
+bool map2d(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
+           int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  EncodeFn fn = encode_fn();
+  return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                   CUDA_SUCCESS;
+}
+
+template <class K>
+bool set_smem(K kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+         cudaSuccess;
+}
+
+template <int HD>
+int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const void* v,
+           long long ldv, const void* o, long long ldo, const void* dout, long long lddo,
+           const float* lse, void* dq, long long lddq, void* dk, long long lddk, void* dv,
+           long long lddv, float* delta, int T, int seq, int nq, int nk, float scale,
+           cudaStream_t s) {
+  const long long warps = (long long)T * nq;
+  delta_kernel<HD><<<(int)((warps + 7) / 8), 256, 0, s>>>((const bf16*)o, ldo, (const bf16*)dout,
+                                                         lddo, delta, T, nq);
+  CUtensorMap mk128, mv128, mq64, mdo64, mq128, mdo128;
+  if (!map2d(&mk128, k, T, (long long)nk * HD, ldk, 128) ||
+      !map2d(&mv128, v, T, (long long)nk * HD, ldv, 128) ||
+      !map2d(&mq64, q, T, (long long)nq * HD, ldq, 64) ||
+      !map2d(&mdo64, dout, T, (long long)nq * HD, lddo, 64) ||
+      !map2d(&mq128, q, T, (long long)nq * HD, ldq, 128) ||
+      !map2d(&mdo128, dout, T, (long long)nq * HD, lddo, 128))
+    return RP_E_CUDA;
+  static bool cfg = false;
+  if (!cfg) {
+    if (!set_smem(attn_bwd_dkv_kernel<HD>, DkvSmem<HD>::BYTES) ||
+        !set_smem(attn_bwd_dq_kernel<HD>, DqSmem<HD>::BYTES))
+      return RP_E_CUDA;
+    cfg = true;
+  }
+  attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nk), 192, DkvSmem<HD>::BYTES, s>>>(
+      mk128, mv128, mq64, mdo64, lse, delta, (bf16*)dk, lddk, (bf16*)dv, lddv, T, seq, nq, nk,
+      scale);
+  attn_bwd_dq_kernel<HD><<<dim3(T / B_T, nq), 192, DqSmem<HD>::BYTES, s>>>(
+      mq128, mdo128, mk128, mv128, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
+  return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
+}
+
+}  // namespace
+}  // namespace rp
+
+// tcgen05 backward: dq/dk/dv (bf16) from q/k/v/o/dO/lse; `delta` is an fp32
+// [nq, T] workspace. Deterministic (no atomics). Same layouts as rp_attn_bwd.
+extern "C" __attribute__((visibility("default"))) int rp_attn_bwd_tc(
+    const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
+    const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse, void* dq,
+    int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta, int32_t T,
+    int32_t seq, int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream) {
+  if (T <= 0 || seq % 128 || T % seq || nk <= 0 || nq % nk || (head_dim != 64 && head_dim != 128))
+    return RP_E_INPUT;
+  auto s = (cudaStream_t)stream;
+  return head_dim == 128
+             ? rp::bwd_tc<128>(q, ldq, k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk,
+                               dv, lddv, delta, T, seq, nq, nk, scale, s)
+             : rp::bwd_tc<64>(q, ldq, k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk,
+                              dv, lddv, delta, T, seq, nq, nk, scale, s);
+}

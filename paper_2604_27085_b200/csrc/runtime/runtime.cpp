@@ -730,9 +730,9 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   gemm(st, G.dx16, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
   {
     const int pi_ = prof_begin(st);
-    RP_K(rp_attn_bwd(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, G.dattn, qd, A.lse, G.dq_t,
-                   qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.dq_acc, G.delta, T, cfg.seq_len,
-                   s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
+    RP_K(rp_attn_bwd_tc(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, G.dattn, qd, A.lse,
+                      G.dq_t, qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.delta, T, cfg.seq_len,
+                      s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
     prof_end(pi_, st, 1, 5.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }
   {

@@ -205,6 +205,34 @@ def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
 
 
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
+                                            (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
+                                            (2048, 1024, 16, 4, 128)])
+def test_flash_attention_bwd_tcgen05(T, seq, nq, nk, hd):
+    from paper_2604_27085_b200 import kernels as K
+    qkv = rnd(T, (nq + 2 * nk) * hd, seed=40, scale=1.5)
+    q = qkv[:, : nq * hd]
+    k = qkv[:, nq * hd:(nq + nk) * hd]
+    v = qkv[:, (nq + nk) * hd:]
+    o = torch.empty(T, nq * hd, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(nq, T, device="cuda")
+    K.attn_fwd_tc(q, k, v, o, lse, seq, nq, nk, hd)
+    qf = q.float().requires_grad_(True)
+    kf = k.float().requires_grad_(True)
+    vf = v.float().requires_grad_(True)
+    oref, _ = _attn_ref(qf, kf, vf, seq, nq, nk, hd)
+    do = rnd(T, nq * hd, seed=41)
+    oref.backward(do.float())
+    dqkv = torch.zeros_like(qkv)
+    dq, dk, dv = dqkv[:, : nq * hd], dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:]
+    delta = torch.empty(nq, T, device="cuda")
+    K.attn_bwd_tc(q, k, v, o, do, lse, dq, dk, dv, delta, seq, nq, nk, hd)
+    torch.cuda.synchronize()
+    assert rel(dq, qf.grad) < 2e-2
+    assert rel(dk, kf.grad) < 2e-2
+    assert rel(dv, vf.grad) < 2e-2
+
+
+@pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64)])
 def test_flash_attention_fwd_bwd(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K

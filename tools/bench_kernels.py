@@ -43,6 +43,11 @@ def main():
                                   dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:],
                                   dq_acc, delta, seq, nq, nk, hd))
     out.append({"kernel": "attn_bwd", "ms": ms, "tflops": 2.5 * flops / ms / 1e9})
+    ms = bench(lambda: K.attn_bwd_tc(q, k, v, o, do, lse, dqkv[:, :nq * hd],
+                                     dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:],
+                                     delta, seq, nq, nk, hd))
+    out.append({"kernel": "attn_bwd_tc", "ms": ms, "tflops": 2.5 * flops / ms / 1e9,
+                "executed_tflops": 3.5 * flops / ms / 1e9})
 
     x = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     w = torch.ones(h, device="cuda", dtype=torch.bfloat16)
