@@ -83,35 +83,40 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, long lon
 // dx_total = dx + dres (optional fp32 residual grad); written fp32 and/or bf16.
 // dw[c] += sum_rows dy * xhat. Each block walks a contiguous row range.
 template <int THREADS, int MAXC>
-__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
-                                   const __nv_bfloat16* __restrict__ x,
-                                   const __nv_bfloat16* __restrict__ w,
-                                   const float* __restrict__ rstd,
-                                   const float* __restrict__ dres, float* __restrict__ dx32,
-                                   __nv_bfloat16* __restrict__ dx16, float* __restrict__ dw,
-                                   int rows, int h) {
+__global__ void __launch_bounds__(THREADS)
+    rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                       const float* __restrict__ dres, float* __restrict__ dx32,
+                       __nv_bfloat16* __restrict__ dx16, float* __restrict__ dw, int rows, int h) {
+  // one read of dy/x per row (kept in registers across the reduction), w
+  // loaded once per block, dw partials in registers until the block ends
   __shared__ float red[THREADS / 32];
-  float dw_acc[MAXC][8];
+  float g[MAXC][8], dw_acc[MAXC][8];
 #pragma unroll
-  for (int j = 0; j < MAXC; ++j)
+  for (int j = 0; j < MAXC; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 8;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) dw_acc[j][i] = 0.f;
+    for (int i = 0; i < 8; ++i) dw_acc[j][i] = g[j][i] = 0.f;
+    if (c < h) load8(w + c, g[j]);
+  }
   const int per = (rows + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
   for (int row = r0; row < r1; ++row) {
     const long long off = (long long)row * h;
     const float r = rstd[row];
+    float a[MAXC][8], b[MAXC][8];
     float dot = 0.f;
 #pragma unroll
     for (int j = 0; j < MAXC; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 8;
       if (c < h) {
-        float a[8], b[8], g[8];
-        load8(dy + off + c, a);
-        load8(x + off + c, b);
-        load8(w + c, g);
+        load8(dy + off + c, a[j]);
+        load8(x + off + c, b[j]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dot += a[i] * g[i] * b[i] * r;
+        for (int i = 0; i < 8; ++i) {
+          b[j][i] *= r;  // xhat
+          dot += a[j][i] * g[j][i] * b[j][i];
+        }
       }
     }
     const float mean = block_sum<THREADS>(dot, red) / h;
@@ -119,15 +124,11 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
     for (int j = 0; j < MAXC; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 8;
       if (c < h) {
-        float a[8], b[8], g[8], o[8];
-        load8(dy + off + c, a);
-        load8(x + off + c, b);
-        load8(w + c, g);
+        float o[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float xh = b[i] * r;
-          o[i] = r * (a[i] * g[i] - xh * mean);
-          dw_acc[j][i] += a[i] * xh;
+          o[i] = r * (a[j][i] * g[j][i] - b[j][i] * mean);
+          dw_acc[j][i] += a[j][i] * b[j][i];
         }
         if (dres) {
           const float4 d0 = *reinterpret_cast<const float4*>(dres + off + c);
@@ -155,117 +156,125 @@ __global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
 }
 
 // ------------------------------------------------------- QK-norm + RoPE
-// One warp per (token, head); lane l holds E = hd/32 consecutive elements,
-// its rotate_half partner lives in lane l ^ 16.
-template <int E>
-__global__ void qk_norm_rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld,
-                                        int nq, int nk, const __nv_bfloat16* __restrict__ qw,
-                                        const __nv_bfloat16* __restrict__ kw,
-                                        const float2* __restrict__ cs, int seq,
-                                        __nv_bfloat16* __restrict__ qo,
-                                        __nv_bfloat16* __restrict__ ko,
-                                        float* __restrict__ rstd_q, float* __restrict__ rstd_k,
-                                        int T, float eps) {
-  constexpr int HD = 32 * E, HALF = HD / 2;
-  const int lane = threadIdx.x % 32;
-  const long long warp_id = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+// A head of HD elements is handled by TPH = HD/8 consecutive lanes, 8
+// elements (16 bytes) each; the per-head RMS reduces over those lanes and the
+// rotate_half partner (element e +- HD/2) lives in lane ^ TPH/2.
+template <int HD>
+__global__ void __launch_bounds__(256)
+    qk_norm_rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
+                            const __nv_bfloat16* __restrict__ qw,
+                            const __nv_bfloat16* __restrict__ kw, const float2* __restrict__ cs,
+                            int seq, __nv_bfloat16* __restrict__ qo, __nv_bfloat16* __restrict__ ko,
+                            float* __restrict__ rstd_q, float* __restrict__ rstd_k, int T,
+                            float eps) {
+  constexpr int TPH = HD / 8, HALF = HD / 2;
   const int heads = nq + nk;
-  if (warp_id >= (long long)T * heads) return;
-  const int t = (int)(warp_id / heads), hh = (int)(warp_id % heads);
-  const bool is_q = hh < nq;
-  const __nv_bfloat16* src = qkv + (long long)t * ld + (long long)hh * HD + lane * E;
-  const __nv_bfloat16* wgt = (is_q ? qw : kw) + lane * E;
-  float v[E];
+  const long long total = (long long)T * heads * TPH;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += stride) {
+    const long long hidx = gt / TPH;
+    const int sub = (int)(gt % TPH);
+    const int t = (int)(hidx / heads), hh = (int)(hidx % heads);
+    const bool is_q = hh < nq;
+    float v[8], wv[8];
+    load8(qkv + (long long)t * ld + (long long)hh * HD + sub * 8, v);
+    load8((is_q ? qw : kw) + sub * 8, wv);
+    float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < E; ++i) v[i] = bf2f(src[i]);
-  float ss = 0.f;
+    for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
 #pragma unroll
-  for (int i = 0; i < E; ++i) ss += v[i] * v[i];
-  const float r = rsqrtf(warp_sum(ss) / HD + eps);
-  float n[E];
+    for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float r = rsqrtf(ss / HD + eps);
+    float n[8];
 #pragma unroll
-  for (int i = 0; i < E; ++i) n[i] = bf2f(f2bf(bf2f(wgt[i]) * (v[i] * r)));
-  const int pos = t % seq;
-  const bool lo = lane < 16;
-  __nv_bfloat16 out[E];
+    for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf(wv[i] * (v[i] * r)));
+    const bool lo = sub < TPH / 2;
+    const int pos = t % seq;
+    const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
+    float out[8];
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const float partner = __shfl_xor_sync(0xffffffffu, n[i], 16);
-    const int j = (lane * E + i) % HALF;
-    const float2 c = cs[(long long)pos * HALF + j];  // (cos, sin)
-    out[i] = f2bf(lo ? n[i] * c.x - partner * c.y : n[i] * c.x + partner * c.y);
-  }
-  __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD + lane * E
-                            : ko + ((long long)t * nk + (hh - nq)) * HD + lane * E;
-#pragma unroll
-  for (int i = 0; i < E; ++i) dst[i] = out[i];
-  if (lane == 0) {
-    if (is_q) rstd_q[(long long)t * nq + hh] = r;
-    else rstd_k[(long long)t * nk + (hh - nq)] = r;
+    for (int i = 0; i < 8; i += 2) {
+      const float4 c = c4[i / 2];  // (cos, sin) of elements i, i+1
+      const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
+      const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
+      out[i] = lo ? n[i] * c.x - p0 * c.y : n[i] * c.x + p0 * c.y;
+      out[i + 1] = lo ? n[i + 1] * c.z - p1 * c.w : n[i + 1] * c.z + p1 * c.w;
+    }
+    __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD : ko + ((long long)t * nk + (hh - nq)) * HD;
+    store8(dst + sub * 8, out);
+    if (sub == 0) {
+      if (is_q) rstd_q[(long long)t * nq + hh] = r;
+      else rstd_k[(long long)t * nk + (hh - nq)] = r;
+    }
   }
 }
 
-// Backward: undo the rotation (R^T), then per-head RMSNorm backward.
-// dqkv[:, q/k slots] = dx; dqw/dkw[hd] += sum(dn * xhat).
-template <int E>
-__global__ void qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq,
-                                        const __nv_bfloat16* __restrict__ dk,
-                                        const __nv_bfloat16* __restrict__ qkv, long long ld,
-                                        int nq, int nk, const __nv_bfloat16* __restrict__ qw,
-                                        const __nv_bfloat16* __restrict__ kw,
-                                        const float* __restrict__ rstd_q,
-                                        const float* __restrict__ rstd_k,
-                                        const float2* __restrict__ cs, int seq,
-                                        __nv_bfloat16* __restrict__ dqkv, long long ldd,
-                                        float* __restrict__ dqw, float* __restrict__ dkw, int T) {
-  constexpr int HD = 32 * E, HALF = HD / 2;
+// Backward: undo the rotation (R^T), then per-head RMSNorm backward;
+// dqkv[:, q/k slots] = dx; dqw/dkw[HD] += sum(dn * xhat) (registers -> smem
+// -> one atomic per column per block).
+template <int HD>
+__global__ void __launch_bounds__(256)
+    qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
+                            const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
+                            const __nv_bfloat16* __restrict__ qw,
+                            const __nv_bfloat16* __restrict__ kw, const float* __restrict__ rstd_q,
+                            const float* __restrict__ rstd_k, const float2* __restrict__ cs, int seq,
+                            __nv_bfloat16* __restrict__ dqkv, long long ldd, float* __restrict__ dqw,
+                            float* __restrict__ dkw, int T) {
+  constexpr int TPH = HD / 8, HALF = HD / 2;
   __shared__ float sq[HD], sk[HD];
   for (int i = threadIdx.x; i < HD; i += blockDim.x) sq[i] = sk[i] = 0.f;
   __syncthreads();
-  const int lane = threadIdx.x % 32;
   const int heads = nq + nk;
-  float accq[E], acck[E];
+  const long long total = (long long)T * heads * TPH;
+  const long long stride = (long long)gridDim.x * blockDim.x;  // multiple of TPH
+  float aq[8], ak[8];
 #pragma unroll
-  for (int i = 0; i < E; ++i) accq[i] = acck[i] = 0.f;
-  const long long total = (long long)T * heads;
-  const long long nwarps = (long long)gridDim.x * (blockDim.x / 32);
-  for (long long wid = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; wid < total;
-       wid += nwarps) {
-    const int t = (int)(wid / heads), hh = (int)(wid % heads);
+  for (int i = 0; i < 8; ++i) aq[i] = ak[i] = 0.f;
+  int my_sub = 0;
+  for (long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += stride) {
+    const long long hidx = gt / TPH;
+    const int sub = (int)(gt % TPH);
+    my_sub = sub;
+    const int t = (int)(hidx / heads), hh = (int)(hidx % heads);
     const bool is_q = hh < nq;
-    const __nv_bfloat16* g = is_q ? dq + ((long long)t * nq + hh) * HD
-                                  : dk + ((long long)t * nk + (hh - nq)) * HD;
     const float r = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
-    const __nv_bfloat16* src = qkv + (long long)t * ld + (long long)hh * HD + lane * E;
-    const __nv_bfloat16* wgt = (is_q ? qw : kw) + lane * E;
+    float gv[8], xv[8], wv[8];
+    load8((is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) + sub * 8, gv);
+    load8(qkv + (long long)t * ld + (long long)hh * HD + sub * 8, xv);
+    load8((is_q ? qw : kw) + sub * 8, wv);
+    const bool lo = sub < TPH / 2;
     const int pos = t % seq;
-    const bool lo = lane < 16;
-    float dn[E];
+    const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
+    float dn[8];
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      const float gi = bf2f(g[lane * E + i]);
-      const float partner = __shfl_xor_sync(0xffffffffu, gi, 16);
-      const int j = (lane * E + i) % HALF;
-      const float2 c = cs[(long long)pos * HALF + j];
-      dn[i] = lo ? gi * c.x + partner * c.y : gi * c.x - partner * c.y;
+    for (int i = 0; i < 8; i += 2) {
+      const float4 c = c4[i / 2];
+      const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
+      const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
+      dn[i] = lo ? gv[i] * c.x + p0 * c.y : gv[i] * c.x - p0 * c.y;
+      dn[i + 1] = lo ? gv[i + 1] * c.z + p1 * c.w : gv[i + 1] * c.z - p1 * c.w;
     }
-    float xh[E], gx[E], dot = 0.f;
+    float dot = 0.f, gx[8];
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      xh[i] = bf2f(src[i]) * r;
-      gx[i] = dn[i] * bf2f(wgt[i]);
-      dot += gx[i] * xh[i];
-      if (is_q) accq[i] += dn[i] * xh[i]; else acck[i] += dn[i] * xh[i];
+    for (int i = 0; i < 8; ++i) {
+      xv[i] *= r;  // xhat
+      gx[i] = dn[i] * wv[i];
+      dot += gx[i] * xv[i];
+      if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
     }
-    const float mean = warp_sum(dot) / HD;
-    __nv_bfloat16* dst = dqkv + (long long)t * ldd + (long long)hh * HD + lane * E;
 #pragma unroll
-    for (int i = 0; i < E; ++i) dst[i] = f2bf(r * (gx[i] - xh[i] * mean));
+    for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float mean = dot / HD;
+    float out[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
+    store8(dqkv + (long long)t * ldd + (long long)hh * HD + sub * 8, out);
   }
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    atomicAdd(&sq[lane * E + i], accq[i]);
-    atomicAdd(&sk[lane * E + i], acck[i]);
+  for (int i = 0; i < 8; ++i) {
+    atomicAdd(&sq[my_sub * 8 + i], aq[i]);
+    atomicAdd(&sk[my_sub * 8 + i], ak[i]);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < HD; i += blockDim.x) {
@@ -504,16 +513,17 @@ RP_API int rp_rmsnorm_fwd(const void* x, int64_t ldx, const void* w, void* y, in
 RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
                           const float* dres, float* dx32, void* dx16, float* dw, int32_t rows,
                           int32_t h, void* stream) {
-  if (h % 8 || rows <= 0 || h > 256 * 8 * 4) return RP_E_INPUT;
+  if (h % 8 || rows <= 0 || h > 512 * 8 * 2) return RP_E_INPUT;
   const int grid = rows < 148 * 4 ? rows : 148 * 4;
-  if (h <= 256 * 8)
-    rmsnorm_bwd_kernel<256, 1><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd, dres,
-        dx32, (__nv_bfloat16*)dx16, dw, rows, h);
-  else
-    rmsnorm_bwd_kernel<256, 4><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd, dres,
-        dx32, (__nv_bfloat16*)dx16, dw, rows, h);
+  auto st = (cudaStream_t)stream;
+  auto args = [&](auto kern, int threads) {
+    kern<<<grid, threads, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                   (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
+                                   dw, rows, h);
+  };
+  if (h <= 256 * 8) args(rmsnorm_bwd_kernel<256, 1>, 256);
+  else if (h <= 512 * 8) args(rmsnorm_bwd_kernel<512, 1>, 512);
+  else args(rmsnorm_bwd_kernel<512, 2>, 512);
   return status();
 }
 
@@ -522,16 +532,17 @@ RP_API int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t 
                                const float* cos_sin, int32_t seq, void* q_out, void* k_out,
                                float* rstd_q, float* rstd_k, int32_t T, float eps,
                                void* stream) {
-  const long long warps = (long long)T * (nq + nk);
-  const int grid = (int)((warps + 7) / 8);
+  if (ld % 8 || T % 128) return RP_E_INPUT;
+  const long long threads = (long long)T * (nq + nk) * (head_dim / 8);
+  const int grid = grid_for(threads, 256, 148 * 16);
   auto s = (cudaStream_t)stream;
   if (head_dim == 128)
-    qk_norm_rope_fwd_kernel<4><<<grid, 256, 0, s>>>(
+    qk_norm_rope_fwd_kernel<128><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
   else if (head_dim == 64)
-    qk_norm_rope_fwd_kernel<2><<<grid, 256, 0, s>>>(
+    qk_norm_rope_fwd_kernel<64><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
@@ -545,15 +556,16 @@ RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, 
                                const void* kw, const float* rstd_q, const float* rstd_k,
                                const float* cos_sin, int32_t seq, void* dqkv, int64_t ldd,
                                float* dqw, float* dkw, int32_t T, void* stream) {
+  if (ld % 8 || ldd % 8 || T % 128) return RP_E_INPUT;
   auto s = (cudaStream_t)stream;
-  const int grid = 148 * 2;
+  const int grid = 148 * 4;  // grid*256 is a multiple of every TPH
   if (head_dim == 128)
-    qk_norm_rope_bwd_kernel<4><<<grid, 256, 0, s>>>(
+    qk_norm_rope_bwd_kernel<128><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
   else if (head_dim == 64)
-    qk_norm_rope_bwd_kernel<2><<<grid, 256, 0, s>>>(
+    qk_norm_rope_bwd_kernel<64><<<grid, 256, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);

@@ -48,6 +48,66 @@ struct Params {
   int vec;                 // 16-byte vector stores/loads legal for D (and R)
 };
 
+// Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok, int col0_,
+                                          const uint32_t (&v)[32]) {
+        const int col0 = col0_;
+        if (row_ok && col0 < p.N) {
+        const bool full_chunk = p.vec && col0 + 32 <= p.N;
+        if (EPI == EPI_BF16) {
+          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col0;
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
+          if (p.R) {
+            const __nv_bfloat16* r = p.R + (long long)row * p.ldr + col0;
+            if (full_chunk) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                uint4 rv = *reinterpret_cast<const uint4*>(r + i);
+                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[i + j] += __bfloat162float(rb[j]);
+              }
+            } else {
+              for (int i = 0; i < 32 && col0 + i < p.N; ++i) f[i] += __bfloat162float(r[i]);
+            }
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 o;
+              o.x = pack_bf16x2(f[i], f[i + 1]);
+              o.y = pack_bf16x2(f[i + 2], f[i + 3]);
+              o.z = pack_bf16x2(f[i + 4], f[i + 5]);
+              o.w = pack_bf16x2(f[i + 6], f[i + 7]);
+              *reinterpret_cast<uint4*>(d + i) = o;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) d[i] = __float2bfloat16_rn(f[i]);
+          }
+        } else {
+          float* d = reinterpret_cast<float*>(p.D) + (long long)row * p.ldd + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                     __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+              if (EPI == EPI_F32_ACC) {
+                const float4 old = *reinterpret_cast<const float4*>(d + i);
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              *reinterpret_cast<float4*>(d + i) = o;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+              d[i] = (EPI == EPI_F32_ACC ? d[i] : 0.f) + __uint_as_float(v[i]);
+          }
+        }
+        }
+}
+
 template <int A_MN, int B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
@@ -158,60 +218,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
         tmem_ld_wait();
-        const int col0 = n0 + c;
-        if (row_ok && col0 < p.N) {
-        const bool full_chunk = p.vec && col0 + 32 <= p.N;
-        if (EPI == EPI_BF16) {
-          __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col0;
-          float f[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(v[i]);
-          if (p.R) {
-            const __nv_bfloat16* r = p.R + (long long)row * p.ldr + col0;
-            if (full_chunk) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 8) {
-                uint4 rv = *reinterpret_cast<const uint4*>(r + i);
-                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) f[i + j] += __bfloat162float(rb[j]);
-              }
-            } else {
-              for (int i = 0; i < 32 && col0 + i < p.N; ++i) f[i] += __bfloat162float(r[i]);
-            }
-          }
-          if (full_chunk) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              uint4 o;
-              o.x = pack_bf16x2(f[i], f[i + 1]);
-              o.y = pack_bf16x2(f[i + 2], f[i + 3]);
-              o.z = pack_bf16x2(f[i + 4], f[i + 5]);
-              o.w = pack_bf16x2(f[i + 6], f[i + 7]);
-              *reinterpret_cast<uint4*>(d + i) = o;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) d[i] = __float2bfloat16_rn(f[i]);
-          }
-        } else {
-          float* d = reinterpret_cast<float*>(p.D) + (long long)row * p.ldd + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 o = make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
-                                     __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-              if (EPI == EPI_F32_ACC) {
-                const float4 old = *reinterpret_cast<const float4*>(d + i);
-                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-              }
-              *reinterpret_cast<float4*>(d + i) = o;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-              d[i] = (EPI == EPI_F32_ACC ? d[i] : 0.f) + __uint_as_float(v[i]);
-          }
-        }
-        }
+        epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -224,6 +231,207 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+// ---- 2-CTA (cta_group::2) variant ---------------------------------------------------
+// A CTA pair (cluster of 2 on one TPC) computes a 256x256 tile: CTA r loads
+// A rows [128r, 128r+128) and B columns [128r, 128r+128) of the tile (32 KB
+// per 64-deep stage instead of 48 KB), the leader issues
+// tcgen05.mma.cta_group::2 M256 N256 K16 reading both CTAs' shared memory,
+// and each CTA's TMEM receives its 128 rows. Both CTAs' TMA loads complete on
+// the leader's full barrier; MMA commits multicast to both CTAs' barriers;
+// epilogue warps of both CTAs release the accumulator on the leader's barrier.
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB
+constexpr int P_B_BYTES = 128 * BK * 2;     // 16 KB
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 int32_t c0, int32_t c1) {
+  // completes on the LEADER CTA's barrier (peer bit cleared)
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {  // arrive on both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // remote arrive on CTA 0
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int A_MN, int B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
+                     const __grid_constant__ CUtensorMap tma_b, Params p, int n_fastest) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* acc_full = empty + P_STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + BN - 1) / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = (p.K + BK - 1) / BK;
+  auto tile_mn = [&](int tile, int& m0, int& n0) {
+    const int mt = n_fastest ? tile / n_tiles : tile % m_tiles;
+    const int nt = n_fastest ? tile % n_tiles : tile / m_tiles;
+    m0 = mt * 256;
+    n0 = nt * BN;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tma_a);
+    tma_prefetch(&tma_b);
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_slot)),
+                 "n"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer (both CTAs; each loads its halves) ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      int m0, n0;
+      tile_mn(tile, m0, n0);
+      const int am = m0 + 128 * rank, bn = n0 + 128 * rank;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * P_STAGE_BYTES;
+        uint8_t* sb = sa + P_A_BYTES;
+        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+        const int k0 = kb * BK;
+        if (A_MN) {
+          tma_load_2d_pair(sa, &tma_a, &full[stage], am, k0);
+          tma_load_2d_pair(sa + 8192, &tma_a, &full[stage], am + 64, k0);
+        } else {
+          tma_load_2d_pair(sa, &tma_a, &full[stage], k0, am);
+        }
+        if (B_MN) {
+          tma_load_2d_pair(sb, &tma_b, &full[stage], bn, k0);
+          tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bn + 64, k0);
+        } else {
+          tma_load_2d_pair(sb, &tma_b, &full[stage], k0, bn);
+        }
+        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && leader) {
+    // ---------------- MMA issuer (leader only) ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(256, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t a_addr = smem_u32(smem + stage * P_STAGE_BYTES);
+        const uint32_t b_addr = a_addr + P_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint64_t ad = A_MN ? umma_desc_sw128(a_addr + kk * 2048, 8192, 1024)
+                                   : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+          const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
+                                   : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
+          umma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+        }
+        umma_commit_pair(&empty[stage]);
+        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+      }
+      umma_commit_pair(&acc_full[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (both CTAs, 128 rows each) ----------------
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      int m0, n0;
+      tile_mn(tile, m0, n0);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + 128 * rank + q * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+        tmem_ld_wait();
+        epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&acc_empty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "n"(TMEM_COLS)
+                 : "memory");
   }
 }
 
@@ -271,8 +479,22 @@ int num_sms() {
 }
 
 template <int A_MN, int B_MN, int EPI>
-cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                   cudaStream_t stream) {
+cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, bool pair,
+                   int n_fastest, cudaStream_t stream) {
+  if (pair) {
+    auto kern = gemm_pair_kernel<A_MN, B_MN, EPI>;
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           P_SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
+    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+    kern<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, p, n_fastest);
+    return cudaGetLastError();
+  }
   auto kern = gemm_kernel<A_MN, B_MN, EPI>;
   static bool configured = false;
   if (!configured) {
@@ -289,11 +511,11 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 
 template <int A_MN, int B_MN>
 cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                         cudaStream_t s) {
+                         bool pair, int n_fastest, cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, p, s);
-    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, p, s);
-    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, p, s);
+    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, p, pair, n_fastest, s);
+    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, p, pair, n_fastest, s);
+    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, p, pair, n_fastest, s);
   }
 }
 
@@ -308,11 +530,15 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
       (reinterpret_cast<uintptr_t>(g->B) & 15))
     return RP_E_INPUT;
+  // CTA pairs (cta_group::2, 256-row tiles) whenever M fills a pair tile
+  const bool pair = g->M >= 256;
   CUtensorMap ta, tb;
   bool ok = g->a_mn_major ? make_map(&ta, g->A, g->K, g->M, g->lda, 64, 64)
                           : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
   ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
-                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64, BN));
+                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64, pair ? 128 : BN));
+  // raster: keep the larger operand's tile hot (walk the other dimension fastest)
+  const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
   if (!ok) return RP_E_CUDA;
   const int esz = g->out_f32 ? 4 : 2;
   const bool vec = (g->ldd * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
@@ -324,8 +550,10 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (g->a_mn_major)
-    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, p, s) : dispatch_epi<1, 0>(epi, ta, tb, p, s);
+    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, p, pair, n_fastest, s)
+                      : dispatch_epi<1, 0>(epi, ta, tb, p, pair, n_fastest, s);
   else
-    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, p, s) : dispatch_epi<0, 0>(epi, ta, tb, p, s);
+    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, p, pair, n_fastest, s)
+                      : dispatch_epi<0, 0>(epi, ta, tb, p, pair, n_fastest, s);
   return e == cudaSuccess ? RP_OK : RP_E_CUDA;
 }
