@@ -90,14 +90,15 @@ int rp_attn_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const vo
 int rp_attn_fwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
                    int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
-/* Backward on the 5th-gen tensor cores: a key-major dK/dV kernel and a
- * query-major dQ kernel (recomputes S and dP; no atomics, deterministic).
- * delta: fp32 [nq, T] workspace. Layouts as rp_attn_bwd. */
+/* Backward on the 5th-gen tensor cores: a key-major dK/dV kernel (one CTA per
+ * key block and query head, GQA partials summed in fp32) and a query-major
+ * dQ kernel (recomputes S and dP; no dQ atomics). Workspaces: delta fp32
+ * [nq, T]; dkv_acc fp32 [2, T, nk*head_dim]. Layouts as rp_attn_bwd. */
 int rp_attn_bwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
                    const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                   int64_t lddv, float* delta, int32_t T, int32_t seq, int32_t nq, int32_t nk,
-                   int32_t head_dim, float scale, void* stream);
+                   int64_t lddv, float* delta, float* dkv_acc, int32_t T, int32_t seq,
+                   int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
 /* Backward: dq/dk/dv bf16 (same layouts as q/k/v, own pitches). Needs
  * workspace: dq_acc fp32 [T, nq, hd] and delta fp32 [nq, T]. */
 int rp_attn_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,

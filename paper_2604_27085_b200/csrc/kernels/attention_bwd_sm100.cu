@@ -1,17 +1,19 @@
 // Causal GQA flash-attention BACKWARD on the 5th-gen tensor cores (sm_100a),
-// as two deterministic kernels (no atomics):
+// as two kernels:
 //
-//  (A) dK/dV, key-major. CTA = 128 keys x 1 KV head; loops over the G query
-//      heads of the group and every query tile (64 queries) at or after the
-//      diagonal. Per tile: S^T = K Q^T and dP^T = V dO^T (tcgen05, M128 N64)
-//      into double-buffered TMEM; 4 softmax warps (thread = key row) form
-//      P^T = exp2(S^T*scale*log2e - lse*log2e) and dS^T = P^T (dP^T - delta)
-//      in bf16 smem; then dV += P^T dO and dK += dS^T Q (M128 N=hd K64)
-//      accumulate in TMEM for the whole loop. Epilogue: dK*scale, dV -> bf16.
+//  (A) dK/dV, key-major. CTA = 128 keys x 1 query head; loops over every query
+//      tile (64 queries) at or after the diagonal. Per tile: S^T = K Q^T and
+//      dP^T = V dO^T (tcgen05, M128 N64) into double-buffered TMEM; 4 softmax
+//      warps (thread = key row) form P^T = exp2(S^T*scale*log2e - lse*log2e)
+//      and dS^T = P^T (dP^T - delta) in bf16 smem; then dV += P^T dO and
+//      dK += dS^T Q (M128 N=hd K64) accumulate in TMEM for the whole loop.
+//      Epilogue: the G query heads of a KV group sum their partials into fp32
+//      (16-byte atomics; G adds per element), a cast kernel writes bf16.
 //  (B) dQ, query-major. CTA = 128 queries x 1 head; loops over key tiles
-//      (128 keys) up to the diagonal: S = Q K^T and dP = dO V^T (M128 N128)
-//      -> softmax warps (thread = query row) write dS to smem -> dQ += dS K
-//      (M128 N=hd K128, K as an MN-major operand). Epilogue: dQ*scale -> bf16.
+//      (64 keys) up to the diagonal: S = Q K^T and dP = dO V^T (M128 N64,
+//      double-buffered in TMEM) -> softmax warps (thread = query row) write
+//      dS to double-buffered smem -> dQ += dS K (M128 N=hd K64, K as an
+//      MN-major operand). Epilogue: dQ*scale -> bf16.
 // (B) recomputes S and dP instead of reducing dQ partials through atomics.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -49,19 +51,23 @@ struct DkvSmem {
   static constexpr int DO_OFF = NSUB * SUB64;         // dO after Q inside a stage
   static constexpr int PS = Q0 + 2 * STAGE;           // buffer b: P^T at PS + b*2*SUB128/2
   static constexpr int PS_BUF = 2 * (A_BK * A_BQ * 2);  // P^T + dS^T (16 KB each)
-  static constexpr int BAR = PS + 2 * PS_BUF;
+  static constexpr int LD = PS + 2 * PS_BUF;          // [2][2][A_BQ] lse*log2e, delta
+  static constexpr int BAR = LD + 2 * 2 * A_BQ * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
+// CTA = (128-key block, query head): the causal work per key block shrinks
+// linearly, so one CTA per (block, head) with the heaviest blocks first keeps
+// the ~7 waves balanced; the G heads of a KV group reduce their dK/dV
+// partials with 16-byte fp32 atomics into dk_acc / dv_acc.
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v,
                         const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
-                        const float* __restrict__ delta, bf16* __restrict__ dk, long long lddk,
-                        bf16* __restrict__ dv, long long lddv, int T, int seq, int nq, int nk,
-                        float scale) {
+                        const float* __restrict__ delta, float* __restrict__ dk_acc,
+                        float* __restrict__ dv_acc, int T, int seq, int nq, int nk, float scale) {
   using L = DkvSmem<HD>;
   constexpr int NSUB = L::NSUB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -79,12 +85,12 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kb = blockIdx.x, kvh = blockIdx.y;
+  const int kb = blockIdx.x, hq = blockIdx.y;
+  const int kvh = hq / (nq / nk);
   const int k0 = kb * A_BK;
   const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
-  const int G = nq / nk;
   const int nqt = (s_end - k0) / A_BQ;  // query tiles at/after the diagonal
-  const int iters = G * nqt;
+  const int iters = nqt;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_k);
@@ -96,8 +102,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
       mbar_init(&sd_full[i], 1);
-      mbar_init(&sd_free[i], 4);
-      mbar_init(&ps_full[i], 4);
+      mbar_init(&sd_free[i], 8);
+      mbar_init(&ps_full[i], 8);
       mbar_init(&ps_empty[i], 1);
     }
     mbar_init(acc_done, 1);
@@ -120,8 +126,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int it = 0; it < iters; ++it) {
       const int s = it & 1;
       mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-      const int hq = kvh * G + it / nqt;
-      const int qs = k0 + (it % nqt) * A_BQ;
+      const int qs = k0 + it * A_BQ;
       uint8_t* qd = sm + L::Q0 + s * L::STAGE;
       mbar_arrive_expect_tx(&q_full[s], L::STAGE);
       for (int sub = 0; sub < NSUB; ++sub) {
@@ -175,43 +180,49 @@ __global__ void __launch_bounds__(192, 1)
     }
     issue_grads(iters - 1);
     umma_commit(acc_done);
-  } else if (warp >= 2) {
-    const int quarter = warp & 3;
+  } else if (warp >= 4) {
+    // 8 softmax warps: lane quarter = warp % 4 (TMEM lanes = key rows), column
+    // half = (warp - 4) / 4 (32 of the tile's 64 queries each)
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // key row within the tile
     const int key = k0 + r;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const float sl2 = scale * kLog2e;
+    const int c0 = half * 32;
     for (int it = 0; it < iters; ++it) {
       const int b = it & 1;
-      const int hq = kvh * G + it / nqt;
-      const int qs = k0 + (it % nqt) * A_BQ;
-      const float* lse_t = lse + (long long)hq * T + qs;
-      const float* del_t = delta + (long long)hq * T + qs;
+      const int qs = k0 + it * A_BQ;
+      // stage this tile's 64 lse*log2e / delta values in smem (double-buffered)
+      float* lse_t = reinterpret_cast<float*>(sm + L::LD) + b * 2 * A_BQ;
+      float* del_t = lse_t + A_BQ;
+      const int st = threadIdx.x - 128;  // 0..255 across the softmax warps
+      if (st < A_BQ) lse_t[st] = lse[(long long)hq * T + qs + st] * kLog2e;
+      else if (st < 2 * A_BQ) del_t[st - A_BQ] = delta[(long long)hq * T + qs + st - A_BQ];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(&sd_full[b], (it >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[64], dpv[64];
-      tmem_ld_32x32b_x32(lane_base + b * 128, *reinterpret_cast<uint32_t(*)[32]>(sv));
-      tmem_ld_32x32b_x32(lane_base + b * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-      tmem_ld_32x32b_x32(lane_base + b * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(dpv));
-      tmem_ld_32x32b_x32(lane_base + b * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(dpv + 32));
+      uint32_t sv[32], dpv[32];
+      tmem_ld_32x32b_x32(lane_base + b * 128 + c0, sv);
+      tmem_ld_32x32b_x32(lane_base + b * 128 + 64 + c0, dpv);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sd_free[b]);
-      uint32_t pk[32], dk2[32];
-      const bool diag = qs < key + 1 && qs + A_BQ > k0;  // tile crosses this key block
+      uint32_t pk[16], dk2[16];
+      const bool diag = qs + A_BQ > k0 && qs < k0 + A_BK;  // tile crosses this key block
 #pragma unroll
-      for (int c = 0; c < A_BQ; c += 2) {
-        float p0 = ex2b(fmaf(__uint_as_float(sv[c]), sl2, -lse_t[c] * kLog2e));
-        float p1 = ex2b(fmaf(__uint_as_float(sv[c + 1]), sl2, -lse_t[c + 1] * kLog2e));
+      for (int i = 0; i < 32; i += 2) {
+        const int c = c0 + i;
+        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c]));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1]));
         if (diag) {
           if (qs + c < key) p0 = 0.f;
           if (qs + c + 1 < key) p1 = 0.f;
         }
-        const float d0 = p0 * (__uint_as_float(dpv[c]) - del_t[c]);
-        const float d1 = p1 * (__uint_as_float(dpv[c + 1]) - del_t[c + 1]);
-        pk[c / 2] = pack_bf16x2(p0, p1);
-        dk2[c / 2] = pack_bf16x2(d0, d1);
+        const float d0 = p0 * (__uint_as_float(dpv[i]) - del_t[c]);
+        const float d1 = p1 * (__uint_as_float(dpv[i + 1]) - del_t[c + 1]);
+        pk[i / 2] = pack_bf16x2(p0, p1);
+        dk2[i / 2] = pack_bf16x2(d0, d1);
       }
       if (it >= 2) {
         mbar_wait(&ps_empty[b], ((it >> 1) & 1) ^ 1);
@@ -220,42 +231,37 @@ __global__ void __launch_bounds__(192, 1)
       uint8_t* prow = sm + L::PS + b * L::PS_BUF + (r >> 3) * 1024 + (r & 7) * 128;
       uint8_t* drow = prow + A_BK * A_BQ * 2;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const int off = (ch ^ (r & 7)) << 4;
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int off = ((half * 4 + q4) ^ (r & 7)) << 4;
         *reinterpret_cast<uint4*>(prow + off) =
-            make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+            make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
         *reinterpret_cast<uint4*>(drow + off) =
-            make_uint4(dk2[ch * 4], dk2[ch * 4 + 1], dk2[ch * 4 + 2], dk2[ch * 4 + 3]);
+            make_uint4(dk2[q4 * 4], dk2[q4 * 4 + 1], dk2[q4 * 4 + 2], dk2[q4 * 4 + 3]);
       }
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps_full[b]);
     }
-    // epilogue: dK (scaled) and dV rows -> bf16
+    // epilogue: dK (scaled) and dV rows, reduced over the G heads in fp32
     mbar_wait(acc_done, 0);
     tc_fence_after();
-    bf16* dkr = dk + (long long)key * lddk + (long long)kvh * HD;
-    bf16* dvr = dv + (long long)key * lddv + (long long)kvh * HD;
+    float* dkr = dk_acc + (long long)key * nk * HD + (long long)kvh * HD;
+    float* dvr = dv_acc + (long long)key * nk * HD + (long long)kvh * HD;
 #pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
+    for (int c = half * (HD / 2); c < (half + 1) * (HD / 2); c += 32) {
       uint32_t a[32], v[32];
       tmem_ld_32x32b_x32(lane_base + TM_DK + c, a);
       tmem_ld_32x32b_x32(lane_base + TM_DV + c, v);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 u, w;
-        u.x = pack_bf16x2(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale);
-        u.y = pack_bf16x2(__uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale);
-        u.z = pack_bf16x2(__uint_as_float(a[i + 4]) * scale, __uint_as_float(a[i + 5]) * scale);
-        u.w = pack_bf16x2(__uint_as_float(a[i + 6]) * scale, __uint_as_float(a[i + 7]) * scale);
-        w.x = pack_bf16x2(__uint_as_float(v[i]), __uint_as_float(v[i + 1]));
-        w.y = pack_bf16x2(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-        w.z = pack_bf16x2(__uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
-        w.w = pack_bf16x2(__uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
-        *reinterpret_cast<uint4*>(dkr + c + i) = u;
-        *reinterpret_cast<uint4*>(dvr + c + i) = w;
+      for (int i = 0; i < 32; i += 4) {
+        atomicAdd(reinterpret_cast<float4*>(dkr + c + i),
+                  make_float4(__uint_as_float(a[i]) * scale, __uint_as_float(a[i + 1]) * scale,
+                              __uint_as_float(a[i + 2]) * scale, __uint_as_float(a[i + 3]) * scale));
+        atomicAdd(reinterpret_cast<float4*>(dvr + c + i),
+                  make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                              __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])));
       }
     }
   }
@@ -268,7 +274,12 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ======================================================================== (B) dQ
-constexpr int B_T = 128;  // queries per CTA and keys per tile
+// 128 queries per CTA, key tiles of 64 so that S and dP (64 TMEM columns
+// each) are double-buffered next to the dQ accumulator: the tensor core
+// computes S/dP of tile j+1 and dQ of tile j-1 while the softmax warps turn
+// tile j into dS.
+constexpr int B_Q = 128;  // queries per CTA
+constexpr int B_K = 64;   // keys per tile
 
 template <int HD>
 struct DqSmem {
@@ -276,14 +287,14 @@ struct DqSmem {
   static constexpr int Q = 0;
   static constexpr int DO = Q + NSUB * SUB128;
   static constexpr int KV0 = DO + NSUB * SUB128;     // stage s: K at KV0 + s*STAGE, V after
-  static constexpr int STAGE = 2 * NSUB * SUB128;
-  static constexpr int DS = KV0 + 2 * STAGE;         // dS [128 q][128 keys], 2 sub-tiles
+  static constexpr int STAGE = 2 * NSUB * SUB64;
+  static constexpr int DS = KV0 + 2 * STAGE;         // dS[b]: [128 q][64 keys] (16 KB)
   static constexpr int BAR = DS + 2 * SUB128;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k,
@@ -299,19 +310,20 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* q_full = bar + 0;
   uint64_t* kv_full = bar + 1;   // [2]
   uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* sd_full = bar + 5;
-  uint64_t* sd_free = bar + 6;
-  uint64_t* ds_full = bar + 7;
-  uint64_t* dq_done = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* sd_full = bar + 5;   // [2]
+  uint64_t* sd_free = bar + 7;   // [2]
+  uint64_t* ds_full = bar + 9;   // [2]
+  uint64_t* ds_free = bar + 11;  // [2]  (dQ MMA of the tile done reading dS[b])
+  uint64_t* dq_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qblocks = T / B_T;
+  const int qblocks = T / B_Q;
   const int qb = qblocks - 1 - blockIdx.x;
   const int h = blockIdx.y, kvh = h / (nq / nk);
-  const int q0 = qb * B_T;
+  const int q0 = qb * B_Q;
   const int s0 = (q0 / seq) * seq;
-  const int ntiles = (q0 - s0) / B_T + 1;
+  const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -322,10 +334,11 @@ __global__ void __launch_bounds__(192, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&sd_free[i], 8);
+      mbar_init(&ds_full[i], 8);
+      mbar_init(&ds_free[i], 1);
     }
-    mbar_init(sd_full, 1);
-    mbar_init(sd_free, 4);
-    mbar_init(ds_full, 4);
     mbar_init(dq_done, 1);
     fence_barrier_init();
   }
@@ -334,7 +347,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256;
+  // TMEM: S[b] at b*128, dP[b] at b*128 + 64 (64 cols each), dQ at 256
+  const uint32_t TM_DQ = 256;
 
   if (warp == 0 && lane == 0) {
     mbar_arrive_expect_tx(q_full, 2 * NSUB * SUB128);
@@ -345,100 +359,110 @@ __global__ void __launch_bounds__(192, 1)
     for (int j = 0; j < ntiles; ++j) {
       const int st = j & 1;
       mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-      const int k0 = s0 + j * B_T;
+      const int k0 = s0 + j * B_K;
       uint8_t* kd = sm + L::KV0 + st * L::STAGE;
       mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
       for (int sub = 0; sub < NSUB; ++sub) {
-        tma_load_2d(kd + sub * SUB128, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
-        tma_load_2d(kd + NSUB * SUB128 + sub * SUB128, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
+        tma_load_2d(kd + sub * SUB64, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
+        tma_load_2d(kd + NSUB * SUB64 + sub * SUB64, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
                     k0);
       }
     }
   } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(B_T, B_T, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(B_T, HD, 0, 1);
+    constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
     const uint32_t q_addr = smem_u32(sm + L::Q), do_addr = smem_u32(sm + L::DO);
-    const uint32_t ds_addr = smem_u32(sm + L::DS);
-    mbar_wait(q_full, 0);
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&kv_full[st], (j >> 1) & 1);
-      if (j >= 1) mbar_wait(sd_free, (j - 1) & 1);
+    auto issue_dq = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&ds_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + st * L::STAGE);
-      const uint32_t v_addr = k_addr + NSUB * SUB128;
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + b * L::STAGE);
+      const uint32_t ds_addr = smem_u32(sm + L::DS + b * SUB128);
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t o = (kk >> 2) * SUB128 + (kk & 3) * 32;
-        umma_f16(tmem + TM_S, umma_desc_sw128(q_addr + o, 16, 1024),
-                 umma_desc_sw128(k_addr + o, 16, 1024), idesc_s, kk != 0);
-        umma_f16(tmem + TM_DP, umma_desc_sw128(do_addr + o, 16, 1024),
-                 umma_desc_sw128(v_addr + o, 16, 1024), idesc_s, kk != 0);
-      }
-      umma_commit(sd_full);
-      mbar_wait(ds_full, j & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < B_T / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(ds_addr + (kk >> 2) * SUB128 + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB128, 1024);
+      for (int kk = 0; kk < B_K / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
         umma_f16(tmem + TM_DQ, ad, bd, idesc_q, (j | kk) != 0);
       }
-      umma_commit(dq_done);
-      umma_commit(&kv_empty[st]);
+      umma_commit(&ds_free[b]);
+      umma_commit(&kv_empty[b]);
+    };
+    mbar_wait(q_full, 0);
+    for (int j = 0; j < ntiles; ++j) {
+      const int b = j & 1;
+      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      if (j >= 2) mbar_wait(&sd_free[b], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + b * L::STAGE);
+      const uint32_t v_addr = k_addr + NSUB * SUB64;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
+        const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
+        umma_f16(tmem + b * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
+                 umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
+        umma_f16(tmem + b * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
+                 umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(&sd_full[b]);
+      if (j >= 1) issue_dq(j - 1);
     }
-  } else if (warp >= 2) {
-    const int quarter = warp & 3;
+    issue_dq(ntiles - 1);
+    umma_commit(dq_done);
+  } else if (warp >= 4) {
+    // 8 softmax warps: lane quarter = warp % 4 (query rows), key half = (warp-4)/4
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // query row
     const int qrow = q0 + r;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const float sl2 = scale * kLog2e;
     const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
     const float dl = delta[(long long)h * T + qrow];
-    uint8_t* ds_row = sm + L::DS + (r >> 3) * 1024 + (r & 7) * 128;
+    const int c0 = half * 32;
     for (int j = 0; j < ntiles; ++j) {
-      mbar_wait(sd_full, j & 1);
+      const int b = j & 1;
+      mbar_wait(&sd_full[b], (j >> 1) & 1);
       tc_fence_after();
-      if (j >= 1) mbar_wait(dq_done, (j - 1) & 1);  // previous dQ MMA done reading dS
-      const bool diag = j == ntiles - 1;
-#pragma unroll 1
-      for (int c = 0; c < B_T; c += 32) {
-        uint32_t sv[32], dpv[32];
-        tmem_ld_32x32b_x32(lane_base + TM_S + c, sv);
-        tmem_ld_32x32b_x32(lane_base + TM_DP + c, dpv);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
-          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
-          if (diag) {
-            if (c + i > r) p0 = 0.f;
-            if (c + i + 1 > r) p1 = 0.f;
-          }
-          pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
-                                  p1 * (__uint_as_float(dpv[i + 1]) - dl));
-        }
-        const int sub = c >> 6;
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int ch = ((c & 63) >> 3) + q4;
-          *reinterpret_cast<uint4*>(ds_row + sub * SUB128 + ((ch ^ (r & 7)) << 4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-        }
-      }
+      uint32_t sv[32], dpv[32];
+      tmem_ld_32x32b_x32(lane_base + b * 128 + c0, sv);
+      tmem_ld_32x32b_x32(lane_base + b * 128 + 64 + c0, dpv);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(sd_free);
+      if (lane == 0) mbar_arrive(&sd_free[b]);
+      const int kbase = s0 + j * B_K + c0;  // first key of this thread's columns
+      const bool diag = kbase + 31 > q0;
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
+        if (diag) {
+          if (kbase + i > qrow) p0 = 0.f;
+          if (kbase + i + 1 > qrow) p1 = 0.f;
+        }
+        pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
+                                p1 * (__uint_as_float(dpv[i + 1]) - dl));
+      }
+      if (j >= 2) {  // dQ MMA of tile j-2 done reading dS[b]
+        mbar_wait(&ds_free[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+      }
+      uint8_t* ds_row = sm + L::DS + b * SUB128 + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        *reinterpret_cast<uint4*>(ds_row + (((half * 4 + q4) ^ (r & 7)) << 4)) =
+            make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
       fence_proxy_async();
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
+      if (lane == 0) mbar_arrive(&ds_full[b]);
     }
-    mbar_wait(dq_done, (ntiles - 1) & 1);
+    mbar_wait(dq_done, 0);
     tc_fence_after();
     bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
 #pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
+    for (int c = half * (HD / 2); c < (half + 1) * (HD / 2); c += 32) {
       uint32_t v[32];
       tmem_ld_32x32b_x32(lane_base + TM_DQ + c, v);
       tmem_ld_wait();
@@ -483,6 +507,27 @@ __global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf
   if (lane == 0) delta[(long long)h * T + t] = acc;
 }
 
+// dk/dv (bf16, strided) = dk_acc/dv_acc (fp32 [T, nk*HD])
+__global__ void dkv_cast_kernel(const float* __restrict__ dka, const float* __restrict__ dva,
+                                bf16* __restrict__ dk, long long lddk, bf16* __restrict__ dv,
+                                long long lddv, int T, int cols) {
+  const long long n4 = (long long)T * cols / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i * 4, t = e / cols;
+    const int c = (int)(e % cols);
+    const float4 a = reinterpret_cast<const float4*>(dka)[i];
+    const float4 b = reinterpret_cast<const float4*>(dva)[i];
+    uint2 ua, ub;
+    ua.x = pack_bf16x2(a.x, a.y);
+    ua.y = pack_bf16x2(a.z, a.w);
+    ub.x = pack_bf16x2(b.x, b.y);
+    ub.y = pack_bf16x2(b.z, b.w);
+    *reinterpret_cast<uint2*>(dk + t * lddk + c) = ua;
+    *reinterpret_cast<uint2*>(dv + t * lddv + c) = ub;
+  }
+}
+
 // ---- host ------------------------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -520,8 +565,8 @@ template <int HD>
 int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const void* v,
            long long ldv, const void* o, long long ldo, const void* dout, long long lddo,
            const float* lse, void* dq, long long lddq, void* dk, long long lddk, void* dv,
-           long long lddv, float* delta, int T, int seq, int nq, int nk, float scale,
-           cudaStream_t s) {
+           long long lddv, float* delta, float* dkv_acc, int T, int seq, int nq, int nk,
+           float scale, cudaStream_t s) {
   const long long warps = (long long)T * nq;
   delta_kernel<HD><<<(int)((warps + 7) / 8), 256, 0, s>>>((const bf16*)o, ldo, (const bf16*)dout,
                                                          lddo, delta, T, nq);
@@ -540,11 +585,18 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       return RP_E_CUDA;
     cfg = true;
   }
-  attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nk), 192, DkvSmem<HD>::BYTES, s>>>(
-      mk128, mv128, mq64, mdo64, lse, delta, (bf16*)dk, lddk, (bf16*)dv, lddv, T, seq, nq, nk,
-      scale);
-  attn_bwd_dq_kernel<HD><<<dim3(T / B_T, nq), 192, DqSmem<HD>::BYTES, s>>>(
-      mq128, mdo128, mk128, mv128, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
+  const long long acc_n = (long long)T * nk * HD;
+  if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
+  attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nq), 384, DkvSmem<HD>::BYTES, s>>>(
+      mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
+  dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
+                                          lddv, T, nk * HD);
+  CUtensorMap mk64, mv64;
+  if (!map2d(&mk64, k, T, (long long)nk * HD, ldk, 64) ||
+      !map2d(&mv64, v, T, (long long)nk * HD, ldv, 64))
+    return RP_E_CUDA;
+  attn_bwd_dq_kernel<HD><<<dim3(T / B_Q, nq), 384, DqSmem<HD>::BYTES, s>>>(
+      mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
 }
 
@@ -556,14 +608,14 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
 extern "C" __attribute__((visibility("default"))) int rp_attn_bwd_tc(
     const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
     const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse, void* dq,
-    int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta, int32_t T,
-    int32_t seq, int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream) {
+    int64_t lddq, void* dk, int64_t lddk, void* dv, int64_t lddv, float* delta, float* dkv_acc,
+    int32_t T, int32_t seq, int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream) {
   if (T <= 0 || seq % 128 || T % seq || nk <= 0 || nq % nk || (head_dim != 64 && head_dim != 128))
     return RP_E_INPUT;
   auto s = (cudaStream_t)stream;
   return head_dim == 128
              ? rp::bwd_tc<128>(q, ldq, k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk,
-                               dv, lddv, delta, T, seq, nq, nk, scale, s)
+                               dv, lddv, delta, dkv_acc, T, seq, nq, nk, scale, s)
              : rp::bwd_tc<64>(q, ldq, k, ldk, v, ldv, o, ldo, dout, lddo, lse, dq, lddq, dk, lddk,
-                              dv, lddv, delta, T, seq, nq, nk, scale, s);
+                              dv, lddv, delta, dkv_acc, T, seq, nq, nk, scale, s);
 }

@@ -731,7 +731,8 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_attn_bwd_tc(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, G.dattn, qd, A.lse,
-                      G.dq_t, qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.delta, T, cfg.seq_len,
+                      G.dq_t, qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.delta, G.dq_acc, T,
+                      cfg.seq_len,
                       s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
     prof_end(pi_, st, 1, 5.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }
