@@ -40,6 +40,10 @@ constexpr int A_BK = 128;                 // keys per CTA
 constexpr int A_BQ = 64;                  // queries per tile
 constexpr int SUB128 = 128 * 128;         // 128 rows x 64 bf16 (16 KB)
 constexpr int SUB64 = 64 * 128;           // 64 rows x 64 bf16 (8 KB)
+// Operand rings are 3 deep: a stage is released only after the gradient MMA
+// of its tile, and with 2 stages the next S/dP MMA would wait a full TMA
+// round trip behind that release on every tile.
+constexpr int NST = 3;
 
 template <int HD>
 struct DkvSmem {
@@ -49,11 +53,12 @@ struct DkvSmem {
   static constexpr int Q0 = V + NSUB * SUB128;        // stage s: Q at Q0 + s*STAGE
   static constexpr int STAGE = 2 * NSUB * SUB64;      // Q + dO of one query tile
   static constexpr int DO_OFF = NSUB * SUB64;         // dO after Q inside a stage
-  static constexpr int PS = Q0 + 2 * STAGE;           // buffer b: P^T at PS + b*2*SUB128/2
+  static constexpr int PS = Q0 + NST * STAGE;         // buffer b: P^T at PS + b*PS_BUF
   static constexpr int PS_BUF = 2 * (A_BK * A_BQ * 2);  // P^T + dS^T (16 KB each)
-  static constexpr int LD = PS + 2 * PS_BUF;          // [2][2][A_BQ] lse*log2e, delta
-  static constexpr int BAR = LD + 2 * 2 * A_BQ * 4;
+  static constexpr int LD = PS + 2 * PS_BUF;          // [NST][2][A_BQ] lse, delta
+  static constexpr int BAR = LD + NST * 2 * A_BQ * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
 
 // CTA = (128-key block, query head): the causal work per key block shrinks
@@ -75,14 +80,14 @@ __global__ void __launch_bounds__(384, 1)
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;    // [2]
-  uint64_t* q_empty = bar + 3;   // [2]
-  uint64_t* sd_full = bar + 5;   // [2]
-  uint64_t* sd_free = bar + 7;   // [2]
-  uint64_t* ps_full = bar + 9;   // [2]
-  uint64_t* ps_empty = bar + 11; // [2]
-  uint64_t* acc_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* q_full = bar + 1;    // [NST]
+  uint64_t* q_empty = bar + 4;   // [NST]
+  uint64_t* sd_full = bar + 7;   // [2]
+  uint64_t* sd_free = bar + 9;   // [2]
+  uint64_t* ps_full = bar + 11;  // [2]
+  uint64_t* ps_empty = bar + 13; // [2]
+  uint64_t* acc_done = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kb = blockIdx.x, hq = blockIdx.y;
@@ -98,9 +103,11 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&sd_free[i], 8);
       mbar_init(&ps_full[i], 8);
@@ -124,22 +131,25 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(sm + L::V + sub * SUB128, &tm_v, kv_full, kvh * HD + 64 * sub, k0);
     }
     for (int it = 0; it < iters; ++it) {
-      const int s = it & 1;
-      mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
+      const int s = it % NST;
+      mbar_wait(&q_empty[s], ((it / NST) & 1) ^ 1);
       const int qs = k0 + it * A_BQ;
       uint8_t* qd = sm + L::Q0 + s * L::STAGE;
-      mbar_arrive_expect_tx(&q_full[s], L::STAGE);
+      mbar_arrive_expect_tx(&q_full[s], L::STAGE + 2 * A_BQ * 4);
       for (int sub = 0; sub < NSUB; ++sub) {
         tma_load_2d(qd + sub * SUB64, &tm_q, &q_full[s], hq * HD + 64 * sub, qs);
         tma_load_2d(qd + L::DO_OFF + sub * SUB64, &tm_do, &q_full[s], hq * HD + 64 * sub, qs);
       }
+      float* ld = reinterpret_cast<float*>(sm + L::LD) + s * 2 * A_BQ;
+      bulk_load_1d(ld, lse + (long long)hq * T + qs, A_BQ * 4, &q_full[s]);
+      bulk_load_1d(ld + A_BQ, delta + (long long)hq * T + qs, A_BQ * 4, &q_full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A_BQ, 0, 0);   // K-major x K-major
     constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);     // K-major x MN-major
     const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
     auto issue_grads = [&](int it) {
-      const int s = it & 1, b = it & 1;
+      const int s = it % NST, b = it & 1;
       mbar_wait(&ps_full[b], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t q_addr = smem_u32(sm + L::Q0 + s * L::STAGE);
@@ -160,8 +170,8 @@ __global__ void __launch_bounds__(384, 1)
     };
     mbar_wait(kv_full, 0);
     for (int it = 0; it < iters; ++it) {
-      const int s = it & 1, b = it & 1;
-      mbar_wait(&q_full[s], (it >> 1) & 1);
+      const int s = it % NST, b = it & 1;
+      mbar_wait(&q_full[s], (it / NST) & 1);
       if (it >= 2) mbar_wait(&sd_free[b], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t q_addr = smem_u32(sm + L::Q0 + s * L::STAGE);
@@ -192,13 +202,12 @@ __global__ void __launch_bounds__(384, 1)
     for (int it = 0; it < iters; ++it) {
       const int b = it & 1;
       const int qs = k0 + it * A_BQ;
-      // stage this tile's 64 lse*log2e / delta values in smem (double-buffered)
-      float* lse_t = reinterpret_cast<float*>(sm + L::LD) + b * 2 * A_BQ;
-      float* del_t = lse_t + A_BQ;
-      const int st = threadIdx.x - 128;  // 0..255 across the softmax warps
-      if (st < A_BQ) lse_t[st] = lse[(long long)hq * T + qs + st] * kLog2e;
-      else if (st < 2 * A_BQ) del_t[st - A_BQ] = delta[(long long)hq * T + qs + st - A_BQ];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // lse / delta of this tile arrive with its Q stage; the stage is only
+      // refilled after this tile's gradient MMAs, i.e. after ps_full
+      const int s = it % NST;
+      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + s * 2 * A_BQ;
+      const float* del_t = lse_t + A_BQ;
+      mbar_wait(&q_full[s], (it / NST) & 1);  // lse/delta visibility (already complete)
       mbar_wait(&sd_full[b], (it >> 1) & 1);
       tc_fence_after();
       uint32_t sv[32], dpv[32];
@@ -213,8 +222,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const int c = c0 + i;
-        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c]));
-        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1]));
+        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c] * kLog2e));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1] * kLog2e));
         if (diag) {
           if (qs + c < key) p0 = 0.f;
           if (qs + c + 1 < key) p1 = 0.f;
@@ -288,9 +297,10 @@ struct DqSmem {
   static constexpr int DO = Q + NSUB * SUB128;
   static constexpr int KV0 = DO + NSUB * SUB128;     // stage s: K at KV0 + s*STAGE, V after
   static constexpr int STAGE = 2 * NSUB * SUB64;
-  static constexpr int DS = KV0 + 2 * STAGE;         // dS[b]: [128 q][64 keys] (16 KB)
+  static constexpr int DS = KV0 + NST * STAGE;       // dS[b]: [128 q][64 keys] (16 KB)
   static constexpr int BAR = DS + 2 * SUB128;
   static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
 
 template <int HD>
@@ -308,14 +318,14 @@ __global__ void __launch_bounds__(384, 1)
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* sd_full = bar + 5;   // [2]
-  uint64_t* sd_free = bar + 7;   // [2]
-  uint64_t* ds_full = bar + 9;   // [2]
-  uint64_t* ds_free = bar + 11;  // [2]  (dQ MMA of the tile done reading dS[b])
-  uint64_t* dq_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* kv_full = bar + 1;   // [NST]
+  uint64_t* kv_empty = bar + 4;  // [NST]
+  uint64_t* sd_full = bar + 7;   // [2]
+  uint64_t* sd_free = bar + 9;   // [2]
+  uint64_t* ds_full = bar + 11;  // [2]
+  uint64_t* ds_free = bar + 13;  // [2]  (dQ MMA of the tile done reading dS[b])
+  uint64_t* dq_done = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / B_Q;
@@ -331,9 +341,11 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&sd_free[i], 8);
       mbar_init(&ds_full[i], 8);
@@ -357,8 +369,8 @@ __global__ void __launch_bounds__(384, 1)
       tma_load_2d(sm + L::DO + sub * SUB128, &tm_do, q_full, h * HD + 64 * sub, q0);
     }
     for (int j = 0; j < ntiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+      const int st = j % NST;
+      mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
       const int k0 = s0 + j * B_K;
       uint8_t* kd = sm + L::KV0 + st * L::STAGE;
       mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(384, 1)
       const int b = j & 1;
       mbar_wait(&ds_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + b * L::STAGE);
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % NST) * L::STAGE);
       const uint32_t ds_addr = smem_u32(sm + L::DS + b * SUB128);
 #pragma unroll
       for (int kk = 0; kk < B_K / 16; ++kk) {
@@ -385,15 +397,15 @@ __global__ void __launch_bounds__(384, 1)
         umma_f16(tmem + TM_DQ, ad, bd, idesc_q, (j | kk) != 0);
       }
       umma_commit(&ds_free[b]);
-      umma_commit(&kv_empty[b]);
+      umma_commit(&kv_empty[j % NST]);
     };
     mbar_wait(q_full, 0);
     for (int j = 0; j < ntiles; ++j) {
       const int b = j & 1;
-      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      mbar_wait(&kv_full[j % NST], (j / NST) & 1);
       if (j >= 2) mbar_wait(&sd_free[b], ((j >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + b * L::STAGE);
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % NST) * L::STAGE);
       const uint32_t v_addr = k_addr + NSUB * SUB64;
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {

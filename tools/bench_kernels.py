@@ -48,6 +48,10 @@ def main():
                                      delta, seq, nq, nk, hd))
     out.append({"kernel": "attn_bwd_tc", "ms": ms, "tflops": 2.5 * flops / ms / 1e9,
                 "executed_tflops": 3.5 * flops / ms / 1e9})
+    if "attn" in sys.argv[1:]:
+        for r in out:
+            print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
+        return
 
     x = torch.randn(T, h, device="cuda").to(torch.bfloat16)
     w = torch.ones(h, device="cuda", dtype=torch.bfloat16)
