@@ -37,11 +37,14 @@ $(LIB): $(OBJS)
 REF_INC := /root/reference/proj/include
 NLOHMANN := $(shell python3 -c "import site,os;print(next((os.path.join(p,'include/cudnn_frontend/thirdparty/nlohmann') for p in site.getsitepackages() if os.path.isdir(os.path.join(p,'include/cudnn_frontend/thirdparty/nlohmann'))),''))" 2>/dev/null)
 REF_SO := oracle/_ref/libref_planner.so
+# the system g++ links libstdc++ dynamically (a static copy next to the
+# product's dynamic one breaks iostreams/locales inside one process)
+ORACLE_CXX ?= $(if $(wildcard /usr/bin/g++),/usr/bin/g++,$(CXX))
 
 oracle: $(REF_SO)
 $(REF_SO): oracle/ref_planner_shim.cpp $(PKG)/csrc/planner/cabi_planner.inc include/rp/cabi.h
 	@mkdir -p oracle/_ref
-	$(CXX) -std=c++20 -O2 -fPIC -shared -fvisibility=hidden -fvisibility-inlines-hidden -Wl,-Bsymbolic -I$(REF_INC) -I$(NLOHMANN) -Iinclude \
+	$(ORACLE_CXX) -std=c++20 -O2 -fPIC -shared -fvisibility=hidden -fvisibility-inlines-hidden -Wl,-Bsymbolic -I$(REF_INC) -I$(NLOHMANN) -Iinclude \
 	  -DROUNDPIPE_CONFIG_DIR=\"/root/reference/proj/configs\" $< -o $@
 
 clean:

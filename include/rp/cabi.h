@@ -192,6 +192,17 @@ int rp_interior_bubble(const rp_timed_event_t* events, int64_t n,
 
 /* transfer_planner::plan (transfer_planner.hpp:73). ids[i] are the tensor ids
  * (ordering key), out[] lists chunks window by window in placement order. */
+/* svg::render_gantt (svg.hpp:26) of a simulated or measured timeline;
+ * slot_kinds: 0 fwd, 1 fused, 2 bwd (optional legend). NUL-terminated SVG
+ * into out; cap 0 = size query, *len = length without the NUL. */
+int rp_render_gantt(const rp_timed_event_t* events, int64_t n, int32_t num_gpus,
+                    const int32_t* slot_kinds, const rp_layer_range_t* slot_layers,
+                    int32_t n_slots, int32_t width, char* out, int64_t cap, int64_t* len);
+
+/* SimReport scalars (simulator.hpp:134-151) over a measured timeline. */
+int rp_timeline_report(const rp_timed_event_t* events, int64_t n, int32_t num_gpus,
+                       rp_sim_report_t* report, int64_t* busy_per_gpu);
+
 int rp_transfer_plan(const char* const* ids, const int64_t* bytes,
                      const int32_t* directions, int32_t n_items,
                      int32_t num_windows, int64_t max_chunk_bytes,

@@ -106,6 +106,14 @@ const char* rp_runtime_last_error(void);
  * algorithmic work and launch count. */
 int rp_runtime_profile(rp_runtime_t* rt, int32_t enable);
 int rp_runtime_profile_read(rp_runtime_t* rt, double* time_ms, double* work, int64_t* launches);
+/* Per-launch records of the profiled steps (same clock as rp_timeline):
+ * category as above, worker, lane (0 compute stream, 1 optimizer stream). */
+typedef struct {
+  int32_t cat, worker, lane, pad;
+  int64_t start_ns, end_ns;
+  double work;
+} rp_prof_record_t;
+int rp_runtime_profile_records(rp_runtime_t* rt, rp_prof_record_t* out, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -192,6 +192,7 @@ struct Runtime {
     int cat;
     cudaEvent_t a, b;
     double work;
+    int worker, lane;  // lane 0 = compute stream, 1 = optimizer stream
   };
   bool prof_on = false;
   std::vector<ProfRec> prof;
@@ -203,7 +204,12 @@ struct Runtime {
   }
   int prof_begin(cudaStream_t st) {
     if (!prof_on) return -1;
-    ProfRec r{0, prof_event(), prof_event(), 0.0};
+    ProfRec r{0, prof_event(), prof_event(), 0.0, 0, 0};
+    for (const Gpu& G : gpus)
+      if (G.compute == st || G.opt_comp == st) {
+        r.worker = G.id;
+        r.lane = G.opt_comp == st;
+      }
     RP_CUDA(cudaEventRecord(r.a, st));
     prof.push_back(r);
     return (int)prof.size() - 1;
@@ -1362,6 +1368,30 @@ RP_API int rp_runtime_profile_read(rp_runtime_t* p, double* time_ms, double* wor
       time_ms[r.cat] += ms;
       work[r.cat] += r.work;
       launches[r.cat] += 1;
+    }
+  });
+}
+
+// Per-launch records of the profiled steps (same clock as rp_timeline).
+RP_API int rp_runtime_profile_records(rp_runtime_t* p, rp_prof_record_t* out, int64_t cap,
+                                      int64_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    *n = (int64_t)rt->prof.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "profile record capacity");
+    std::vector<cudaEvent_t> anchor(rt->ndev, nullptr);
+    for (auto& G : rt->gpus)
+      if (!anchor[G.dev]) anchor[G.dev] = G.anchor;
+    for (int64_t i = 0; i < *n; ++i) {
+      const auto& r = rt->prof[(std::size_t)i];
+      const int dev = rt->gpus[r.worker].dev;
+      float a = 0.f, b = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&a, anchor[dev], r.a));
+      RP_CUDA(cudaEventElapsedTime(&b, anchor[dev], r.b));
+      out[i] = rp_prof_record_t{r.cat, r.worker, r.lane, 0,
+                                (int64_t)std::llround((double)a * 1e6),
+                                (int64_t)std::llround((double)b * 1e6), r.work};
     }
   });
 }

@@ -387,6 +387,34 @@ class Planner:
                    C.byref(den), C.byref(r))
         return r.value, num.value, den.value
 
+    # -- reporting (measured or simulated timelines) -------------------------------
+    def timeline_report(self, timeline: np.ndarray, num_gpus: int) -> SimReport:
+        """SimReport scalars over a measured timeline (simulator.hpp:134-151)."""
+        ev = np.ascontiguousarray(timeline, dtype=EVENT_DTYPE)
+        rep = SimReportC()
+        busy = np.zeros(num_gpus, dtype=np.int64)
+        self._call("timeline_report", ev.ctypes.data_as(C.c_void_p), I64(len(ev)),
+                   I32(num_gpus), C.byref(rep), busy.ctypes.data_as(P(I64)))
+        return SimReport(rep.makespan_ns, rep.span_ns, rep.busy_total_ns, busy.tolist(),
+                         rep.bubble_num, rep.bubble_den, rep.bubble_ratio, ev)
+
+    def render_gantt(self, timeline: np.ndarray, num_gpus: int,
+                     plan: Optional[StagePlan] = None, width: int = 1200) -> str:
+        """svg::render_gantt (svg.hpp:26): one lane per GPU, colour per slot."""
+        ev = np.ascontiguousarray(timeline, dtype=EVENT_DTYPE)
+        sl = plan.slots() if plan is not None else []
+        kinds = np.asarray([{"fwd": 0, "fused": 1, "bwd": 2}[k] for k, _ in sl] or [0],
+                           dtype=np.int32)
+        rng = (RangeC * max(len(sl), 1))(*[RangeC(r.first, r.last) for _, r in sl])
+        n = I64()
+        args = (ev.ctypes.data_as(C.c_void_p), I64(len(ev)), I32(num_gpus),
+                kinds.ctypes.data_as(P(I32)), rng, I32(len(sl)), I32(width))
+        self._call("render_gantt", *args, None, I64(0), C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        self._call("render_gantt", *args, buf, I64(n.value + 1), C.byref(n))
+        return buf.value.decode()
+
+
     # -- transfer planner --------------------------------------------------------
     def plan(self, items: Sequence[tuple], num_windows: int,
              max_chunk_bytes: int = 0) -> TransferPlan:
@@ -480,3 +508,18 @@ class Planner:
 
 def planner() -> Planner:
     return Planner()
+
+
+def report_json(rep: SimReport, num_gpus: int) -> dict:
+    """The reference CLI's report schema (proj/tools/roundpipe.cpp:70-90) for a
+    simulated or measured SimReport."""
+    tl = rep.timeline
+    return {
+        "makespan_ns": int(rep.makespan_ns), "span_ns": int(rep.span_ns),
+        "bubble_ratio": float(rep.bubble_ratio), "bubble_num": int(rep.bubble_num),
+        "bubble_den": int(rep.bubble_den),
+        "gpus": [{"id": g, "busy_ns": int(rep.busy_per_gpu_ns[g])} for g in range(num_gpus)],
+        "events": [{"iter": int(e["iteration"]), "round": int(e["round"]),
+                    "slot": int(e["slot"]), "mb": int(e["mb"]), "gpu": int(e["gpu"]),
+                    "start_ns": int(e["start_ns"]), "end_ns": int(e["end_ns"])} for e in tl],
+    }

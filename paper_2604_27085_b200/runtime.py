@@ -233,3 +233,16 @@ class RoundPipe:
         self._call("rp_runtime_profile_read", self.h, t, w, n)
         return {c: {"ms": t[i], "work": w[i], "launches": n[i]}
                 for i, c in enumerate(self.PROFILE_CATEGORIES)}
+
+    PROF_DTYPE = np.dtype([("cat", "<i4"), ("worker", "<i4"), ("lane", "<i4"), ("pad", "<i4"),
+                           ("start_ns", "<i8"), ("end_ns", "<i8"), ("work", "<f8")])
+
+    def profile_records(self) -> np.ndarray:
+        """Per-launch (category, worker, lane, start_ns, end_ns, work) of the
+        profiled steps; lane 0 = compute stream, 1 = optimizer stream."""
+        n = I64()
+        cap = 1 << 20
+        rec = np.zeros(cap, dtype=self.PROF_DTYPE)
+        self._call("rp_runtime_profile_records", self.h, rec.ctypes.data_as(VP), I64(cap),
+                   C.byref(n))
+        return rec[: n.value].copy()

@@ -299,3 +299,35 @@ def test_cost_tables_bundled_models(product, oracle):
             for head in (False, True):
                 assert np.array_equal(product.layer_costs(m, s, b, g, head),
                                       oracle.layer_costs(m, s, b, g, head))
+
+
+def test_gantt_and_measured_report(product, oracle):
+    """svg::render_gantt of simulated and 'measured' (jittered) timelines is
+    byte-identical to the reference's; the measured-timeline report equals
+    simulate()'s scalars on a simulated timeline (simulator.hpp:134-151)."""
+    from paper_2604_27085_b200.planner import report_json
+    rng = random.Random(55)
+    for trial in range(12):
+        N = rng.randint(1, 6)
+        L = rng.randint(2, 12)
+        c = rand_costs(rng, L + 1, head=True)
+        M = N * rng.randint(1, 3)
+        plan = product.optimal_partition(c, N, M)
+        durs = product.slot_durations(plan, c)
+        s = product.synthesize("roundpipe", N, M, 0, 3, durs)
+        rep = product.simulate(s)
+        tl = rep.timeline.copy()
+        if trial % 2:  # measured timelines start late / stretch / shrink
+            tl["start_ns"] += rng.randint(0, 50)
+            tl["end_ns"] = tl["start_ns"] + (tl["dur_ns"] * rng.uniform(0.8, 1.3)).astype(np.int64)
+        for p in (None, plan):
+            a = product.render_gantt(tl, N, p, width=900)
+            assert a == oracle.render_gantt(tl, N, p, width=900)
+            assert a.startswith("<svg") and a.count("<rect") >= len(tl)
+        mr = product.timeline_report(rep.timeline, N)
+        assert (mr.makespan_ns, mr.span_ns, mr.busy_total_ns, mr.bubble_num, mr.bubble_den,
+                mr.bubble_ratio, mr.busy_per_gpu_ns) == \
+            (rep.makespan_ns, rep.span_ns, rep.busy_total_ns, rep.bubble_num, rep.bubble_den,
+             rep.bubble_ratio, rep.busy_per_gpu_ns)
+        j = report_json(mr, N)
+        assert len(j["events"]) == len(tl) and j["bubble_den"] == N * j["span_ns"]
