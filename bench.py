@@ -50,6 +50,24 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def ncu_gemm_traffic():
+    """DRAM bytes of the captured tcgen05 GEMM launch (ncu --set full, committed
+    under profiles/), with that launch's algorithmic bytes for comparison."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_full.json")), reverse=True):
+        try:
+            for r in json.load(open(path)):
+                if "gemm" in r.get("kernel", "") and r.get("dram_bytes"):
+                    # the capture is tools/bench_gemm.py gu_fwd: 4096 x 24576 x 4096 bf16
+                    algo = 2 * (4096 * 4096 + 24576 * 4096 + 4096 * 24576)
+                    return {"traffic": int(r["dram_bytes"]), "algorithmic_bytes": algo,
+                            "launch": "gate_up fwd 4096x24576x4096",
+                            "source": os.path.relpath(path, ROOT)}
+        except Exception:
+            continue
+    return None
+
+
 def step_flops(d, seq, tokens, recompute_layers):
     """Executed FLOPs of one step: 3x fwd per layer (+1 fwd for recomputed
     layers), causal attention, head fwd+dgrad+wgrad."""
@@ -245,6 +263,18 @@ def run_ours(args):
     sim = pl.simulate(sched, args.mode != "async")
     sim_bub = (pl.interior_bubble(sim.timeline, args.gpus, 1, max(3, args.steps) - 2)[0]
                if args.mode == "async" else sim.bubble_ratio)
+    if args.report_dir:  # measured timeline in the reference CLI's report schema + Gantt
+        from paper_2604_27085_b200.planner import report_json
+        os.makedirs(args.report_dir, exist_ok=True)
+        rep = pl.timeline_report(tl, args.gpus)
+        tag = f"{args.model}_n{args.gpus}_{args.mode}"
+        with open(os.path.join(args.report_dir, f"timeline_{tag}.json"), "w") as f:
+            json.dump({"measured": report_json(rep, args.gpus),
+                       "simulated": {k: v for k, v in report_json(sim, args.gpus).items()
+                                     if k != "events"},
+                       "transfers": rt.transfer_timeline().tolist()}, f)
+        with open(os.path.join(args.report_dir, f"gantt_{tag}.svg"), "w") as f:
+            f.write(pl.render_gantt(tl, args.gpus, plan))
     # one profiled step (not timed): kernel-level roofline
     rt.profile(True)
     rt.forward_backward(tokens, labels)
@@ -285,7 +315,9 @@ def run_ours(args):
         "gpu_launches": int(gpu_launches),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all linear layers of the step)",
                      "achieved": round(gemm_tf, 1), "peak": sustained, "unit": "TFLOP/s",
-                     "frac": round(gemm_tf / sustained, 4), "traffic": None,
+                     "frac": round(gemm_tf / sustained, 4),
+                     "traffic": (ncu_gemm_traffic() or {}).get("traffic"),
+                     "traffic_detail": ncu_gemm_traffic(),
                      "peak_source": f"{src} bf16_tflops_sustained (kernel inside a long step)",
                      "launches": gemm["launches"]},
         "kernels": {"attention_tflops": round(attn_tf, 1),
@@ -328,6 +360,8 @@ def main():
     ap.add_argument("--micro-batches", type=int, default=16)
     ap.add_argument("--mode", default="async", choices=["async", "sync"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--report-dir", default=None,
+                    help="write the measured timeline (report JSON + SVG Gantt) here")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))

@@ -75,6 +75,12 @@ int rp_get_params(rp_runtime_t* rt, int32_t group, int32_t which, float* out, in
 
 /* tokens/labels: host int32 [M, b, s]; labels < 0 are ignored. *loss = mean
  * token cross-entropy of the step (returned as soon as it is known). */
+/* Host-state checkpoint / resume: fp32 master, Adam m/v,
+ * step counters and the bf16 master of every group, plus which groups hold
+ * an unpublished (staleness-1) AdamW result. Drains the runtime first. */
+int rp_runtime_save(rp_runtime_t* rt, const char* path);
+int rp_runtime_load(rp_runtime_t* rt, const char* path);
+
 int rp_forward_backward(rp_runtime_t* rt, const int32_t* tokens, const int32_t* labels,
                         float* loss);
 int rp_step(rp_runtime_t* rt);
@@ -113,6 +119,11 @@ typedef struct {
   int64_t start_ns, end_ns;
   double work;
 } rp_prof_record_t;
+/* Measured cost table (L+1 rows) from the profiled steps: per layer the mean
+ * kernel ns of one micro-batch's forward (t_fwd) and forward+backward
+ * (t_bwd); bytes from the cost model. Feed back as rp_runtime_config_t.costs
+ * (or to rp_partition) to re-plan on measured costs. */
+int rp_runtime_measured_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
 int rp_runtime_profile_records(rp_runtime_t* rt, rp_prof_record_t* out, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus

@@ -15,6 +15,8 @@
 //      dS to double-buffered smem -> dQ += dS K (M128 N=hd K64, K as an
 //      MN-major operand). Epilogue: dQ*scale -> bf16.
 // (B) recomputes S and dP instead of reducing dQ partials through atomics.
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -282,6 +284,242 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ============================================================ (A2) dK / dV, ping-pong
+// CTA = 128 keys x TWO query heads (ha, ha+1) of one KV group. Both heads'
+// dV/dK land in the SAME TMEM accumulators (dV_kv = sum_h P_h^T dO_h), and
+// the two softmax warpgroups alternate with the tensor core, which runs
+//   S/dP_a(j) | grads_b(j-1) | S/dP_b(j) | grads_a(j) | S/dP_a(j+1) | ...
+// so each warpgroup's P^T/dS^T work hides behind ~1024 cycles of the other
+// head's MMAs. Query tiles of 64 stream through a 3-slot (Q, dO, lse, delta)
+// ring in the order (j, a), (j, b), (j+1, a), ...
+constexpr int A2_THREADS = 384;
+
+template <int HD>
+struct Dkv2Smem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int K = 0;
+  static constexpr int V = K + NSUB * SUB128;
+  static constexpr int R0 = V + NSUB * SUB128;        // ring slot s at R0 + s*STAGE
+  static constexpr int STAGE = 2 * NSUB * SUB64;      // Q + dO of one (tile, head)
+  static constexpr int DO_OFF = NSUB * SUB64;
+  static constexpr int PS = R0 + 3 * STAGE;           // head w: P^T at PS + w*PS_BUF, dS^T after
+  static constexpr int PS_BUF = 2 * (A_BK * A_BQ * 2);
+  static constexpr int LD = PS + 2 * PS_BUF;          // [3][2][A_BQ] lse, delta
+  static constexpr int BAR = LD + 3 * 2 * A_BQ * 4;
+  static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(A2_THREADS, 1)
+    attn_bwd_dkv_pp_kernel(const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v,
+                           const __grid_constant__ CUtensorMap tm_q,
+                           const __grid_constant__ CUtensorMap tm_do,
+                           const float* __restrict__ lse, const float* __restrict__ delta,
+                           float* __restrict__ dk_acc, float* __restrict__ dv_acc, int T, int seq,
+                           int nq, int nk, float scale) {
+  using L = Dkv2Smem<HD>;
+  constexpr int NSUB = L::NSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* st_full = bar + 1;   // [3]
+  uint64_t* st_empty = bar + 4;  // [3]
+  uint64_t* sd_full = bar + 7;   // [2] per head
+  uint64_t* ps_full = bar + 9;   // [2]
+  uint64_t* ps_free = bar + 11;  // [2]
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kb = blockIdx.x, ha = 2 * (int)blockIdx.y;
+  const int kvh = ha / (nq / nk);
+  const int k0 = kb * A_BK;
+  const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
+  const int nqt = (s_end - k0) / A_BQ;  // query tiles at/after the diagonal
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ps_full[i], 4);
+      mbar_init(&ps_free[i], 1);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM: head w: S^T at w*128 (64 cols), dP^T at w*128 + 64; dV at 256, dK at 384
+  const uint32_t TM_DV = 256, TM_DK = 384;
+
+  if (warp == 0 && lane == 0) {
+    mbar_arrive_expect_tx(kv_full, 2 * NSUB * SUB128);
+    for (int sub = 0; sub < NSUB; ++sub) {
+      tma_load_2d(sm + L::K + sub * SUB128, &tm_k, kv_full, kvh * HD + 64 * sub, k0);
+      tma_load_2d(sm + L::V + sub * SUB128, &tm_v, kv_full, kvh * HD + 64 * sub, k0);
+    }
+    for (int idx = 0; idx < 2 * nqt; ++idx) {
+      const int s = idx % 3, w = idx & 1, hq = ha + w;
+      mbar_wait(&st_empty[s], ((idx / 3) & 1) ^ 1);
+      const int qs = k0 + (idx >> 1) * A_BQ;
+      uint8_t* qd = sm + L::R0 + s * L::STAGE;
+      mbar_arrive_expect_tx(&st_full[s], L::STAGE + 2 * A_BQ * 4);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(qd + sub * SUB64, &tm_q, &st_full[s], hq * HD + 64 * sub, qs);
+        tma_load_2d(qd + L::DO_OFF + sub * SUB64, &tm_do, &st_full[s], hq * HD + 64 * sub, qs);
+      }
+      float* ld = reinterpret_cast<float*>(sm + L::LD) + s * 2 * A_BQ;
+      bulk_load_1d(ld, lse + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
+      bulk_load_1d(ld + A_BQ, delta + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A_BQ, 0, 0);   // K-major x K-major
+    constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);     // K-major x MN-major
+    const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
+    auto stage = [&](int idx) { return smem_u32(sm + L::R0 + (idx % 3) * L::STAGE); };
+    auto issue_sdp = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&st_full[idx % 3], (idx / 3) & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
+        const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
+        umma_f16(tmem + w * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
+                 umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
+        umma_f16(tmem + w * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
+                 umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(&sd_full[w]);
+    };
+    auto issue_grads = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&ps_full[w], j & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      const uint32_t p_addr = smem_u32(sm + L::PS + w * L::PS_BUF);
+      const uint32_t ds_addr = p_addr + A_BK * A_BQ * 2;
+#pragma unroll
+      for (int kk = 0; kk < A_BQ / 16; ++kk) {
+        const uint64_t pa = umma_desc_sw128(p_addr + kk * 32, 16, 1024);
+        const uint64_t da = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
+        const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
+        const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
+        umma_f16(tmem + TM_DV, pa, ob, idesc_g, (idx | kk) != 0);
+        umma_f16(tmem + TM_DK, da, qb, idesc_g, (idx | kk) != 0);
+      }
+      umma_commit(&ps_free[w]);
+      umma_commit(&st_empty[idx % 3]);
+    };
+    mbar_wait(kv_full, 0);
+    issue_sdp(0, 0);
+    issue_sdp(0, 1);
+    for (int j = 0; j < nqt; ++j) {
+      issue_grads(j, 0);
+      if (j + 1 < nqt) issue_sdp(j + 1, 0);
+      issue_grads(j, 1);
+      if (j + 1 < nqt) issue_sdp(j + 1, 1);
+    }
+    umma_commit(acc_done);
+  } else if (warp >= 4) {
+    // two softmax warpgroups: w = head slot, thread = key row
+    const int w = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int key = k0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    uint8_t* prow = sm + L::PS + w * L::PS_BUF + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* drow = prow + A_BK * A_BQ * 2;
+    for (int j = 0; j < nqt; ++j) {
+      const int idx = 2 * j + w, s = idx % 3;
+      const int qs = k0 + j * A_BQ;
+      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + s * 2 * A_BQ;
+      const float* del_t = lse_t + A_BQ;
+      mbar_wait(&st_full[s], (idx / 3) & 1);  // lse/delta visibility (already complete)
+      mbar_wait(&sd_full[w], j & 1);
+      tc_fence_after();
+      const bool diag = qs < k0 + A_BK;  // tile overlaps this key block's diagonal
+      // grads of (j-1, w) were issued before S/dP(j, w), so their release of
+      // this head's P^T / dS^T buffers has already landed
+      if (j >= 1) mbar_wait(&ps_free[w], (j - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t sv[32], dpv[32], pk[16], dk2[16];
+        tmem_ld_32x32b_x32(lane_base + w * 128 + half * 32, sv);
+        tmem_ld_32x32b_x32(lane_base + w * 128 + 64 + half * 32, dpv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int c = half * 32 + i;
+          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c] * kLog2e));
+          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1] * kLog2e));
+          if (diag) {
+            if (qs + c < key) p0 = 0.f;
+            if (qs + c + 1 < key) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dpv[i]) - del_t[c]);
+          const float d1 = p1 * (__uint_as_float(dpv[i + 1]) - del_t[c + 1]);
+          pk[i / 2] = pack_bf16x2(p0, p1);
+          dk2[i / 2] = pack_bf16x2(d0, d1);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int off = ((half * 4 + q4) ^ (r & 7)) << 4;
+          *reinterpret_cast<uint4*>(prow + off) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+          *reinterpret_cast<uint4*>(drow + off) =
+              make_uint4(dk2[q4 * 4], dk2[q4 * 4 + 1], dk2[q4 * 4 + 2], dk2[q4 * 4 + 3]);
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps_full[w]);
+    }
+    // epilogue: warpgroup a -> dK (scaled), warpgroup b -> dV; fp32 atomics
+    // reduce the G/2 head pairs of the KV group
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    float* dst = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
+    const uint32_t col = w == 0 ? TM_DK : TM_DV;
+    const float f = w == 0 ? scale : 1.f;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(lane_base + col + c, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        atomicAdd(reinterpret_cast<float4*>(dst + c + i),
+                  make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
+                              __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ======================================================================== (B) dQ
 // 128 queries per CTA, key tiles of 64 so that S and dP (64 TMEM columns
 // each) are double-buffered next to the dQ accumulator: the tensor core
@@ -497,6 +735,215 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ============================================================ (B2) dQ, ping-pong
+// CTA = 128 queries x TWO query heads of one KV group: K_j / V_j (64 keys) are
+// loaded once for both heads, and the two softmax warpgroups alternate with
+// the tensor core:  S/dP_a(j) | dQ_b(j-1) | S/dP_b(j) | dQ_a(j) | S/dP_a(j+1) ...
+template <int HD>
+struct Dq2Smem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int QT = NSUB * SUB128;           // one 128-row Q or dO tile
+  static constexpr int Q0 = 0;                       // head w: Q at Q0 + 2w*QT, dO after
+  static constexpr int KV0 = Q0 + 4 * QT;            // stage s: K at KV0 + s*STAGE, V after
+  static constexpr int STAGE = 2 * NSUB * SUB64;
+  static constexpr int DS = KV0 + 2 * STAGE;         // head w: dS [128 q][64 keys]
+  static constexpr int BAR = DS + 2 * SUB128;
+  static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
+                          const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ lse,
+                          const float* __restrict__ delta, bf16* __restrict__ dq, long long lddq,
+                          int T, int seq, int nq, int nk, float scale) {
+  using L = Dq2Smem<HD>;
+  constexpr int NSUB = L::NSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* sd_full = bar + 5;   // [2] per head
+  uint64_t* ds_full = bar + 7;   // [2]
+  uint64_t* ds_free = bar + 9;   // [2]
+  uint64_t* dq_done = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qblocks = T / B_Q;
+  const int qb = qblocks - 1 - (int)blockIdx.x;
+  const int ha = 2 * (int)blockIdx.y, kvh = ha / (nq / nk);
+  const int q0 = qb * B_Q;
+  const int s0 = (q0 / seq) * seq;
+  const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ds_full[i], 4);
+      mbar_init(&ds_free[i], 1);
+    }
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM: head w: S at w*128 (64 cols), dP at w*128 + 64; dQ_w at 256 + w*HD
+
+  if (warp == 0 && lane == 0) {
+    mbar_arrive_expect_tx(q_full, 4 * L::QT);
+    for (int w = 0; w < 2; ++w)
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(sm + L::Q0 + 2 * w * L::QT + sub * SUB128, &tm_q, q_full,
+                    (ha + w) * HD + 64 * sub, q0);
+        tma_load_2d(sm + L::Q0 + (2 * w + 1) * L::QT + sub * SUB128, &tm_do, q_full,
+                    (ha + w) * HD + 64 * sub, q0);
+      }
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j & 1;
+      mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+      const int k0 = s0 + j * B_K;
+      uint8_t* kd = sm + L::KV0 + st * L::STAGE;
+      mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(kd + sub * SUB64, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
+        tma_load_2d(kd + NSUB * SUB64 + sub * SUB64, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
+                    k0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
+    auto issue_sdp = [&](int j, int w) {
+      if (w == 0) {
+        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        tc_fence_after();
+      }
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j & 1) * L::STAGE);
+      const uint32_t v_addr = k_addr + NSUB * SUB64;
+      const uint32_t q_addr = smem_u32(sm + L::Q0 + 2 * w * L::QT), do_addr = q_addr + L::QT;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
+        const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
+        umma_f16(tmem + w * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
+                 umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
+        umma_f16(tmem + w * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
+                 umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(&sd_full[w]);
+    };
+    auto issue_dq = [&](int j, int w) {
+      mbar_wait(&ds_full[w], j & 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j & 1) * L::STAGE);
+      const uint32_t ds_addr = smem_u32(sm + L::DS + w * SUB128);
+#pragma unroll
+      for (int kk = 0; kk < B_K / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
+        umma_f16(tmem + 256 + w * HD, ad, bd, idesc_q, (j | kk) != 0);
+      }
+      umma_commit(&ds_free[w]);
+      if (w == 1) umma_commit(&kv_empty[j & 1]);
+    };
+    mbar_wait(q_full, 0);
+    issue_sdp(0, 0);
+    issue_sdp(0, 1);
+    for (int j = 0; j < ntiles; ++j) {
+      issue_dq(j, 0);
+      if (j + 1 < ntiles) issue_sdp(j + 1, 0);
+      issue_dq(j, 1);
+      if (j + 1 < ntiles) issue_sdp(j + 1, 1);
+    }
+    umma_commit(dq_done);
+  } else if (warp >= 4) {
+    const int w = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // query row
+    const int qrow = q0 + r, h = ha + w;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
+    const float dl = delta[(long long)h * T + qrow];
+    uint8_t* ds_row = sm + L::DS + w * SUB128 + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int j = 0; j < ntiles; ++j) {
+      mbar_wait(&sd_full[w], j & 1);
+      tc_fence_after();
+      // dQ(j-1, w) was issued before S/dP(j, w): its release of dS_w has landed
+      if (j >= 1) mbar_wait(&ds_free[w], (j - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t sv[32], dpv[32], pk[16];
+        tmem_ld_32x32b_x32(lane_base + w * 128 + half * 32, sv);
+        tmem_ld_32x32b_x32(lane_base + w * 128 + 64 + half * 32, dpv);
+        tmem_ld_wait();
+        const int kbase = s0 + j * B_K + half * 32;  // first key of these columns
+        const bool diag = kbase + 31 > q0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
+          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
+          if (diag) {
+            if (kbase + i > qrow) p0 = 0.f;
+            if (kbase + i + 1 > qrow) p1 = 0.f;
+          }
+          pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
+                                  p1 * (__uint_as_float(dpv[i + 1]) - dl));
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          *reinterpret_cast<uint4*>(ds_row + (((half * 4 + q4) ^ (r & 7)) << 4)) =
+              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[w]);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(lane_base + 256 + w * HD + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
+        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
+        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
+        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
+        *reinterpret_cast<uint4*>(dqr + c + i) = u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // delta[h, t] = sum_d dO[t,h,d] * O[t,h,d]; one warp per (t, h), 16-byte loads
 template <int HD>
 __global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf16* __restrict__ d,
@@ -599,16 +1046,37 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   }
   const long long acc_n = (long long)T * nk * HD;
   if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
-  attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nq), 384, DkvSmem<HD>::BYTES, s>>>(
-      mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
+  static const bool v1 = getenv("RP_ATTN_BWD_V1") != nullptr;
+  if ((nq / nk) % 2 == 0 && !v1) {  // two heads of one KV group per CTA
+    static bool cfg2 = false;
+    if (!cfg2) {
+      if (!set_smem(attn_bwd_dkv_pp_kernel<HD>, Dkv2Smem<HD>::BYTES)) return RP_E_CUDA;
+      cfg2 = true;
+    }
+    attn_bwd_dkv_pp_kernel<HD><<<dim3(T / A_BK, nq / 2), A2_THREADS, Dkv2Smem<HD>::BYTES, s>>>(
+        mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
+  } else {
+    attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nq), 384, DkvSmem<HD>::BYTES, s>>>(
+        mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
+  }
   dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
                                           lddv, T, nk * HD);
   CUtensorMap mk64, mv64;
   if (!map2d(&mk64, k, T, (long long)nk * HD, ldk, 64) ||
       !map2d(&mv64, v, T, (long long)nk * HD, ldv, 64))
     return RP_E_CUDA;
-  attn_bwd_dq_kernel<HD><<<dim3(T / B_Q, nq), 384, DqSmem<HD>::BYTES, s>>>(
-      mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
+  if ((nq / nk) % 2 == 0 && !v1) {
+    static bool cfg3 = false;
+    if (!cfg3) {
+      if (!set_smem(attn_bwd_dq_pp_kernel<HD>, Dq2Smem<HD>::BYTES)) return RP_E_CUDA;
+      cfg3 = true;
+    }
+    attn_bwd_dq_pp_kernel<HD><<<dim3(T / B_Q, nq / 2), 384, Dq2Smem<HD>::BYTES, s>>>(
+        mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
+  } else {
+    attn_bwd_dq_kernel<HD><<<dim3(T / B_Q, nq), 384, DqSmem<HD>::BYTES, s>>>(
+        mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
+  }
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
 }
 

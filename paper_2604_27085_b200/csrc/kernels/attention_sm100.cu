@@ -11,6 +11,8 @@
 //       written to swizzled smem for the PV MMA; final O / l, bf16 store, LSE.
 // S_{j+1} is issued before PV_j, so the tensor core computes the next scores
 // while the softmax warps work on the current tile.
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -284,6 +286,265 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ======================================================================
+// Ping-pong variant: one CTA = 128 query rows x TWO query heads of the same
+// KV group (GQA), so both Q tiles consume the same K/V tiles (loaded once)
+// and two softmax warpgroups alternate with the tensor core:
+//   w0      TMA: Q0, Q1 once; then K_0, V_0, K_1, V_1, ... through a 3-slot ring
+//   w1      MMA: S0_{j+1} = Q0 K^T and S1_{j+1} = Q1 K^T interleaved with
+//           O0 += P0_j V_j and O1 += P1_j V_j (TMEM: S0 | S1 | O0 | O1)
+//   w4-7    softmax of head 0 (thread = query row),  w8-11  softmax of head 1
+// While one warpgroup turns its S into P the tensor core runs the other
+// head's MMAs, so the MUFU/FMA work of the two heads hides behind the MMAs.
+constexpr int PP_THREADS = 384;
+
+template <int HD>
+struct PpSmem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int QT = NSUB * SUB;       // one Q tile (128 rows x HD)
+  static constexpr int KVT = NSUB * SUB;      // one K or V tile (128 keys x HD)
+  static constexpr int Q0 = 0;
+  static constexpr int RING = Q0 + 2 * QT;    // 3 slots
+  static constexpr int P = RING + 3 * KVT;    // P0, P1: 128 x 128 bf16 each (2 SUB)
+  static constexpr int BAR = P + 2 * 2 * SUB;
+  static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds 227 KB of shared memory");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(PP_THREADS, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, bf16* __restrict__ o,
+                       long long ldo, float* __restrict__ lse, int T, int seq, int nq, int nk,
+                       float scale) {
+  using L = PpSmem<HD>;
+  constexpr int NSUB = L::NSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [3]
+  uint64_t* kv_empty = bar + 4;  // [3]
+  uint64_t* s_full = bar + 7;    // [2] per head
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* o_done = bar + 11;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qblocks = T / TILE;
+  const int qb = qblocks - 1 - (int)blockIdx.x;  // heaviest tiles first
+  const int h0 = 2 * (int)blockIdx.y;            // heads h0, h0+1 share a KV head
+  const int kvh = h0 / (nq / nk);
+  const int q0 = qb * TILE;
+  const int s0 = (q0 / seq) * seq;
+  const int ntiles = (q0 - s0) / TILE + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S_w at w*128, O_w at 256 + w*HD
+
+  if (warp == 0 && lane == 0) {
+    // ------------------------------------------------------------ TMA producer
+    mbar_arrive_expect_tx(q_full, 2 * L::QT);
+    for (int w = 0; w < 2; ++w)
+      for (int sub = 0; sub < NSUB; ++sub)
+        tma_load_2d(sm + L::Q0 + w * L::QT + sub * SUB, &tm_q, q_full, (h0 + w) * HD + 64 * sub,
+                    q0);
+    for (int idx = 0; idx < 2 * ntiles; ++idx) {
+      const int slot = idx % 3;
+      mbar_wait(&kv_empty[slot], ((idx / 3) & 1) ^ 1);
+      const int k0 = s0 + (idx >> 1) * TILE;
+      uint8_t* dst = sm + L::RING + slot * L::KVT;
+      mbar_arrive_expect_tx(&kv_full[slot], L::KVT);
+      const CUtensorMap* map = (idx & 1) ? &tm_v : &tm_k;
+      for (int sub = 0; sub < NSUB; ++sub)
+        tma_load_2d(dst + sub * SUB, map, &kv_full[slot], kvh * HD + 64 * sub, k0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = umma_idesc_bf16(TILE, TILE, 0, 0);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(TILE, HD, 0, 1);
+    const uint32_t q_addr = smem_u32(sm + L::Q0);
+    const uint32_t p_addr = smem_u32(sm + L::P);
+    auto ring = [&](int idx) { return smem_u32(sm + L::RING + (idx % 3) * L::KVT); };
+    auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % 3], (idx / 3) & 1); };
+    auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T
+      const uint32_t qa = q_addr + w * L::QT, ka = ring(2 * j);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
+        umma_f16(tmem + w * TILE, umma_desc_sw128(qa + off, 16, 1024),
+                 umma_desc_sw128(ka + off, 16, 1024), idesc_s, kk != 0);
+      }
+      umma_commit(&s_full[w]);
+    };
+    auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j
+      mbar_wait(&p_full[w], j & 1);
+      tc_fence_after();
+      const uint32_t pa = p_addr + w * 2 * SUB, va = ring(2 * j + 1);
+#pragma unroll
+      for (int kk = 0; kk < TILE / 16; ++kk) {
+        const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = umma_desc_sw128(va + kk * 2048, SUB, 1024);
+        umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+      }
+      umma_commit(&o_done[w]);
+    };
+    mbar_wait(q_full, 0);
+    wait_kv(0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    umma_commit(&kv_empty[0]);
+    for (int j = 0; j < ntiles; ++j) {
+      wait_kv(2 * j + 1);
+      tc_fence_after();
+      issue_pv(0, j);
+      const bool more = j + 1 < ntiles;
+      if (more) {
+        wait_kv(2 * j + 2);
+        tc_fence_after();
+        issue_s(0, j + 1);  // S0 was read before P0_j was published
+      }
+      issue_pv(1, j);
+      umma_commit(&kv_empty[(2 * j + 1) % 3]);
+      if (more) {
+        issue_s(1, j + 1);
+        umma_commit(&kv_empty[(2 * j + 2) % 3]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int w = (warp - 4) >> 2;      // head slot of this warpgroup
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // query row within the tile
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const uint32_t s_col = w * TILE, o_col = 256 + w * HD;
+    const float sl2 = scale * 1.4426950408889634f;
+    float m = 0.f, l = 0.f;
+    uint8_t* p_row = sm + L::P + w * 2 * SUB + (r >> 3) * 1024 + (r & 7) * 128;
+    for (int j = 0; j < ntiles; ++j) {
+      mbar_wait(&s_full[w], j & 1);
+      tc_fence_after();
+      float s[TILE];
+#pragma unroll
+      for (int c = 0; c < TILE; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(lane_base + s_col + c, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(v[i]);
+      }
+      if (j == ntiles - 1) {  // diagonal tile: key c > query r is masked
+#pragma unroll
+        for (int c = 0; c < TILE; ++c)
+          if (c > r) s[c] = -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < TILE; ++c) mx = fmaxf(mx, s[c]);
+      const float mxs = mx * sl2;
+      bool o_ready = false;
+      if (j == 0) {
+        m = mxs;
+      } else if (__any_sync(0xffffffffu, mxs > m + 8.f)) {
+        // some row's max grew by > 2^8: rescale this warp's O rows after PV_{j-1}
+        mbar_wait(&o_done[w], (j - 1) & 1);
+        tc_fence_after();
+        o_ready = true;
+        const float m_new = fmaxf(m, mxs);
+        const float f = ex2(m - m_new);
+        m = m_new;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(lane_base + o_col + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * f);
+          tmem_st_32x32b_x32(lane_base + o_col + c, v);
+        }
+        tmem_st_wait();
+        l *= f;
+      }
+      if (j >= 1 && !o_ready) {  // PV_{j-1} must be done reading this head's P buffer
+        mbar_wait(&o_done[w], (j - 1) & 1);
+        tc_fence_after();
+      }
+      float lsum = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < TILE / 8; ++ch) {  // 16-byte chunks of the swizzled row
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = ex2(fmaf(s[ch * 8 + 2 * e], sl2, -m));
+          const float p1 = ex2(fmaf(s[ch * 8 + 2 * e + 1], sl2, -m));
+          lsum += p0 + p1;
+          pk[e] = pack_bf16x2(p0, p1);
+        }
+        const int sub = ch >> 3, c8 = ch & 7;
+        *reinterpret_cast<uint4*>(p_row + sub * SUB + ((c8 ^ (r & 7)) << 4)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l += lsum;
+      fence_proxy_async();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[w]);
+    }
+    // epilogue: O / l -> bf16, LSE
+    mbar_wait(&o_done[w], (ntiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    const int qrow = q0 + r;
+    const int h = h0 + w;
+    bf16* orow = o + (long long)qrow * ldo + (long long)h * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(lane_base + o_col + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[i]) * inv, __uint_as_float(v[i + 1]) * inv);
+        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * inv, __uint_as_float(v[i + 3]) * inv);
+        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * inv, __uint_as_float(v[i + 5]) * inv);
+        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * inv, __uint_as_float(v[i + 7]) * inv);
+        *reinterpret_cast<uint4*>(orow + c + i) = u;
+      }
+    }
+    lse[(long long)h * T + qrow] = (m + __log2f(l)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ---- host ----------------------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -319,6 +580,21 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   if (!map_tile(&mq, q, T, (long long)nq * HD, ldq) || !map_tile(&mk, k, T, (long long)nk * HD, ldk) ||
       !map_tile(&mv, v, T, (long long)nk * HD, ldv))
     return RP_E_CUDA;
+  static const bool force_v1 = getenv("RP_ATTN_FWD_V1") != nullptr;
+  if ((nq / nk) % 2 == 0 && !force_v1) {  // two heads of one KV group per CTA
+    auto kern = attn_fwd_pp_kernel<HD>;
+    static bool cfg = false;
+    if (!cfg) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               PpSmem<HD>::BYTES) != cudaSuccess)
+        return RP_E_CUDA;
+      cfg = true;
+    }
+    dim3 grid(T / TILE, nq / 2);
+    kern<<<grid, PP_THREADS, PpSmem<HD>::BYTES, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq,
+                                                      nk, scale);
+    return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
+  }
   auto kern = attn_fwd_tc_kernel<HD>;
   static bool cfg = false;
   if (!cfg) {

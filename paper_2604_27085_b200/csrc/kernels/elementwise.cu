@@ -51,27 +51,54 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // ---------------------------------------------------------------- RMSNorm
-// y = bf16(w * x * rstd), rstd = 1/sqrt(mean(x^2) + eps). One block per row.
-template <int THREADS>
-__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
-                                   const __nv_bfloat16* __restrict__ w,
-                                   __nv_bfloat16* __restrict__ y, long long ldy,
-                                   float* __restrict__ rstd, int h, float eps) {
-  __shared__ float red[THREADS / 32];
+// y = bf16(w * x * rstd), rstd = 1/sqrt(mean(x^2) + eps). One 128-thread
+// block per row, the row held in registers (VPT 16-byte vectors per thread),
+// so x is read once; many rows in flight per SM.
+
+template <int NW>
+__device__ __forceinline__ float rn_block_sum(float v, float* red) {
+  v = warp_sum(v);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) t += red[i];
+  return t;
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = bf2f(b[i]);
+}
+
+template <int RN_THREADS, int VPT>
+__global__ void __launch_bounds__(RN_THREADS)
+    rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, long long ldx,
+                       const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ y,
+                       long long ldy, float* __restrict__ rstd, int h, float eps) {
+  __shared__ float red[RN_THREADS / 32];
   const long long row = blockIdx.x;
   const __nv_bfloat16* xr = x + row * ldx;
+  uint4 xv[VPT];
   float ss = 0.f;
-  for (int c = threadIdx.x * 8; c < h; c += THREADS * 8) {
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int c = (threadIdx.x + j * RN_THREADS) * 8;
+    xv[j] = c < h ? *reinterpret_cast<const uint4*>(xr + c) : make_uint4(0, 0, 0, 0);
     float f[8];
-    load8(xr + c, f);
+    unpack8(xv[j], f);
 #pragma unroll
     for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
   }
-  const float r = rsqrtf(block_sum<THREADS>(ss, red) / h + eps);
+  const float r = rsqrtf(rn_block_sum<RN_THREADS / 32>(ss, red) / h + eps);
   if (threadIdx.x == 0 && rstd) rstd[row] = r;
-  for (int c = threadIdx.x * 8; c < h; c += THREADS * 8) {
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int c = (threadIdx.x + j * RN_THREADS) * 8;
+    if (c >= h) continue;
     float f[8], g[8];
-    load8(xr + c, f);
+    unpack8(xv[j], f);
     load8(w + c, g);
 #pragma unroll
     for (int i = 0; i < 8; ++i) f[i] = g[i] * (f[i] * r);
@@ -81,76 +108,94 @@ __global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, long lon
 
 // dx = rstd * (g - xhat * mean(g * xhat)),  g = dy * w,  xhat = x * rstd
 // dx_total = dx + dres (optional fp32 residual grad); written fp32 and/or bf16.
-// dw[c] += sum_rows dy * xhat. Each block walks a contiguous row range.
-template <int THREADS, int MAXC>
-__global__ void __launch_bounds__(THREADS)
+// dw[c] += sum_rows dy * xhat. A block walks rows with a stride of gridDim.x
+// (several blocks per SM keep rows in flight); dw partials stay in registers
+// until one float4 atomic per 4 columns per block.
+template <int RN_THREADS, int VPT>
+__global__ void __launch_bounds__(RN_THREADS)
     rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                        const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
                        const float* __restrict__ dres, float* __restrict__ dx32,
                        __nv_bfloat16* __restrict__ dx16, float* __restrict__ dw, int rows, int h) {
-  // one read of dy/x per row (kept in registers across the reduction), w
-  // loaded once per block, dw partials in registers until the block ends
-  __shared__ float red[THREADS / 32];
-  float g[MAXC][8], dw_acc[MAXC][8];
+  __shared__ float red[2][RN_THREADS / 32];
+  uint4 wv[VPT];
+  float dwa[VPT][8];
 #pragma unroll
-  for (int j = 0; j < MAXC; ++j) {
-    const int c = (threadIdx.x + j * THREADS) * 8;
+  for (int j = 0; j < VPT; ++j) {
+    const int c = (threadIdx.x + j * RN_THREADS) * 8;
+    wv[j] = c < h ? *reinterpret_cast<const uint4*>(w + c) : make_uint4(0, 0, 0, 0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) dw_acc[j][i] = g[j][i] = 0.f;
-    if (c < h) load8(w + c, g[j]);
+    for (int i = 0; i < 8; ++i) dwa[j][i] = 0.f;
   }
-  const int per = (rows + gridDim.x - 1) / gridDim.x;
-  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  for (int row = r0; row < r1; ++row) {
+  int par = 0;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1) {
     const long long off = (long long)row * h;
+    uint4 av[VPT], bv[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      if (c < h) {
+        av[j] = *reinterpret_cast<const uint4*>(dy + off + c);
+        bv[j] = *reinterpret_cast<const uint4*>(x + off + c);
+      } else {
+        av[j] = bv[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
     const float r = rstd[row];
-    float a[MAXC][8], b[MAXC][8];
     float dot = 0.f;
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j) {
-      const int c = (threadIdx.x + j * THREADS) * 8;
-      if (c < h) {
-        load8(dy + off + c, a[j]);
-        load8(x + off + c, b[j]);
+    for (int j = 0; j < VPT; ++j) {
+      float a[8], b[8], g[8];
+      unpack8(av[j], a);
+      unpack8(bv[j], b);
+      unpack8(wv[j], g);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          b[j][i] *= r;  // xhat
-          dot += a[j][i] * g[j][i] * b[j][i];
-        }
-      }
+      for (int i = 0; i < 8; ++i) dot += a[i] * g[i] * (b[i] * r);
     }
-    const float mean = block_sum<THREADS>(dot, red) / h;
+    dot = warp_sum(dot);
+    if (threadIdx.x % 32 == 0) red[par][threadIdx.x / 32] = dot;
+    __syncthreads();  // red[par] is rewritten two rows later, after another barrier
+    float tot = 0.f;
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j) {
-      const int c = (threadIdx.x + j * THREADS) * 8;
-      if (c < h) {
-        float o[8];
+    for (int i = 0; i < RN_THREADS / 32; ++i) tot += red[par][i];
+    const float mean = tot / h;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          o[i] = r * (a[j][i] * g[j][i] - b[j][i] * mean);
-          dw_acc[j][i] += a[j][i] * b[j][i];
-        }
-        if (dres) {
-          const float4 d0 = *reinterpret_cast<const float4*>(dres + off + c);
-          const float4 d1 = *reinterpret_cast<const float4*>(dres + off + c + 4);
-          o[0] += d0.x; o[1] += d0.y; o[2] += d0.z; o[3] += d0.w;
-          o[4] += d1.x; o[5] += d1.y; o[6] += d1.z; o[7] += d1.w;
-        }
-        if (dx32) {
-          *reinterpret_cast<float4*>(dx32 + off + c) = make_float4(o[0], o[1], o[2], o[3]);
-          *reinterpret_cast<float4*>(dx32 + off + c + 4) = make_float4(o[4], o[5], o[6], o[7]);
-        }
-        if (dx16) store8(dx16 + off + c, o);
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      if (c >= h) continue;
+      float a[8], b[8], g[8], o[8];
+      unpack8(av[j], a);
+      unpack8(bv[j], b);
+      unpack8(wv[j], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = b[i] * r;
+        o[i] = r * (a[i] * g[i] - xh * mean);
+        dwa[j][i] += a[i] * xh;
       }
+      if (dres) {
+        const float4 d0 = *reinterpret_cast<const float4*>(dres + off + c);
+        const float4 d1 = *reinterpret_cast<const float4*>(dres + off + c + 4);
+        o[0] += d0.x; o[1] += d0.y; o[2] += d0.z; o[3] += d0.w;
+        o[4] += d1.x; o[5] += d1.y; o[6] += d1.z; o[7] += d1.w;
+      }
+      if (dx32) {
+        *reinterpret_cast<float4*>(dx32 + off + c) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(dx32 + off + c + 4) = make_float4(o[4], o[5], o[6], o[7]);
+      }
+      if (dx16) store8(dx16 + off + c, o);
     }
   }
-  if (dw && r1 > r0) {
+  if (dw && (int)blockIdx.x < rows) {
 #pragma unroll
-    for (int j = 0; j < MAXC; ++j) {
-      const int c = (threadIdx.x + j * THREADS) * 8;
-      if (c < h)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) atomicAdd(dw + c + i, dw_acc[j][i]);
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      if (c < h) {
+        atomicAdd(reinterpret_cast<float4*>(dw + c),
+                  make_float4(dwa[j][0], dwa[j][1], dwa[j][2], dwa[j][3]));
+        atomicAdd(reinterpret_cast<float4*>(dw + c + 4),
+                  make_float4(dwa[j][4], dwa[j][5], dwa[j][6], dwa[j][7]));
+      }
     }
   }
 }
@@ -158,53 +203,69 @@ __global__ void __launch_bounds__(THREADS)
 // ------------------------------------------------------- QK-norm + RoPE
 // A head of HD elements is handled by TPH = HD/8 consecutive lanes, 8
 // elements (16 bytes) each; the per-head RMS reduces over those lanes and the
-// rotate_half partner (element e +- HD/2) lives in lane ^ TPH/2.
+// rotate_half partner (element e +- HD/2) lives in lane ^ TPH/2. A 128-thread
+// block covers 128/TPH heads of one token at a time and walks heads then
+// tokens (grid-stride); a thread's (cos, sin) pairs depend only on its lane
+// slot and the token, so they are loaded once per token.
+constexpr int QK_THREADS = 128;
+
 template <int HD>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(QK_THREADS)
     qk_norm_rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
                             const __nv_bfloat16* __restrict__ qw,
                             const __nv_bfloat16* __restrict__ kw, const float2* __restrict__ cs,
                             int seq, __nv_bfloat16* __restrict__ qo, __nv_bfloat16* __restrict__ ko,
                             float* __restrict__ rstd_q, float* __restrict__ rstd_k, int T,
                             float eps) {
-  constexpr int TPH = HD / 8, HALF = HD / 2;
+  constexpr int TPH = HD / 8, HALF = HD / 2, HPB = QK_THREADS / TPH;
   const int heads = nq + nk;
-  const long long total = (long long)T * heads * TPH;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += stride) {
-    const long long hidx = gt / TPH;
-    const int sub = (int)(gt % TPH);
-    const int t = (int)(hidx / heads), hh = (int)(hidx % heads);
-    const bool is_q = hh < nq;
-    float v[8], wv[8];
-    load8(qkv + (long long)t * ld + (long long)hh * HD + sub * 8, v);
-    load8((is_q ? qw : kw) + sub * 8, wv);
-    float ss = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
-#pragma unroll
-    for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float r = rsqrtf(ss / HD + eps);
-    float n[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf(wv[i] * (v[i] * r)));
-    const bool lo = sub < TPH / 2;
+  const int sub = threadIdx.x % TPH, hl = threadIdx.x / TPH;
+  const bool lo = sub < TPH / 2;
+  float wq[8], wk[8];
+  load8(qw + sub * 8, wq);
+  load8(kw + sub * 8, wk);
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
     const int pos = t % seq;
     const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
-    float out[8];
+    float4 c[4];
 #pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      const float4 c = c4[i / 2];  // (cos, sin) of elements i, i+1
-      const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
-      const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
-      out[i] = lo ? n[i] * c.x - p0 * c.y : n[i] * c.x + p0 * c.y;
-      out[i + 1] = lo ? n[i + 1] * c.z - p1 * c.w : n[i + 1] * c.z + p1 * c.w;
-    }
-    __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD : ko + ((long long)t * nk + (hh - nq)) * HD;
-    store8(dst + sub * 8, out);
-    if (sub == 0) {
-      if (is_q) rstd_q[(long long)t * nq + hh] = r;
-      else rstd_k[(long long)t * nk + (hh - nq)] = r;
+    for (int i = 0; i < 4; ++i) c[i] = c4[i];
+    const __nv_bfloat16* row = qkv + (long long)t * ld;
+    // every lane runs every pass (the shuffles below are warp-wide); lanes
+    // whose head is past the end compute on zeros and store nothing
+    for (int base = 0; base < heads; base += HPB) {
+      const int hh = base + hl;
+      const bool act = hh < heads;
+      const bool is_q = hh < nq;
+      float v[8];
+      if (act) load8(row + hh * HD + sub * 8, v);
+      else for (int i = 0; i < 8; ++i) v[i] = 0.f;
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
+#pragma unroll
+      for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float r = rsqrtf(ss / HD + eps);
+      float n[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf((is_q ? wq[i] : wk[i]) * (v[i] * r)));
+      float out[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float4 cc = c[i / 2];  // (cos, sin) of elements i, i+1
+        const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
+        const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
+        out[i] = lo ? n[i] * cc.x - p0 * cc.y : n[i] * cc.x + p0 * cc.y;
+        out[i + 1] = lo ? n[i + 1] * cc.z - p1 * cc.w : n[i + 1] * cc.z + p1 * cc.w;
+      }
+      if (!act) continue;
+      __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD
+                                : ko + ((long long)t * nk + (hh - nq)) * HD;
+      store8(dst + sub * 8, out);
+      if (sub == 0) {
+        if (is_q) rstd_q[(long long)t * nq + hh] = r;
+        else rstd_k[(long long)t * nk + (hh - nq)] = r;
+      }
     }
   }
 }
@@ -213,7 +274,7 @@ __global__ void __launch_bounds__(256)
 // dqkv[:, q/k slots] = dx; dqw/dkw[HD] += sum(dn * xhat) (registers -> smem
 // -> one atomic per column per block).
 template <int HD>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(QK_THREADS)
     qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
                             const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
                             const __nv_bfloat16* __restrict__ qw,
@@ -221,60 +282,67 @@ __global__ void __launch_bounds__(256)
                             const float* __restrict__ rstd_k, const float2* __restrict__ cs, int seq,
                             __nv_bfloat16* __restrict__ dqkv, long long ldd, float* __restrict__ dqw,
                             float* __restrict__ dkw, int T) {
-  constexpr int TPH = HD / 8, HALF = HD / 2;
+  constexpr int TPH = HD / 8, HALF = HD / 2, HPB = QK_THREADS / TPH;
   __shared__ float sq[HD], sk[HD];
   for (int i = threadIdx.x; i < HD; i += blockDim.x) sq[i] = sk[i] = 0.f;
   __syncthreads();
   const int heads = nq + nk;
-  const long long total = (long long)T * heads * TPH;
-  const long long stride = (long long)gridDim.x * blockDim.x;  // multiple of TPH
-  float aq[8], ak[8];
+  const int sub = threadIdx.x % TPH, hl = threadIdx.x / TPH;
+  const bool lo = sub < TPH / 2;
+  float wq[8], wk[8], aq[8], ak[8];
+  load8(qw + sub * 8, wq);
+  load8(kw + sub * 8, wk);
 #pragma unroll
   for (int i = 0; i < 8; ++i) aq[i] = ak[i] = 0.f;
-  int my_sub = 0;
-  for (long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x; gt < total; gt += stride) {
-    const long long hidx = gt / TPH;
-    const int sub = (int)(gt % TPH);
-    my_sub = sub;
-    const int t = (int)(hidx / heads), hh = (int)(hidx % heads);
-    const bool is_q = hh < nq;
-    const float r = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
-    float gv[8], xv[8], wv[8];
-    load8((is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) + sub * 8, gv);
-    load8(qkv + (long long)t * ld + (long long)hh * HD + sub * 8, xv);
-    load8((is_q ? qw : kw) + sub * 8, wv);
-    const bool lo = sub < TPH / 2;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
     const int pos = t % seq;
     const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
-    float dn[8];
+    float4 c[4];
 #pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      const float4 c = c4[i / 2];
-      const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
-      const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
-      dn[i] = lo ? gv[i] * c.x + p0 * c.y : gv[i] * c.x - p0 * c.y;
-      dn[i + 1] = lo ? gv[i + 1] * c.z + p1 * c.w : gv[i + 1] * c.z - p1 * c.w;
+    for (int i = 0; i < 4; ++i) c[i] = c4[i];
+    for (int base = 0; base < heads; base += HPB) {  // warp-uniform passes (shuffles)
+      const int hh = base + hl;
+      const bool act = hh < heads;
+      const bool is_q = hh < nq;
+      float r = 0.f, gv[8], xv[8];
+      if (act) {
+        r = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
+        load8((is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) +
+                  sub * 8, gv);
+        load8(qkv + (long long)t * ld + hh * HD + sub * 8, xv);
+      } else {
+        for (int i = 0; i < 8; ++i) gv[i] = xv[i] = 0.f;
+      }
+      float dn[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float4 cc = c[i / 2];
+        const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
+        const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
+        dn[i] = lo ? gv[i] * cc.x + p0 * cc.y : gv[i] * cc.x - p0 * cc.y;
+        dn[i + 1] = lo ? gv[i + 1] * cc.z + p1 * cc.w : gv[i + 1] * cc.z - p1 * cc.w;
+      }
+      float dot = 0.f, gx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        xv[i] *= r;  // xhat
+        gx[i] = dn[i] * (is_q ? wq[i] : wk[i]);
+        dot += gx[i] * xv[i];
+        if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
+      }
+#pragma unroll
+      for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const float mean = dot / HD;
+      float out[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
+      if (act) store8(dqkv + (long long)t * ldd + hh * HD + sub * 8, out);
     }
-    float dot = 0.f, gx[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      xv[i] *= r;  // xhat
-      gx[i] = dn[i] * wv[i];
-      dot += gx[i] * xv[i];
-      if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
-    }
-#pragma unroll
-    for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const float mean = dot / HD;
-    float out[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
-    store8(dqkv + (long long)t * ldd + (long long)hh * HD + sub * 8, out);
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    atomicAdd(&sq[my_sub * 8 + i], aq[i]);
-    atomicAdd(&sk[my_sub * 8 + i], ak[i]);
+    atomicAdd(&sq[sub * 8 + i], aq[i]);
+    atomicAdd(&sk[sub * 8 + i], ak[i]);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < HD; i += blockDim.x) {
@@ -284,43 +352,43 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------------ SwiGLU
-// gu row = [gate(0..m) | up(0..m)];  act = silu(g) * u
-__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
-                                  __nv_bfloat16* __restrict__ act, long long T, int m) {
-  const long long n8 = T * m / 8;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i * 8, t = e / m;
-    const int c = (int)(e % m);
+// gu row = [gate(0..m) | up(0..m)];  act = silu(g) * u. Block-per-row (no
+// integer division in the index math); 8-wide vectors.
+__global__ void __launch_bounds__(256) swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu,
+                                                         __nv_bfloat16* __restrict__ act, int m) {
+  const long long t = blockIdx.x;
+  const __nv_bfloat16* g_row = gu + t * 2 * m;
+  __nv_bfloat16* a_row = act + t * m;
+  for (int c = threadIdx.x * 8; c < m; c += 256 * 8) {
     float g[8], u[8], o[8];
-    load8(gu + t * 2 * m + c, g);
-    load8(gu + t * 2 * m + m + c, u);
+    load8(g_row + c, g);
+    load8(g_row + m + c, u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.f + __expf(-g[k])) * u[k];
-    store8(act + e, o);
+    store8(a_row + c, o);
   }
 }
 
-__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact,
-                                  const __nv_bfloat16* __restrict__ gu,
-                                  __nv_bfloat16* __restrict__ dgu, long long T, int m) {
-  const long long n8 = T * m / 8;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i * 8, t = e / m;
-    const int c = (int)(e % m);
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact,
+                                                         const __nv_bfloat16* __restrict__ gu,
+                                                         __nv_bfloat16* __restrict__ dgu, int m) {
+  const long long t = blockIdx.x;
+  const __nv_bfloat16* g_row = gu + t * 2 * m;
+  __nv_bfloat16* d_row = dgu + t * 2 * m;
+  const __nv_bfloat16* a_row = dact + t * m;
+  for (int c = threadIdx.x * 8; c < m; c += 256 * 8) {
     float d[8], g[8], u[8], dg[8], du[8];
-    load8(dact + e, d);
-    load8(gu + t * 2 * m + c, g);
-    load8(gu + t * 2 * m + m + c, u);
+    load8(a_row + c, d);
+    load8(g_row + c, g);
+    load8(g_row + m + c, u);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const float s = 1.f / (1.f + __expf(-g[k]));
-      du[k] = d[k] * g[k] * s;
-      dg[k] = d[k] * u[k] * s * (1.f + g[k] * (1.f - s));
+      const float sg = 1.f / (1.f + __expf(-g[k]));
+      du[k] = d[k] * g[k] * sg;
+      dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
     }
-    store8(dgu + t * 2 * m + c, dg);
-    store8(dgu + t * 2 * m + m + c, du);
+    store8(d_row + c, dg);
+    store8(d_row + m + c, du);
   }
 }
 
@@ -502,28 +570,59 @@ int status() { return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA; }
 using namespace rp;
 #define RP_API extern "C" __attribute__((visibility("default")))
 
+// 128 threads per row up to h = 4096, 256 above (h <= 8192); VPT vectors each
+template <class Go, class F128_1, class F128_2, class F128_3, class F128_4, class F256_3,
+          class F256_4>
+void rn_dispatch(int h, Go go, F128_1 a, F128_2 b, F128_3 c, F128_4 d, F256_3 e, F256_4 f) {
+  const int th = h <= 128 * 8 * 4 ? 128 : 256;
+  const int vpt = (h + th * 8 - 1) / (th * 8);
+  if (th == 128) {
+    if (vpt <= 1) go(a, 128);
+    else if (vpt <= 2) go(b, 128);
+    else if (vpt <= 3) go(c, 128);
+    else go(d, 128);
+  } else {
+    if (vpt <= 3) go(e, 256);
+    else go(f, 256);
+  }
+}
+
 RP_API int rp_rmsnorm_fwd(const void* x, int64_t ldx, const void* w, void* y, int64_t ldy,
                           float* rstd, int32_t rows, int32_t h, float eps, void* stream) {
-  if (h % 8 || ldx % 8 || ldy % 8 || rows <= 0) return RP_E_INPUT;
-  rmsnorm_fwd_kernel<256><<<rows, 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, ldx, (const __nv_bfloat16*)w, (__nv_bfloat16*)y, ldy, rstd, h, eps);
+  if (h % 8 || ldx % 8 || ldy % 8 || rows <= 0 || h > 256 * 8 * 4) return RP_E_INPUT;
+  auto st = (cudaStream_t)stream;
+  auto go = [&](auto kern, int th) {
+    kern<<<rows, th, 0, st>>>((const __nv_bfloat16*)x, ldx, (const __nv_bfloat16*)w,
+                              (__nv_bfloat16*)y, ldy, rstd, h, eps);
+  };
+  rn_dispatch(h, go, rmsnorm_fwd_kernel<128, 1>, rmsnorm_fwd_kernel<128, 2>,
+              rmsnorm_fwd_kernel<128, 3>, rmsnorm_fwd_kernel<128, 4>,
+              rmsnorm_fwd_kernel<256, 3>, rmsnorm_fwd_kernel<256, 4>);
   return status();
 }
 
 RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
                           const float* dres, float* dx32, void* dx16, float* dw, int32_t rows,
                           int32_t h, void* stream) {
-  if (h % 8 || rows <= 0 || h > 512 * 8 * 2) return RP_E_INPUT;
-  const int grid = rows < 148 * 4 ? rows : 148 * 4;
+  if (h % 8 || rows <= 0 || h > 256 * 8 * 4) return RP_E_INPUT;
   auto st = (cudaStream_t)stream;
-  auto args = [&](auto kern, int threads) {
-    kern<<<grid, threads, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                   (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
-                                   dw, rows, h);
+  // exactly the resident blocks (one wave); each walks rows grid-stride,
+  // keeping dw in registers
+  auto go = [&](auto kern, int th) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const int grid = rows < sms * per_sm ? rows : sms * per_sm;
+    kern<<<grid, th, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                              (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
+                              dw, rows, h);
   };
-  if (h <= 256 * 8) args(rmsnorm_bwd_kernel<256, 1>, 256);
-  else if (h <= 512 * 8) args(rmsnorm_bwd_kernel<512, 1>, 512);
-  else args(rmsnorm_bwd_kernel<512, 2>, 512);
+  rn_dispatch(h, go, rmsnorm_bwd_kernel<128, 1>, rmsnorm_bwd_kernel<128, 2>,
+              rmsnorm_bwd_kernel<128, 3>, rmsnorm_bwd_kernel<128, 4>,
+              rmsnorm_bwd_kernel<256, 3>, rmsnorm_bwd_kernel<256, 4>);
   return status();
 }
 
@@ -532,17 +631,16 @@ RP_API int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t 
                                const float* cos_sin, int32_t seq, void* q_out, void* k_out,
                                float* rstd_q, float* rstd_k, int32_t T, float eps,
                                void* stream) {
-  if (ld % 8 || T % 128) return RP_E_INPUT;
-  const long long threads = (long long)T * (nq + nk) * (head_dim / 8);
-  const int grid = grid_for(threads, 256, 148 * 16);
+  if (ld % 8 || T % 128 || T <= 0) return RP_E_INPUT;
+  const int grid = T < 148 * 16 ? T : 148 * 16;
   auto s = (cudaStream_t)stream;
   if (head_dim == 128)
-    qk_norm_rope_fwd_kernel<128><<<grid, 256, 0, s>>>(
+    qk_norm_rope_fwd_kernel<128><<<grid, QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
   else if (head_dim == 64)
-    qk_norm_rope_fwd_kernel<64><<<grid, 256, 0, s>>>(
+    qk_norm_rope_fwd_kernel<64><<<grid, QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
@@ -556,16 +654,16 @@ RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, 
                                const void* kw, const float* rstd_q, const float* rstd_k,
                                const float* cos_sin, int32_t seq, void* dqkv, int64_t ldd,
                                float* dqw, float* dkw, int32_t T, void* stream) {
-  if (ld % 8 || ldd % 8 || T % 128) return RP_E_INPUT;
+  if (ld % 8 || ldd % 8 || T % 128 || T <= 0) return RP_E_INPUT;
   auto s = (cudaStream_t)stream;
-  const int grid = 148 * 4;  // grid*256 is a multiple of every TPH
+  const int grid = T < 148 * 8 ? T : 148 * 8;
   if (head_dim == 128)
-    qk_norm_rope_bwd_kernel<128><<<grid, 256, 0, s>>>(
+    qk_norm_rope_bwd_kernel<128><<<grid, QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
   else if (head_dim == 64)
-    qk_norm_rope_bwd_kernel<64><<<grid, 256, 0, s>>>(
+    qk_norm_rope_bwd_kernel<64><<<grid, QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
@@ -576,16 +674,18 @@ RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, 
 
 RP_API int rp_swiglu_fwd(const void* gu, void* act, int64_t T, int32_t m, void* stream) {
   if (m % 8) return RP_E_INPUT;
-  swiglu_fwd_kernel<<<grid_for(T * m / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, T, m);
+  if (T <= 0) return RP_OK;
+  swiglu_fwd_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, m);
   return status();
 }
 
 RP_API int rp_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t T, int32_t m,
                          void* stream) {
   if (m % 8) return RP_E_INPUT;
-  swiglu_bwd_kernel<<<grid_for(T * m / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, T, m);
+  if (T <= 0) return RP_OK;
+  swiglu_bwd_kernel<<<(unsigned)T, 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, m);
   return status();
 }
 

@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <thread>
 
@@ -193,7 +194,16 @@ struct Runtime {
     cudaEvent_t a, b;
     double work;
     int worker, lane;  // lane 0 = compute stream, 1 = optimizer stream
+    int unit, inst;    // (layer, phase) being executed and its call instance
   };
+  // current compute unit for the profile records: layer l (L = head) and
+  // phase (0 fwd, 1 bwd, 2 recompute fwd, 3 head fwd+bwd), one instance per call
+  int prof_layer = -1, prof_phase = 0, prof_inst = 0;
+  void prof_unit(int layer, int phase) {
+    prof_layer = layer;
+    prof_phase = phase;
+    ++prof_inst;
+  }
   bool prof_on = false;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> prof_pool;
@@ -204,7 +214,7 @@ struct Runtime {
   }
   int prof_begin(cudaStream_t st) {
     if (!prof_on) return -1;
-    ProfRec r{0, prof_event(), prof_event(), 0.0, 0, 0};
+    ProfRec r{0, prof_event(), prof_event(), 0.0, 0, 0, prof_layer * 4 + prof_phase, prof_inst};
     for (const Gpu& G : gpus)
       if (G.compute == st || G.opt_comp == st) {
         r.worker = G.id;
@@ -870,6 +880,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         wait_group(l + 1);
         uint16_t* out = x == G.xbuf[0] ? G.xbuf[1] : G.xbuf[0];
         RP_CUDA(cudaStreamWaitEvent(st, ck.ready, 0));  // x_l is overwritten next layer
+        prof_unit(l, 0);
         layer_fwd(G, l, x, G.acts[0], out);
         x = out;
       }
@@ -890,12 +901,17 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         const int l = a + i;
         wait_group(l + 1);
         uint16_t* out = (i + 1 < nl) ? G.acts[i + 1].x : G.xbuf[1];
+        prof_unit(l, 0);
         layer_fwd(G, l, x, G.acts[i], out);
         x = out;
       }
       wait_group(s.L + 1);
+      prof_unit(s.L, 3);
       head_fwd_bwd(G, x, gmb, first, grad_scale);
-      for (int i = nl - 1; i >= 0; --i) layer_bwd(G, a + i, G.acts[i], first);
+      for (int i = nl - 1; i >= 0; --i) {
+        prof_unit(a + i, 1);
+        layer_bwd(G, a + i, G.acts[i], first);
+      }
       if (in_buf) RP_CUDA(cudaEventRecord(in_buf->read, st));
     } else {  // Backward: incoming dL/dx_{b+1} from the previous slot
       Slotbuf& gi = G.hand_grad[hb];
@@ -909,7 +925,9 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         RP_CUDA(cudaStreamWaitEvent(st, ck.ready, 0));
         wait_group(l + 1);
         LayerActs& A = G.acts[0];
+        prof_unit(l, 2);
         layer_fwd(G, l, static_cast<const uint16_t*>(ck.p), A, G.xbuf[1]);  // recompute
+        prof_unit(l, 1);
         layer_bwd(G, l, A, first);
         RP_CUDA(cudaEventRecord(ck.read, st));
       }
@@ -1270,6 +1288,110 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
   });
 }
 
+// ---- host-state checkpoint / resume ------------------------------------------------
+// File: "RPCKPT01", int32 {L, h, nq, nk, m, V, ngroups, async}, then per group
+// {int64 n, int32 step, int32 pending}, then per group the fp32 master, m, v
+// and the bf16 master the GPUs upload. In async mode a group whose AdamW
+// result still waits for its p_copy (staleness 1: the next iteration uploads
+// the OLD bf16 master) is saved as pending; the pending bf16 weights are
+// bf16(fp32 master) by construction (adamw_kernel), so resume re-creates them.
+namespace {
+constexpr char kCkptMagic[8] = {'R', 'P', 'C', 'K', 'P', 'T', '0', '1'};
+struct FileCloser {
+  void operator()(FILE* f) const { if (f) std::fclose(f); }
+};
+void xwrite(FILE* f, const void* p, std::size_t n) {
+  if (n && std::fwrite(p, 1, n, f) != n) throw RtError(RP_E_INTERNAL, "checkpoint write failed");
+}
+void xread(FILE* f, void* p, std::size_t n) {
+  if (n && std::fread(p, 1, n, f) != n) throw RtError(RP_E_INPUT, "checkpoint truncated");
+}
+}  // namespace
+
+RP_API int rp_runtime_save(rp_runtime_t* p, const char* path) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    if (!path) throw RtError(RP_E_INPUT, "null path");
+    rt->sync_all();
+    std::unique_ptr<FILE, FileCloser> f(std::fopen(path, "wb"));
+    if (!f) throw RtError(RP_E_INPUT, std::string("cannot open ") + path);
+    const int ng = rt->ngroups();
+    const int32_t hdr[8] = {rt->s.L, rt->s.h, rt->s.nq, rt->s.nk, rt->s.m, rt->s.V, ng,
+                            rt->cfg.async_optimizer};
+    xwrite(f.get(), kCkptMagic, 8);
+    xwrite(f.get(), hdr, sizeof(hdr));
+    for (int g = 0; g < ng; ++g) {
+      const int64_t n = rt->host[g].n;
+      const int32_t st[2] = {rt->host[g].step, rt->pend_owner[g] >= 0 ? 1 : 0};
+      xwrite(f.get(), &n, 8);
+      xwrite(f.get(), st, 8);
+    }
+    for (int g = 0; g < ng; ++g) {
+      const auto& H = rt->host[g];
+      xwrite(f.get(), H.master, H.n * 4);
+      xwrite(f.get(), H.m, H.n * 4);
+      xwrite(f.get(), H.v, H.n * 4);
+      xwrite(f.get(), H.w16, H.n * 2);
+    }
+  });
+}
+
+RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    if (!path) throw RtError(RP_E_INPUT, "null path");
+    rt->sync_all();
+    std::unique_ptr<FILE, FileCloser> f(std::fopen(path, "rb"));
+    if (!f) throw RtError(RP_E_INPUT, std::string("cannot open ") + path);
+    char magic[8];
+    int32_t hdr[8];
+    xread(f.get(), magic, 8);
+    xread(f.get(), hdr, sizeof(hdr));
+    const int ng = rt->ngroups();
+    if (std::memcmp(magic, kCkptMagic, 8) || hdr[0] != rt->s.L || hdr[1] != rt->s.h ||
+        hdr[2] != rt->s.nq || hdr[3] != rt->s.nk || hdr[4] != rt->s.m || hdr[5] != rt->s.V ||
+        hdr[6] != ng)
+      throw RtError(RP_E_INPUT, "checkpoint does not match this model");
+    std::vector<int32_t> steps(ng), pending(ng);
+    for (int g = 0; g < ng; ++g) {
+      int64_t n;
+      int32_t st[2];
+      xread(f.get(), &n, 8);
+      xread(f.get(), st, 8);
+      if (n != rt->host[g].n) throw RtError(RP_E_INPUT, "checkpoint group size mismatch");
+      steps[g] = st[0];
+      pending[g] = st[1];
+    }
+    if (!rt->cfg.async_optimizer)
+      for (int g = 0; g < ng; ++g)
+        if (pending[g]) throw RtError(RP_E_INPUT, "async checkpoint loaded into a sync runtime");
+    for (int g = 0; g < ng; ++g) {
+      auto& H = rt->host[g];
+      xread(f.get(), H.master, H.n * 4);
+      xread(f.get(), H.m, H.n * 4);
+      xread(f.get(), H.v, H.n * 4);
+      xread(f.get(), H.w16, H.n * 2);
+      H.step = steps[g];
+    }
+    // device caches hold stale versions; pending AdamW outputs are re-created
+    for (auto& G : rt->gpus)
+      for (auto& D : G.groups) D.loaded[0] = D.loaded[1] = -1;
+    std::vector<uint16_t> tmp;
+    for (int g = 0; g < ng; ++g) {
+      rt->pend_owner[g] = -1;
+      if (!pending[g]) continue;
+      auto& H = rt->host[g];
+      rp::rt::Gpu& G = rt->gpus[0];
+      rt->set_dev(G);
+      tmp.resize((std::size_t)H.n);
+      for (int64_t i = 0; i < H.n; ++i) tmp[(std::size_t)i] = f32_to_bf16_host(H.master[i]);
+      RP_CUDA(cudaMemcpy(G.groups[g].pend, tmp.data(), H.n * 2, cudaMemcpyHostToDevice));
+      rt->pend_owner[g] = 0;
+    }
+    rt->grads_pending = false;
+  });
+}
+
 RP_API int rp_forward_backward(rp_runtime_t* p, const int32_t* tokens, const int32_t* labels,
                                float* loss) {
   return rt_guard([&] {
@@ -1368,6 +1490,53 @@ RP_API int rp_runtime_profile_read(rp_runtime_t* p, double* time_ms, double* wor
       time_ms[r.cat] += ms;
       work[r.cat] += r.work;
       launches[r.cat] += 1;
+    }
+  });
+}
+
+// Measured cost table: per decoder layer the mean kernel time
+// of one micro-batch's forward (t_fwd) and of forward + backward (t_bwd, the
+// reference's fused/backward stage unit, cost_model.hpp:194), from the
+// profiled steps; the head row is the LM-head+CE kernel time (t_bwd = all
+// of it, t_fwd = a third: the logits GEMM is one of its three GEMMs). Byte columns come from the cost
+// model. Layers without samples keep the cost model's row.
+RP_API int rp_runtime_measured_costs(rp_runtime_t* p, rp_layer_cost_t* out, int32_t cap,
+                                     int32_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    rt->sync_all();
+    const int L = rt->s.L;
+    *n = L + 1;
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "cost capacity");
+    // per call instance: (unit, summed kernel ns)
+    std::vector<std::pair<int, double>> inst;
+    for (const auto& r : rt->prof) {
+      if (r.lane != 0 || r.unit < 0) continue;
+      if ((int)inst.size() <= r.inst) inst.resize(r.inst + 1, {-1, 0.0});
+      float ms = 0.f;
+      RP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      inst[r.inst].first = r.unit;
+      inst[r.inst].second += (double)ms * 1e6;
+    }
+    std::vector<double> sum((L + 1) * 4, 0.0), cnt((L + 1) * 4, 0.0);
+    for (const auto& [u, ns] : inst)
+      if (u >= 0 && u < (L + 1) * 4) sum[u] += ns, cnt[u] += 1;
+    for (int l = 0; l <= L; ++l) {
+      rp_layer_cost_t c{rt->costs[l].t_fwd_ns, rt->costs[l].t_bwd_ns, rt->costs[l].param_bytes,
+                        rt->costs[l].act_ckpt_bytes, rt->costs[l].act_full_bytes};
+      if (l < L) {
+        const double nf = cnt[l * 4 + 0] + cnt[l * 4 + 2], nb = cnt[l * 4 + 1];
+        if (nf > 0 && nb > 0) {
+          const double tf = (sum[l * 4 + 0] + sum[l * 4 + 2]) / nf;
+          c.t_fwd_ns = (int64_t)std::llround(tf);
+          c.t_bwd_ns = (int64_t)std::llround(tf + sum[l * 4 + 1] / nb);
+        }
+      } else if (cnt[L * 4 + 3] > 0) {
+        const double tb = sum[L * 4 + 3] / cnt[L * 4 + 3];
+        c.t_bwd_ns = (int64_t)std::llround(tb);
+        c.t_fwd_ns = (int64_t)std::llround(tb / 3.0);  // logits GEMM = 1 of its 3 GEMMs
+      }
+      out[l] = c;
     }
   });
 }

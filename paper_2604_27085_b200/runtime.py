@@ -122,6 +122,24 @@ class RoundPipe:
         self._call("rp_runtime_costs", self.h, out.ctypes.data_as(VP), I32(len(out)), C.byref(n))
         return out[: n.value]
 
+    def save(self, path: str):
+        """Checkpoint the host state (fp32 master, Adam m/v, steps, bf16 master)."""
+        self._call("rp_runtime_save", self.h, str(path).encode())
+
+    def load(self, path: str):
+        """Resume from rp_runtime_save's file (same model); device caches reset."""
+        self._call("rp_runtime_load", self.h, str(path).encode())
+
+    def measured_costs(self) -> np.ndarray:
+        """Cost table measured on the profiled steps: per layer
+        t_fwd / t_bwd (fwd+bwd) kernel ns of one micro-batch; bytes from the
+        cost model. Pass as ``costs=`` to re-plan on measured costs."""
+        out = np.zeros(4096, dtype=COST_DTYPE)
+        n = I32()
+        self._call("rp_runtime_measured_costs", self.h, out.ctypes.data_as(VP), I32(len(out)),
+                   C.byref(n))
+        return out[: n.value]
+
     # -- parameters --------------------------------------------------------------------
     def param_count(self, group: int) -> int:
         n = I64()

@@ -21,7 +21,7 @@ def rnd(*shape, seed=0, scale=1.0, dtype=torch.bfloat16):
     return (torch.randn(*shape, device="cuda", generator=g) * scale).to(dtype)
 
 
-@pytest.mark.parametrize("T,h", [(256, 256), (1024, 4096), (77, 2048)])
+@pytest.mark.parametrize("T,h", [(256, 256), (1024, 4096), (77, 2048), (300, 5120), (64, 8192), (33, 3072)])
 def test_rmsnorm_fwd_bwd(T, h):
     from paper_2604_27085_b200 import kernels as K
     x, w, dy = rnd(T, h, seed=1), rnd(h, seed=2, scale=0.5) + 1, rnd(T, h, seed=3)
@@ -183,7 +183,8 @@ def _attn_ref(q, k, v, seq, nq, nk, hd):
 
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
-                                            (2048, 1024, 16, 4, 128)])
+                                            (2048, 1024, 16, 4, 128), (768, 256, 6, 2, 128),
+                                            (1024, 1024, 16, 2, 128)])
 def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K
     qkv = rnd(T, (nq + 2 * nk) * hd, seed=30, scale=2.0)
@@ -206,7 +207,8 @@ def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
 
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
-                                            (2048, 1024, 16, 4, 128)])
+                                            (2048, 1024, 16, 4, 128), (768, 256, 6, 2, 128),
+                                            (1024, 1024, 16, 2, 128)])
 def test_flash_attention_bwd_tcgen05(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K
     qkv = rnd(T, (nq + 2 * nk) * hd, seed=40, scale=1.5)

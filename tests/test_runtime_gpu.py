@@ -159,3 +159,80 @@ def test_step_parity_four_workers_seven_slots(mode):
     for g in range(4):  # FIFO per worker: measured intervals do not overlap
         ev = tl[tl["gpu"] == g]
         assert np.all(ev["start_ns"][1:] >= ev["end_ns"][:-1] - 1000)
+
+
+@pytest.mark.parametrize("mode", ["async", "sync"])
+def test_checkpoint_resume(mode, tmp_path):
+    """Host-state checkpoint (SURVEY 8(f)3): save after 2 steps, continue 2;
+    a fresh runtime resumed from the file reproduces steps 3-4 (losses and the
+    fp32 master), including async mode's unpublished staleness-1 update."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    params = O.init_params(s, seed=0)
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+
+    def make():
+        rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=1,
+                       async_optimizer=(mode == "async"),
+                       adam=AdamW(HP["lr"], HP["betas"], HP["eps"], HP["weight_decay"]),
+                       skip_init=True)
+        return rt
+
+    rt = make()
+    rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+    for _ in range(2):
+        rt.forward_backward(tok.numpy(), lab.numpy())
+        rt.step()
+    ck = str(tmp_path / "state.rpck")
+    rt.save(ck)
+    ref = []
+    for _ in range(2):
+        ref.append(rt.forward_backward(tok.numpy(), lab.numpy()))
+        rt.step()
+    rt.sync()
+    m_ref = rt.read_state(s.layers, which=0)
+    rt.close()
+    rt2 = make()
+    rt2.load(ck)
+    got = []
+    for _ in range(2):
+        got.append(rt2.forward_backward(tok.numpy(), lab.numpy()))
+        rt2.step()
+    rt2.sync()
+    m_got = rt2.read_state(s.layers, which=0)
+    rt2.close()
+    for a, b in zip(got, ref):
+        assert abs(a - b) / abs(b) < 1e-4, (got, ref)
+    for k in m_ref:
+        a, b = np.asarray(m_got[k], np.float64), np.asarray(m_ref[k], np.float64)
+        assert np.linalg.norm(a - b) <= 1e-5 * np.linalg.norm(b) + 1e-9, k
+
+
+def test_measured_costs_replan():
+    """Measured cost table: a profiled step yields
+    per-layer kernel times; re-planning N=4 on them with the reference
+    partitioner and running that plan gives the same first-step loss."""
+    from paper_2604_27085_b200.planner import Planner
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    params = O.init_params(s, seed=0)
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=1,
+                   async_optimizer=False, adam=AdamW(**{"lr": 0.0}), skip_init=True)
+    rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+    rt.profile(True)
+    loss1 = rt.forward_backward(tok.numpy(), lab.numpy())
+    rt.sync()
+    mc = rt.measured_costs()
+    rt.profile(False)
+    rt.close()
+    assert len(mc) == s.layers + 1
+    assert (mc["t_fwd_ns"] > 0).all() and (mc["t_bwd_ns"] > mc["t_fwd_ns"]).all()
+    plan = Planner().optimal_partition(mc, 4, 4)
+    rt4 = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=4,
+                    async_optimizer=False, adam=AdamW(**{"lr": 0.0}), costs=mc, skip_init=True)
+    rt4.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+    assert rt4.plan()[0] == plan
+    loss4 = rt4.forward_backward(tok.numpy(), lab.numpy())
+    rt4.close()
+    assert abs(loss4 - loss1) / loss1 < 1e-3

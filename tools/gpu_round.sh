@@ -6,12 +6,15 @@ TAG=${1:-r}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 if [ "$2" != "skip-tests" ]; then
-  timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.txt 2>&1
-  echo "pytest exit $?" >> gpurun_out/${TAG}_pytest_gpu.txt
+  : > gpurun_out/${TAG}_pytest_gpu.txt
+  for f in tests/test_kernels_gpu.py tests/test_gemm_gpu.py tests/test_runtime_gpu.py; do
+    timeout 420 python -m pytest $f -m gpu -q >> gpurun_out/${TAG}_pytest_gpu.txt 2>&1
+    echo "pytest $f exit $?" >> gpurun_out/${TAG}_pytest_gpu.txt
+  done
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1
   echo "smoke exit $?" >> gpurun_out/${TAG}_smoke.txt
 fi
-timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 900 python bench.py --report-dir gpurun_out > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 echo "bench exit $?" >> gpurun_out/${TAG}_bench.err
 timeout 300 python tools/bench_gemm.py > gpurun_out/${TAG}_gemm.jsonl 2>&1
 timeout 300 python tools/bench_kernels.py > gpurun_out/${TAG}_kernels.jsonl 2>&1
