@@ -290,9 +290,13 @@ __global__ void __launch_bounds__(384, 1)
 // the two softmax warpgroups alternate with the tensor core, which runs
 //   S/dP_a(j) | grads_b(j-1) | S/dP_b(j) | grads_a(j) | S/dP_a(j+1) | ...
 // so each warpgroup's P^T/dS^T work hides behind ~1024 cycles of the other
-// head's MMAs. Query tiles of 64 stream through a 3-slot (Q, dO, lse, delta)
-// ring in the order (j, a), (j, b), (j+1, a), ...
+// head's MMAs. P^T and dS^T (bf16) are written back into the TMEM columns of
+// the S^T / dP^T they came from and feed the dV / dK MMAs as TMEM A operands
+// (tcgen05.mma ... [a_tmem]); the shared memory this saves deepens the
+// (Q, dO, lse, delta) ring to 4 slots, consumed in the order (j, a), (j, b),
+// (j+1, a), ... so each tile's TMA load has ~2 K cycles of lead.
 constexpr int A2_THREADS = 384;
+constexpr int A2_NST = 4;
 
 template <int HD>
 struct Dkv2Smem {
@@ -302,10 +306,8 @@ struct Dkv2Smem {
   static constexpr int R0 = V + NSUB * SUB128;        // ring slot s at R0 + s*STAGE
   static constexpr int STAGE = 2 * NSUB * SUB64;      // Q + dO of one (tile, head)
   static constexpr int DO_OFF = NSUB * SUB64;
-  static constexpr int PS = R0 + 3 * STAGE;           // head w: P^T at PS + w*PS_BUF, dS^T after
-  static constexpr int PS_BUF = 2 * (A_BK * A_BQ * 2);
-  static constexpr int LD = PS + 2 * PS_BUF;          // [3][2][A_BQ] lse, delta
-  static constexpr int BAR = LD + 3 * 2 * A_BQ * 4;
+  static constexpr int LD = R0 + A2_NST * STAGE;      // [A2_NST][2][A_BQ] lse, delta
+  static constexpr int BAR = LD + A2_NST * 2 * A_BQ * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
@@ -326,13 +328,12 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* kv_full = bar + 0;
-  uint64_t* st_full = bar + 1;   // [3]
-  uint64_t* st_empty = bar + 4;  // [3]
-  uint64_t* sd_full = bar + 7;   // [2] per head
-  uint64_t* ps_full = bar + 9;   // [2]
-  uint64_t* ps_free = bar + 11;  // [2]
-  uint64_t* acc_done = bar + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t* st_full = bar + 1;            // [A2_NST]
+  uint64_t* st_empty = bar + 1 + A2_NST;  // [A2_NST]
+  uint64_t* sd_full = bar + 1 + 2 * A2_NST;  // [2] per head
+  uint64_t* ps_full = sd_full + 2;           // [2]
+  uint64_t* acc_done = ps_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int kb = blockIdx.x, ha = 2 * (int)blockIdx.y;
@@ -347,14 +348,13 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < A2_NST; ++i) {
       mbar_init(&st_full[i], 1);
       mbar_init(&st_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&ps_full[i], 4);
-      mbar_init(&ps_free[i], 1);
     }
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -364,7 +364,9 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: head w: S^T at w*128 (64 cols), dP^T at w*128 + 64; dV at 256, dK at 384
+  // TMEM: head w: S^T at w*128 (64 cols), dP^T at w*128 + 64; after the
+  // softmax pass P^T (bf16 pairs) occupies w*128 + [0, 32) and dS^T
+  // w*128 + 64 + [0, 32). dV at 256, dK at 384.
   const uint32_t TM_DV = 256, TM_DK = 384;
 
   if (warp == 0 && lane == 0) {
@@ -374,8 +376,8 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
       tma_load_2d(sm + L::V + sub * SUB128, &tm_v, kv_full, kvh * HD + 64 * sub, k0);
     }
     for (int idx = 0; idx < 2 * nqt; ++idx) {
-      const int s = idx % 3, w = idx & 1, hq = ha + w;
-      mbar_wait(&st_empty[s], ((idx / 3) & 1) ^ 1);
+      const int s = idx % A2_NST, w = idx & 1, hq = ha + w;
+      mbar_wait(&st_empty[s], ((idx / A2_NST) & 1) ^ 1);
       const int qs = k0 + (idx >> 1) * A_BQ;
       uint8_t* qd = sm + L::R0 + s * L::STAGE;
       mbar_arrive_expect_tx(&st_full[s], L::STAGE + 2 * A_BQ * 4);
@@ -387,56 +389,58 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
       bulk_load_1d(ld, lse + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
       bulk_load_1d(ld + A_BQ, delta + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {  // whole warp: uniform descriptors, elected issue
     constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A_BQ, 0, 0);   // K-major x K-major
     constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);     // K-major x MN-major
     const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
-    auto stage = [&](int idx) { return smem_u32(sm + L::R0 + (idx % 3) * L::STAGE); };
+    auto stage = [&](int idx) { return smem_u32(sm + L::R0 + (idx % A2_NST) * L::STAGE); };
     auto issue_sdp = [&](int j, int w) {
       const int idx = 2 * j + w;
-      mbar_wait(&st_full[idx % 3], (idx / 3) & 1);
+      mbar_wait(&st_full[idx % A2_NST], (idx / A2_NST) & 1);
       tc_fence_after();
       const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
-        const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
-        umma_f16(tmem + w * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
-                 umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
-        umma_f16(tmem + w * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
-                 umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
+          umma_f16(tmem + w * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
+                   umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
+          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
+                   umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&sd_full[w]);
       }
-      umma_commit(&sd_full[w]);
+      __syncwarp();
     };
     auto issue_grads = [&](int j, int w) {
       const int idx = 2 * j + w;
       mbar_wait(&ps_full[w], j & 1);
       tc_fence_after();
       const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
-      const uint32_t p_addr = smem_u32(sm + L::PS + w * L::PS_BUF);
-      const uint32_t ds_addr = p_addr + A_BK * A_BQ * 2;
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < A_BQ / 16; ++kk) {
-        const uint64_t pa = umma_desc_sw128(p_addr + kk * 32, 16, 1024);
-        const uint64_t da = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
-        const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
-        const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
-        umma_f16(tmem + TM_DV, pa, ob, idesc_g, (idx | kk) != 0);
-        umma_f16(tmem + TM_DK, da, qb, idesc_g, (idx | kk) != 0);
+        for (int kk = 0; kk < A_BQ / 16; ++kk) {
+          const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
+          const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
+          umma_f16_ts(tmem + TM_DV, tmem + w * 128 + kk * 8, ob, idesc_g, (idx | kk) != 0);
+          umma_f16_ts(tmem + TM_DK, tmem + w * 128 + 64 + kk * 8, qb, idesc_g, (idx | kk) != 0);
+        }
+        umma_commit(&st_empty[idx % A2_NST]);
       }
-      umma_commit(&ps_free[w]);
-      umma_commit(&st_empty[idx % 3]);
+      __syncwarp();
     };
     mbar_wait(kv_full, 0);
     issue_sdp(0, 0);
     issue_sdp(0, 1);
     for (int j = 0; j < nqt; ++j) {
       issue_grads(j, 0);
-      if (j + 1 < nqt) issue_sdp(j + 1, 0);
+      if (j + 1 < nqt) issue_sdp(j + 1, 0);  // in-order after grads_a(j) read P^T_a
       issue_grads(j, 1);
       if (j + 1 < nqt) issue_sdp(j + 1, 1);
     }
-    umma_commit(acc_done);
+    if (elect_one()) umma_commit(acc_done);
+    __syncwarp();
   } else if (warp >= 4) {
     // two softmax warpgroups: w = head slot, thread = key row
     const int w = (warp - 4) >> 2, quarter = warp & 3;
@@ -444,21 +448,15 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
     const int key = k0 + r;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const float sl2 = scale * kLog2e;
-    uint8_t* prow = sm + L::PS + w * L::PS_BUF + (r >> 3) * 1024 + (r & 7) * 128;
-    uint8_t* drow = prow + A_BK * A_BQ * 2;
     for (int j = 0; j < nqt; ++j) {
-      const int idx = 2 * j + w, s = idx % 3;
+      const int idx = 2 * j + w, s = idx % A2_NST;
       const int qs = k0 + j * A_BQ;
       const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + s * 2 * A_BQ;
       const float* del_t = lse_t + A_BQ;
-      mbar_wait(&st_full[s], (idx / 3) & 1);  // lse/delta visibility (already complete)
+      mbar_wait(&st_full[s], (idx / A2_NST) & 1);  // lse/delta visibility (already complete)
       mbar_wait(&sd_full[w], j & 1);
       tc_fence_after();
       const bool diag = qs < k0 + A_BK;  // tile overlaps this key block's diagonal
-      // grads of (j-1, w) were issued before S/dP(j, w), so their release of
-      // this head's P^T / dS^T buffers has already landed
-      if (j >= 1) mbar_wait(&ps_free[w], (j - 1) & 1);
-      tc_fence_after();
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         uint32_t sv[32], dpv[32], pk[16], dk2[16];
@@ -479,16 +477,11 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
           pk[i / 2] = pack_bf16x2(p0, p1);
           dk2[i / 2] = pack_bf16x2(d0, d1);
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int off = ((half * 4 + q4) ^ (r & 7)) << 4;
-          *reinterpret_cast<uint4*>(prow + off) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-          *reinterpret_cast<uint4*>(drow + off) =
-              make_uint4(dk2[q4 * 4], dk2[q4 * 4 + 1], dk2[q4 * 4 + 2], dk2[q4 * 4 + 3]);
-        }
+        // bf16 pairs back over columns this thread has already read
+        tmem_st_32x32b_x16(lane_base + w * 128 + half * 16, pk);
+        tmem_st_32x32b_x16(lane_base + w * 128 + 64 + half * 16, dk2);
       }
-      fence_proxy_async();
+      tmem_st_wait_all();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps_full[w]);
@@ -739,6 +732,10 @@ __global__ void __launch_bounds__(384, 1)
 // CTA = 128 queries x TWO query heads of one KV group: K_j / V_j (64 keys) are
 // loaded once for both heads, and the two softmax warpgroups alternate with
 // the tensor core:  S/dP_a(j) | dQ_b(j-1) | S/dP_b(j) | dQ_a(j) | S/dP_a(j+1) ...
+// dS (bf16 pairs) goes back into the TMEM columns of the S it came from and is
+// the TMEM A operand of dQ += dS K; the K/V ring is 3 deep.
+constexpr int B2_NST = 3;
+
 template <int HD>
 struct Dq2Smem {
   static constexpr int NSUB = HD / 64;
@@ -746,8 +743,7 @@ struct Dq2Smem {
   static constexpr int Q0 = 0;                       // head w: Q at Q0 + 2w*QT, dO after
   static constexpr int KV0 = Q0 + 4 * QT;            // stage s: K at KV0 + s*STAGE, V after
   static constexpr int STAGE = 2 * NSUB * SUB64;
-  static constexpr int DS = KV0 + 2 * STAGE;         // head w: dS [128 q][64 keys]
-  static constexpr int BAR = DS + 2 * SUB128;
+  static constexpr int BAR = KV0 + B2_NST * STAGE;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
@@ -767,13 +763,12 @@ __global__ void __launch_bounds__(384, 1)
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* sd_full = bar + 5;   // [2] per head
-  uint64_t* ds_full = bar + 7;   // [2]
-  uint64_t* ds_free = bar + 9;   // [2]
-  uint64_t* dq_done = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar + 1;            // [B2_NST]
+  uint64_t* kv_empty = bar + 1 + B2_NST;  // [B2_NST]
+  uint64_t* sd_full = kv_empty + B2_NST;  // [2] per head
+  uint64_t* ds_full = sd_full + 2;        // [2]
+  uint64_t* dq_done = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / B_Q;
@@ -789,12 +784,13 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < B2_NST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sd_full[i], 1);
       mbar_init(&ds_full[i], 4);
-      mbar_init(&ds_free[i], 1);
     }
     mbar_init(dq_done, 1);
     fence_barrier_init();
@@ -804,7 +800,8 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM: head w: S at w*128 (64 cols), dP at w*128 + 64; dQ_w at 256 + w*HD
+  // TMEM: head w: S at w*128 (64 cols; dS pairs overwrite [0, 32) of it),
+  // dP at w*128 + 64; dQ_w at 256 + w*HD
 
   if (warp == 0 && lane == 0) {
     mbar_arrive_expect_tx(q_full, 4 * L::QT);
@@ -816,8 +813,8 @@ __global__ void __launch_bounds__(384, 1)
                     (ha + w) * HD + 64 * sub, q0);
       }
     for (int j = 0; j < ntiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+      const int st = j % B2_NST;
+      mbar_wait(&kv_empty[st], ((j / B2_NST) & 1) ^ 1);
       const int k0 = s0 + j * B_K;
       uint8_t* kd = sm + L::KV0 + st * L::STAGE;
       mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
@@ -827,52 +824,56 @@ __global__ void __launch_bounds__(384, 1)
                     k0);
       }
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {  // whole warp: uniform descriptors, elected issue
     constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
     constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
     auto issue_sdp = [&](int j, int w) {
       if (w == 0) {
-        mbar_wait(&kv_full[j & 1], (j >> 1) & 1);
+        mbar_wait(&kv_full[j % B2_NST], (j / B2_NST) & 1);
         tc_fence_after();
       }
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j & 1) * L::STAGE);
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % B2_NST) * L::STAGE);
       const uint32_t v_addr = k_addr + NSUB * SUB64;
       const uint32_t q_addr = smem_u32(sm + L::Q0 + 2 * w * L::QT), do_addr = q_addr + L::QT;
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
-        const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
-        umma_f16(tmem + w * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
-                 umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
-        umma_f16(tmem + w * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
-                 umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
+          const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
+          umma_f16(tmem + w * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
+                   umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
+          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
+                   umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&sd_full[w]);
       }
-      umma_commit(&sd_full[w]);
+      __syncwarp();
     };
     auto issue_dq = [&](int j, int w) {
       mbar_wait(&ds_full[w], j & 1);
       tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j & 1) * L::STAGE);
-      const uint32_t ds_addr = smem_u32(sm + L::DS + w * SUB128);
+      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % B2_NST) * L::STAGE);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < B_K / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
-        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
-        umma_f16(tmem + 256 + w * HD, ad, bd, idesc_q, (j | kk) != 0);
+        for (int kk = 0; kk < B_K / 16; ++kk) {
+          const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
+          umma_f16_ts(tmem + 256 + w * HD, tmem + w * 128 + kk * 8, bd, idesc_q, (j | kk) != 0);
+        }
+        if (w == 1) umma_commit(&kv_empty[j % B2_NST]);
       }
-      umma_commit(&ds_free[w]);
-      if (w == 1) umma_commit(&kv_empty[j & 1]);
+      __syncwarp();
     };
     mbar_wait(q_full, 0);
     issue_sdp(0, 0);
     issue_sdp(0, 1);
     for (int j = 0; j < ntiles; ++j) {
       issue_dq(j, 0);
-      if (j + 1 < ntiles) issue_sdp(j + 1, 0);
+      if (j + 1 < ntiles) issue_sdp(j + 1, 0);  // in-order after dQ_a(j) read dS_a
       issue_dq(j, 1);
       if (j + 1 < ntiles) issue_sdp(j + 1, 1);
     }
-    umma_commit(dq_done);
+    if (elect_one()) umma_commit(dq_done);
+    __syncwarp();
   } else if (warp >= 4) {
     const int w = (warp - 4) >> 2, quarter = warp & 3;
     const int r = quarter * 32 + lane;  // query row
@@ -881,12 +882,8 @@ __global__ void __launch_bounds__(384, 1)
     const float sl2 = scale * kLog2e;
     const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
     const float dl = delta[(long long)h * T + qrow];
-    uint8_t* ds_row = sm + L::DS + w * SUB128 + (r >> 3) * 1024 + (r & 7) * 128;
     for (int j = 0; j < ntiles; ++j) {
       mbar_wait(&sd_full[w], j & 1);
-      tc_fence_after();
-      // dQ(j-1, w) was issued before S/dP(j, w): its release of dS_w has landed
-      if (j >= 1) mbar_wait(&ds_free[w], (j - 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -905,14 +902,11 @@ __global__ void __launch_bounds__(384, 1)
             if (kbase + i + 1 > qrow) p1 = 0.f;
           }
           pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
-                                  p1 * (__uint_as_float(dpv[i + 1]) - dl));
+                                      p1 * (__uint_as_float(dpv[i + 1]) - dl));
         }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          *reinterpret_cast<uint4*>(ds_row + (((half * 4 + q4) ^ (r & 7)) << 4)) =
-              make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+        tmem_st_32x32b_x16(lane_base + w * 128 + half * 16, pk);  // over read columns
       }
-      fence_proxy_async();
+      tmem_st_wait_all();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ds_full[w]);

@@ -381,8 +381,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       for (int sub = 0; sub < NSUB; ++sub)
         tma_load_2d(dst + sub * SUB, map, &kv_full[slot], kvh * HD + 64 * sub, k0);
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // (whole warp: uniform descriptors; one elected lane issues)
     constexpr uint32_t idesc_s = umma_idesc_bf16(TILE, TILE, 0, 0);
     constexpr uint32_t idesc_o = umma_idesc_bf16(TILE, HD, 0, 1);
     const uint32_t q_addr = smem_u32(sm + L::Q0);
@@ -391,32 +392,39 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % 3], (idx / 3) & 1); };
     auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T
       const uint32_t qa = q_addr + w * L::QT, ka = ring(2 * j);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-        umma_f16(tmem + w * TILE, umma_desc_sw128(qa + off, 16, 1024),
-                 umma_desc_sw128(ka + off, 16, 1024), idesc_s, kk != 0);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
+          umma_f16(tmem + w * TILE, umma_desc_sw128(qa + off, 16, 1024),
+                   umma_desc_sw128(ka + off, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&s_full[w]);
       }
-      umma_commit(&s_full[w]);
+      __syncwarp();
     };
     auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j
       mbar_wait(&p_full[w], j & 1);
       tc_fence_after();
       const uint32_t pa = p_addr + w * 2 * SUB, va = ring(2 * j + 1);
+      if (elect_one()) {
 #pragma unroll
-      for (int kk = 0; kk < TILE / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = umma_desc_sw128(va + kk * 2048, SUB, 1024);
-        umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+        for (int kk = 0; kk < TILE / 16; ++kk) {
+          const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
+          const uint64_t bd = umma_desc_sw128(va + kk * 2048, SUB, 1024);
+          umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+        }
+        umma_commit(&o_done[w]);
       }
-      umma_commit(&o_done[w]);
+      __syncwarp();
     };
     mbar_wait(q_full, 0);
     wait_kv(0);
     tc_fence_after();
     issue_s(0, 0);
     issue_s(1, 0);
-    umma_commit(&kv_empty[0]);
+    if (elect_one()) umma_commit(&kv_empty[0]);
+    __syncwarp();
     for (int j = 0; j < ntiles; ++j) {
       wait_kv(2 * j + 1);
       tc_fence_after();
@@ -428,10 +436,12 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         issue_s(0, j + 1);  // S0 was read before P0_j was published
       }
       issue_pv(1, j);
-      umma_commit(&kv_empty[(2 * j + 1) % 3]);
+      if (elect_one()) umma_commit(&kv_empty[(2 * j + 1) % 3]);
+      __syncwarp();
       if (more) {
         issue_s(1, j + 1);
-        umma_commit(&kv_empty[(2 * j + 2) % 3]);
+        if (elect_one()) umma_commit(&kv_empty[(2 * j + 2) % 3]);
+        __syncwarp();
       }
     }
   } else if (warp >= 4) {
@@ -461,9 +471,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         for (int c = 0; c < TILE; ++c)
           if (c > r) s[c] = -INFINITY;
       }
-      float mx = -INFINITY;
+      float mx8[8];  // 8 independent max chains (latency, not a 128-deep chain)
 #pragma unroll
-      for (int c = 0; c < TILE; ++c) mx = fmaxf(mx, s[c]);
+      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+#pragma unroll
+      for (int c = 8; c < TILE; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float mxs = mx * sl2;
       bool o_ready = false;
       if (j == 0) {
@@ -492,21 +506,26 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         mbar_wait(&o_done[w], (j - 1) & 1);
         tc_fence_after();
       }
-      float lsum = 0.f;
+      // P = 2^(s*scale*log2e - m); four independent row-sum chains
+      float2 lsum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+      const float2 sl2v = make_float2(sl2, sl2), negm = make_float2(-m, -m);
 #pragma unroll
       for (int ch = 0; ch < TILE / 8; ++ch) {  // 16-byte chunks of the swizzled row
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = ex2(fmaf(s[ch * 8 + 2 * e], sl2, -m));
-          const float p1 = ex2(fmaf(s[ch * 8 + 2 * e + 1], sl2, -m));
-          lsum += p0 + p1;
-          pk[e] = pack_bf16x2(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(s[ch * 8 + 2 * e], s[ch * 8 + 2 * e + 1]), sl2v, negm);
+          const float2 pv = make_float2(ex2(x.x), ex2(x.y));
+          lsum4[e] = __fadd2_rn(lsum4[e], pv);
+          pk[e] = pack_bf16x2(pv.x, pv.y);
         }
         const int sub = ch >> 3, c8 = ch & 7;
         *reinterpret_cast<uint4*>(p_row + sub * SUB + ((c8 ^ (r & 7)) << 4)) =
             make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
+      const float2 ls = __fadd2_rn(__fadd2_rn(lsum4[0], lsum4[1]), __fadd2_rn(lsum4[2], lsum4[3]));
+      const float lsum = ls.x + ls.y;
       l += lsum;
       fence_proxy_async();
       tc_fence_before();
@@ -583,12 +602,12 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   static const bool force_v1 = getenv("RP_ATTN_FWD_V1") != nullptr;
   if ((nq / nk) % 2 == 0 && !force_v1) {  // two heads of one KV group per CTA
     auto kern = attn_fwd_pp_kernel<HD>;
-    static bool cfg = false;
-    if (!cfg) {
+    static bool cfg_pp = false;
+    if (!cfg_pp) {
       if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                PpSmem<HD>::BYTES) != cudaSuccess)
         return RP_E_CUDA;
-      cfg = true;
+      cfg_pp = true;
     }
     dim3 grid(T / TILE, nq / 2);
     kern<<<grid, PP_THREADS, PpSmem<HD>::BYTES, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq,

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -46,6 +48,7 @@ struct Params {
   const __nv_bfloat16* R;  // optional bf16 residual for EPI_BF16
   long long ldr;
   int vec;                 // 16-byte vector stores/loads legal for D (and R)
+  int tma_out;             // fp32 D written through the TMA map (pair kernel)
 };
 
 // Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
@@ -246,7 +249,10 @@ constexpr int P_STAGES = 6;
 constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB
 constexpr int P_B_BYTES = 128 * BK * 2;     // 16 KB
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+// fp32 epilogue staging for TMA store / reduce-add: per epilogue warp two
+// 32 x 32 fp32 chunks (SWIZZLE_128B rows of 128 B)
+constexpr int P_EPI_BYTES = 4 * 2 * 32 * 32 * 4;  // 32 KB
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + P_EPI_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -289,14 +295,44 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {  // remote a
       : "memory");
 }
 
+// fp32 tile chunk smem -> global through the TMA: plain store, or an L2-side
+// add (cp.reduce.async.bulk .add.f32) for the accumulate epilogue, so the
+// epilogue never waits on a global load of the old value.
+template <bool ADD>
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int32_t c0,
+                                             int32_t c1) {
+  if (ADD)
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::
+            "l"(reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int A_MN, int B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
-                     const __grid_constant__ CUtensorMap tma_b, Params p, int n_fastest) {
+                     const __grid_constant__ CUtensorMap tma_b,
+                     const __grid_constant__ CUtensorMap tma_d, Params p, int n_fastest) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+  uint8_t* epi_smem = smem + P_STAGES * P_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + P_EPI_BYTES);
   uint64_t* empty = full + P_STAGES;
   uint64_t* acc_full = empty + P_STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
@@ -403,6 +439,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue (both CTAs, 128 rows each) ----------------
     const int q = warp & 3;
+    uint32_t epi_chunk_no = 0;  // fp32 TMA epilogue: chunks issued by this warp
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs) {
@@ -410,20 +447,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tile_mn(tile, m0, n0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + 128 * rank + q * 32 + lane;
+      const int row0 = m0 + 128 * rank + q * 32;
+      const int row = row0 + lane;
       const bool row_ok = row < p.M;
+      if (EPI != EPI_BF16 && p.tma_out) {
+        // fp32: 32x32 chunks through swizzled smem and the TMA (store or L2 add),
+        // two chunk buffers per warp in flight
+        uint8_t* wbuf = epi_smem + q * (2 * 4096);
+        // chunks wholly outside D are skipped (warp-uniform), so every written
+        // buffer belongs to a committed store and "two chunks ago" holds
+        const int c_end = min(BN, p.N - n0);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
-        tmem_ld_wait();
-        epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
+        for (int c = 0; c < c_end && row0 < p.M; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+          tmem_ld_wait();
+          uint8_t* buf = wbuf + (epi_chunk_no++ & 1) * 4096;  // alternates across tiles too
+          if (lane == 0) bulk_wait_read<1>();  // the store from this buffer two chunks ago
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            *reinterpret_cast<uint4*>(buf + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d<EPI == EPI_F32_ACC>(&tma_d, buf, n0 + c, row0);
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+          tmem_ld_wait();
+          epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_leader(&acc_empty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (EPI != EPI_BF16 && p.tma_out && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync();
@@ -468,6 +535,22 @@ bool make_map(CUtensorMap* map, const void* base, long long rows, long long cols
          CUDA_SUCCESS;
 }
 
+// fp32 [rows, cols] (row pitch ld elements), box {32 cols, 32 rows}, SWIZZLE_128B:
+// the epilogue's TMA store / reduce-add target
+bool make_map_f32(CUtensorMap* map, const void* base, long long rows, long long cols,
+                  long long ld) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t elem[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+            elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -479,8 +562,8 @@ int num_sms() {
 }
 
 template <int A_MN, int B_MN, int EPI>
-cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, bool pair,
-                   int n_fastest, cudaStream_t stream) {
+cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+                   const Params& p, bool pair, int n_fastest, cudaStream_t stream) {
   if (pair) {
     auto kern = gemm_pair_kernel<A_MN, B_MN, EPI>;
     static bool configured = false;
@@ -492,7 +575,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
     }
     const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
     const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    kern<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, p, n_fastest);
+    kern<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, td, p, n_fastest);
     return cudaGetLastError();
   }
   auto kern = gemm_kernel<A_MN, B_MN, EPI>;
@@ -510,12 +593,13 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p
 }
 
 template <int A_MN, int B_MN>
-cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p,
-                         bool pair, int n_fastest, cudaStream_t s) {
+cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+                         const CUtensorMap& td, const Params& p, bool pair, int n_fastest,
+                         cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, p, pair, n_fastest, s);
-    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, p, pair, n_fastest, s);
-    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, p, pair, n_fastest, s);
+    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, td, p, pair, n_fastest, s);
+    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, td, p, pair, n_fastest, s);
+    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, td, p, pair, n_fastest, s);
   }
 }
 
@@ -543,17 +627,24 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   const int esz = g->out_f32 ? 4 : 2;
   const bool vec = (g->ldd * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                    (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0));
+  // fp32 outputs of the pair kernel go through a TMA map (store / L2 reduce-add)
+  CUtensorMap td;
+  std::memset(&td, 0, sizeof(td));
+  static const bool no_tma_out = getenv("RP_GEMM_NO_TMA_EPI") != nullptr;
+  const bool tma_out = pair && g->out_f32 && !no_tma_out && (g->ldd * 4) % 16 == 0 &&
+                       (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
+                       make_map_f32(&td, g->D, g->M, g->N, g->ldd);
   Params p{g->M, g->N, g->K, g->D, g->ldd, reinterpret_cast<const __nv_bfloat16*>(g->R), g->ldr,
-           vec ? 1 : 0};
+           vec ? 1 : 0, tma_out ? 1 : 0};
   const int epi = g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
   if (g->out_f32 && g->R) return RP_E_INPUT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (g->a_mn_major)
-    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, p, pair, n_fastest, s)
-                      : dispatch_epi<1, 0>(epi, ta, tb, p, pair, n_fastest, s);
+    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, td, p, pair, n_fastest, s)
+                      : dispatch_epi<1, 0>(epi, ta, tb, td, p, pair, n_fastest, s);
   else
-    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, p, pair, n_fastest, s)
-                      : dispatch_epi<0, 0>(epi, ta, tb, p, pair, n_fastest, s);
+    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, td, p, pair, n_fastest, s)
+                      : dispatch_epi<0, 0>(epi, ta, tb, td, p, pair, n_fastest, s);
   return e == cudaSuccess ? RP_OK : RP_E_CUDA;
 }

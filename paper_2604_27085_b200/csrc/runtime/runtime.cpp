@@ -986,6 +986,17 @@ void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, flo
     RP_CUDA(cudaEventRecord(G.ev_tokens, G.act));
     h2d_bytes += (int64_t)M * T * 8;
   }
+  // async: publish AdamW(it-1)'s result now (p_copy, edge 1: every upload of
+  // version `it` was enqueued by the previous iteration's prefetch) and queue
+  // the uploads of it+1 behind it (edge 2) BEFORE this iteration's compute.
+  // CUDA's launch queue lets the host run only ~1K launches ahead of the GPU,
+  // so anything enqueued after the compute walk would only start near the end
+  // of the iteration and stall the next one on its weights.
+  if (cfg.async_optimizer) {
+    for (int g = 0; g < ngroups(); ++g)
+      if (pend_owner[g] >= 0) p_copy(g);
+    prefetch(it + 1);
+  }
   // walk the dispatch list of this iteration in emission order
   int first_round = -1;
   for (std::size_t i = 0; i < sched.tasks.size();) {
@@ -1001,9 +1012,6 @@ void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, flo
     run_slot(G, it, t.round, t.slot, first_round, grad_scale);
     i += MR;  // a (round, slot) is MR consecutive tasks on one worker
   }
-  // async: the next iteration's weights (published by p_copy(l, it)) stream
-  // in under this iteration's compute, ahead of this step's AdamW traffic
-  if (cfg.async_optimizer) prefetch(it + 1);
   // early return: the loss is known once the fused slots are done
   double total = 0.0;
   for (Gpu& G : gpus) {
@@ -1389,6 +1397,9 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
       rt->pend_owner[g] = 0;
     }
     rt->grads_pending = false;
+    // the next iteration runs on the restored bf16 master: queue its uploads
+    // now, ahead of the p_copy that will publish the pending update (edge 1)
+    rt->prefetch(rt->iter);
   });
 }
 

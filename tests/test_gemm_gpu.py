@@ -39,7 +39,8 @@ def test_gemm_bf16_out(M, N, K, a_mn, b_mn):
     assert _rel(D, ref) < 8e-3
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (200, 300, 320), (1024, 768, 4096)])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (200, 300, 320), (1024, 768, 4096),
+                                    (300, 200, 192), (520, 136, 64)])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 1), (0, 1)])
 def test_gemm_f32_and_accumulate(M, N, K, a_mn, b_mn):
     from paper_2604_27085_b200 import kernels
