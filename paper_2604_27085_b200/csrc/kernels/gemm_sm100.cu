@@ -245,14 +245,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // and each CTA's TMEM receives its 128 rows. Both CTAs' TMA loads complete on
 // the leader's full barrier; MMA commits multicast to both CTAs' barriers;
 // epilogue warps of both CTAs release the accumulator on the leader's barrier.
-constexpr int P_STAGES = 6;
-constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB
-constexpr int P_B_BYTES = 128 * BK * 2;     // 16 KB
-constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+// Tile N is 256 (PBN; 128 is an opt-in variant, see pair_tile_n).
+constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB (this CTA's 128 rows of A)
 // fp32 epilogue staging for TMA store / reduce-add: per epilogue warp two
 // 32 x 32 fp32 chunks (SWIZZLE_128B rows of 128 B)
 constexpr int P_EPI_BYTES = 4 * 2 * 32 * 32 * 4;  // 32 KB
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + P_EPI_BYTES + 1024 + 256;
+template <int PBN>
+struct PairCfg {
+  static constexpr int B_BYTES = (PBN / 2) * BK * 2;       // this CTA's half of B
+  static constexpr int STAGE = P_A_BYTES + B_BYTES;
+  static constexpr int STAGES = PBN == 256 ? 6 : 8;
+  static constexpr int SMEM = STAGES * STAGE + P_EPI_BYTES + 1024 + 256;
+  static_assert(SMEM <= 232448, "pair GEMM shared memory");
+};
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -323,18 +328,19 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int A_MN, int B_MN, int EPI>
+template <int A_MN, int B_MN, int EPI, int PBN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                      const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_d, Params p, int n_fastest) {
+  using Cfg = PairCfg<PBN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi_smem = smem + P_STAGES * P_STAGE_BYTES;
+  uint8_t* epi_smem = smem + Cfg::STAGES * Cfg::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + P_EPI_BYTES);
-  uint64_t* empty = full + P_STAGES;
-  uint64_t* acc_full = empty + P_STAGES;  // [2]
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -342,20 +348,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + BN - 1) / BN;
+  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + PBN - 1) / PBN;
   const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = (p.K + BK - 1) / BK;
   auto tile_mn = [&](int tile, int& m0, int& n0) {
     const int mt = n_fastest ? tile / n_tiles : tile % m_tiles;
     const int nt = n_fastest ? tile % n_tiles : tile / m_tiles;
     m0 = mt * 256;
-    n0 = nt * BN;
+    n0 = nt * PBN;
   };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma_a);
     tma_prefetch(&tma_b);
-    for (int s = 0; s < P_STAGES; ++s) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -384,12 +390,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int tile = pair; tile < num_tiles; tile += npairs) {
       int m0, n0;
       tile_mn(tile, m0, n0);
-      const int am = m0 + 128 * rank, bn = n0 + 128 * rank;
+      const int am = m0 + 128 * rank, bn = n0 + (PBN / 2) * rank;
       for (int kb = 0; kb < k_blocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sa = smem + stage * P_STAGE_BYTES;
+        uint8_t* sa = smem + stage * Cfg::STAGE;
         uint8_t* sb = sa + P_A_BYTES;
-        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
         const int k0 = kb * BK;
         if (A_MN) {
           tma_load_2d_pair(sa, &tma_a, &full[stage], am, k0);
@@ -399,16 +405,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         if (B_MN) {
           tma_load_2d_pair(sb, &tma_b, &full[stage], bn, k0);
-          tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bn + 64, k0);
+          if (PBN == 256) tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bn + 64, k0);
         } else {
           tma_load_2d_pair(sb, &tma_b, &full[stage], k0, bn);
         }
-        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (leader only) ----------------
-    constexpr uint32_t idesc = umma_idesc_bf16(256, BN, A_MN, B_MN);
+    constexpr uint32_t idesc = umma_idesc_bf16(256, PBN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -416,11 +422,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int tile = pair; tile < num_tiles; tile += npairs) {
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * PBN;
       for (int kb = 0; kb < k_blocks; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint32_t a_addr = smem_u32(smem + stage * P_STAGE_BYTES);
+        const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE);
         const uint32_t b_addr = a_addr + P_A_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
@@ -431,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           umma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
         }
         umma_commit_pair(&empty[stage]);
-        if (++stage == P_STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
       umma_commit_pair(&acc_full[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
@@ -456,11 +462,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint8_t* wbuf = epi_smem + q * (2 * 4096);
         // chunks wholly outside D are skipped (warp-uniform), so every written
         // buffer belongs to a committed store and "two chunks ago" holds
-        const int c_end = min(BN, p.N - n0);
+        const int c_end = min(PBN, p.N - n0);
 #pragma unroll 1
         for (int c = 0; c < c_end && row0 < p.M; c += 32) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
           tmem_ld_wait();
           uint8_t* buf = wbuf + (epi_chunk_no++ & 1) * 4096;  // alternates across tiles too
           if (lane == 0) bulk_wait_read<1>();  // the store from this buffer two chunks ago
@@ -478,9 +484,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < PBN; c += 32) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c, v);
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
           tmem_ld_wait();
           epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
         }
@@ -561,21 +567,37 @@ int num_sms() {
   return n;
 }
 
+// Tile N for the CTA-pair kernel: 256. (256x128 pair tiles would fill the 74
+// pairs' last wave better for 4096-wide GEMMs, but measured at ~1.0 PF/s vs
+// ~1.35 for 256x256 on B200 — half-size MMAs double the per-k-block pipeline
+// overhead; RP_GEMM_TILE_N=128 keeps the variant selectable for study.)
+int pair_tile_n(int M, int N) {
+  (void)M;
+  (void)N;
+  static const int forced = [] {
+    const char* e = getenv("RP_GEMM_TILE_N");
+    return e ? atoi(e) : 0;
+  }();
+  return forced == 128 ? 128 : 256;
+}
+
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                    const Params& p, bool pair, int n_fastest, cudaStream_t stream) {
   if (pair) {
-    auto kern = gemm_pair_kernel<A_MN, B_MN, EPI>;
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           P_SMEM_BYTES);
+    const bool narrow = pair_tile_n(p.M, p.N) == 128;
+    auto kern = narrow ? gemm_pair_kernel<A_MN, B_MN, EPI, 128> : gemm_pair_kernel<A_MN, B_MN, EPI, 256>;
+    const int smem = narrow ? PairCfg<128>::SMEM : PairCfg<256>::SMEM;
+    static bool configured[2] = {false, false};
+    if (!configured[narrow]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      configured = true;
+      configured[narrow] = true;
     }
-    const int tiles = ((p.M + 255) / 256) * ((p.N + BN - 1) / BN);
+    const int pbn = narrow ? 128 : 256;
+    const int tiles = ((p.M + 255) / 256) * ((p.N + pbn - 1) / pbn);
     const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    kern<<<2 * pairs, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, td, p, n_fastest);
+    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, p, n_fastest);
     return cudaGetLastError();
   }
   auto kern = gemm_kernel<A_MN, B_MN, EPI>;
@@ -620,7 +642,8 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   bool ok = g->a_mn_major ? make_map(&ta, g->A, g->K, g->M, g->lda, 64, 64)
                           : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
   ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
-                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64, pair ? 128 : BN));
+                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64,
+                                       pair ? pair_tile_n(g->M, g->N) / 2 : BN));
   // raster: keep the larger operand's tile hot (walk the other dimension fastest)
   const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
   if (!ok) return RP_E_CUDA;

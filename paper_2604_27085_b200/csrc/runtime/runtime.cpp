@@ -216,9 +216,9 @@ struct Runtime {
     if (!prof_on) return -1;
     ProfRec r{0, prof_event(), prof_event(), 0.0, 0, 0, prof_layer * 4 + prof_phase, prof_inst};
     for (const Gpu& G : gpus)
-      if (G.compute == st || G.opt_comp == st) {
+      if (G.compute == st || G.opt_comp == st || G.wgrad == st) {
         r.worker = G.id;
-        r.lane = G.opt_comp == st;
+        r.lane = G.opt_comp == st ? 1 : (G.wgrad == st ? 2 : 0);
       }
     RP_CUDA(cudaEventRecord(r.a, st));
     prof.push_back(r);
@@ -461,6 +461,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   };
   mk(&G.compute, hi);
   mk(&G.act, hi);
+  mk(&G.wgrad, hi + 1 <= lo ? hi + 1 : hi);
   mk(&G.w_h2d, lo);
   mk(&G.opt_h2d, lo);
   mk(&G.opt_d2h, lo);
@@ -508,15 +509,23 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     A.rstd_q = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
     A.rstd_k = static_cast<float*>(dalloc((int64_t)T * s.nk * 4, 3));
     A.lse = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
+    A.ev_free = new_event(false);
   }
   G.dx32[0] = static_cast<float*>(dalloc(Th * 4, 4));
   G.dx32[1] = static_cast<float*>(dalloc(Th * 4, 4));
-  G.dx16 = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+  for (int b = 0; b < 2; ++b) {
+    G.dx16s[b] = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+    G.dgus[b] = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
+    G.dqkvs[b] = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 4));
+    G.ev_dx16_free[b] = new_event(false);
+    G.ev_dgu_free[b] = new_event(false);
+    G.ev_dqkv_free[b] = new_event(false);
+  }
+  G.ev_wgrad = new_event(false);
+  G.dx16 = G.dx16s[0];
   G.dh = static_cast<uint16_t*>(dalloc(Th * 2, 4));
   G.dact = static_cast<uint16_t*>(dalloc((int64_t)T * s.m * 2, 4));
-  G.dgu = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
   G.dattn = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 4));
-  G.dqkv = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 4));
   G.dq_t = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 4));
   G.dk_t = static_cast<uint16_t*>(dalloc((int64_t)T * s.kd() * 2, 4));
   G.dq_acc = static_cast<float*>(dalloc((int64_t)T * s.qd() * 4, 4));
@@ -675,6 +684,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
   const uint16_t* W = G.groups[l + 1].w[exec_iter & 1];
   cudaStream_t st = G.compute;
   const int h = s.h, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
+  RP_CUDA(cudaStreamWaitEvent(st, A.ev_free, 0));  // last weight-gradient reads of A
   A.xin = x;
   {
     const int pi_ = prof_begin(st);
@@ -716,55 +726,86 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
 // Backward of decoder layer l. In: G.dx32[0] (fp32) / G.dx16 (bf16) =
 // dL/d(layer output). Out: the same buffers = dL/d(layer input). Weight grads
 // go to grad[t%2]: the first micro-batch overwrites, later ones accumulate.
+// The dgrad chain runs on `compute`; the four weight-gradient GEMMs run on the
+// `wgrad` stream as soon as their inputs exist (event per input), so they fill
+// the persistent GEMMs' partial last waves and overlap the chain's
+// elementwise / attention kernels. Buffers they read are double-buffered
+// (dx16 A/B, dgu and dqkv by layer parity) and released by events.
 void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   DevGroup& D = G.groups[l + 1];
   const uint16_t* W = D.w[exec_iter & 1];
   float* dW = D.grad[last_iter & 1];
-  cudaStream_t st = G.compute;
+  cudaStream_t st = G.compute, ws = G.wgrad;
   const int h = s.h, m = s.m, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
+  const int xa = G.dx16 == G.dx16s[0] ? 0 : 1, xb = xa ^ 1;  // dY in, post-norm dY
+  uint16_t* dx_a = G.dx16s[xa];
+  uint16_t* dx_b = G.dx16s[xb];
+  const int p = G.bwd_par;
+  G.bwd_par ^= 1;
+  uint16_t* dgu = G.dgus[p];
+  uint16_t* dqkv = G.dqkvs[p];
+  auto to_ws = [&]() {  // the wgrad stream waits for everything enqueued on compute so far
+    cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
+    if (!e) e = new_event(false);
+    RP_CUDA(cudaEventRecord(e, st));
+    RP_CUDA(cudaStreamWaitEvent(ws, e, 0));
+  };
   if (first)
     for (const Tensor* t : {&LL.in_norm, &LL.q_norm, &LL.k_norm, &LL.post_norm})
       RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
   // MLP:  x3 = x2 + act(gu(h2)) Wd^T
-  gemm(st, G.dx16, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
-  gemm(st, G.dx16, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
+  to_ws();
+  gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
+  gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
+  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], ws));
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[p], 0));  // wgrad two layers ago read it
   {
     const int pi_ = prof_begin(st);
-    RP_K(rp_swiglu_bwd(G.dact, A.gu, G.dgu, T, m, st));
+    RP_K(rp_swiglu_bwd(G.dact, A.gu, dgu, T, m, st));
     prof_end(pi_, st, 2, 10.0 * T * m);
   }
-  gemm(st, G.dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
-  gemm(st, G.dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
+  to_ws();
+  gemm(ws, dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
+  RP_CUDA(cudaEventRecord(G.ev_dgu_free[p], ws));
+  gemm(st, dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xb], 0));
   {
     const int pi_ = prof_begin(st);
-    RP_K(rp_rmsnorm_bwd(G.dh, A.x2, W + LL.post_norm.off, A.rstd2, G.dx32[0], G.dx32[1], G.dx16,
-                      dW + LL.post_norm.off, T, h, st));
+    RP_K(rp_rmsnorm_bwd(G.dh, A.x2, W + LL.post_norm.off, A.rstd2, G.dx32[0], G.dx32[1], dx_b,
+                        dW + LL.post_norm.off, T, h, st));
     prof_end(pi_, st, 2, 14.0 * T * h);
   }
   // attention:  x2 = x + attn(qkv(h1)) Wo^T
-  gemm(st, G.dx16, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
-  gemm(st, G.dx16, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
+  to_ws();
+  gemm(ws, dx_b, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
+  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xb], ws));
+  gemm(st, dx_b, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dqkv_free[p], 0));
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_attn_bwd_tc(A.q, qd, A.k, kd, A.qkv + qd + kd, qkvd, A.o, qd, G.dattn, qd, A.lse,
-                      G.dq_t, qd, G.dk_t, kd, G.dqkv + qd + kd, qkvd, G.delta, G.dq_acc, T,
-                      cfg.seq_len,
-                      s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
+                        G.dq_t, qd, G.dk_t, kd, dqkv + qd + kd, qkvd, G.delta, G.dq_acc, T,
+                        cfg.seq_len, s.nq, s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
     prof_end(pi_, st, 1, 5.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_qk_norm_rope_bwd(G.dq_t, G.dk_t, A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off,
-                           W + LL.k_norm.off, A.rstd_q, A.rstd_k, G.cos_sin, cfg.seq_len, G.dqkv,
-                           qkvd, dW + LL.q_norm.off, dW + LL.k_norm.off, T, st));
+                             W + LL.k_norm.off, A.rstd_q, A.rstd_k, G.cos_sin, cfg.seq_len, dqkv,
+                             qkvd, dW + LL.q_norm.off, dW + LL.k_norm.off, T, st));
     prof_end(pi_, st, 2, 8.0 * T * (s.nq + s.nk) * s.hd);
   }
-  gemm(st, G.dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
-  gemm(st, G.dqkv, qkvd, true, A.h1, h, true, dW + LL.qkv.off, h, true, !first, qkvd, h, T);
+  to_ws();
+  gemm(ws, dqkv, qkvd, true, A.h1, h, true, dW + LL.qkv.off, h, true, !first, qkvd, h, T);
+  RP_CUDA(cudaEventRecord(G.ev_dqkv_free[p], ws));
+  RP_CUDA(cudaEventRecord(A.ev_free, ws));  // act / h2 / o / h1 no longer needed
+  RP_CUDA(cudaEventRecord(G.ev_wgrad, ws));
+  gemm(st, dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xa], 0));  // wgrad(down) read dx_a
   {
     const int pi_ = prof_begin(st);
-    RP_K(rp_rmsnorm_bwd(G.dh, A.xin, W + LL.in_norm.off, A.rstd1, G.dx32[1], G.dx32[0], G.dx16,
-                      dW + LL.in_norm.off, T, h, st));
+    RP_K(rp_rmsnorm_bwd(G.dh, A.xin, W + LL.in_norm.off, A.rstd1, G.dx32[1], G.dx32[0], dx_a,
+                        dW + LL.in_norm.off, T, h, st));
     prof_end(pi_, st, 2, 14.0 * T * h);
   }
   kernels += 8;
@@ -798,6 +839,7 @@ void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float
          !(first && r0 == 0), V, h, nr);
     kernels += 1;
   }
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
   RP_K(rp_rmsnorm_bwd(G.dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.dx32[0], G.dx16,
                       dW + HL.final_norm.off, T, h, st));
   kernels += 2;
@@ -917,6 +959,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
       Slotbuf& gi = G.hand_grad[hb];
       RP_CUDA(cudaStreamWaitEvent(st, gi.ready, 0));
       RP_CUDA(cudaMemcpyAsync(G.dx32[0], gi.p, Th4, cudaMemcpyDeviceToDevice, st));
+      RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
       RP_K(rp_f32_to_bf16(G.dx32[0], G.dx16, (int64_t)T * s.h, st));
       ++kernels;
       RP_CUDA(cudaEventRecord(gi.read, st));
@@ -954,8 +997,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
       records.push_back(rec);
     }
   }
-  // last compute read of the slot's weights; grads complete (GradWrite)
+  // last compute read of the slot's weights; grads complete (GradWrite) once
+  // the weight-gradient stream has drained into `compute`
   for (int g : gs) RP_CUDA(cudaEventRecord(G.groups[g].ev_lastuse[it & 1], st));
+  if (has_grads) RP_CUDA(cudaStreamWaitEvent(st, G.ev_wgrad, 0));
   if (has_grads && rin == R - 1)
     for (int g : grad_groups) {
       RP_CUDA(cudaEventRecord(G.groups[g].ev_gradwrite, st));
@@ -1109,7 +1154,7 @@ Runtime::~Runtime() {
   for (auto e : event_pool) cudaEventDestroy(e);
   for (Gpu& G : gpus) {
     cudaSetDevice(G.dev);
-    for (cudaStream_t st : {G.compute, G.act, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp})
+    for (cudaStream_t st : {G.compute, G.act, G.wgrad, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp})
       if (st) cudaStreamDestroy(st);
   }
   if (loss_host) cudaFreeHost(loss_host);
@@ -1522,7 +1567,7 @@ RP_API int rp_runtime_measured_costs(rp_runtime_t* p, rp_layer_cost_t* out, int3
     // per call instance: (unit, summed kernel ns)
     std::vector<std::pair<int, double>> inst;
     for (const auto& r : rt->prof) {
-      if (r.lane != 0 || r.unit < 0) continue;
+      if (r.lane == 1 || r.unit < 0) continue;  // compute + weight-gradient lanes
       if ((int)inst.size() <= r.inst) inst.resize(r.inst + 1, {-1, 0.0});
       float ms = 0.f;
       RP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));

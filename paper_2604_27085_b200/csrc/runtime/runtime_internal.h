@@ -92,6 +92,7 @@ struct LayerActs {
   uint16_t *x, *h1, *qkv, *q, *k, *o, *x2, *h2, *gu, *act;
   float *rstd1, *rstd_q, *rstd_k, *lse, *rstd2;
   const uint16_t* xin = nullptr;  // the input actually used by layer_fwd
+  cudaEvent_t ev_free = nullptr;  // weight-gradient GEMMs done reading act/h2/o/h1
 };
 
 // A hand-off / checkpoint buffer with its producer and consumer events.
@@ -108,6 +109,22 @@ struct Gpu {
   int id = 0, dev = 0;
   cudaStream_t compute = nullptr, act = nullptr, w_h2d = nullptr;
   cudaStream_t opt_h2d = nullptr, opt_d2h = nullptr, opt_comp = nullptr;
+  // weight-gradient GEMMs run here, off the dgrad chain on `compute`, so the
+  // persistent GEMMs' partial last waves and the chain's HBM-bound kernels
+  // overlap them; scratch gradients they read are double-buffered
+  cudaStream_t wgrad = nullptr;
+  uint16_t* dx16s[2] = {nullptr, nullptr};
+  uint16_t* dgus[2] = {nullptr, nullptr};
+  uint16_t* dqkvs[2] = {nullptr, nullptr};
+  cudaEvent_t ev_dx16_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_dgu_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_dqkv_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_wgrad = nullptr;  // last weight-gradient GEMM enqueued
+  int bwd_par = 0;
+  // cross-stream fork events, reused round-robin (a wait captures the event's
+  // state when it is enqueued, so re-recording an old one is safe)
+  cudaEvent_t fork_ev[64] = {};
+  int fork_i = 0;
   std::vector<DevGroup> groups;           // index g = group + 1 (0 = embedding)
   std::vector<LayerActs> acts;            // per decoder layer of the fused stage
   float* dx32[2] = {nullptr, nullptr};
