@@ -735,7 +735,9 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   DevGroup& D = G.groups[l + 1];
   const uint16_t* W = D.w[exec_iter & 1];
   float* dW = D.grad[last_iter & 1];
-  cudaStream_t st = G.compute, ws = G.wgrad;
+  // profiled steps serialise the weight-gradient GEMMs onto `compute` so each
+  // kernel's CUDA-event time is its own (the timed steps overlap them)
+  cudaStream_t st = G.compute, ws = prof_on ? G.compute : G.wgrad;
   const int h = s.h, m = s.m, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
   const int xa = G.dx16 == G.dx16s[0] ? 0 : 1, xb = xa ^ 1;  // dY in, post-norm dY
   uint16_t* dx_a = G.dx16s[xa];
