@@ -349,6 +349,11 @@ def run_ours(args):
                    "slots": plan.num_slots(), "iterations": [it_lo, it_hi]},
         "loss": {"first": losses[0], "last": losses[-1]},
         "setup_s": round(setup_s, 1),
+        "optimizer_state": {"resident_params_hbm": int(st1["resident_params"]),
+                            "streamed_params_host": int(st1["params_total"] - st1["resident_params"]),
+                            "note": "fp32 AdamW state of the largest groups that fit in free HBM "
+                                    "stays resident (single device); the rest streams from "
+                                    "pinned host memory every step"},
     }
     if not args.no_cpu_baseline:
         try:

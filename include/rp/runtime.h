@@ -56,6 +56,8 @@ typedef struct {
   int64_t h2d_bytes, d2h_bytes, p2p_bytes; /* cumulative */
   int32_t iterations_done;
   int32_t kernels_launched;    /* cumulative count of this library's kernel launches */
+  int32_t pad_;
+  int64_t resident_params;     /* params whose fp32 AdamW state lives in HBM (1 device) */
 } rp_runtime_stats_t;
 
 int rp_runtime_create(const rp_runtime_config_t* cfg, rp_runtime_t** out);

@@ -32,6 +32,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -261,6 +262,10 @@ struct Runtime {
   void head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale);
   void step();
   void adam_group(Gpu& G, int g, int parity);
+  void place_resident_state();      // choose groups whose fp32 state lives in HBM
+  void push_resident(int g);        // host master/m/v -> device state
+  void pull_resident(int g);        // device state -> host master/m/v (if stale)
+  int64_t resident_params = 0;
   void sync_all();
   void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
             bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_, int N_, int K_,
@@ -389,6 +394,61 @@ void Runtime::init(const rp_runtime_config_t& c) {
   }
   if (!(cfg.flags & RP_RT_SKIP_INIT)) init_weights();
   sync_all();
+  place_resident_state();
+}
+
+// Optimizer state in free HBM (single device only: with N devices a group's
+// grads land on a different device every iteration). Greedy over groups,
+// largest first, until the free memory minus a reserve is used; the rest
+// streams from pinned host memory as before. RP_RESIDENT_GB caps it (0 = off).
+void Runtime::place_resident_state() {
+  if (ndev != 1) return;
+  double cap_gb = 1e9;
+  if (const char* e = getenv("RP_RESIDENT_GB")) cap_gb = atof(e);
+  if (cap_gb <= 0) return;
+  set_dev(gpus[0]);
+  std::size_t free_b = 0, total_b = 0;
+  RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const std::size_t reserve = std::size_t(6) << 30;  // allocator, cuBLAS-free kernels, slack
+  int64_t budget = (int64_t)std::min<double>((double)free_b - (double)reserve, cap_gb * 1e9);
+  std::vector<int> order(ngroups());
+  for (int g = 0; g < ngroups(); ++g) order[g] = g;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return host[a].n > host[b].n; });
+  for (int g : order) {
+    const int64_t bytes = host[g].n * 12;
+    if (bytes > budget) continue;
+    void* p = nullptr;
+    if (cudaMalloc(&p, (std::size_t)bytes) != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    host[g].d_state = static_cast<float*>(p);
+    budget -= bytes;
+    resident_params += host[g].n;
+    gpus[0].allocated[5] += (std::size_t)bytes;
+    push_resident(g);
+  }
+}
+
+void Runtime::push_resident(int g) {
+  HostGroup& H = host[g];
+  if (!H.d_state) return;
+  set_dev(gpus[0]);
+  RP_CUDA(cudaMemcpy(H.d_state, H.master, H.n * 4, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(H.d_state + H.n, H.m, H.n * 4, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(H.d_state + 2 * H.n, H.v, H.n * 4, cudaMemcpyHostToDevice));
+  H.host_stale = false;
+}
+
+void Runtime::pull_resident(int g) {
+  HostGroup& H = host[g];
+  if (!H.d_state || !H.host_stale) return;
+  set_dev(gpus[0]);
+  RP_CUDA(cudaMemcpy(H.master, H.d_state, H.n * 4, cudaMemcpyDeviceToHost));
+  RP_CUDA(cudaMemcpy(H.m, H.d_state + H.n, H.n * 4, cudaMemcpyDeviceToHost));
+  RP_CUDA(cudaMemcpy(H.v, H.d_state + 2 * H.n, H.n * 4, cudaMemcpyDeviceToHost));
+  H.host_stale = false;
 }
 
 void Runtime::build_plan() {
@@ -1084,6 +1144,20 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   const int step_no = ++H.step;
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_gradwrite, 0));  // edge (3)
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_pcopy, 0));      // pend free again
+  if (H.d_state) {  // HBM-resident fp32 state: one fused pass, no PCIe
+    cudaEvent_t xa = xfer_begin(G.opt_comp);
+    const int pi_ = prof_begin(G.opt_comp);
+    RP_K(rp_adamw(H.d_state, H.d_state + H.n, H.d_state + 2 * H.n, D.grad[parity], D.pend, H.n,
+                  &cfg.adam, step_no, G.opt_comp));
+    prof_end(pi_, G.opt_comp, 3, 30.0 * H.n);
+    ++kernels;
+    RP_CUDA(cudaEventRecord(D.ev_adam[parity], G.opt_comp));
+    xfer_end(xa, G.opt_comp, 2, g - 1, last_iter, G.id);
+    H.host_stale = true;
+    pend_owner[g] = G.id;
+    if (!cfg.async_optimizer) p_copy(g);
+    return;
+  }
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
   cudaEvent_t xa = xfer_begin(G.opt_h2d);
   for (int64_t off = 0; off < H.n; off += chunk_elems) {
@@ -1160,6 +1234,8 @@ Runtime::~Runtime() {
       if (st) cudaStreamDestroy(st);
   }
   if (loss_host) cudaFreeHost(loss_host);
+  for (auto& H : host)
+    if (H.d_state) cudaFree(H.d_state);
 }
 
 }  // namespace rt
@@ -1312,6 +1388,8 @@ RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, in
       H.v[i] = 0.f;
     }
     H.step = 0;
+    H.host_stale = false;
+    rt->push_resident(g);
     for (auto& G : rt->gpus) G.groups[g].loaded[0] = G.groups[g].loaded[1] = -1;
   });
 }
@@ -1323,6 +1401,7 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
     rp::rt::HostGroup& H = rt->host[g];
     if (n != H.n || !out) throw RtError(RP_E_INPUT, "size mismatch");
     rt->sync_all();
+    rt->pull_resident(g);
     switch (which) {
       case 0: std::memcpy(out, H.master, n * 4); break;
       case 1:
@@ -1368,6 +1447,7 @@ RP_API int rp_runtime_save(rp_runtime_t* p, const char* path) {
     Runtime* rt = R(p);
     if (!path) throw RtError(RP_E_INPUT, "null path");
     rt->sync_all();
+    for (int g = 0; g < rt->ngroups(); ++g) rt->pull_resident(g);
     std::unique_ptr<FILE, FileCloser> f(std::fopen(path, "wb"));
     if (!f) throw RtError(RP_E_INPUT, std::string("cannot open ") + path);
     const int ng = rt->ngroups();
@@ -1427,6 +1507,8 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
       xread(f.get(), H.v, H.n * 4);
       xread(f.get(), H.w16, H.n * 2);
       H.step = steps[g];
+      H.host_stale = false;
+      rt->push_resident(g);
     }
     // device caches hold stale versions; pending AdamW outputs are re-created
     for (auto& G : rt->gpus)
@@ -1521,6 +1603,7 @@ RP_API int rp_runtime_stats(rp_runtime_t* p, rp_runtime_stats_t* st) {
     st->p2p_bytes = rt->p2p_bytes;
     st->iterations_done = rt->iter;
     st->kernels_launched = (int32_t)rt->kernels;
+    st->resident_params = rt->resident_params;
   });
 }
 

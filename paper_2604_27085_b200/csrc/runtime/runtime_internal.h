@@ -70,6 +70,11 @@ struct HostGroup {
   float* m = nullptr;
   float* v = nullptr;
   int step = 0;
+  // single-device runs keep the fp32 state of some groups resident in free
+  // HBM (device 0): AdamW then runs without the PCIe round trip; the host
+  // copy is refreshed on demand (read_state / save) and re-uploaded on writes
+  float* d_state = nullptr;  // [master | m | v], 3n fp32, or null (streamed)
+  bool host_stale = false;   // host master/m/v older than d_state
 };
 
 // Device-side state of one parameter group on one worker.

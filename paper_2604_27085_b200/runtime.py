@@ -39,7 +39,7 @@ class StatsC(C.Structure):
     _fields_ = [("num_layers", I32), ("num_slots", I32), ("params_total", I64),
                 ("host_bytes_pinned", I64), ("device_bytes", I64 * 8), ("h2d_bytes", I64),
                 ("d2h_bytes", I64), ("p2p_bytes", I64), ("iterations_done", I32),
-                ("kernels_launched", I32)]
+                ("kernels_launched", I32), ("pad_", I32), ("resident_params", I64)]
 
 
 LAYER_TENSORS = ["input_norm", "qkv", "q_norm", "k_norm", "o", "post_norm", "gate_up", "down"]
@@ -236,7 +236,8 @@ class RoundPipe:
                 "params_total": st.params_total, "host_bytes_pinned": st.host_bytes_pinned,
                 "device_bytes": list(st.device_bytes), "h2d_bytes": st.h2d_bytes,
                 "d2h_bytes": st.d2h_bytes, "p2p_bytes": st.p2p_bytes,
-                "iterations_done": st.iterations_done, "kernels_launched": st.kernels_launched}
+                "iterations_done": st.iterations_done, "kernels_launched": st.kernels_launched,
+                "resident_params": st.resident_params}
 
     # -- profiling ----------------------------------------------------------------
     PROFILE_CATEGORIES = ("gemm", "attention", "hbm_kernels", "adamw")

@@ -134,8 +134,13 @@ def test_multi_worker_grads_match_single_fused_stage():
     assert worst[1] < 1e-2, worst
 
 
+@pytest.mark.parametrize("resident", ["hbm", "streamed"])
 @pytest.mark.parametrize("mode", ["sync", "async"])
-def test_step_parity_single_fused_stage(mode):
+def test_step_parity_single_fused_stage(mode, resident, monkeypatch):
+    """Single fused stage; the fp32 optimizer state either resident in free HBM
+    (single-device default) or streamed from pinned host memory every step."""
+    if resident == "streamed":
+        monkeypatch.setenv("RP_RESIDENT_GB", "0")
     losses, g0, master, _, (plan, durs) = run_case(mode, 1)
     assert plan.num_slots() == 1 and plan.fused_stage.first == 0
     check(mode, losses, g0, master)
@@ -161,12 +166,15 @@ def test_step_parity_four_workers_seven_slots(mode):
         assert np.all(ev["start_ns"][1:] >= ev["end_ns"][:-1] - 1000)
 
 
+@pytest.mark.parametrize("resident", ["hbm", "streamed"])
 @pytest.mark.parametrize("mode", ["async", "sync"])
-def test_checkpoint_resume(mode, tmp_path):
+def test_checkpoint_resume(mode, resident, tmp_path, monkeypatch):
     """Host-state checkpoint (SURVEY 8(f)3): save after 2 steps, continue 2;
     a fresh runtime resumed from the file reproduces steps 3-4 (losses and the
     fp32 master), including async mode's unpublished staleness-1 update."""
     from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    if resident == "streamed":
+        monkeypatch.setenv("RP_RESIDENT_GB", "0")
     s = O.Shape.from_config("tiny")
     params = O.init_params(s, seed=0)
     tok, lab = O.synthetic_batch(s, 4, 1, 256)
