@@ -257,9 +257,11 @@ struct Runtime {
   std::vector<int> slot_groups(const roundpipe::StageSlot& ss) const;
   int exec_iter = 0;  // iteration whose compute is being enqueued
   void p_copy(int g);
-  void layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out);
+  void layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out,
+                 cudaStream_t on = nullptr);
   void layer_bwd(Gpu& G, int l, LayerActs& A, bool first);
-  void head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale);
+  void head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale,
+                    cudaStream_t on = nullptr);
   void step();
   void adam_group(Gpu& G, int g, int parity);
   void place_resident_state();      // choose groups whose fp32 state lives in HBM
@@ -553,7 +555,15 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   }
   const int nsets = std::max(1, s.L - plan.fused_stage.first);
   G.acts.resize(nsets);
-  for (auto& A : G.acts) {
+  // opt-in (RP_FUSED_PIPELINE=1): measured no faster at Qwen3-8B, where the
+  // step runs at the 1 kW power cap (the overlap lowers SM clocks instead),
+  // while the second activation set costs 20.6 GB of HBM that otherwise holds
+  // optimizer state
+  const char* pe = getenv("RP_FUSED_PIPELINE");
+  const bool pipe = plan.fused_stage.first == 0 && MR >= 2 && pe && pe[0] == '1';
+  if (pipe) G.acts2.resize(nsets);
+  for (auto* set : {&G.acts, &G.acts2})
+  for (auto& A : *set) {
     A.x = static_cast<uint16_t*>(dalloc(Th * 2, 3));
     A.h1 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
     A.qkv = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 3));
@@ -570,6 +580,18 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     A.rstd_k = static_cast<float*>(dalloc((int64_t)T * s.nk * 4, 3));
     A.lse = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
     A.ev_free = new_event(false);
+    A.ev_chain_free = new_event(false);
+  }
+  if (pipe) {
+    int lo2 = 0, hi2 = 0;
+    RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo2, &hi2));
+    RP_CUDA(cudaStreamCreateWithPriority(&G.fwd2, cudaStreamNonBlocking, hi2));
+    G.hdx32 = static_cast<float*>(dalloc(Th * 4, 4));
+    G.hdx16 = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+    G.hdh = static_cast<uint16_t*>(dalloc(Th * 2, 4));
+    G.ev_head_done = new_event(false);
+    G.ev_hdx_free = new_event(false);
+    G.ev_fwd_join = new_event(false);
   }
   G.dx32[0] = static_cast<float*>(dalloc(Th * 4, 4));
   G.dx32[1] = static_cast<float*>(dalloc(Th * 4, 4));
@@ -740,11 +762,13 @@ void Runtime::p_copy(int g) {
 }
 
 // ---- decoder layer -------------------------------------------------------------------
-void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out) {
+void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t* x_out,
+                        cudaStream_t on) {
   const uint16_t* W = G.groups[l + 1].w[exec_iter & 1];
-  cudaStream_t st = G.compute;
+  cudaStream_t st = on ? on : G.compute;
   const int h = s.h, qd = s.qd(), kd = s.kd(), qkvd = s.qkvd();
-  RP_CUDA(cudaStreamWaitEvent(st, A.ev_free, 0));  // last weight-gradient reads of A
+  RP_CUDA(cudaStreamWaitEvent(st, A.ev_free, 0));        // last weight-gradient reads of A
+  RP_CUDA(cudaStreamWaitEvent(st, A.ev_chain_free, 0));  // last dgrad-chain reads of A
   A.xin = x;
   {
     const int pi_ = prof_begin(st);
@@ -870,17 +894,24 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
                         dW + LL.in_norm.off, T, h, st));
     prof_end(pi_, st, 2, 14.0 * T * h);
   }
+  RP_CUDA(cudaEventRecord(A.ev_chain_free, st));
   kernels += 8;
 }
 
 // Head pseudo-layer: final RMSNorm + LM head + CE forward and backward,
 // chunked over token rows: only a [rows, V] logits chunk ever exists, and the
 // CE kernel overwrites it in place with dlogits.
-void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale) {
+void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float grad_scale,
+                           cudaStream_t on) {
   DevGroup& D = G.groups[s.L + 1];
   const uint16_t* W = D.w[exec_iter & 1];
   float* dW = D.grad[last_iter & 1];
-  cudaStream_t st = G.compute;
+  cudaStream_t st = on ? on : G.compute;
+  // pipelined fused stage: the head runs beside the previous micro-batch's
+  // backward, so it uses its own dh and hands its output gradient over in
+  // hdx32 / hdx16 (copied into dx32[0] / dx16 by the backward stream)
+  const bool piped = on && on != G.compute;
+  uint16_t* dh = piped ? G.hdh : G.dh;
   const int h = s.h, V = s.V;
   if (first) RP_CUDA(cudaMemsetAsync(dW + HL.final_norm.off, 0, (size_t)h * 4, st));
   RP_K(rp_rmsnorm_fwd(x, h, W + HL.final_norm.off, G.hN, h, G.rstdN, T, h, (float)s.eps, st));
@@ -895,15 +926,21 @@ void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float
                        G.loss_dev, nullptr, st));
     prof_end(pi_, st, 2, 6.0 * nr * (double)V);
   }
-    gemm(st, G.logits, V, false, W + HL.lm_head.off, h, true, G.dh + (int64_t)r0 * h, h, false,
+    gemm(st, G.logits, V, false, W + HL.lm_head.off, h, true, dh + (int64_t)r0 * h, h, false,
          false, nr, h, V);
     gemm(st, G.logits, V, true, G.hN + (int64_t)r0 * h, h, true, dW + HL.lm_head.off, h, true,
          !(first && r0 == 0), V, h, nr);
     kernels += 1;
   }
-  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
-  RP_K(rp_rmsnorm_bwd(G.dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.dx32[0], G.dx16,
-                      dW + HL.final_norm.off, T, h, st));
+  if (piped) {
+    RP_CUDA(cudaStreamWaitEvent(st, G.ev_hdx_free, 0));  // previous hand-over consumed
+    RP_K(rp_rmsnorm_bwd(dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.hdx32, G.hdx16,
+                        dW + HL.final_norm.off, T, h, st));
+  } else {
+    RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
+    RP_K(rp_rmsnorm_bwd(dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.dx32[0], G.dx16,
+                        dW + HL.final_norm.off, T, h, st));
+  }
   kernels += 2;
 }
 
@@ -940,6 +977,72 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
   const bool want_tl = cfg.flags & RP_RT_RECORD_TIMELINE;
   const std::size_t Th2 = (std::size_t)T * s.h * 2, Th4 = (std::size_t)T * s.h * 4;
 
+  // Pipelined fused stage (whole model in one slot): forward + head of
+  // micro-batch k+1 on `fwd2` beside the backward of k on `compute`.
+  // Profiled steps run the plain order so kernel times stay their own.
+  if (ss.kind == StageKind::Fused && a == 0 && !G.acts2.empty() && !prof_on) {
+    cudaStream_t F = G.fwd2;
+    {
+      cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
+      if (!e) e = new_event(false);
+      RP_CUDA(cudaEventRecord(e, st));  // uploads, tokens, edge-4 waits so far
+      RP_CUDA(cudaStreamWaitEvent(F, e, 0));
+    }
+    auto wait_on = [&](cudaStream_t q, int g) {
+      RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_upload[it & 1], 0));
+    };
+    const int nl = s.L;
+    for (int mb = 0; mb < MR; ++mb) {
+      const int gmb = rin * MR + mb;
+      const bool first = rin == 0 && mb == 0;
+      LayerActs* acts = (mb & 1) ? G.acts2.data() : G.acts.data();
+      TaskRecord rec{};
+      if (want_tl) {
+        rec.task = roundpipe::Task{it, round, slot, mb, G.id, ss.dur_ns};
+        rec.worker = G.id;
+        rec.start = new_event(true);
+        rec.end = new_event(true);
+        RP_CUDA(cudaEventRecord(rec.start, st));
+      }
+      // forward + LM head of mb on F
+      const int32_t* ids = G.tokens_dev + (int64_t)gmb * T;
+      RP_CUDA(cudaStreamWaitEvent(F, acts[0].ev_free, 0));
+      RP_CUDA(cudaStreamWaitEvent(F, acts[0].ev_chain_free, 0));
+      wait_on(F, 0);
+      RP_K(rp_embed_fwd(ids, G.groups[0].w[it & 1], acts[0].x, T, s.h, F));
+      ++kernels;
+      const uint16_t* x = acts[0].x;
+      for (int i = 0; i < nl; ++i) {
+        wait_on(F, i + 1);
+        uint16_t* out = (i + 1 < nl) ? acts[i + 1].x : G.xbuf[1];
+        prof_unit(i, 0);
+        layer_fwd(G, i, x, acts[i], out, F);
+        x = out;
+      }
+      wait_on(F, s.L + 1);
+      prof_unit(s.L, 3);
+      head_fwd_bwd(G, x, gmb, first, grad_scale, F);
+      RP_CUDA(cudaEventRecord(G.ev_head_done, F));
+      // backward of mb on compute, starting from the head's hand-over
+      RP_CUDA(cudaStreamWaitEvent(st, G.ev_head_done, 0));
+      RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
+      RP_CUDA(cudaMemcpyAsync(G.dx32[0], G.hdx32, Th4, cudaMemcpyDeviceToDevice, st));
+      RP_CUDA(cudaMemcpyAsync(G.dx16, G.hdx16, Th2, cudaMemcpyDeviceToDevice, st));
+      RP_CUDA(cudaEventRecord(G.ev_hdx_free, st));
+      for (int i = nl - 1; i >= 0; --i) {
+        prof_unit(i, 1);
+        layer_bwd(G, i, acts[i], first);
+      }
+      float* dE = G.groups[0].grad[it & 1];  // embedding gradient (scatter-add of dL/dx_0)
+      if (first) RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+      RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
+      ++kernels;
+      if (want_tl) {
+        RP_CUDA(cudaEventRecord(rec.end, st));
+        records.push_back(rec);
+      }
+    }
+  } else
   for (int mb = 0; mb < MR; ++mb) {
     const int gmb = rin * MR + mb;
     const bool first = rin == 0 && mb == 0;

@@ -97,7 +97,8 @@ struct LayerActs {
   uint16_t *x, *h1, *qkv, *q, *k, *o, *x2, *h2, *gu, *act;
   float *rstd1, *rstd_q, *rstd_k, *lse, *rstd2;
   const uint16_t* xin = nullptr;  // the input actually used by layer_fwd
-  cudaEvent_t ev_free = nullptr;  // weight-gradient GEMMs done reading act/h2/o/h1
+  cudaEvent_t ev_free = nullptr;        // weight-gradient GEMMs done reading act/h2/o/h1
+  cudaEvent_t ev_chain_free = nullptr;  // the dgrad chain done with this layer's activations
 };
 
 // A hand-off / checkpoint buffer with its producer and consumer events.
@@ -132,6 +133,14 @@ struct Gpu {
   int fork_i = 0;
   std::vector<DevGroup> groups;           // index g = group + 1 (0 = embedding)
   std::vector<LayerActs> acts;            // per decoder layer of the fused stage
+  // pipelined fused stage (whole model fused, N <= 2): the forward + LM head of
+  // micro-batch k+1 runs on `fwd2` while micro-batch k's backward runs on
+  // `compute`; micro-batches alternate between two activation sets
+  std::vector<LayerActs> acts2;
+  cudaStream_t fwd2 = nullptr;
+  float* hdx32 = nullptr;                 // head output gradient, handed to the backward
+  uint16_t *hdx16 = nullptr, *hdh = nullptr;
+  cudaEvent_t ev_head_done = nullptr, ev_hdx_free = nullptr, ev_fwd_join = nullptr;
   float* dx32[2] = {nullptr, nullptr};
   uint16_t *dx16 = nullptr, *dh = nullptr, *dact = nullptr, *dgu = nullptr, *dattn = nullptr;
   uint16_t *dqkv = nullptr, *dq_t = nullptr, *dk_t = nullptr;

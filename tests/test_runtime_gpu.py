@@ -134,13 +134,16 @@ def test_multi_worker_grads_match_single_fused_stage():
     assert worst[1] < 1e-2, worst
 
 
-@pytest.mark.parametrize("resident", ["hbm", "streamed"])
+@pytest.mark.parametrize("variant", ["hbm", "streamed", "pipelined"])
 @pytest.mark.parametrize("mode", ["sync", "async"])
-def test_step_parity_single_fused_stage(mode, resident, monkeypatch):
+def test_step_parity_single_fused_stage(mode, variant, monkeypatch):
     """Single fused stage; the fp32 optimizer state either resident in free HBM
-    (single-device default) or streamed from pinned host memory every step."""
-    if resident == "streamed":
+    (single-device default) or streamed from pinned host memory every step;
+    'pipelined' runs micro-batch k+1's forward beside k's backward."""
+    if variant == "streamed":
         monkeypatch.setenv("RP_RESIDENT_GB", "0")
+    if variant == "pipelined":
+        monkeypatch.setenv("RP_FUSED_PIPELINE", "1")
     losses, g0, master, _, (plan, durs) = run_case(mode, 1)
     assert plan.num_slots() == 1 and plan.fused_stage.first == 0
     check(mode, losses, g0, master)
