@@ -217,9 +217,10 @@ struct Runtime {
     if (!prof_on) return -1;
     ProfRec r{0, prof_event(), prof_event(), 0.0, 0, 0, prof_layer * 4 + prof_phase, prof_inst};
     for (const Gpu& G : gpus)
-      if (G.compute == st || G.opt_comp == st || G.wgrad == st) {
+      if (G.compute == st || G.opt_comp == st || G.opt_res == st || G.wgrad == st ||
+          G.fwd2 == st) {
         r.worker = G.id;
-        r.lane = G.opt_comp == st ? 1 : (G.wgrad == st ? 2 : 0);
+        r.lane = (G.opt_comp == st || G.opt_res == st) ? 1 : (G.wgrad == st ? 2 : 0);
       }
     RP_CUDA(cudaEventRecord(r.a, st));
     prof.push_back(r);
@@ -268,6 +269,13 @@ struct Runtime {
   void push_resident(int g);        // host master/m/v -> device state
   void pull_resident(int g);        // device state -> host master/m/v (if stale)
   int64_t resident_params = 0;
+  // before the first grad write of an HBM-resident group g in an iteration:
+  // AdamW of the previous iteration has consumed its single grad buffer (edge 4)
+  void grad_free(Gpu& G, int g, cudaStream_t q) {
+    if (!host[g].d_state) return;  // streamed groups: two buffers, waited at slot start
+    RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_adam[0], 0));
+    RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_adam[1], 0));
+  }
   void sync_all();
   void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
             bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_, int N_, int K_,
@@ -417,18 +425,35 @@ void Runtime::place_resident_state() {
   for (int g = 0; g < ngroups(); ++g) order[g] = g;
   std::stable_sort(order.begin(), order.end(),
                    [&](int a, int b) { return host[a].n > host[b].n; });
+  // A resident group needs 12 B/param of state but only ONE fp32 grad buffer
+  // (its AdamW finishes within milliseconds of GradWrite, long before the next
+  // iteration's first write of that group), so converting a group costs a net
+  // 8 B/param: free grad[1] on every worker first, then allocate the state.
   for (int g : order) {
-    const int64_t bytes = host[g].n * 12;
-    if (bytes > budget) continue;
+    const int64_t n = host[g].n;
+    const int64_t freed = n * 4 * (int64_t)gpus.size();
+    if (n * 12 > budget + freed) continue;
+    for (Gpu& G : gpus) {
+      DevGroup& D = G.groups[g];
+      RP_CUDA(cudaFree(D.grad[1]));
+      D.grad[1] = D.grad[0];
+      G.allocated[1] -= (std::size_t)n * 4;
+    }
+    budget += freed;
     void* p = nullptr;
-    if (cudaMalloc(&p, (std::size_t)bytes) != cudaSuccess) {
+    if (cudaMalloc(&p, (std::size_t)(n * 12)) != cudaSuccess) {
       cudaGetLastError();
+      for (Gpu& G : gpus) {  // undo: back to two buffers
+        DevGroup& D = G.groups[g];
+        RP_CUDA(cudaMalloc(&D.grad[1], (std::size_t)n * 4));
+        G.allocated[1] += (std::size_t)n * 4;
+      }
       break;
     }
     host[g].d_state = static_cast<float*>(p);
-    budget -= bytes;
-    resident_params += host[g].n;
-    gpus[0].allocated[5] += (std::size_t)bytes;
+    budget -= n * 12;
+    resident_params += n;
+    gpus[0].allocated[5] += (std::size_t)(n * 12);
     push_resident(g);
   }
 }
@@ -528,6 +553,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   mk(&G.opt_h2d, lo);
   mk(&G.opt_d2h, lo);
   mk(&G.opt_comp, lo);
+  mk(&G.opt_res, lo);
   G.allocated.assign(8, 0);
   auto dalloc = [&](std::size_t bytes, int cat) -> void* {
     void* p = nullptr;
@@ -836,9 +862,11 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
     RP_CUDA(cudaEventRecord(e, st));
     RP_CUDA(cudaStreamWaitEvent(ws, e, 0));
   };
-  if (first)
+  if (first) {
+    grad_free(G, l + 1, st);
     for (const Tensor* t : {&LL.in_norm, &LL.q_norm, &LL.k_norm, &LL.post_norm})
       RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
+  }
   // MLP:  x3 = x2 + act(gu(h2)) Wd^T
   to_ws();
   gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
@@ -913,7 +941,10 @@ void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float
   const bool piped = on && on != G.compute;
   uint16_t* dh = piped ? G.hdh : G.dh;
   const int h = s.h, V = s.V;
-  if (first) RP_CUDA(cudaMemsetAsync(dW + HL.final_norm.off, 0, (size_t)h * 4, st));
+  if (first) {
+    grad_free(G, s.L + 1, st);
+    RP_CUDA(cudaMemsetAsync(dW + HL.final_norm.off, 0, (size_t)h * 4, st));
+  }
   RP_K(rp_rmsnorm_fwd(x, h, W + HL.final_norm.off, G.hN, h, G.rstdN, T, h, (float)s.eps, st));
   const int rows = std::min(T, logits_rows);
   for (int r0 = 0; r0 < T; r0 += rows) {
@@ -971,7 +1002,11 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     if (b == s.L) grad_groups.push_back(s.L + 1);
     if (a == 0) grad_groups.push_back(0);
     // grad[t%2] may be overwritten once AdamW consumed it (edge 4, parity form)
-    for (int g : grad_groups) RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_adam[it & 1], 0));
+    // HBM-resident groups keep ONE grad buffer: they wait last iteration's
+    // AdamW right before their first grad write instead (grad_free), so the
+    // slot does not stall on the whole resident optimizer pass
+    for (int g : grad_groups)
+      if (!host[g].d_state) RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_adam[it & 1], 0));
   }
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_tokens, 0));
   const bool want_tl = cfg.flags & RP_RT_RECORD_TIMELINE;
@@ -1034,7 +1069,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         layer_bwd(G, i, acts[i], first);
       }
       float* dE = G.groups[0].grad[it & 1];  // embedding gradient (scatter-add of dL/dx_0)
-      if (first) RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+      if (first) {
+          grad_free(G, 0, st);
+          RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+        }
       RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
       ++kernels;
       if (want_tl) {
@@ -1143,7 +1181,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     if (has_grads) {
       if (a == 0) {  // embedding gradient (scatter-add of dL/dx_0)
         float* dE = G.groups[0].grad[it & 1];
-        if (first) RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+        if (first) {
+          grad_free(G, 0, st);
+          RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+        }
         RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
         ++kernels;
       } else {  // hand dL/dx_a to the next (backward) slot
@@ -1248,14 +1289,17 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_gradwrite, 0));  // edge (3)
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_pcopy, 0));      // pend free again
   if (H.d_state) {  // HBM-resident fp32 state: one fused pass, no PCIe
-    cudaEvent_t xa = xfer_begin(G.opt_comp);
-    const int pi_ = prof_begin(G.opt_comp);
+    cudaStream_t q = G.opt_res;
+    RP_CUDA(cudaStreamWaitEvent(q, D.ev_gradwrite, 0));  // edge (3)
+    RP_CUDA(cudaStreamWaitEvent(q, D.ev_pcopy, 0));      // pend free again
+    cudaEvent_t xa = xfer_begin(q);
+    const int pi_ = prof_begin(q);
     RP_K(rp_adamw(H.d_state, H.d_state + H.n, H.d_state + 2 * H.n, D.grad[parity], D.pend, H.n,
-                  &cfg.adam, step_no, G.opt_comp));
-    prof_end(pi_, G.opt_comp, 3, 30.0 * H.n);
+                  &cfg.adam, step_no, q));
+    prof_end(pi_, q, 3, 30.0 * H.n);
     ++kernels;
-    RP_CUDA(cudaEventRecord(D.ev_adam[parity], G.opt_comp));
-    xfer_end(xa, G.opt_comp, 2, g - 1, last_iter, G.id);
+    RP_CUDA(cudaEventRecord(D.ev_adam[parity], q));
+    xfer_end(xa, q, 2, g - 1, last_iter, G.id);
     H.host_stale = true;
     pend_owner[g] = G.id;
     if (!cfg.async_optimizer) p_copy(g);
@@ -1333,7 +1377,8 @@ Runtime::~Runtime() {
   for (auto e : event_pool) cudaEventDestroy(e);
   for (Gpu& G : gpus) {
     cudaSetDevice(G.dev);
-    for (cudaStream_t st : {G.compute, G.act, G.wgrad, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp})
+    for (cudaStream_t st : {G.compute, G.act, G.wgrad, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp,
+                            G.opt_res, G.fwd2})
       if (st) cudaStreamDestroy(st);
   }
   if (loss_host) cudaFreeHost(loss_host);

@@ -115,6 +115,7 @@ struct Gpu {
   int id = 0, dev = 0;
   cudaStream_t compute = nullptr, act = nullptr, w_h2d = nullptr;
   cudaStream_t opt_h2d = nullptr, opt_d2h = nullptr, opt_comp = nullptr;
+  cudaStream_t opt_res = nullptr;  // AdamW of HBM-resident groups (never queued behind PCIe)
   // weight-gradient GEMMs run here, off the dgrad chain on `compute`, so the
   // persistent GEMMs' partial last waves and the chain's HBM-bound kernels
   // overlap them; scratch gradients they read are double-buffered
