@@ -186,7 +186,7 @@ struct Runtime {
   std::vector<cudaEvent_t> event_pool;
   int64_t h2d_bytes = 0, d2h_bytes = 0, p2p_bytes = 0, kernels = 0;
   int64_t chunk_elems = 32ll << 20;  // optimizer chunk (elements)
-  int logits_rows = 1024;            // LM-head chunk rows
+  int logits_rows = 2048;            // LM-head chunk rows (2 chunks per 4K micro-batch)
   int parities = 1;                  // hand-off / checkpoint buffer sets
   // kernel profiling (one step at a time): per category CUDA-event pairs
   // around each launch on its own stream, with the launch's algorithmic work
@@ -363,6 +363,10 @@ void Runtime::init(const rp_runtime_config_t& c) {
     }
   LL = make_layer_layout(s);
   HL = make_head_layout(s);
+  if (const char* e = getenv("RP_LOGITS_ROWS")) {  // LM-head chunk rows (study knob)
+    const int r = atoi(e);
+    if (r >= 128 && r % 128 == 0) logits_rows = r;
+  }
   if (!(cfg.residency_factor > 0)) cfg.residency_factor = 2.0;
   if (cfg.adam.lr == 0.f && cfg.adam.beta1 == 0.f) {
     cfg.adam = rp_adam_hparams_t{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f, 1.0f};
