@@ -298,39 +298,44 @@ __global__ void __launch_bounds__(192, 1)
 // head's MMAs, so the MUFU/FMA work of the two heads hides behind the MMAs.
 constexpr int PP_THREADS = 384;
 
-template <int HD>
+// PT: P goes back into the TMEM columns of its S (bf16 pairs) and feeds the
+// PV MMA as a TMEM A operand — no P store to shared memory, whose port the
+// SS MMAs at N=128 already saturate — and the freed smem deepens the K/V ring.
+template <int HD, bool PT>
 struct PpSmem {
   static constexpr int NSUB = HD / 64;
   static constexpr int QT = NSUB * SUB;       // one Q tile (128 rows x HD)
   static constexpr int KVT = NSUB * SUB;      // one K or V tile (128 keys x HD)
+  static constexpr int NSLOT = PT ? 4 : 3;    // K/V ring slots
   static constexpr int Q0 = 0;
-  static constexpr int RING = Q0 + 2 * QT;    // 3 slots
-  static constexpr int P = RING + 3 * KVT;    // P0, P1: 128 x 128 bf16 each (2 SUB)
-  static constexpr int BAR = P + 2 * 2 * SUB;
+  static constexpr int RING = Q0 + 2 * QT;
+  static constexpr int P = RING + NSLOT * KVT;  // P0, P1: 128 x 128 bf16 each (2 SUB), !PT
+  static constexpr int BAR = P + (PT ? 0 : 2 * 2 * SUB);
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds 227 KB of shared memory");
 };
 
-template <int HD>
+template <int HD, bool PT>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, bf16* __restrict__ o,
                        long long ldo, float* __restrict__ lse, int T, int seq, int nq, int nk,
                        float scale) {
-  using L = PpSmem<HD>;
+  using L = PpSmem<HD, PT>;
+  constexpr int NS = L::NSLOT;
   constexpr int NSUB = L::NSUB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [3]
-  uint64_t* kv_empty = bar + 4;  // [3]
-  uint64_t* s_full = bar + 7;    // [2] per head
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* o_done = bar + 11;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* kv_full = bar + 1;        // [NS]
+  uint64_t* kv_empty = bar + 1 + NS;  // [NS]
+  uint64_t* s_full = kv_empty + NS;   // [2] per head
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_done = p_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / TILE;
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
     mbar_init(q_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
@@ -372,8 +377,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tma_load_2d(sm + L::Q0 + w * L::QT + sub * SUB, &tm_q, q_full, (h0 + w) * HD + 64 * sub,
                     q0);
     for (int idx = 0; idx < 2 * ntiles; ++idx) {
-      const int slot = idx % 3;
-      mbar_wait(&kv_empty[slot], ((idx / 3) & 1) ^ 1);
+      const int slot = idx % NS;
+      mbar_wait(&kv_empty[slot], ((idx / NS) & 1) ^ 1);
       const int k0 = s0 + (idx >> 1) * TILE;
       uint8_t* dst = sm + L::RING + slot * L::KVT;
       mbar_arrive_expect_tx(&kv_full[slot], L::KVT);
@@ -388,8 +393,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     constexpr uint32_t idesc_o = umma_idesc_bf16(TILE, HD, 0, 1);
     const uint32_t q_addr = smem_u32(sm + L::Q0);
     const uint32_t p_addr = smem_u32(sm + L::P);
-    auto ring = [&](int idx) { return smem_u32(sm + L::RING + (idx % 3) * L::KVT); };
-    auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % 3], (idx / 3) & 1); };
+    auto ring = [&](int idx) { return smem_u32(sm + L::RING + (idx % NS) * L::KVT); };
+    auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % NS], (idx / NS) & 1); };
     auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T
       const uint32_t qa = q_addr + w * L::QT, ka = ring(2 * j);
       if (elect_one()) {
@@ -410,9 +415,13 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < TILE / 16; ++kk) {
-          const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
           const uint64_t bd = umma_desc_sw128(va + kk * 2048, SUB, 1024);
-          umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+          if (PT) {  // P: bf16 pairs in S_w's columns, 8 columns per K=16 step
+            umma_f16_ts(tmem + 256 + w * HD, tmem + w * TILE + kk * 8, bd, idesc_o, (j | kk) != 0);
+          } else {
+            const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
+            umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+          }
         }
         umma_commit(&o_done[w]);
       }
@@ -436,11 +445,11 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         issue_s(0, j + 1);  // S0 was read before P0_j was published
       }
       issue_pv(1, j);
-      if (elect_one()) umma_commit(&kv_empty[(2 * j + 1) % 3]);
+      if (elect_one()) umma_commit(&kv_empty[(2 * j + 1) % NS]);
       __syncwarp();
       if (more) {
         issue_s(1, j + 1);
-        if (elect_one()) umma_commit(&kv_empty[(2 * j + 2) % 3]);
+        if (elect_one()) umma_commit(&kv_empty[(2 * j + 2) % NS]);
         __syncwarp();
       }
     }
@@ -453,7 +462,7 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     const uint32_t s_col = w * TILE, o_col = 256 + w * HD;
     const float sl2 = scale * 1.4426950408889634f;
     float m = 0.f, l = 0.f;
-    uint8_t* p_row = sm + L::P + w * 2 * SUB + (r >> 3) * 1024 + (r & 7) * 128;
+    uint8_t* p_row = sm + L::P + w * 2 * SUB + (r >> 3) * 1024 + (r & 7) * 128;  // !PT
     for (int j = 0; j < ntiles; ++j) {
       mbar_wait(&s_full[w], j & 1);
       tc_fence_after();
@@ -502,14 +511,16 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tmem_st_wait();
         l *= f;
       }
-      if (j >= 1 && !o_ready) {  // PV_{j-1} must be done reading this head's P buffer
+      if (!PT && j >= 1 && !o_ready) {  // PV_{j-1} must be done reading this head's P buffer
         mbar_wait(&o_done[w], (j - 1) & 1);
         tc_fence_after();
       }
+      // (PT: PV_{j-1} read P_{j-1} from these TMEM columns before S_j overwrote them)
       // P = 2^(s*scale*log2e - m); four independent row-sum chains
       float2 lsum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
       const float2 sl2v = make_float2(sl2, sl2), negm = make_float2(-m, -m);
+      uint32_t pt[16];  // PT: 32 probabilities = 16 TMEM columns per store
 #pragma unroll
       for (int ch = 0; ch < TILE / 8; ++ch) {  // 16-byte chunks of the swizzled row
         uint32_t pk[4];
@@ -520,14 +531,21 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
           lsum4[e] = __fadd2_rn(lsum4[e], pv);
           pk[e] = pack_bf16x2(pv.x, pv.y);
         }
-        const int sub = ch >> 3, c8 = ch & 7;
-        *reinterpret_cast<uint4*>(p_row + sub * SUB + ((c8 ^ (r & 7)) << 4)) =
-            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        if (PT) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pt[(ch & 3) * 4 + e] = pk[e];
+          if ((ch & 3) == 3) tmem_st_32x32b_x16(lane_base + s_col + (ch >> 2) * 16, pt);
+        } else {
+          const int sub = ch >> 3, c8 = ch & 7;
+          *reinterpret_cast<uint4*>(p_row + sub * SUB + ((c8 ^ (r & 7)) << 4)) =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
       }
       const float2 ls = __fadd2_rn(__fadd2_rn(lsum4[0], lsum4[1]), __fadd2_rn(lsum4[2], lsum4[3]));
       const float lsum = ls.x + ls.y;
       l += lsum;
-      fence_proxy_async();
+      if (PT) tmem_st_wait_all();
+      else fence_proxy_async();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[w]);
@@ -601,17 +619,18 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
     return RP_E_CUDA;
   static const bool force_v1 = getenv("RP_ATTN_FWD_V1") != nullptr;
   if ((nq / nk) % 2 == 0 && !force_v1) {  // two heads of one KV group per CTA
-    auto kern = attn_fwd_pp_kernel<HD>;
+    static const bool p_smem = getenv("RP_ATTN_FWD_PSMEM") != nullptr;  // A/B knob
+    auto kern = p_smem ? attn_fwd_pp_kernel<HD, false> : attn_fwd_pp_kernel<HD, true>;
+    const int bytes = p_smem ? PpSmem<HD, false>::BYTES : PpSmem<HD, true>::BYTES;
     static bool cfg_pp = false;
     if (!cfg_pp) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               PpSmem<HD>::BYTES) != cudaSuccess)
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
+          cudaSuccess)
         return RP_E_CUDA;
       cfg_pp = true;
     }
     dim3 grid(T / TILE, nq / 2);
-    kern<<<grid, PP_THREADS, PpSmem<HD>::BYTES, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq,
-                                                      nk, scale);
+    kern<<<grid, PP_THREADS, bytes, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);
     return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
   }
   auto kern = attn_fwd_tc_kernel<HD>;
