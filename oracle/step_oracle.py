@@ -212,8 +212,8 @@ class StepOracle:
 
 
 def synthetic_batch(s: Shape, M: int, b: int, S: int, seed: int = 1234):
-    """Token ids ~ U{0..V-1} (seeded), labels = ids shifted by one, last
-    position of each sequence ignored (-100)."""
+    """Token ids ~ U{0..V-1} (seeded), labels = ids shifted by one (every
+    position labelled; callers mask positions with -100 to ignore them)."""
     g = torch.Generator().manual_seed(seed)
     ids = torch.randint(0, s.vocab, (M, b, S + 1), generator=g)
     tokens = ids[..., :S].contiguous()
