@@ -938,6 +938,222 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ============================================================ (B3) dQ, operands in TMEM
+// CTA = 128 queries x 1 head. Q and dO are staged ONCE into TMEM (bf16 pairs,
+// row = lane) and are the A operands of S = Q K^T and dP = dO V^T, so the
+// shared-memory port only carries the K/V tiles (B operands); S/dP are
+// double-buffered so the tensor core computes S/dP(j+1) and dQ(j) while 8
+// softmax warps (2 per lane quarter, one 32-key half each) turn tile j into
+// dS, written back as bf16 pairs into the columns of S they read (half 0 ->
+// cols [0,16), half 1 -> [32,48)), the A operand of dQ += dS K.
+constexpr int B3_NST = 5;
+
+template <int HD>
+struct Dq3Smem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int STAGE = 2 * NSUB * SUB64;  // K_j + V_j (64 keys)
+  static constexpr int BAR = B3_NST * STAGE;
+  static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dq3_kernel(const bf16* __restrict__ q, long long ldq, const bf16* __restrict__ dout,
+                        long long lddo, const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ lse,
+                        const float* __restrict__ delta, bf16* __restrict__ dq, long long lddq,
+                        int T, int seq, int nq, int nk, float scale) {
+  using L = Dq3Smem<HD>;
+  constexpr int NSUB = L::NSUB;
+  constexpr uint32_t TQ = 0, TDO = HD / 2, TS = HD, TDQ = HD + 256;  // TMEM columns
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* q_ready = bar + 0;
+  uint64_t* kv_full = bar + 1;            // [B3_NST]
+  uint64_t* kv_empty = bar + 1 + B3_NST;  // [B3_NST]
+  uint64_t* sd_full = kv_empty + B3_NST;  // [2]
+  uint64_t* ds_full = sd_full + 2;        // [2]
+  uint64_t* dq_done = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qblocks = T / B_Q;
+  const int qb = qblocks - 1 - (int)blockIdx.x;
+  const int h = blockIdx.y, kvh = h / (nq / nk);
+  const int q0 = qb * B_Q;
+  const int s0 = (q0 / seq) * seq;
+  const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    mbar_init(q_ready, 8);
+    for (int i = 0; i < B3_NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ds_full[i], 8);
+    }
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int j = 0; j < ntiles; ++j) {
+      const int st = j % B3_NST;
+      mbar_wait(&kv_empty[st], ((j / B3_NST) & 1) ^ 1);
+      const int k0 = s0 + j * B_K;
+      uint8_t* kd = sm + st * L::STAGE;
+      mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(kd + sub * SUB64, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
+        tma_load_2d(kd + NSUB * SUB64 + sub * SUB64, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
+                    k0);
+      }
+    }
+  } else if (warp == 1) {  // MMA: whole warp, uniform descriptors, elected issue
+    constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
+    constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
+    auto issue_sdp = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&kv_full[j % B3_NST], (j / B3_NST) & 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sm + (j % B3_NST) * L::STAGE);
+      const uint32_t v_addr = k_addr + NSUB * SUB64;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
+          umma_f16_ts(tmem + TS + b * 128, tmem + TQ + kk * 8,
+                      umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
+          umma_f16_ts(tmem + TS + b * 128 + 64, tmem + TDO + kk * 8,
+                      umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&sd_full[b]);
+      }
+      __syncwarp();
+    };
+    auto issue_dq = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&ds_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sm + (j % B3_NST) * L::STAGE);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < B_K / 16; ++kk) {  // dS keys 16kk..: cols 0,8 | 32,40
+          const uint32_t a = tmem + TS + b * 128 + (kk < 2 ? kk * 8 : 32 + (kk - 2) * 8);
+          umma_f16_ts(tmem + TDQ, a, umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024), idesc_q,
+                      (j | kk) != 0);
+        }
+        umma_commit(&kv_empty[j % B3_NST]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_ready, 0);
+    tc_fence_after();
+    issue_sdp(0);
+    for (int j = 0; j < ntiles; ++j) {
+      if (j + 1 < ntiles) issue_sdp(j + 1);  // S/dP[b^1] free: dQ(j-1) issued before it
+      issue_dq(j);
+    }
+    if (elect_one()) umma_commit(dq_done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    // 8 softmax warps: lane quarter = warp % 4 (query rows), half = 32-key half
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int r = quarter * 32 + lane;
+    const int qrow = q0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    // stage Q (half 0) or dO (half 1) row r into TMEM as bf16 pairs
+    {
+      const bf16* src = half == 0 ? q + (long long)qrow * ldq + (long long)h * HD
+                                  : dout + (long long)qrow * lddo + (long long)h * HD;
+      const uint32_t col = half == 0 ? TQ : TDO;
+#pragma unroll
+      for (int c = 0; c < HD / 2; c += 16) {  // 16 columns = 32 bf16 = 4 x 16 B
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src + 2 * c + 8 * i);
+          v[4 * i] = u.x;
+          v[4 * i + 1] = u.y;
+          v[4 * i + 2] = u.z;
+          v[4 * i + 3] = u.w;
+        }
+        tmem_st_32x32b_x16(lane_base + col + c, v);
+      }
+      tmem_st_wait_all();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_ready);
+    }
+    const float sl2 = scale * kLog2e;
+    const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
+    const float dl = delta[(long long)h * T + qrow];
+    for (int j = 0; j < ntiles; ++j) {
+      const int b = j & 1;
+      mbar_wait(&sd_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[32], dpv[32], pk[16];
+      tmem_ld_32x32b_x32(lane_base + TS + b * 128 + half * 32, sv);
+      tmem_ld_32x32b_x32(lane_base + TS + b * 128 + 64 + half * 32, dpv);
+      tmem_ld_wait();
+      const int kbase = s0 + j * B_K + half * 32;  // first key of these columns
+      const bool diag = kbase + 31 > q0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
+        if (diag) {
+          if (kbase + i > qrow) p0 = 0.f;
+          if (kbase + i + 1 > qrow) p1 = 0.f;
+        }
+        pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
+                                p1 * (__uint_as_float(dpv[i + 1]) - dl));
+      }
+      tmem_st_32x32b_x16(lane_base + TS + b * 128 + half * 32, pk);  // over own read columns
+      tmem_st_wait_all();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[b]);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
+#pragma unroll 1
+    for (int c = half * (HD / 2); c < (half + 1) * (HD / 2); c += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(lane_base + TDQ + c, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 u;
+        u.x = pack_bf16x2(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
+        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
+        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
+        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
+        *reinterpret_cast<uint4*>(dqr + c + i) = u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // delta[h, t] = sum_d dO[t,h,d] * O[t,h,d]; one warp per (t, h), 16-byte loads
 template <int HD>
 __global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf16* __restrict__ d,
@@ -1059,7 +1275,17 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   if (!map2d(&mk64, k, T, (long long)nk * HD, ldk, 64) ||
       !map2d(&mv64, v, T, (long long)nk * HD, ldv, 64))
     return RP_E_CUDA;
-  if ((nq / nk) % 2 == 0 && !v1) {
+  static const bool dq_pp = getenv("RP_ATTN_DQ_PP") != nullptr;  // A/B knob
+  if (!v1 && !dq_pp) {
+    static bool cfg4 = false;
+    if (!cfg4) {
+      if (!set_smem(attn_bwd_dq3_kernel<HD>, Dq3Smem<HD>::BYTES)) return RP_E_CUDA;
+      cfg4 = true;
+    }
+    attn_bwd_dq3_kernel<HD><<<dim3(T / B_Q, nq), 384, Dq3Smem<HD>::BYTES, s>>>(
+        (const bf16*)q, ldq, (const bf16*)dout, lddo, mk64, mv64, lse, delta, (bf16*)dq, lddq, T,
+        seq, nq, nk, scale);
+  } else if ((nq / nk) % 2 == 0 && !v1) {
     static bool cfg3 = false;
     if (!cfg3) {
       if (!set_smem(attn_bwd_dq_pp_kernel<HD>, Dq2Smem<HD>::BYTES)) return RP_E_CUDA;
