@@ -513,6 +513,233 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
   }
 }
 
+// ============================================================ (A3) dK / dV, operands in TMEM
+// CTA = 128 keys x TWO query heads of one KV group. K and V are staged ONCE
+// into TMEM (bf16 pairs, row = key = lane) and are the A operands of
+// S^T = K Q^T and dP^T = V dO^T, so shared memory only carries the small
+// (32-query) Q / dO tiles; with 32-query tiles two heads ping-pong in TMEM:
+//   K | V | S^T_a dP^T_a | S^T_b dP^T_b | dV | dK   (64+64+64+64+128+128 cols)
+// P^T / dS^T go back as bf16 pairs over the columns they came from and are
+// the A operands of dV += P^T dO and dK += dS^T Q (both heads into the same
+// accumulators). The (Q, dO, lse, delta) ring is 10 deep.
+constexpr int A3_BQ = 32;
+constexpr int A3_NST = 10;
+
+template <int HD>
+struct Dkv3Smem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int QT = A3_BQ * 128;               // one 32-row x 64-col sub-tile (4 KB)
+  static constexpr int STAGE = 2 * NSUB * QT;          // Q + dO of one (tile, head)
+  static constexpr int DO_OFF = NSUB * QT;
+  static constexpr int LD = A3_NST * STAGE;            // [A3_NST][2][A3_BQ] lse, delta
+  static constexpr int BAR = LD + A3_NST * 2 * A3_BQ * 4;
+  static constexpr int BYTES = BAR + 512 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_dkv3_kernel(const bf16* __restrict__ kg, long long ldk, const bf16* __restrict__ vg,
+                         long long ldv, const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_do,
+                         const float* __restrict__ lse, const float* __restrict__ delta,
+                         float* __restrict__ dk_acc, float* __restrict__ dv_acc, int T, int seq,
+                         int nq, int nk, float scale) {
+  using L = Dkv3Smem<HD>;
+  constexpr int NSUB = L::NSUB;
+  constexpr uint32_t TK = 0, TV = HD / 2, TH = HD, TDV = 256, TDK = 384;  // TMEM columns
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_ready = bar + 0;
+  uint64_t* st_full = bar + 1;             // [A3_NST]
+  uint64_t* st_empty = bar + 1 + A3_NST;   // [A3_NST]
+  uint64_t* sd_full = st_empty + A3_NST;   // [2] per head
+  uint64_t* ps_full = sd_full + 2;         // [2]
+  uint64_t* acc_done = ps_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kb = blockIdx.x, ha = 2 * (int)blockIdx.y;
+  const int kvh = ha / (nq / nk);
+  const int k0 = kb * A_BK;
+  const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
+  const int nqt = (s_end - k0) / A3_BQ;  // query tiles at/after the diagonal
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_ready, 8);
+    for (int i = 0; i < A3_NST; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ps_full[i], 4);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int idx = 0; idx < 2 * nqt; ++idx) {
+      const int st = idx % A3_NST, w = idx & 1, hq = ha + w;
+      mbar_wait(&st_empty[st], ((idx / A3_NST) & 1) ^ 1);
+      const int qs = k0 + (idx >> 1) * A3_BQ;
+      uint8_t* qd = sm + st * L::STAGE;
+      mbar_arrive_expect_tx(&st_full[st], L::STAGE + 2 * A3_BQ * 4);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(qd + sub * L::QT, &tm_q, &st_full[st], hq * HD + 64 * sub, qs);
+        tma_load_2d(qd + L::DO_OFF + sub * L::QT, &tm_do, &st_full[st], hq * HD + 64 * sub, qs);
+      }
+      float* ld = reinterpret_cast<float*>(sm + L::LD) + st * 2 * A3_BQ;
+      bulk_load_1d(ld, lse + (long long)hq * T + qs, A3_BQ * 4, &st_full[st]);
+      bulk_load_1d(ld + A3_BQ, delta + (long long)hq * T + qs, A3_BQ * 4, &st_full[st]);
+    }
+  } else if (warp == 1) {  // MMA: whole warp, uniform descriptors, elected issue
+    constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A3_BQ, 0, 0);   // A TMEM x B K-major
+    constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);      // A TMEM x B MN-major
+    auto stage = [&](int idx) { return smem_u32(sm + (idx % A3_NST) * L::STAGE); };
+    auto issue_sdp = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&st_full[idx % A3_NST], (idx / A3_NST) & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t qo = (kk >> 2) * L::QT + (kk & 3) * 32;
+          umma_f16_ts(tmem + TH + w * 64, tmem + TK + kk * 8, umma_desc_sw128(q_addr + qo, 16, 1024),
+                      idesc_s, kk != 0);
+          umma_f16_ts(tmem + TH + w * 64 + 32, tmem + TV + kk * 8,
+                      umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&sd_full[w]);
+      }
+      __syncwarp();
+    };
+    auto issue_grads = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&ps_full[w], j & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < A3_BQ / 16; ++kk) {  // 16 query rows of the MN-major B per step
+          const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, L::QT, 1024);
+          const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, L::QT, 1024);
+          umma_f16_ts(tmem + TDV, tmem + TH + w * 64 + kk * 8, ob, idesc_g, (idx | kk) != 0);
+          umma_f16_ts(tmem + TDK, tmem + TH + w * 64 + 32 + kk * 8, qb, idesc_g, (idx | kk) != 0);
+        }
+        umma_commit(&st_empty[idx % A3_NST]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_ready, 0);
+    tc_fence_after();
+    issue_sdp(0, 0);
+    issue_sdp(0, 1);
+    for (int j = 0; j < nqt; ++j) {
+      issue_grads(j, 0);
+      if (j + 1 < nqt) issue_sdp(j + 1, 0);  // in-order after grads_a(j) read P^T_a
+      issue_grads(j, 1);
+      if (j + 1 < nqt) issue_sdp(j + 1, 1);
+    }
+    if (elect_one()) umma_commit(acc_done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int w = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int key = k0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    // stage K (warpgroup a) or V (warpgroup b) row `key` into TMEM
+    {
+      const bf16* src = w == 0 ? kg + (long long)key * ldk + (long long)kvh * HD
+                               : vg + (long long)key * ldv + (long long)kvh * HD;
+      const uint32_t col = w == 0 ? TK : TV;
+#pragma unroll
+      for (int c = 0; c < HD / 2; c += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint4 u = *reinterpret_cast<const uint4*>(src + 2 * c + 8 * i);
+          v[4 * i] = u.x;
+          v[4 * i + 1] = u.y;
+          v[4 * i + 2] = u.z;
+          v[4 * i + 3] = u.w;
+        }
+        tmem_st_32x32b_x16(lane_base + col + c, v);
+      }
+      tmem_st_wait_all();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(kv_ready);
+    }
+    const float sl2 = scale * kLog2e;
+    for (int j = 0; j < nqt; ++j) {
+      const int idx = 2 * j + w, st = idx % A3_NST;
+      const int qs = k0 + j * A3_BQ;
+      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + st * 2 * A3_BQ;
+      const float* del_t = lse_t + A3_BQ;
+      mbar_wait(&st_full[st], (idx / A3_NST) & 1);  // lse/delta visibility
+      mbar_wait(&sd_full[w], j & 1);
+      tc_fence_after();
+      uint32_t sv[32], dpv[32], pk[16], dk2[16];
+      tmem_ld_32x32b_x32(lane_base + TH + w * 64, sv);
+      tmem_ld_32x32b_x32(lane_base + TH + w * 64 + 32, dpv);
+      tmem_ld_wait();
+      const bool diag = qs < k0 + A_BK;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[i] * kLog2e));
+        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[i + 1] * kLog2e));
+        if (diag) {
+          if (qs + i < key) p0 = 0.f;
+          if (qs + i + 1 < key) p1 = 0.f;
+        }
+        pk[i / 2] = pack_bf16x2(p0, p1);
+        dk2[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - del_t[i]),
+                                 p1 * (__uint_as_float(dpv[i + 1]) - del_t[i + 1]));
+      }
+      tmem_st_32x32b_x16(lane_base + TH + w * 64, pk);        // over read S^T columns
+      tmem_st_32x32b_x16(lane_base + TH + w * 64 + 32, dk2);  // over read dP^T columns
+      tmem_st_wait_all();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps_full[w]);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    float* dst = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
+    const uint32_t col = w == 0 ? TDK : TDV;
+    const float f = w == 0 ? scale : 1.f;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(lane_base + col + c, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        atomicAdd(reinterpret_cast<float4*>(dst + c + i),
+                  make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
+                              __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ======================================================================== (B) dQ
 // 128 queries per CTA, key tiles of 64 so that S and dP (64 TMEM columns
 // each) are double-buffered next to the dQ accumulator: the tensor core
@@ -1257,7 +1484,23 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   const long long acc_n = (long long)T * nk * HD;
   if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
   static const bool v1 = getenv("RP_ATTN_BWD_V1") != nullptr;
-  if ((nq / nk) % 2 == 0 && !v1) {  // two heads of one KV group per CTA
+  // opt-in: K/V-in-TMEM variant with 32-query tiles — correct, but measured
+  // 2 % slower than the 64-query ping-pong kernel below (0.596 vs 0.586 ms)
+  static const bool dkv3 = getenv("RP_ATTN_DKV3") != nullptr;
+  if ((nq / nk) % 2 == 0 && !v1 && dkv3) {  // K/V in TMEM, two heads, 32-query tiles
+    CUtensorMap mq32, mdo32;
+    if (!map2d(&mq32, q, T, (long long)nq * HD, ldq, A3_BQ) ||
+        !map2d(&mdo32, dout, T, (long long)nq * HD, lddo, A3_BQ))
+      return RP_E_CUDA;
+    static bool cfg5 = false;
+    if (!cfg5) {
+      if (!set_smem(attn_bwd_dkv3_kernel<HD>, Dkv3Smem<HD>::BYTES)) return RP_E_CUDA;
+      cfg5 = true;
+    }
+    attn_bwd_dkv3_kernel<HD><<<dim3(T / A_BK, nq / 2), 384, Dkv3Smem<HD>::BYTES, s>>>(
+        (const bf16*)k, ldk, (const bf16*)v, ldv, mq32, mdo32, lse, delta, dkv_acc,
+        dkv_acc + acc_n, T, seq, nq, nk, scale);
+  } else if ((nq / nk) % 2 == 0 && !v1) {  // two heads of one KV group per CTA
     static bool cfg2 = false;
     if (!cfg2) {
       if (!set_smem(attn_bwd_dkv_pp_kernel<HD>, Dkv2Smem<HD>::BYTES)) return RP_E_CUDA;

@@ -6,6 +6,8 @@ fp32-exact computation -> rel-L2 <= 1e-2; fp32 outputs <= 1e-4; attention
 """
 import math
 
+import os
+
 import pytest
 import torch
 
@@ -263,3 +265,15 @@ def test_flash_attention_fwd_bwd(T, seq, nq, nk, hd):
     assert rel(dq, qf.grad) < 2e-2
     assert rel(dk, kf.grad) < 2e-2
     assert rel(dv, vf.grad) < 2e-2
+
+
+def test_flash_attention_bwd_dkv3_variant():
+    """The opt-in K/V-in-TMEM dK/dV kernel (RP_ATTN_DKV3=1) matches torch too
+    (own process: the knob is read once per process)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, RP_ATTN_DKV3="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "test_flash_attention_bwd_tcgen05", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
