@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -49,6 +50,14 @@ struct Params {
   long long ldr;
   int vec;                 // 16-byte vector stores/loads legal for D (and R)
   int tma_out;             // fp32 D written through the TMA map (pair kernel)
+  // split-K of the last partial wave (pair kernel): work units [0, full) are
+  // whole tiles, units beyond are the two K halves of tile full + (u-full)/2;
+  // the first half parks its fp32 partial in `ws` and raises a per-warp flag
+  // (= epoch), the second adds it in its epilogue
+  int units, full;
+  float* ws;
+  unsigned* flags;
+  unsigned epoch;
 };
 
 // Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
@@ -357,6 +366,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     m0 = mt * 256;
     n0 = nt * PBN;
   };
+  // work unit -> (tile, k-block range, K half: -1 whole, 0 first, 1 second)
+  auto unit_info = [&](int u, int& tile, int& kb0, int& kb1, int& khalf) {
+    if (u < p.full) {
+      tile = u, kb0 = 0, kb1 = k_blocks, khalf = -1;
+    } else {
+      const int mid = k_blocks / 2;
+      tile = p.full + ((u - p.full) >> 1);
+      khalf = (u - p.full) & 1;
+      kb0 = khalf ? mid : 0;
+      kb1 = khalf ? k_blocks : mid;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma_a);
@@ -387,11 +408,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ---------------- TMA producer (both CTAs; each loads its halves) ----------------
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs) {
-      int m0, n0;
+    for (int u = pair; u < p.units; u += npairs) {
+      int tile, kb0, kb1, khalf, m0, n0;
+      unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
       const int am = m0 + 128 * rank, bn = n0 + (PBN / 2) * rank;
-      for (int kb = 0; kb < k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE;
         uint8_t* sb = sa + P_A_BYTES;
@@ -419,11 +441,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs) {
+    for (int u = pair; u < p.units; u += npairs) {
+      int tile, kb0, kb1, khalf;
+      unit_info(u, tile, kb0, kb1, khalf);
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * PBN;
-      for (int kb = 0; kb < k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE);
@@ -434,7 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                                    : umma_desc_sw128(a_addr + kk * 32, 16, 1024);
           const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + kk * 2048, 8192, 1024)
                                    : umma_desc_sw128(b_addr + kk * 32, 16, 1024);
-          umma_f16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          umma_f16_pair(d_tmem, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
         }
         umma_commit_pair(&empty[stage]);
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
@@ -448,15 +472,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t epi_chunk_no = 0;  // fp32 TMA epilogue: chunks issued by this warp
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs) {
-      int m0, n0;
+    for (int u = pair; u < p.units; u += npairs) {
+      int tile, kb0, kb1, khalf, m0, n0;
+      unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row0 = m0 + 128 * rank + q * 32;
       const int row = row0 + lane;
       const bool row_ok = row < p.M;
-      if (EPI != EPI_BF16 && p.tma_out) {
+      // split-K: this warp's 32 x PBN slab of the partial in the workspace
+      const int slab = ((tile - p.full) * 2 + (int)rank) * 4 + q;
+      float* part = khalf >= 0 ? p.ws + (long long)slab * 32 * PBN + lane * PBN : nullptr;
+      if (khalf == 0) {  // park the first K half's partial, then raise the flag
+#pragma unroll 1
+        for (int c = 0; c < PBN; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            *reinterpret_cast<uint4*>(part + c + i) = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.flags + slab), "r"(p.epoch)
+                       : "memory");
+      } else if (khalf == 1) {  // wait for the first half's partial
+        unsigned f = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.flags + slab) : "memory");
+        } while (f != p.epoch);
+      }
+      auto add_part = [&](int c, uint32_t (&v)[32]) {
+        if (khalf != 1) return;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 o = *reinterpret_cast<const float4*>(part + c + i);
+          v[i] = __float_as_uint(__uint_as_float(v[i]) + o.x);
+          v[i + 1] = __float_as_uint(__uint_as_float(v[i + 1]) + o.y);
+          v[i + 2] = __float_as_uint(__uint_as_float(v[i + 2]) + o.z);
+          v[i + 3] = __float_as_uint(__uint_as_float(v[i + 3]) + o.w);
+        }
+      };
+      if (khalf == 0) {
+        // nothing to store: the partial is parked
+      } else if (EPI != EPI_BF16 && p.tma_out) {
         // fp32: 32x32 chunks through swizzled smem and the TMA (store or L2 add),
         // two chunk buffers per warp in flight
         uint8_t* wbuf = epi_smem + q * (2 * 4096);
@@ -468,6 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t v[32];
           tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
           tmem_ld_wait();
+          add_part(c, v);
           uint8_t* buf = wbuf + (epi_chunk_no++ & 1) * 4096;  // alternates across tiles too
           if (lane == 0) bulk_wait_read<1>();  // the store from this buffer two chunks ago
           __syncwarp();
@@ -488,6 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t v[32];
           tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
           tmem_ld_wait();
+          add_part(c, v);
           epi_chunk<EPI>(p, row, row_ok, n0 + c, v);
         }
       }
@@ -567,6 +631,34 @@ int num_sms() {
   return n;
 }
 
+// Split-K workspace per stream (GEMMs on the compute and weight-gradient
+// streams may run concurrently): fp32 partial slabs + per-warp flags that
+// carry a launch epoch, so they never need resetting.
+struct SplitWs {
+  float* ws = nullptr;
+  unsigned* flags = nullptr;
+  std::size_t ws_elems = 0, n_flags = 0;
+  unsigned epoch = 0;
+};
+SplitWs& split_ws(cudaStream_t st, std::size_t elems, std::size_t flags) {
+  static std::unordered_map<cudaStream_t, SplitWs> pool;
+  SplitWs& w = pool[st];
+  if (w.ws_elems < elems || w.n_flags < flags) {
+    if (w.ws) cudaFree(w.ws);
+    if (w.flags) cudaFree(w.flags);
+    w.ws_elems = std::max<std::size_t>(elems, (std::size_t)37 * 2 * 128 * 256);
+    w.n_flags = std::max<std::size_t>(flags, 37 * 8);
+    if (cudaMalloc(&w.ws, w.ws_elems * 4) != cudaSuccess ||
+        cudaMalloc(&w.flags, w.n_flags * 4) != cudaSuccess ||
+        cudaMemset(w.flags, 0, w.n_flags * 4) != cudaSuccess) {
+      cudaGetLastError();
+      w = SplitWs{};
+    }
+    w.epoch = 0;
+  }
+  return w;
+}
+
 // Tile N for the CTA-pair kernel: 256. (256x128 pair tiles would fill the 74
 // pairs' last wave better for 4096-wide GEMMs, but measured at ~1.0 PF/s vs
 // ~1.35 for 256x256 on B200 — half-size MMAs double the per-k-block pipeline
@@ -596,8 +688,28 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     }
     const int pbn = narrow ? 128 : 256;
     const int tiles = ((p.M + 255) / 256) * ((p.N + pbn - 1) / pbn);
-    const int pairs = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, p, n_fastest);
+    const int npairs = num_sms() / 2;
+    Params q = p;
+    q.units = q.full = tiles;
+    // split-K of a short last wave: its tiles become two K halves each, so
+    // the wave finishes in about half the time. Only for long K (>= 8192):
+    // measured +6 % on 4096x4096x12288 and 4096x4096x24576, but -2..-5 % at
+    // K = 4096, where parking and re-reading the 128 KB fp32 partial per CTA
+    // costs about what the shorter wave saves
+    const int full = (tiles / npairs) * npairs, tail = tiles - full;
+    static const bool no_split = getenv("RP_GEMM_NO_SPLITK") != nullptr;
+    if (!no_split && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
+      SplitWs& w = split_ws(stream, (std::size_t)tail * 2 * 128 * pbn, (std::size_t)tail * 8);
+      if (w.ws) {
+        q.full = full;
+        q.units = full + 2 * tail;
+        q.ws = w.ws;
+        q.flags = w.flags;
+        q.epoch = ++w.epoch;
+      }
+    }
+    const int pairs = q.units < npairs ? q.units : npairs;
+    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, q, n_fastest);
     return cudaGetLastError();
   }
   auto kern = gemm_kernel<A_MN, B_MN, EPI>;
@@ -658,7 +770,7 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
                        (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                        make_map_f32(&td, g->D, g->M, g->N, g->ldd);
   Params p{g->M, g->N, g->K, g->D, g->ldd, reinterpret_cast<const __nv_bfloat16*>(g->R), g->ldr,
-           vec ? 1 : 0, tma_out ? 1 : 0};
+           vec ? 1 : 0, tma_out ? 1 : 0, 0, 0, nullptr, nullptr, 0};
   const int epi = g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
   if (g->out_f32 && g->R) return RP_E_INPUT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

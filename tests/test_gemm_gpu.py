@@ -85,3 +85,32 @@ def test_linear_layer_three_gemms():
     assert _rel(Y, X.float() @ W.float().t()) < 8e-3
     assert _rel(dX, dY.float() @ W.float()) < 8e-3
     assert _rel(dW, dY.float().t() @ X.float()) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(4096, 4096, 8192, 0, 0), (4096, 4096, 8192, 0, 1),
+                                             (4096, 4096, 8192, 1, 1), (2048, 2560, 8192, 0, 0),
+                                             (4000, 4040, 12288, 0, 0)])
+def test_gemm_split_k_last_wave(M, N, K, a_mn, b_mn):
+    """Shapes whose last wave over the 74 CTA pairs is short (e.g. 256 tiles =
+    3 waves + 34) run that wave as split-K halves: bf16, bf16+residual, fp32
+    and fp32-accumulate epilogues all match torch, repeated launches (epochs)
+    included; RP_GEMM_NO_SPLITK would disable it."""
+    from paper_2604_27085_b200 import kernels
+    A, B, R = _mk(M, K, 11), _mk(N, K, 12), _mk(M, N, 13)
+    Aop = A.t().contiguous() if a_mn else A
+    Bop = B.t().contiguous() if b_mn else B
+    ref = A.float() @ B.float().t()
+    D16 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        kernels.gemm(Aop, Bop, D16, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn))
+    torch.cuda.synchronize()
+    assert _rel(D16, ref) < 8e-3
+    if not a_mn:
+        kernels.gemm(Aop, Bop, D16, b_mn_major=bool(b_mn), residual=R)
+        torch.cuda.synchronize()
+        assert _rel(D16, ref + R.float()) < 8e-3
+    D32 = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    kernels.gemm(Aop, Bop, D32, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn))
+    kernels.gemm(Aop, Bop, D32, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn), accumulate=True)
+    torch.cuda.synchronize()
+    assert _rel(D32, 2 * ref) < 1e-5
