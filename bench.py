@@ -255,9 +255,16 @@ def run_ours(args):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         w0 = time.perf_counter()
+        # non-blocking forward_backward: step t's loss is read (D2H) while
+        # t+1 is enqueued, so S=1 plans on N>1 GPUs overlap iterations
+        prev = None
         for _ in range(args.steps):
-            losses.append(rt.forward_backward(tokens, labels))
+            cur = rt.forward_backward_async(tokens, labels)
             rt.step()
+            if prev is not None:
+                losses.append(rt.loss(prev))
+            prev = cur
+        losses.append(rt.loss(prev))
         rt.sync()
         w1 = time.perf_counter()
         ev1.record()

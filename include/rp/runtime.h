@@ -85,6 +85,14 @@ int rp_runtime_load(rp_runtime_t* rt, const char* path);
 
 int rp_forward_backward(rp_runtime_t* rt, const int32_t* tokens, const int32_t* labels,
                         float* loss);
+/* Non-blocking form: enqueue the iteration on every worker and return at
+ * once (*iteration = its index); rp_loss() waits for the loss of one of the
+ * two most recent iterations. With S=1 plans on N>1 GPUs this lets iteration
+ * t+1 run on the next GPU while t finishes (the blocking call serialises
+ * them, since S=1's loss is known only at the end). */
+int rp_forward_backward_async(rp_runtime_t* rt, const int32_t* tokens, const int32_t* labels,
+                              int32_t* iteration);
+int rp_loss(rp_runtime_t* rt, int32_t iteration, float* loss);
 int rp_step(rp_runtime_t* rt);
 int rp_sync(rp_runtime_t* rt);
 

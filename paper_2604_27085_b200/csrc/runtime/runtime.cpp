@@ -161,8 +161,15 @@ struct Runtime {
   std::vector<char> fused_worker;    // worker ran a fused task this iteration
   int iter = 0, last_iter = -1;
   bool grads_pending = false;
-  float* loss_host = nullptr;        // pinned [N]
+  float* loss_host = nullptr;        // pinned [2][N] (iteration parity)
   std::vector<cudaEvent_t> ev_loss;  // per worker, after its last fused task
+  // per iteration parity: which workers ran a fused slot, the loss scale, and
+  // the iteration number (non-blocking forward_backward / rp_loss)
+  std::vector<char> fused_par[2];
+  float grad_scale_par[2] = {0.f, 0.f};
+  int iter_par[2] = {-1, -1};
+  void enqueue_iteration(const int32_t* tokens, const int32_t* labels);
+  float wait_loss(int it);
   std::vector<TaskRecord> records;
   // transfer / optimizer intervals for the measured timeline
   struct XferRecord {
@@ -398,7 +405,7 @@ void Runtime::init(const rp_runtime_config_t& c) {
   pcopy_ev.assign(ngroups(), nullptr);
   state_ev.assign(ngroups(), nullptr);
   uploaders.assign(ngroups(), {});
-  RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N));
+  RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N * 2));
   gpus.resize(N);
   for (int w = 0; w < N; ++w) alloc_worker(gpus[w], w);
   ev_loss.resize(N);
@@ -647,9 +654,16 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   G.hN = static_cast<uint16_t*>(dalloc(Th * 2, 4));
   G.rstdN = static_cast<float*>(dalloc((std::size_t)T * 4, 4));
   G.logits = static_cast<uint16_t*>(dalloc((int64_t)std::min(T, logits_rows) * s.V * 2, 4));
-  G.loss_dev = static_cast<float*>(dalloc(64, 4));
-  G.tokens_dev = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
-  G.labels_dev = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
+  for (int b = 0; b < 2; ++b) {
+    G.loss_par[b] = static_cast<float*>(dalloc(64, 4));
+    G.tokens_par[b] = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
+    G.labels_par[b] = static_cast<int32_t*>(dalloc((int64_t)M * T * 4, 4));
+    G.ev_iter_done[b] = new_event(false);
+    G.ev_loss_par[b] = new_event(false);
+  }
+  G.loss_dev = G.loss_par[0];
+  G.tokens_dev = G.tokens_par[0];
+  G.labels_dev = G.labels_par[0];
   G.ev_tokens = new_event(false);
   {  // RoPE (cos, sin) table: float64 on the host, rounded (as the oracle)
     const int half = s.hd / 2;
@@ -1223,16 +1237,31 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
 }
 
 void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, float* loss) {
+  enqueue_iteration(tokens, labels);
+  const float l = wait_loss(last_iter);  // early return: once the fused slots are done
+  if (loss) *loss = l;
+}
+
+// Enqueue one iteration on all workers and return without waiting (the
+// non-blocking form of forward_backward: with S=1 plans on N>1 GPUs the next
+// iteration runs on another GPU while this one finishes).
+void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
   const int it = iter++;
   last_iter = it;
   exec_iter = it;
   ensure_horizon(it);
+  const int par = it & 1;
   int64_t n_valid = 0;
   for (int64_t i = 0; i < (int64_t)M * T; ++i) n_valid += labels[i] >= 0;
   const float grad_scale = n_valid > 0 ? 1.0f / (float)n_valid : 0.f;
   fused_worker.assign(N, 0);
   for (Gpu& G : gpus) {
     set_dev(G);
+    G.tokens_dev = G.tokens_par[par];
+    G.labels_dev = G.labels_par[par];
+    G.loss_dev = G.loss_par[par];
+    // iteration it-2 on this worker is done with this parity's buffers
+    RP_CUDA(cudaStreamWaitEvent(G.act, G.ev_iter_done[par], 0));
     RP_CUDA(cudaMemcpyAsync(G.tokens_dev, tokens, (size_t)M * T * 4, cudaMemcpyHostToDevice,
                             G.act));
     RP_CUDA(cudaMemcpyAsync(G.labels_dev, labels, (size_t)M * T * 4, cudaMemcpyHostToDevice,
@@ -1267,18 +1296,35 @@ void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, flo
     run_slot(G, it, t.round, t.slot, first_round, grad_scale);
     i += MR;  // a (round, slot) is MR consecutive tasks on one worker
   }
-  // early return: the loss is known once the fused slots are done
+  for (Gpu& G : gpus) {  // this parity's buffers are free once `compute` gets here
+    set_dev(G);
+    RP_CUDA(cudaEventRecord(G.ev_iter_done[par], G.compute));
+    if (fused_worker[G.id]) {
+      RP_CUDA(cudaStreamWaitEvent(G.act, ev_loss[G.id], 0));
+      RP_CUDA(cudaMemcpyAsync(loss_host + par * N + G.id, G.loss_dev, 4, cudaMemcpyDeviceToHost,
+                              G.act));
+      RP_CUDA(cudaEventRecord(G.ev_loss_par[par], G.act));
+    }
+  }
+  fused_par[par] = fused_worker;
+  grad_scale_par[par] = grad_scale;
+  iter_par[par] = it;
+  grads_pending = true;
+}
+
+// Mean token loss of iteration `it` (one of the last two enqueued).
+float Runtime::wait_loss(int it) {
+  const int par = it & 1;
+  if (it < 0 || iter_par[par] != it)
+    throw RtError(RP_E_INPUT, "loss of iteration " + std::to_string(it) + " is no longer held");
   double total = 0.0;
   for (Gpu& G : gpus) {
-    if (!fused_worker[G.id]) continue;
+    if (!fused_par[par][G.id]) continue;
     set_dev(G);
-    RP_CUDA(cudaStreamWaitEvent(G.act, ev_loss[G.id], 0));
-    RP_CUDA(cudaMemcpyAsync(loss_host + G.id, G.loss_dev, 4, cudaMemcpyDeviceToHost, G.act));
-    RP_CUDA(cudaStreamSynchronize(G.act));
-    total += loss_host[G.id];
+    RP_CUDA(cudaEventSynchronize(G.ev_loss_par[par]));
+    total += loss_host[par * N + G.id];
   }
-  if (loss) *loss = (float)(total * grad_scale);
-  grads_pending = true;
+  return (float)(total * grad_scale_par[par]);
 }
 
 // ---- optimizer lane -------------------------------------------------------------------
@@ -1689,6 +1735,22 @@ RP_API int rp_forward_backward(rp_runtime_t* p, const int32_t* tokens, const int
   return rt_guard([&] {
     if (!tokens || !labels) throw RtError(RP_E_INPUT, "null tokens/labels");
     R(p)->forward_backward(tokens, labels, loss);
+  });
+}
+
+RP_API int rp_forward_backward_async(rp_runtime_t* p, const int32_t* tokens,
+                                     const int32_t* labels, int32_t* iteration) {
+  return rt_guard([&] {
+    if (!tokens || !labels) throw RtError(RP_E_INPUT, "null tokens/labels");
+    R(p)->enqueue_iteration(tokens, labels);
+    if (iteration) *iteration = R(p)->last_iter;
+  });
+}
+
+RP_API int rp_loss(rp_runtime_t* p, int32_t iteration, float* loss) {
+  return rt_guard([&] {
+    if (!loss) throw RtError(RP_E_INPUT, "null loss");
+    *loss = R(p)->wait_loss(iteration);
   });
 }
 

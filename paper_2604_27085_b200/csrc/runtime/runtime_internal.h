@@ -149,7 +149,13 @@ struct Gpu {
   uint16_t* xbuf[2] = {nullptr, nullptr};
   uint16_t *hN = nullptr, *logits = nullptr;
   float *rstdN = nullptr, *loss_dev = nullptr;
-  int32_t *tokens_dev = nullptr, *labels_dev = nullptr;
+  int32_t *tokens_dev = nullptr, *labels_dev = nullptr;  // current iteration's parity set
+  // per iteration parity: token/label/loss buffers, so iteration t+1 can be
+  // enqueued (non-blocking forward_backward) while t still runs
+  int32_t *tokens_par[2] = {nullptr, nullptr}, *labels_par[2] = {nullptr, nullptr};
+  float* loss_par[2] = {nullptr, nullptr};
+  cudaEvent_t ev_iter_done[2] = {nullptr, nullptr};  // last read of parity set (compute)
+  cudaEvent_t ev_loss_par[2] = {nullptr, nullptr};
   float* cos_sin = nullptr;
   float* opt_buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   cudaEvent_t opt_free[2] = {nullptr, nullptr};

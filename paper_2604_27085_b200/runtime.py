@@ -202,6 +202,23 @@ class RoundPipe:
                    labels.ctypes.data_as(P(I32)), C.byref(loss))
         return loss.value
 
+    def forward_backward_async(self, tokens: np.ndarray, labels: np.ndarray) -> int:
+        """Enqueue the iteration and return its index without waiting; the
+        host buffers may be reused at once. Read the loss with loss(it)."""
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        assert tokens.size == self.micro_batches * self.micro_batch * self.seq_len
+        it = I32()
+        self._call("rp_forward_backward_async", self.h, tokens.ctypes.data_as(P(I32)),
+                   labels.ctypes.data_as(P(I32)), C.byref(it))
+        return it.value
+
+    def loss(self, iteration: int) -> float:
+        """Mean token loss of one of the two most recently enqueued iterations."""
+        out = F32()
+        self._call("rp_loss", self.h, I32(iteration), C.byref(out))
+        return out.value
+
     def step(self):
         self._call("rp_step", self.h)
 

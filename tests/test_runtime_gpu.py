@@ -282,3 +282,44 @@ def test_step_parity_two_sequences_per_micro_batch_and_ignored_labels(N):
         a = torch.from_numpy(np.asarray(g0[k])).reshape(ref_g[k].shape)
         rel = ((a - ref_g[k]).norm() / ref_g[k].norm()).item()
         assert rel < 3e-2, (k, rel)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_non_blocking_forward_backward_matches_blocking(N):
+    """rp_forward_backward_async + rp_loss (iteration t+1 enqueued before t's
+    loss is read; token/label/loss buffers by iteration parity) gives the same
+    losses as the blocking call, async optimizer, N=1 and N=2 workers (S=1:
+    iterations alternate workers)."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    params = O.init_params(s, seed=0)
+    batches = [O.synthetic_batch(s, 4, 1, 256, seed=100 + i) for i in range(4)]
+
+    def make():
+        rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=N,
+                       async_optimizer=True,
+                       adam=AdamW(HP["lr"], HP["betas"], HP["eps"], HP["weight_decay"]),
+                       skip_init=True)
+        rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+        return rt
+    rt = make()
+    ref = []
+    for tok, lab in batches:
+        ref.append(rt.forward_backward(tok.numpy(), lab.numpy()))
+        rt.step()
+    rt.close()
+    rt = make()
+    got, prev = [], None
+    for tok, lab in batches:
+        cur = rt.forward_backward_async(tok.numpy(), lab.numpy())
+        rt.step()
+        if prev is not None:
+            got.append(rt.loss(prev))
+        prev = cur
+    got.append(rt.loss(prev))
+    with pytest.raises(Exception):
+        rt.loss(0)  # only the two most recent iterations are held
+    rt.sync()
+    rt.close()
+    for a, b in zip(got, ref):
+        assert abs(a - b) / abs(b) < 1e-4, (got, ref)
