@@ -68,14 +68,20 @@ def ncu_gemm_traffic():
     return None
 
 
-def step_flops(d, seq, tokens, recompute_layers):
+def step_flops(d, seq, tokens, recompute_layers, lora_rank=0):
     """Executed FLOPs of one step: 3x fwd per layer (+1 fwd for recomputed
-    layers), causal attention, head fwd+dgrad+wgrad."""
+    layers), causal attention, head fwd+dgrad+wgrad. LoRA: no base wgrad
+    (frozen), plus the rank-r adapter GEMMs (2 fwd + 4 bwd per linear)."""
     qkvd = (d["nq"] + 2 * d["nk"]) * d["hd"]
     lin = 2 * tokens * (d["h"] * qkvd + d["nq"] * d["hd"] * d["h"] + 3 * d["h"] * d["m"])
     attn = 2 * d["nq"] * d["hd"] * tokens * seq  # causal fwd (QK^T + PV)
     layer_fwd = lin + attn
     head = 2 * tokens * d["h"] * d["V"]
+    if lora_rank:
+        io = (d["h"] + qkvd) + (d["nq"] * d["hd"] + d["h"]) + (d["h"] + 2 * d["m"]) + (d["m"] + d["h"])
+        adapters = 2 * tokens * lora_rank * io  # one pass of X A^T + U B^T over the 4 linears
+        per_layer = 2 * lin + 3.5 * attn + 3 * adapters
+        return d["L"] * per_layer + recompute_layers * (layer_fwd + adapters) + 2 * head
     return d["L"] * 3 * layer_fwd + recompute_layers * layer_fwd + 3 * head
 
 
@@ -215,7 +221,8 @@ def weight_gb(model):
 
 
 def config_dict(args):
-    return {"workload": f"{args.model} full fine-tune, seq {args.seq}, b=1, M={args.micro_batches} "
+    kind = f"LoRA r={args.lora_rank} fine-tune" if getattr(args, "lora_rank", 0) else "full fine-tune"
+    return {"workload": f"{args.model} {kind}, seq {args.seq}, b=1, M={args.micro_batches} "
                         f"micro-batches/step, RoundPipe-{'async' if args.mode == 'async' else 'sync'}, "
                         "fp32 AdamW states in pinned host memory",
             "model": args.model, "global_batch": args.micro_batches, "seq_len": args.seq,
@@ -235,7 +242,7 @@ def run_ours(args):
     t_setup = time.time()
     rt = RoundPipe(args.model, seq_len=args.seq, micro_batch=1, micro_batches=args.micro_batches,
                    num_gpus=args.gpus, async_optimizer=args.mode == "async", adam=AdamW(lr=1e-5),
-                   record_timeline=True)
+                   record_timeline=True, lora_rank=args.lora_rank, lora_alpha=args.lora_alpha)
     setup_s = time.time() - t_setup
     d = MODEL_DIMS[args.model]
     g = torch.Generator().manual_seed(1234)
@@ -316,7 +323,7 @@ def run_ours(args):
     h2d = (st1["h2d_bytes"] - st0["h2d_bytes"]) / args.steps
     d2h = (st1["d2h_bytes"] - st0["d2h_bytes"]) / args.steps
     recompute = sum(r.size() for r in plan.bwd_stages)
-    flops = step_flops(d, args.seq, tokens_step, recompute)
+    flops = step_flops(d, args.seq, tokens_step, recompute, args.lora_rank)
     t_comp = flops / (sustained * 1e12) / args.gpus
     t_link = max(h2d / (PCIE_H2D_GBS * 1e9), d2h / (PCIE_D2H_GBS * 1e9)) / args.gpus
     value = args.steps * tokens_step / (ms * 1e-3)
@@ -387,6 +394,9 @@ def main():
     ap.add_argument("--micro-batches", type=int, default=16)
     ap.add_argument("--mode", default="async", choices=["async", "sync"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lora-rank", type=int, default=0,
+                    help="LoRA fine-tune (base frozen, rank-r adapters); 0 = full fine-tune")
+    ap.add_argument("--lora-alpha", type=float, default=0.0)
     ap.add_argument("--report-dir", default=None,
                     help="write the measured timeline (report JSON + SVG Gantt) here")
     args = ap.parse_args()

@@ -73,6 +73,8 @@ int rp_adamw(float* master, float* m, float* v, const float* grad, void* w16, in
 int rp_f32_to_bf16(const float* a, void* b, int64_t n, void* stream);
 int rp_bf16_to_f32(const void* a, float* b, int64_t n, void* stream);
 int rp_add_f32(float* a, const float* b, int64_t n, void* stream);
+/* a[i] *= f (bf16 in place; LoRA scaling of the rank-r projections) */
+int rp_scale_bf16(void* a, int64_t n, float f, void* stream);
 /* Deterministic N(0, std) rounded to bf16 (counter hash + Box-Muller); f32
  * (optional) receives the exact widening of the bf16 value. */
 int rp_init_normal(float* f32, void* b16, int64_t n, uint64_t seed, float std, void* stream);

@@ -45,6 +45,13 @@ typedef struct {
   uint64_t init_seed;
   float init_std;
   int32_t flags;               /* RP_RT_* */
+  /* LoRA: rank r > 0 freezes every base weight
+   * (embedding, norms, linears, LM head) and trains rank-r adapters on the
+   * four linears of each layer: Y = X W^T + (alpha/r) (X A^T) B^T. Base
+   * weights still stream from pinned host memory; grads and AdamW state exist
+   * only for the adapters. 0 = full fine-tune. */
+  int32_t lora_rank;
+  float lora_alpha;
 } rp_runtime_config_t;
 
 typedef struct {
@@ -111,7 +118,8 @@ int rp_transfer_timeline(rp_runtime_t* rt, rp_xfer_event_t* out, int64_t cap, in
 /* The cost table the plan was built from (L+1 rows). */
 int rp_runtime_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
 /* Flat layout of a group: (offset, rows, cols) per tensor, order
- * embedding: [table]; layer: in_norm qkv q_norm k_norm o post_norm gate_up down;
+ * embedding: [table]; layer: in_norm qkv q_norm k_norm o post_norm gate_up down
+ * (+ LoRA: qkv_A qkv_B o_A o_B gate_up_A gate_up_B down_A down_B);
  * head: final_norm lm_head. */
 int rp_param_layout(rp_runtime_t* rt, int32_t group, int64_t* offs, int64_t* rows,
                     int64_t* cols, int32_t cap, int32_t* n);

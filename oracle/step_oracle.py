@@ -67,6 +67,27 @@ def layer_param_shapes(s: Shape):
             ("gate_up", (2 * s.inter, s.hidden)), ("down", (s.hidden, s.inter))]
 
 
+def lora_param_shapes(s: Shape, r: int):
+    """LoRA adapters of a layer (PEFT semantics): A [r, in],
+    B [out, r]; in the runtime's flat order after the base tensors."""
+    qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
+    return [("qkv_lora_A", (r, s.hidden)), ("qkv_lora_B", (qd + 2 * kd, r)),
+            ("o_lora_A", (r, qd)), ("o_lora_B", (s.hidden, r)),
+            ("gate_up_lora_A", (r, s.hidden)), ("gate_up_lora_B", (2 * s.inter, r)),
+            ("down_lora_A", (r, s.inter)), ("down_lora_B", (s.hidden, r))]
+
+
+def init_lora_params(s: Shape, r: int, seed: int = 1, std_a: float = 0.02, std_b: float = 0.0):
+    """A ~ N(0, std_a), B ~ N(0, std_b) (PEFT's default B = 0), bf16-rounded."""
+    g = torch.Generator().manual_seed(seed)
+    out = {}
+    for l in range(s.layers):
+        for n, sh in lora_param_shapes(s, r):
+            std = std_a if n.endswith("_A") else std_b
+            out[f"layers.{l}.{n}"] = (torch.randn(sh, generator=g) * std).to(torch.bfloat16).float()
+    return out
+
+
 def head_param_shapes(s: Shape):
     return [("final_norm", (s.hidden,)), ("lm_head", (s.vocab, s.hidden))]
 
@@ -106,12 +127,19 @@ def rotate_half(x):
     return torch.cat([-x[..., h:], x[..., :h]], -1)
 
 
-def decoder_layer(x, p, pre, s: Shape, cos, sin):
-    """x [b, S, h] fp32 -> [b, S, h]; p(name) gives the fp32 weight."""
+def decoder_layer(x, p, pre, s: Shape, cos, sin, lora_scale: float = 0.0):
+    """x [b, S, h] fp32 -> [b, S, h]; p(name) gives the fp32 weight. With
+    lora_scale > 0 every linear adds scale * (x A^T) B^T (PEFT LoRA)."""
     b, S, _ = x.shape
     qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
+
+    def lin(t, name):
+        y = t @ p(pre + name).t()
+        if lora_scale:
+            y = y + lora_scale * ((t @ p(pre + name + "_lora_A").t()) @ p(pre + name + "_lora_B").t())
+        return y
     h1 = rms(x, p(pre + "input_norm"), s.eps)
-    qkv = h1 @ p(pre + "qkv").t()
+    qkv = lin(h1, "qkv")
     q = qkv[..., :qd].view(b, S, s.heads, s.head_dim)
     k = qkv[..., qd:qd + kd].view(b, S, s.kv_heads, s.head_dim)
     v = qkv[..., qd + kd:].view(b, S, s.kv_heads, s.head_dim)
@@ -127,14 +155,14 @@ def decoder_layer(x, p, pre, s: Shape, cos, sin):
     mask = torch.ones(S, S, dtype=torch.bool).triu(1)
     att = att.masked_fill(mask, float("-inf")).softmax(-1)
     o = (att @ v).transpose(1, 2).reshape(b, S, qd)
-    x2 = x + o @ p(pre + "o").t()
+    x2 = x + lin(o, "o")
     h2 = rms(x2, p(pre + "post_norm"), s.eps)
-    gu = h2 @ p(pre + "gate_up").t()
+    gu = lin(h2, "gate_up")
     act = torch.nn.functional.silu(gu[..., :s.inter]) * gu[..., s.inter:]
-    return x2 + act @ p(pre + "down").t()
+    return x2 + lin(act, "down")
 
 
-def forward_loss_sum(params, tokens, labels, s: Shape):
+def forward_loss_sum(params, tokens, labels, s: Shape, lora_scale: float = 0.0):
     """Sum of token cross-entropy (labels < 0 ignored) for tokens [b, S]."""
     b, S = tokens.shape
     cos, sin = rope_cos_sin(S, s.head_dim, s.rope_theta)
@@ -143,7 +171,7 @@ def forward_loss_sum(params, tokens, labels, s: Shape):
         return params[name]
     x = params["embed"][tokens]
     for l in range(s.layers):
-        x = decoder_layer(x, p, f"layers.{l}.", s, cos, sin)
+        x = decoder_layer(x, p, f"layers.{l}.", s, cos, sin, lora_scale)
     x = rms(x, p("head.final_norm"), s.eps)
     logits = x @ p("head.lm_head").t()
     return torch.nn.functional.cross_entropy(
@@ -161,15 +189,20 @@ class StepOracle:
     compute on bf16-rounded weights, sync or async (staleness-1) hand-off."""
 
     def __init__(self, s: Shape, params: dict, lr=1e-3, betas=(0.9, 0.95), eps=1e-8,
-                 weight_decay=0.0, mode="sync", threads: int | None = None):
+                 weight_decay=0.0, mode="sync", threads: int | None = None,
+                 lora_scale: float = 0.0):
+        """lora_scale > 0: LoRA fine-tune — only the *_lora_A/B params train
+        (AdamW), every base weight is frozen (PEFT semantics)."""
         assert mode in ("sync", "async")
         if threads:
             torch.set_num_threads(threads)
         self.s = s
         self.mode = mode
+        self.lora_scale = lora_scale
         self.master = {k: v.clone().float().requires_grad_(False) for k, v in params.items()}
         self.opt_params = {k: torch.nn.Parameter(v.clone()) for k, v in self.master.items()}
-        self.opt = torch.optim.AdamW(list(self.opt_params.values()), lr=lr, betas=betas, eps=eps,
+        train = [v for k, v in self.opt_params.items() if not lora_scale or "_lora_" in k]
+        self.opt = torch.optim.AdamW(train, lr=lr, betas=betas, eps=eps,
                                      weight_decay=weight_decay)
         # weights the next iteration computes with (bf16 master copy)
         self.used = {k: bf16_round(v) for k, v in self.master.items()}
@@ -181,7 +214,7 @@ class StepOracle:
         n_valid = int((labels >= 0).sum())
         total = 0.0
         for mb in range(tokens.shape[0]):
-            loss = forward_loss_sum(w, tokens[mb], labels[mb], self.s) / n_valid
+            loss = forward_loss_sum(w, tokens[mb], labels[mb], self.s, self.lora_scale) / n_valid
             loss.backward()
             total += loss.item()
         return total, {k: v.grad if v.grad is not None else torch.zeros_like(v)

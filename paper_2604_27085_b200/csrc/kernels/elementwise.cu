@@ -345,10 +345,11 @@ __global__ void __launch_bounds__(QK_THREADS)
     atomicAdd(&sk[sub * 8 + i], ak[i]);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < HD; i += blockDim.x) {
-    atomicAdd(dqw + i, sq[i]);
-    atomicAdd(dkw + i, sk[i]);
-  }
+  if (dqw && dkw)  // null: frozen norm weights (LoRA)
+    for (int i = threadIdx.x; i < HD; i += blockDim.x) {
+      atomicAdd(dqw + i, sq[i]);
+      atomicAdd(dkw + i, sk[i]);
+    }
 }
 
 // ------------------------------------------------------------------ SwiGLU
@@ -550,6 +551,12 @@ __global__ void bf16_to_f32_kernel(const __nv_bfloat16* __restrict__ a, float* _
     b[i] = bf2f(a[i]);
 }
 
+__global__ void scale_bf16_kernel(__nv_bfloat16* __restrict__ a, long long n, float f) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = f2bf(bf2f(a[i]) * f);
+}
+
 __global__ void add_f32_kernel(float* __restrict__ a, const float* __restrict__ b, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -734,6 +741,12 @@ RP_API int rp_f32_to_bf16(const float* a, void* b, int64_t n, void* stream) {
 RP_API int rp_bf16_to_f32(const void* a, float* b, int64_t n, void* stream) {
   bf16_to_f32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)a,
                                                                           b, n);
+  return status();
+}
+
+RP_API int rp_scale_bf16(void* a, int64_t n, float f, void* stream) {
+  if (n <= 0) return RP_OK;
+  scale_bf16_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)a, n, f);
   return status();
 }
 

@@ -46,7 +46,7 @@ using roundpipe::StageKind;
 
 static int64_t align128(int64_t x) { return (x + 127) / 128 * 128; }
 
-LayerLayout make_layer_layout(const Shape& s) {
+LayerLayout make_layer_layout(const Shape& s, int lora_rank) {
   LayerLayout L;
   int64_t off = 0;
   auto put = [&](Tensor& t, int64_t rows, int64_t cols) {
@@ -63,6 +63,18 @@ LayerLayout make_layer_layout(const Shape& s) {
   put(L.post_norm, s.h, 1);
   put(L.gate_up, 2LL * s.m, s.h);
   put(L.down, s.h, s.m);
+  L.lora_off = off;
+  if (lora_rank > 0) {
+    const int r = lora_rank;
+    put(L.qkv_A, r, s.h);
+    put(L.qkv_B, s.qkvd(), r);
+    put(L.o_A, r, s.qd());
+    put(L.o_B, s.h, r);
+    put(L.gu_A, r, s.h);
+    put(L.gu_B, 2LL * s.m, r);
+    put(L.down_A, r, s.m);
+    put(L.down_B, s.h, r);
+  }
   L.total = off;
   return L;
 }
@@ -276,6 +288,32 @@ struct Runtime {
   void push_resident(int g);        // host master/m/v -> device state
   void pull_resident(int g);        // device state -> host master/m/v (if stale)
   int64_t resident_params = 0;
+  int lora_r = 0;          // LoRA rank (0 = full fine-tune)
+  float lora_scale = 0.f;  // alpha / r
+  bool trainable(int g) const { return host[g].tn() > 0; }
+  // LoRA: Y += s (X A^T) B^T; keeps Us = s X A^T (T x r) for the backward
+  void lora_fwd(cudaStream_t st, const uint16_t* W, const Tensor& Ta, const Tensor& Tb,
+                const uint16_t* X, int64_t ldx, int in, uint16_t* Us, uint16_t* Y, int64_t ldy,
+                int out) {
+    const int r = lora_r;
+    gemm(st, X, ldx, false, W + Ta.off, in, false, Us, r, false, false, T, r, in);
+    RP_K(rp_scale_bf16(Us, (int64_t)T * r, lora_scale, st));
+    gemm(st, Us, r, false, W + Tb.off, r, false, Y, ldy, false, false, T, out, r, Y, ldy);
+    kernels += 1;
+  }
+  // LoRA backward of one linear (base dgrad dX already in place):
+  // dB += dY^T Us, dU = s dY B, dA += dU^T X, dX += dU A
+  void lora_bwd(Gpu& G, cudaStream_t st, const uint16_t* W, float* dW, const Tensor& Ta,
+                const Tensor& Tb, const uint16_t* X, int64_t ldx, int in, const uint16_t* Us,
+                const uint16_t* dY, int64_t ldy, int out, uint16_t* dX, int64_t lddx, bool first) {
+    const int r = lora_r;
+    gemm(st, dY, ldy, true, Us, r, true, dW + Tb.off, r, true, !first, out, r, T);
+    gemm(st, dY, ldy, false, W + Tb.off, r, true, G.du, r, false, false, T, r, out);
+    RP_K(rp_scale_bf16(G.du, (int64_t)T * r, lora_scale, st));
+    gemm(st, G.du, r, true, X, ldx, true, dW + Ta.off, in, true, !first, r, in, T);
+    gemm(st, G.du, r, false, W + Ta.off, in, true, dX, lddx, false, false, T, in, r, dX, lddx);
+    kernels += 1;
+  }
   // before the first grad write of an HBM-resident group g in an iteration:
   // AdamW of the previous iteration has consumed its single grad buffer (edge 4)
   void grad_free(Gpu& G, int g, cudaStream_t q) {
@@ -368,7 +406,11 @@ void Runtime::init(const rp_runtime_config_t& c) {
       if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) RP_CUDA(e);
       cudaGetLastError();
     }
-  LL = make_layer_layout(s);
+  if (cfg.lora_rank < 0 || cfg.lora_rank > 256 || cfg.lora_rank % 8)
+    throw RtError(RP_E_INPUT, "lora_rank must be 0 or a multiple of 8 up to 256");
+  lora_r = cfg.lora_rank;
+  lora_scale = lora_r > 0 ? (cfg.lora_alpha > 0 ? cfg.lora_alpha : (float)lora_r) / lora_r : 0.f;
+  LL = make_layer_layout(s, lora_r);
   HL = make_head_layout(s);
   if (const char* e = getenv("RP_LOGITS_ROWS")) {  // LM-head chunk rows (study knob)
     const int r = atoi(e);
@@ -386,18 +428,23 @@ void Runtime::init(const rp_runtime_config_t& c) {
     throw RtError(RP_E_INPUT, "multi-round iterations need N == 1 (host grad merge not built)");
   parities = N > 1 ? 2 : 1;
 
-  std::size_t bytes = 0;
-  for (int g = 0; g < ngroups(); ++g)
-    bytes += (std::size_t)group_numel(g) * 14 + 4 * HostArena::kAlign;
-  arena.reserve(bytes);
   host.resize(ngroups());
+  std::size_t bytes = 0;
   for (int g = 0; g < ngroups(); ++g) {
     HostGroup& H = host[g];
     H.n = group_numel(g);
+    H.t_off = lora_r == 0 ? 0 : (g >= 1 && g <= s.L ? LL.lora_off : H.n);
+    bytes += (std::size_t)H.n * 2 + (std::size_t)H.tn() * 12 + 4 * HostArena::kAlign;
+  }
+  arena.reserve(bytes);
+  for (int g = 0; g < ngroups(); ++g) {
+    HostGroup& H = host[g];
     H.w16 = static_cast<uint16_t*>(arena.take(H.n * 2));
-    H.master = static_cast<float*>(arena.take(H.n * 4));
-    H.m = static_cast<float*>(arena.take(H.n * 4));
-    H.v = static_cast<float*>(arena.take(H.n * 4));
+    if (H.tn() > 0) {  // shifted: valid for global offsets >= t_off
+      H.master = static_cast<float*>(arena.take(H.tn() * 4)) - H.t_off;
+      H.m = static_cast<float*>(arena.take(H.tn() * 4)) - H.t_off;
+      H.v = static_cast<float*>(arena.take(H.tn() * 4)) - H.t_off;
+    }
   }
   arena.commit();
   grad_owner.assign(ngroups(), 0);
@@ -435,18 +482,19 @@ void Runtime::place_resident_state() {
   std::vector<int> order(ngroups());
   for (int g = 0; g < ngroups(); ++g) order[g] = g;
   std::stable_sort(order.begin(), order.end(),
-                   [&](int a, int b) { return host[a].n > host[b].n; });
+                   [&](int a, int b) { return host[a].tn() > host[b].tn(); });
   // A resident group needs 12 B/param of state but only ONE fp32 grad buffer
   // (its AdamW finishes within milliseconds of GradWrite, long before the next
   // iteration's first write of that group), so converting a group costs a net
   // 8 B/param: free grad[1] on every worker first, then allocate the state.
   for (int g : order) {
-    const int64_t n = host[g].n;
+    const int64_t n = host[g].tn(), o = host[g].t_off;
+    if (n == 0) continue;  // frozen group
     const int64_t freed = n * 4 * (int64_t)gpus.size();
     if (n * 12 > budget + freed) continue;
     for (Gpu& G : gpus) {
       DevGroup& D = G.groups[g];
-      RP_CUDA(cudaFree(D.grad[1]));
+      RP_CUDA(cudaFree(D.grad[1] + o));
       D.grad[1] = D.grad[0];
       G.allocated[1] -= (std::size_t)n * 4;
     }
@@ -456,7 +504,9 @@ void Runtime::place_resident_state() {
       cudaGetLastError();
       for (Gpu& G : gpus) {  // undo: back to two buffers
         DevGroup& D = G.groups[g];
-        RP_CUDA(cudaMalloc(&D.grad[1], (std::size_t)n * 4));
+        float* q = nullptr;
+        RP_CUDA(cudaMalloc(&q, (std::size_t)n * 4));
+        D.grad[1] = q - o;
         G.allocated[1] += (std::size_t)n * 4;
       }
       break;
@@ -473,9 +523,10 @@ void Runtime::push_resident(int g) {
   HostGroup& H = host[g];
   if (!H.d_state) return;
   set_dev(gpus[0]);
-  RP_CUDA(cudaMemcpy(H.d_state, H.master, H.n * 4, cudaMemcpyHostToDevice));
-  RP_CUDA(cudaMemcpy(H.d_state + H.n, H.m, H.n * 4, cudaMemcpyHostToDevice));
-  RP_CUDA(cudaMemcpy(H.d_state + 2 * H.n, H.v, H.n * 4, cudaMemcpyHostToDevice));
+  const int64_t tn = H.tn(), o = H.t_off;
+  RP_CUDA(cudaMemcpy(H.d_state, H.master + o, tn * 4, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(H.d_state + tn, H.m + o, tn * 4, cudaMemcpyHostToDevice));
+  RP_CUDA(cudaMemcpy(H.d_state + 2 * tn, H.v + o, tn * 4, cudaMemcpyHostToDevice));
   H.host_stale = false;
 }
 
@@ -483,9 +534,10 @@ void Runtime::pull_resident(int g) {
   HostGroup& H = host[g];
   if (!H.d_state || !H.host_stale) return;
   set_dev(gpus[0]);
-  RP_CUDA(cudaMemcpy(H.master, H.d_state, H.n * 4, cudaMemcpyDeviceToHost));
-  RP_CUDA(cudaMemcpy(H.m, H.d_state + H.n, H.n * 4, cudaMemcpyDeviceToHost));
-  RP_CUDA(cudaMemcpy(H.v, H.d_state + 2 * H.n, H.n * 4, cudaMemcpyDeviceToHost));
+  const int64_t tn = H.tn(), o = H.t_off;
+  RP_CUDA(cudaMemcpy(H.master + o, H.d_state, tn * 4, cudaMemcpyDeviceToHost));
+  RP_CUDA(cudaMemcpy(H.m + o, H.d_state + tn, tn * 4, cudaMemcpyDeviceToHost));
+  RP_CUDA(cudaMemcpy(H.v + o, H.d_state + 2 * tn, tn * 4, cudaMemcpyDeviceToHost));
   H.host_stale = false;
 }
 
@@ -582,8 +634,9 @@ void Runtime::alloc_worker(Gpu& G, int id) {
       D.ev_upload[b] = new_event(false);
       D.ev_lastuse[b] = new_event(false);
     }
-    D.grad[0] = static_cast<float*>(dalloc(n * 4, 1));
-    D.grad[1] = static_cast<float*>(dalloc(n * 4, 1));
+    const int64_t tn = host[g].tn(), to = host[g].t_off;  // trainable region only
+    D.grad[0] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
+    D.grad[1] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
     D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
     D.ev_gradwrite = new_event(false);
     D.ev_adam[0] = new_event(false);
@@ -618,7 +671,14 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     A.lse = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
     A.ev_free = new_event(false);
     A.ev_chain_free = new_event(false);
+    if (lora_r) {
+      A.u_qkv = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+      A.u_o = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+      A.u_gu = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+      A.u_down = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+    }
   }
+  if (lora_r) G.du = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 4));
   if (pipe) {
     int lo2 = 0, hi2 = 0;
     RP_CUDA(cudaDeviceGetStreamPriorityRange(&lo2, &hi2));
@@ -710,23 +770,34 @@ void Runtime::init_weights() {
   Gpu& G = gpus[0];
   set_dev(G);
   const float std_ = cfg.init_std > 0 ? cfg.init_std : 0.02f;
+  int64_t nmax = 0;
+  for (int g = 0; g < ngroups(); ++g) nmax = std::max(nmax, host[g].n);
+  float* f32 = nullptr;  // fp32 scratch of the largest group
+  RP_CUDA(cudaMalloc(&f32, (std::size_t)nmax * 4));
   for (int g = 0; g < ngroups(); ++g) {
     HostGroup& H = host[g];
     DevGroup& D = G.groups[g];
-    float* f32 = D.grad[0];  // scratch
     RP_K(rp_init_normal(f32, D.w[0], H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_,
                         G.compute));
-    std::vector<std::pair<int64_t, int64_t>> ones;
-    if (g >= 1 && g <= s.L)
+    std::vector<std::pair<int64_t, int64_t>> ones, zeros;
+    if (g >= 1 && g <= s.L) {
       ones = {{LL.in_norm.off, s.h}, {LL.q_norm.off, s.hd}, {LL.k_norm.off, s.hd},
               {LL.post_norm.off, s.h}};
-    else if (g == s.L + 1)
+      if (lora_r)  // LoRA B starts at zero (the adapted model starts as the base)
+        for (const Tensor* t : {&LL.qkv_B, &LL.o_B, &LL.gu_B, &LL.down_B})
+          zeros.emplace_back(t->off, t->numel());
+    } else if (g == s.L + 1) {
       ones = {{HL.final_norm.off, s.h}};
+    }
     for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, D.w[0] + off, n, 1.0f, G.compute));
-    RP_CUDA(cudaMemcpyAsync(H.master, f32, H.n * 4, cudaMemcpyDeviceToHost, G.compute));
+    for (auto [off, n] : zeros) RP_K(rp_fill(f32 + off, D.w[0] + off, n, 0.0f, G.compute));
+    if (H.tn() > 0)
+      RP_CUDA(cudaMemcpyAsync(H.master + H.t_off, f32 + H.t_off, H.tn() * 4,
+                              cudaMemcpyDeviceToHost, G.compute));
     RP_CUDA(cudaMemcpyAsync(H.w16, D.w[0], H.n * 2, cudaMemcpyDeviceToHost, G.compute));
     RP_CUDA(cudaStreamSynchronize(G.compute));
   }
+  RP_CUDA(cudaFree(f32));
 }
 
 // ---- GPU lane: weight upload ----------------------------------------------------------
@@ -797,9 +868,10 @@ void Runtime::p_copy(int g) {
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[0], 0));
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[1], 0));
   cudaEvent_t xa = xfer_begin(O.opt_d2h);
-  RP_CUDA(cudaMemcpyAsync(H.w16, D.pend, H.n * 2, cudaMemcpyDeviceToHost, O.opt_d2h));
+  RP_CUDA(cudaMemcpyAsync(H.w16 + H.t_off, D.pend + H.t_off, H.tn() * 2, cudaMemcpyDeviceToHost,
+                          O.opt_d2h));  // frozen parts never change
   xfer_end(xa, O.opt_d2h, 1, g - 1, H.step, O.id);
-  d2h_bytes += H.n * 2;
+  d2h_bytes += H.tn() * 2;
   RP_CUDA(cudaEventRecord(D.ev_pcopy, O.opt_d2h));
   pcopy_ev[g] = D.ev_pcopy;
   pend_owner[g] = -1;
@@ -820,6 +892,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
   gemm(st, A.h1, h, false, W + LL.qkv.off, h, false, A.qkv, qkvd, false, false, T, qkvd, h);
+  if (lora_r) lora_fwd(st, W, LL.qkv_A, LL.qkv_B, A.h1, h, h, A.u_qkv, A.qkv, qkvd, qkvd);
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_qk_norm_rope_fwd(A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off, W + LL.k_norm.off,
@@ -834,6 +907,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     prof_end(pi_, st, 1, 2.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }
   gemm(st, A.o, qd, false, W + LL.o.off, qd, false, A.x2, h, false, false, T, h, qd, x, h);
+  if (lora_r) lora_fwd(st, W, LL.o_A, LL.o_B, A.o, qd, qd, A.u_o, A.x2, h, h);
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
@@ -841,6 +915,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
   }
   gemm(st, A.h2, h, false, W + LL.gate_up.off, h, false, A.gu, 2 * s.m, false, false, T, 2 * s.m,
        h);
+  if (lora_r) lora_fwd(st, W, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, A.gu, 2 * s.m, 2 * s.m);
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_swiglu_fwd(A.gu, A.act, T, s.m, st));
@@ -848,6 +923,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
   }
   gemm(st, A.act, s.m, false, W + LL.down.off, s.m, false, x_out, h, false, false, T, h, s.m,
        A.x2, h);
+  if (lora_r) lora_fwd(st, W, LL.down_A, LL.down_B, A.act, s.m, s.m, A.u_down, x_out, h, h);
   kernels += 5;
 }
 
@@ -880,16 +956,21 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
     RP_CUDA(cudaEventRecord(e, st));
     RP_CUDA(cudaStreamWaitEvent(ws, e, 0));
   };
+  const bool full = lora_r == 0;  // LoRA: base weights frozen, adapters trained
   if (first) {
     grad_free(G, l + 1, st);
-    for (const Tensor* t : {&LL.in_norm, &LL.q_norm, &LL.k_norm, &LL.post_norm})
-      RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
+    if (full)
+      for (const Tensor* t : {&LL.in_norm, &LL.q_norm, &LL.k_norm, &LL.post_norm})
+        RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
   }
   // MLP:  x3 = x2 + act(gu(h2)) Wd^T
   to_ws();
-  gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
+  if (full) gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
   gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
-  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], ws));
+  if (!full)
+    lora_bwd(G, st, W, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, G.dact, m,
+             first);
+  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], full ? ws : st));
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[p], 0));  // wgrad two layers ago read it
   {
     const int pi_ = prof_begin(st);
@@ -897,21 +978,27 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
     prof_end(pi_, st, 2, 10.0 * T * m);
   }
   to_ws();
-  gemm(ws, dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
-  RP_CUDA(cudaEventRecord(G.ev_dgu_free[p], ws));
+  if (full)
+    gemm(ws, dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
+  RP_CUDA(cudaEventRecord(G.ev_dgu_free[p], full ? ws : st));
   gemm(st, dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
+  if (!full)
+    lora_bwd(G, st, W, dW, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, dgu, 2 * m, 2 * m, G.dh, h,
+             first);
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xb], 0));
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_rmsnorm_bwd(G.dh, A.x2, W + LL.post_norm.off, A.rstd2, G.dx32[0], G.dx32[1], dx_b,
-                        dW + LL.post_norm.off, T, h, st));
+                        full ? dW + LL.post_norm.off : nullptr, T, h, st));
     prof_end(pi_, st, 2, 14.0 * T * h);
   }
   // attention:  x2 = x + attn(qkv(h1)) Wo^T
   to_ws();
-  gemm(ws, dx_b, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
-  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xb], ws));
+  if (full) gemm(ws, dx_b, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
   gemm(st, dx_b, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
+  if (!full)
+    lora_bwd(G, st, W, dW, LL.o_A, LL.o_B, A.o, qd, qd, A.u_o, dx_b, h, h, G.dattn, qd, first);
+  RP_CUDA(cudaEventRecord(G.ev_dx16_free[xb], full ? ws : st));
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dqkv_free[p], 0));
   {
     const int pi_ = prof_begin(st);
@@ -924,20 +1011,25 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
     const int pi_ = prof_begin(st);
     RP_K(rp_qk_norm_rope_bwd(G.dq_t, G.dk_t, A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off,
                              W + LL.k_norm.off, A.rstd_q, A.rstd_k, G.cos_sin, cfg.seq_len, dqkv,
-                             qkvd, dW + LL.q_norm.off, dW + LL.k_norm.off, T, st));
+                             qkvd, full ? dW + LL.q_norm.off : nullptr,
+                             full ? dW + LL.k_norm.off : nullptr, T, st));
     prof_end(pi_, st, 2, 8.0 * T * (s.nq + s.nk) * s.hd);
   }
   to_ws();
-  gemm(ws, dqkv, qkvd, true, A.h1, h, true, dW + LL.qkv.off, h, true, !first, qkvd, h, T);
+  if (full)
+    gemm(ws, dqkv, qkvd, true, A.h1, h, true, dW + LL.qkv.off, h, true, !first, qkvd, h, T);
   RP_CUDA(cudaEventRecord(G.ev_dqkv_free[p], ws));
   RP_CUDA(cudaEventRecord(A.ev_free, ws));  // act / h2 / o / h1 no longer needed
   RP_CUDA(cudaEventRecord(G.ev_wgrad, ws));
   gemm(st, dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
+  if (!full)
+    lora_bwd(G, st, W, dW, LL.qkv_A, LL.qkv_B, A.h1, h, h, A.u_qkv, dqkv, qkvd, qkvd, G.dh, h,
+             first);
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xa], 0));  // wgrad(down) read dx_a
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_rmsnorm_bwd(G.dh, A.xin, W + LL.in_norm.off, A.rstd1, G.dx32[1], G.dx32[0], dx_a,
-                        dW + LL.in_norm.off, T, h, st));
+                        full ? dW + LL.in_norm.off : nullptr, T, h, st));
     prof_end(pi_, st, 2, 14.0 * T * h);
   }
   RP_CUDA(cudaEventRecord(A.ev_chain_free, st));
@@ -959,7 +1051,8 @@ void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float
   const bool piped = on && on != G.compute;
   uint16_t* dh = piped ? G.hdh : G.dh;
   const int h = s.h, V = s.V;
-  if (first) {
+  const bool train = trainable(s.L + 1);  // LoRA: the head is frozen
+  if (first && train) {
     grad_free(G, s.L + 1, st);
     RP_CUDA(cudaMemsetAsync(dW + HL.final_norm.off, 0, (size_t)h * 4, st));
   }
@@ -977,18 +1070,19 @@ void Runtime::head_fwd_bwd(Gpu& G, const uint16_t* x, int gmb, bool first, float
   }
     gemm(st, G.logits, V, false, W + HL.lm_head.off, h, true, dh + (int64_t)r0 * h, h, false,
          false, nr, h, V);
-    gemm(st, G.logits, V, true, G.hN + (int64_t)r0 * h, h, true, dW + HL.lm_head.off, h, true,
-         !(first && r0 == 0), V, h, nr);
+    if (train)
+      gemm(st, G.logits, V, true, G.hN + (int64_t)r0 * h, h, true, dW + HL.lm_head.off, h, true,
+           !(first && r0 == 0), V, h, nr);
     kernels += 1;
   }
   if (piped) {
     RP_CUDA(cudaStreamWaitEvent(st, G.ev_hdx_free, 0));  // previous hand-over consumed
     RP_K(rp_rmsnorm_bwd(dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.hdx32, G.hdx16,
-                        dW + HL.final_norm.off, T, h, st));
+                        train ? dW + HL.final_norm.off : nullptr, T, h, st));
   } else {
     RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[G.dx16 == G.dx16s[0] ? 0 : 1], 0));
     RP_K(rp_rmsnorm_bwd(dh, x, W + HL.final_norm.off, G.rstdN, nullptr, G.dx32[0], G.dx16,
-                        dW + HL.final_norm.off, T, h, st));
+                        train ? dW + HL.final_norm.off : nullptr, T, h, st));
   }
   kernels += 2;
 }
@@ -1016,9 +1110,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
   // groups whose grads this slot produces
   std::vector<int> grad_groups;
   if (has_grads) {
-    for (int l = a; l <= std::min(b, s.L - 1); ++l) grad_groups.push_back(l + 1);
-    if (b == s.L) grad_groups.push_back(s.L + 1);
-    if (a == 0) grad_groups.push_back(0);
+    for (int l = a; l <= std::min(b, s.L - 1); ++l)
+      if (trainable(l + 1)) grad_groups.push_back(l + 1);
+    if (b == s.L && trainable(s.L + 1)) grad_groups.push_back(s.L + 1);
+    if (a == 0 && trainable(0)) grad_groups.push_back(0);
     // grad[t%2] may be overwritten once AdamW consumed it (edge 4, parity form)
     // HBM-resident groups keep ONE grad buffer: they wait last iteration's
     // AdamW right before their first grad write instead (grad_free), so the
@@ -1086,13 +1181,15 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         prof_unit(i, 1);
         layer_bwd(G, i, acts[i], first);
       }
-      float* dE = G.groups[0].grad[it & 1];  // embedding gradient (scatter-add of dL/dx_0)
-      if (first) {
+      if (trainable(0)) {  // embedding gradient (scatter-add of dL/dx_0)
+        float* dE = G.groups[0].grad[it & 1];
+        if (first) {
           grad_free(G, 0, st);
           RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
         }
-      RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
-      ++kernels;
+        RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
+        ++kernels;
+      }
       if (want_tl) {
         RP_CUDA(cudaEventRecord(rec.end, st));
         records.push_back(rec);
@@ -1198,13 +1295,15 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     }
     if (has_grads) {
       if (a == 0) {  // embedding gradient (scatter-add of dL/dx_0)
-        float* dE = G.groups[0].grad[it & 1];
-        if (first) {
-          grad_free(G, 0, st);
-          RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+        if (trainable(0)) {
+          float* dE = G.groups[0].grad[it & 1];
+          if (first) {
+            grad_free(G, 0, st);
+            RP_CUDA(cudaMemsetAsync(dE, 0, (size_t)s.V * s.h * 4, st));
+          }
+          RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
+          ++kernels;
         }
-        RP_K(rp_embed_bwd(ids, G.dx32[0], dE, T, s.h, st));
-        ++kernels;
       } else {  // hand dL/dx_a to the next (backward) slot
         Slotbuf& nb = next->hand_grad[hb];
         cudaEvent_t gr = new_event(false);
@@ -1344,9 +1443,10 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     RP_CUDA(cudaStreamWaitEvent(q, D.ev_pcopy, 0));      // pend free again
     cudaEvent_t xa = xfer_begin(q);
     const int pi_ = prof_begin(q);
-    RP_K(rp_adamw(H.d_state, H.d_state + H.n, H.d_state + 2 * H.n, D.grad[parity], D.pend, H.n,
-                  &cfg.adam, step_no, q));
-    prof_end(pi_, q, 3, 30.0 * H.n);
+    const int64_t tn = H.tn(), to = H.t_off;
+    RP_K(rp_adamw(H.d_state, H.d_state + tn, H.d_state + 2 * tn, D.grad[parity] + to,
+                  D.pend + to, tn, &cfg.adam, step_no, q));
+    prof_end(pi_, q, 3, 30.0 * tn);
     ++kernels;
     RP_CUDA(cudaEventRecord(D.ev_adam[parity], q));
     xfer_end(xa, q, 2, g - 1, last_iter, G.id);
@@ -1357,7 +1457,7 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   }
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
   cudaEvent_t xa = xfer_begin(G.opt_h2d);
-  for (int64_t off = 0; off < H.n; off += chunk_elems) {
+  for (int64_t off = H.t_off; off < H.n; off += chunk_elems) {  // trainable region
     const int64_t n = std::min<int64_t>(chunk_elems, H.n - off);
     const int sl = G.opt_slot;
     G.opt_slot ^= 1;
@@ -1401,6 +1501,7 @@ void Runtime::step() {
   for (int l = s.L; l >= 0; --l) {
     std::vector<int> gs = l == 0 ? std::vector<int>{1, 0} : std::vector<int>{l + 1};
     for (int g : gs) {
+      if (!trainable(g)) continue;  // frozen (LoRA base): no grads, no optimizer
       Gpu& G = gpus[grad_owner[g]];
       set_dev(G);
       adam_group(G, g, parity);
@@ -1561,6 +1662,10 @@ RP_API int rp_param_layout(rp_runtime_t* p, int32_t group, int64_t* offs, int64_
     else {
       const auto& L = rt->LL;
       ts = {L.in_norm, L.qkv, L.q_norm, L.k_norm, L.o, L.post_norm, L.gate_up, L.down};
+      if (rt->lora_r)  // adapters after the base tensors
+        for (const auto* t : {&L.qkv_A, &L.qkv_B, &L.o_A, &L.o_B, &L.gu_A, &L.gu_B, &L.down_A,
+                              &L.down_B})
+          ts.push_back(*t);
     }
     *n = (int32_t)ts.size();
     if (*n > cap) throw RtError(RP_E_TOOSMALL, "layout capacity");
@@ -1579,9 +1684,9 @@ RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, in
     rp::rt::HostGroup& H = rt->host[g];
     if (n != H.n || !values) throw RtError(RP_E_INPUT, "size mismatch");
     rt->sync_all();
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = 0; i < n; ++i) H.w16[i] = f32_to_bf16_host(values[i]);
+    for (int64_t i = H.t_off; i < n; ++i) {  // trainable region (all of it unless LoRA)
       H.master[i] = values[i];
-      H.w16[i] = f32_to_bf16_host(values[i]);
       H.m[i] = 0.f;
       H.v[i] = 0.f;
     }
@@ -1600,21 +1705,32 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
     if (n != H.n || !out) throw RtError(RP_E_INPUT, "size mismatch");
     rt->sync_all();
     rt->pull_resident(g);
+    // frozen parts (LoRA base): master = the bf16 weights, grads / m / v = 0
+    const int64_t o = H.t_off;
     switch (which) {
-      case 0: std::memcpy(out, H.master, n * 4); break;
+      case 0:
+        for (int64_t i = 0; i < o; ++i) out[i] = bf16_to_f32_host(H.w16[i]);
+        if (n > o) std::memcpy(out + o, H.master + o, (n - o) * 4);
+        break;
       case 1:
         for (int64_t i = 0; i < n; ++i) out[i] = bf16_to_f32_host(H.w16[i]);
         break;
       case 2: {
         if (rt->last_iter < 0) throw RtError(RP_E_INPUT, "no iteration has run");
-        rp::rt::Gpu& G = rt->gpus[rt->grad_owner[g]];
-        rt->set_dev(G);
-        RP_CUDA(cudaMemcpy(out, G.groups[g].grad[rt->last_iter & 1], n * 4,
-                           cudaMemcpyDeviceToHost));
+        std::memset(out, 0, o * 4);
+        if (n > o) {
+          rp::rt::Gpu& G = rt->gpus[rt->grad_owner[g]];
+          rt->set_dev(G);
+          RP_CUDA(cudaMemcpy(out + o, G.groups[g].grad[rt->last_iter & 1] + o, (n - o) * 4,
+                             cudaMemcpyDeviceToHost));
+        }
         break;
       }
-      case 3: std::memcpy(out, H.m, n * 4); break;
-      case 4: std::memcpy(out, H.v, n * 4); break;
+      case 3:
+      case 4:
+        std::memset(out, 0, o * 4);
+        if (n > o) std::memcpy(out + o, (which == 3 ? H.m : H.v) + o, (n - o) * 4);
+        break;
       default: throw RtError(RP_E_INPUT, "bad selector");
     }
   });
@@ -1628,7 +1744,7 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
 // the OLD bf16 master) is saved as pending; the pending bf16 weights are
 // bf16(fp32 master) by construction (adamw_kernel), so resume re-creates them.
 namespace {
-constexpr char kCkptMagic[8] = {'R', 'P', 'C', 'K', 'P', 'T', '0', '1'};
+constexpr char kCkptMagic[8] = {'R', 'P', 'C', 'K', 'P', 'T', '0', '2'};
 struct FileCloser {
   void operator()(FILE* f) const { if (f) std::fclose(f); }
 };
@@ -1654,16 +1770,19 @@ RP_API int rp_runtime_save(rp_runtime_t* p, const char* path) {
     xwrite(f.get(), kCkptMagic, 8);
     xwrite(f.get(), hdr, sizeof(hdr));
     for (int g = 0; g < ng; ++g) {
-      const int64_t n = rt->host[g].n;
+      const int64_t n = rt->host[g].n, to = rt->host[g].t_off;
       const int32_t st[2] = {rt->host[g].step, rt->pend_owner[g] >= 0 ? 1 : 0};
       xwrite(f.get(), &n, 8);
+      xwrite(f.get(), &to, 8);
       xwrite(f.get(), st, 8);
     }
-    for (int g = 0; g < ng; ++g) {
+    for (int g = 0; g < ng; ++g) {  // fp32 state of the trainable region, bf16 of all
       const auto& H = rt->host[g];
-      xwrite(f.get(), H.master, H.n * 4);
-      xwrite(f.get(), H.m, H.n * 4);
-      xwrite(f.get(), H.v, H.n * 4);
+      if (H.tn() > 0) {
+        xwrite(f.get(), H.master + H.t_off, H.tn() * 4);
+        xwrite(f.get(), H.m + H.t_off, H.tn() * 4);
+        xwrite(f.get(), H.v + H.t_off, H.tn() * 4);
+      }
       xwrite(f.get(), H.w16, H.n * 2);
     }
   });
@@ -1687,11 +1806,13 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
       throw RtError(RP_E_INPUT, "checkpoint does not match this model");
     std::vector<int32_t> steps(ng), pending(ng);
     for (int g = 0; g < ng; ++g) {
-      int64_t n;
+      int64_t n, to;
       int32_t st[2];
       xread(f.get(), &n, 8);
+      xread(f.get(), &to, 8);
       xread(f.get(), st, 8);
-      if (n != rt->host[g].n) throw RtError(RP_E_INPUT, "checkpoint group size mismatch");
+      if (n != rt->host[g].n || to != rt->host[g].t_off)
+        throw RtError(RP_E_INPUT, "checkpoint group size / trainable region mismatch");
       steps[g] = st[0];
       pending[g] = st[1];
     }
@@ -1700,9 +1821,11 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
         if (pending[g]) throw RtError(RP_E_INPUT, "async checkpoint loaded into a sync runtime");
     for (int g = 0; g < ng; ++g) {
       auto& H = rt->host[g];
-      xread(f.get(), H.master, H.n * 4);
-      xread(f.get(), H.m, H.n * 4);
-      xread(f.get(), H.v, H.n * 4);
+      if (H.tn() > 0) {
+        xread(f.get(), H.master + H.t_off, H.tn() * 4);
+        xread(f.get(), H.m + H.t_off, H.tn() * 4);
+        xread(f.get(), H.v + H.t_off, H.tn() * 4);
+      }
       xread(f.get(), H.w16, H.n * 2);
       H.step = steps[g];
       H.host_stale = false;
@@ -1718,9 +1841,11 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
       auto& H = rt->host[g];
       rp::rt::Gpu& G = rt->gpus[0];
       rt->set_dev(G);
-      tmp.resize((std::size_t)H.n);
-      for (int64_t i = 0; i < H.n; ++i) tmp[(std::size_t)i] = f32_to_bf16_host(H.master[i]);
-      RP_CUDA(cudaMemcpy(G.groups[g].pend, tmp.data(), H.n * 2, cudaMemcpyHostToDevice));
+      tmp.resize((std::size_t)H.tn());
+      for (int64_t i = H.t_off; i < H.n; ++i)
+        tmp[(std::size_t)(i - H.t_off)] = f32_to_bf16_host(H.master[i]);
+      RP_CUDA(cudaMemcpy(G.groups[g].pend + H.t_off, tmp.data(), H.tn() * 2,
+                         cudaMemcpyHostToDevice));
       rt->pend_owner[g] = 0;
     }
     rt->grads_pending = false;

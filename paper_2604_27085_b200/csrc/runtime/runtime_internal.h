@@ -52,19 +52,28 @@ struct Tensor {
 };
 struct LayerLayout {
   Tensor in_norm, qkv, q_norm, k_norm, o, post_norm, gate_up, down;
+  // LoRA adapters (rank r > 0), after the base tensors: A [r x in], B [out x r]
+  Tensor qkv_A, qkv_B, o_A, o_B, gu_A, gu_B, down_A, down_B;
+  int64_t lora_off = 0;  // start of the adapters (= total without LoRA)
   int64_t total = 0;
 };
 struct HeadLayout {
   Tensor final_norm, lm_head;
   int64_t total = 0;
 };
-LayerLayout make_layer_layout(const Shape& s);
+LayerLayout make_layer_layout(const Shape& s, int lora_rank = 0);
 HeadLayout make_head_layout(const Shape& s);
 
 // Pinned host state of one parameter group: fp32 optimizer copy (master,
 // m, v) and the bf16 master copy the GPUs upload.
 struct HostGroup {
   int64_t n = 0;
+  // trainable region [t_off, n): 0 for full fine-tune; the adapters' offset in
+  // LoRA mode; n for a frozen group. master/m/v (and device grads / resident
+  // state) exist only for it — the pointers are shifted so that global
+  // offsets index them (valid for offsets >= t_off).
+  int64_t t_off = 0;
+  int64_t tn() const { return n - t_off; }
   uint16_t* w16 = nullptr;
   float* master = nullptr;
   float* m = nullptr;
@@ -96,6 +105,7 @@ struct DevGroup {
 struct LayerActs {
   uint16_t *x, *h1, *qkv, *q, *k, *o, *x2, *h2, *gu, *act;
   float *rstd1, *rstd_q, *rstd_k, *lse, *rstd2;
+  uint16_t *u_qkv = nullptr, *u_o = nullptr, *u_gu = nullptr, *u_down = nullptr;  // LoRA: s X A^T
   const uint16_t* xin = nullptr;  // the input actually used by layer_fwd
   cudaEvent_t ev_free = nullptr;        // weight-gradient GEMMs done reading act/h2/o/h1
   cudaEvent_t ev_chain_free = nullptr;  // the dgrad chain done with this layer's activations
@@ -145,6 +155,7 @@ struct Gpu {
   float* dx32[2] = {nullptr, nullptr};
   uint16_t *dx16 = nullptr, *dh = nullptr, *dact = nullptr, *dgu = nullptr, *dattn = nullptr;
   uint16_t *dqkv = nullptr, *dq_t = nullptr, *dk_t = nullptr;
+  uint16_t* du = nullptr;  // LoRA: s dY B of the linear being back-propagated (T x r)
   float *dq_acc = nullptr, *delta = nullptr;
   uint16_t* xbuf[2] = {nullptr, nullptr};
   uint16_t *hN = nullptr, *logits = nullptr;

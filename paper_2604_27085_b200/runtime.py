@@ -32,7 +32,7 @@ class RuntimeConfigC(C.Structure):
                 ("micro_batches", I32), ("round_micro_batches", I32), ("num_gpus", I32),
                 ("async_optimizer", I32), ("mem_limit_bytes", I64), ("residency_factor", F64),
                 ("costs", VP), ("n_costs", I32), ("adam", AdamC), ("init_seed", C.c_uint64),
-                ("init_std", F32), ("flags", I32)]
+                ("init_std", F32), ("flags", I32), ("lora_rank", I32), ("lora_alpha", F32)]
 
 
 class StatsC(C.Structure):
@@ -43,6 +43,8 @@ class StatsC(C.Structure):
 
 
 LAYER_TENSORS = ["input_norm", "qkv", "q_norm", "k_norm", "o", "post_norm", "gate_up", "down"]
+LORA_TENSORS = ["qkv_lora_A", "qkv_lora_B", "o_lora_A", "o_lora_B", "gate_up_lora_A",
+                "gate_up_lora_B", "down_lora_A", "down_lora_B"]
 HEAD_TENSORS = ["final_norm", "lm_head"]
 
 
@@ -61,7 +63,8 @@ class RoundPipe:
     def __init__(self, model="qwen3-8b", seq_len=4096, micro_batch=1, micro_batches=16,
                  num_gpus=1, round_micro_batches=0, async_optimizer=True, adam=AdamW(),
                  costs=None, mem_limit_bytes=0, residency_factor=2.0, init_seed=0,
-                 init_std=0.02, skip_init=False, record_timeline=False):
+                 init_std=0.02, skip_init=False, record_timeline=False, lora_rank=0,
+                 lora_alpha=0.0):
         self.lib = _native.load()
         self._costs = None
         if costs is not None:
@@ -74,7 +77,9 @@ class RoundPipe:
             len(self._costs) if self._costs is not None else 0,
             AdamC(adam.lr, adam.betas[0], adam.betas[1], adam.eps, adam.weight_decay, 1.0),
             init_seed, init_std,
-            (RP_RT_SKIP_INIT if skip_init else 0) | (RP_RT_RECORD_TIMELINE if record_timeline else 0))
+            (RP_RT_SKIP_INIT if skip_init else 0) | (RP_RT_RECORD_TIMELINE if record_timeline else 0),
+            lora_rank, lora_alpha)
+        self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.h = VP()
         self._call("rp_runtime_create", C.byref(cfg), C.byref(self.h))
         self.seq_len, self.micro_batch, self.micro_batches = seq_len, micro_batch, micro_batches
@@ -176,7 +181,7 @@ class RoundPipe:
             self.set_group(group, flat)
         pack(-1, ["embed"])
         for l in range(num_layers):
-            pack(l, [f"layers.{l}.{n}" for n in LAYER_TENSORS])
+            pack(l, [f"layers.{l}.{n}" for n in self.layer_tensors])
         pack(num_layers, [f"head.{n}" for n in HEAD_TENSORS])
 
     def read_state(self, num_layers: int, which: int = 0) -> dict:
@@ -188,7 +193,7 @@ class RoundPipe:
                 out[name] = flat[off:off + r * c].reshape((r, c) if c > 1 else (r,))
         unpack(-1, ["embed"])
         for l in range(num_layers):
-            unpack(l, [f"layers.{l}.{n}" for n in LAYER_TENSORS])
+            unpack(l, [f"layers.{l}.{n}" for n in self.layer_tensors])
         unpack(num_layers, [f"head.{n}" for n in HEAD_TENSORS])
         return out
 
