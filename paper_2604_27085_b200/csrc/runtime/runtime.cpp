@@ -287,6 +287,7 @@ struct Runtime {
   void place_resident_state();      // choose groups whose fp32 state lives in HBM
   void push_resident(int g);        // host master/m/v -> device state
   void pull_resident(int g);        // device state -> host master/m/v (if stale)
+  void pull_w16(int g);             // direct groups: device bf16 of the next iteration -> host
   int64_t resident_params = 0;
   int lora_r = 0;          // LoRA rank (0 = full fine-tune)
   float lora_scale = 0.f;  // alpha / r
@@ -490,25 +491,34 @@ void Runtime::place_resident_state() {
   for (int g : order) {
     const int64_t n = host[g].tn(), o = host[g].t_off;
     if (n == 0) continue;  // frozen group
-    const int64_t freed = n * 4 * (int64_t)gpus.size();
+    const bool direct = N == 1;  // publish straight into the device weights
+    const int64_t freed = n * 4 * (int64_t)gpus.size() + (direct ? host[g].n * 2 : 0);
     if (n * 12 > budget + freed) continue;
     for (Gpu& G : gpus) {
       DevGroup& D = G.groups[g];
       RP_CUDA(cudaFree(D.grad[1] + o));
       D.grad[1] = D.grad[0];
       G.allocated[1] -= (std::size_t)n * 4;
+      if (direct) {
+        RP_CUDA(cudaFree(D.pend));
+        D.pend = nullptr;
+        G.allocated[2] -= (std::size_t)host[g].n * 2;
+      }
     }
+    host[g].direct = direct;
     budget += freed;
     void* p = nullptr;
     if (cudaMalloc(&p, (std::size_t)(n * 12)) != cudaSuccess) {
       cudaGetLastError();
-      for (Gpu& G : gpus) {  // undo: back to two buffers
+      for (Gpu& G : gpus) {  // undo: back to two buffers (and a pend buffer)
         DevGroup& D = G.groups[g];
         float* q = nullptr;
         RP_CUDA(cudaMalloc(&q, (std::size_t)n * 4));
         D.grad[1] = q - o;
         G.allocated[1] += (std::size_t)n * 4;
+        if (!D.pend) RP_CUDA(cudaMalloc(&D.pend, (std::size_t)host[g].n * 2));
       }
+      host[g].direct = false;
       break;
     }
     host[g].d_state = static_cast<float*>(p);
@@ -528,6 +538,20 @@ void Runtime::push_resident(int g) {
   RP_CUDA(cudaMemcpy(H.d_state + tn, H.m + o, tn * 4, cudaMemcpyHostToDevice));
   RP_CUDA(cudaMemcpy(H.d_state + 2 * tn, H.v + o, tn * 4, cudaMemcpyHostToDevice));
   H.host_stale = false;
+}
+
+void Runtime::pull_w16(int g) {
+  HostGroup& H = host[g];
+  if (!H.direct || !H.w16_stale) return;
+  DevGroup& D = gpus[0].groups[g];
+  for (int b = 0; b < 2; ++b)
+    if (D.loaded[b] == iter) {  // the version the next iteration computes with
+      set_dev(gpus[0]);
+      RP_CUDA(cudaMemcpy(H.w16 + H.t_off, D.w[b] + H.t_off, H.tn() * 2, cudaMemcpyDeviceToHost));
+      H.w16_stale = false;
+      return;
+    }
+  throw RtError(RP_E_INTERNAL, "direct group: next iteration's weights not on the device");
 }
 
 void Runtime::pull_resident(int g) {
@@ -811,6 +835,16 @@ void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
   DevGroup& D = G.groups[g];
   HostGroup& H = host[g];
   const int b = it & 1;
+  if (D.loaded[b] != it && H.direct && H.w16_stale) {
+    // direct group without a new update for `it` (no step() in between): the
+    // latest version lives in the other device buffer
+    set_dev(G);
+    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse[b], 0));
+    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_upload[b ^ 1], 0));
+    RP_CUDA(cudaMemcpyAsync(D.w[b], D.w[b ^ 1], H.n * 2, cudaMemcpyDeviceToDevice, G.w_h2d));
+    RP_CUDA(cudaEventRecord(D.ev_upload[b], G.w_h2d));
+    D.loaded[b] = it;
+  }
   if (D.loaded[b] != it) {
     set_dev(G);
     if (pcopy_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.w_h2d, pcopy_ev[g], 0));  // edge (2)
@@ -1444,13 +1478,32 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     cudaEvent_t xa = xfer_begin(q);
     const int pi_ = prof_begin(q);
     const int64_t tn = H.tn(), to = H.t_off;
-    RP_K(rp_adamw(H.d_state, H.d_state + tn, H.d_state + 2 * tn, D.grad[parity] + to,
-                  D.pend + to, tn, &cfg.adam, step_no, q));
+    // direct: the result is version last+2 (async, staleness 1) or last+1
+    // (sync); it overwrites the device buffer of version last (resp. last-1)
+    // once that version's last compute read is done
+    const int ver = last_iter + (cfg.async_optimizer ? 2 : 1), b = ver & 1;
+    uint16_t* out = D.pend;
+    if (H.direct) {
+      RP_CUDA(cudaStreamWaitEvent(q, D.ev_lastuse[b], 0));  // WAR on w[b]
+      // a copy-in of w[b] still in flight (e.g. the version resumed from a checkpoint)
+      RP_CUDA(cudaStreamWaitEvent(q, D.ev_upload[b], 0));
+      out = D.w[b];
+      if (to > 0 && D.loaded[b] < 0)  // frozen part (LoRA base) never written to w[b] yet
+        RP_CUDA(cudaMemcpyAsync(D.w[b], H.w16, to * 2, cudaMemcpyHostToDevice, q));
+    }
+    RP_K(rp_adamw(H.d_state, H.d_state + tn, H.d_state + 2 * tn, D.grad[parity] + to, out + to,
+                  tn, &cfg.adam, step_no, q));
     prof_end(pi_, q, 3, 30.0 * tn);
     ++kernels;
     RP_CUDA(cudaEventRecord(D.ev_adam[parity], q));
     xfer_end(xa, q, 2, g - 1, last_iter, G.id);
     H.host_stale = true;
+    if (H.direct) {  // published in place: no p_copy, no upload
+      RP_CUDA(cudaEventRecord(D.ev_upload[b], q));
+      D.loaded[b] = ver;
+      H.w16_stale = true;
+      return;
+    }
     pend_owner[g] = G.id;
     if (!cfg.async_optimizer) p_copy(g);
     return;
@@ -1692,6 +1745,7 @@ RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, in
     }
     H.step = 0;
     H.host_stale = false;
+    H.w16_stale = false;
     rt->push_resident(g);
     for (auto& G : rt->gpus) G.groups[g].loaded[0] = G.groups[g].loaded[1] = -1;
   });
@@ -1705,6 +1759,7 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
     if (n != H.n || !out) throw RtError(RP_E_INPUT, "size mismatch");
     rt->sync_all();
     rt->pull_resident(g);
+    rt->pull_w16(g);
     // frozen parts (LoRA base): master = the bf16 weights, grads / m / v = 0
     const int64_t o = H.t_off;
     switch (which) {
@@ -1761,7 +1816,10 @@ RP_API int rp_runtime_save(rp_runtime_t* p, const char* path) {
     Runtime* rt = R(p);
     if (!path) throw RtError(RP_E_INPUT, "null path");
     rt->sync_all();
-    for (int g = 0; g < rt->ngroups(); ++g) rt->pull_resident(g);
+    for (int g = 0; g < rt->ngroups(); ++g) {
+      rt->pull_resident(g);
+      rt->pull_w16(g);
+    }
     std::unique_ptr<FILE, FileCloser> f(std::fopen(path, "wb"));
     if (!f) throw RtError(RP_E_INPUT, std::string("cannot open ") + path);
     const int ng = rt->ngroups();
@@ -1771,7 +1829,12 @@ RP_API int rp_runtime_save(rp_runtime_t* p, const char* path) {
     xwrite(f.get(), hdr, sizeof(hdr));
     for (int g = 0; g < ng; ++g) {
       const int64_t n = rt->host[g].n, to = rt->host[g].t_off;
-      const int32_t st[2] = {rt->host[g].step, rt->pend_owner[g] >= 0 ? 1 : 0};
+      // pending staleness-1 update: in pend (streamed) or, for a direct group,
+      // already in the device buffer of the iteration after next
+      const auto& D0 = rt->gpus[0].groups[g];
+      const bool direct_pending = rt->host[g].direct && rt->cfg.async_optimizer &&
+                                  D0.loaded[(rt->iter + 1) & 1] == rt->iter + 1;
+      const int32_t st[2] = {rt->host[g].step, (rt->pend_owner[g] >= 0 || direct_pending) ? 1 : 0};
       xwrite(f.get(), &n, 8);
       xwrite(f.get(), &to, 8);
       xwrite(f.get(), st, 8);
@@ -1837,13 +1900,22 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
     std::vector<uint16_t> tmp;
     for (int g = 0; g < ng; ++g) {
       rt->pend_owner[g] = -1;
-      if (!pending[g]) continue;
       auto& H = rt->host[g];
+      H.w16_stale = false;
+      if (!pending[g]) continue;
       rp::rt::Gpu& G = rt->gpus[0];
       rt->set_dev(G);
       tmp.resize((std::size_t)H.tn());
       for (int64_t i = H.t_off; i < H.n; ++i)
         tmp[(std::size_t)(i - H.t_off)] = f32_to_bf16_host(H.master[i]);
+      if (H.direct) {  // version iter+1: frozen part from the host copy, update on top
+        auto& D = G.groups[g];
+        const int b = (rt->iter + 1) & 1;
+        RP_CUDA(cudaMemcpy(D.w[b], H.w16, H.n * 2, cudaMemcpyHostToDevice));
+        RP_CUDA(cudaMemcpy(D.w[b] + H.t_off, tmp.data(), H.tn() * 2, cudaMemcpyHostToDevice));
+        D.loaded[b] = rt->iter + 1;
+        continue;
+      }
       RP_CUDA(cudaMemcpy(G.groups[g].pend + H.t_off, tmp.data(), H.tn() * 2,
                          cudaMemcpyHostToDevice));
       rt->pend_owner[g] = 0;

@@ -84,6 +84,12 @@ struct HostGroup {
   // copy is refreshed on demand (read_state / save) and re-uploaded on writes
   float* d_state = nullptr;  // [master | m | v], 3n fp32, or null (streamed)
   bool host_stale = false;   // host master/m/v older than d_state
+  // single worker (N = 1): a resident group's AdamW writes its bf16 output
+  // straight into the device weight buffer of the iteration that will use it
+  // (no pend buffer, no p_copy / upload round trip over PCIe); the host bf16
+  // master is then refreshed on demand
+  bool direct = false;
+  bool w16_stale = false;
 };
 
 // Device-side state of one parameter group on one worker.
