@@ -26,6 +26,18 @@ typedef struct {
   const void* R; int64_t ldr;
 } rp_gemm_args_t;
 int rp_gemm_bf16(const rp_gemm_args_t* args, void* stream);
+/* Down-projection dgrad fused with the SwiGLU backward: acc = A . B^T is
+ * dact [M,N] (A [M,K] K-major, B [K,N] MN-major); R = gu = [g | u] [M,2N]
+ * (pitch ldr), D = dgu = [dg | du] [M,2N] bf16 (pitch ldd); dact is never
+ * stored. Equals rp_gemm_bf16 into a bf16 dact followed by rp_swiglu_bwd.
+ * N % 8 == 0, out_f32 = accumulate = 0. */
+int rp_gemm_swiglu_bwd(const rp_gemm_args_t* args, void* stream);
+/* Gate/up projection fused with the SwiGLU forward: B = W_gu [2N, K]
+ * (K-major, gate rows then up rows), A [M, K] K-major; D = gu = [g | u]
+ * [M, 2N] bf16 (kept for the backward) and act = silu(g) * u [M, N] bf16
+ * (pitch ld_act). args->N is N (half of W_gu's rows); R unused. Equals
+ * rp_gemm_bf16 into gu followed by rp_swiglu_fwd. N % 8 == 0. */
+int rp_gemm_swiglu_fwd(const rp_gemm_args_t* args, void* act, int64_t ld_act, void* stream);
 
 /* AdamW hyper-parameters (decoupled weight decay), fp32. */
 typedef struct {

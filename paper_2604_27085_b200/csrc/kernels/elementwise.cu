@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "kernels/swiglu.cuh"
 #include "rp/kernels.h"
 
 namespace rp {
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(256) swiglu_fwd_kernel(const __nv_bfloat16* __
     load8(g_row + c, g);
     load8(g_row + m + c, u);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.f + __expf(-g[k])) * u[k];
+    for (int k = 0; k < 8; ++k) o[k] = rp::swiglu_fwd_elem(g[k], u[k]);
     store8(a_row + c, o);
   }
 }
@@ -383,11 +384,7 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(const __nv_bfloat16* __
     load8(g_row + c, g);
     load8(g_row + m + c, u);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float sg = 1.f / (1.f + __expf(-g[k]));
-      du[k] = d[k] * g[k] * sg;
-      dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
-    }
+    for (int k = 0; k < 8; ++k) rp::swiglu_bwd_elem(d[k], g[k], u[k], dg[k], du[k]);
     store8(d_row + c, dg);
     store8(d_row + m + c, du);
   }

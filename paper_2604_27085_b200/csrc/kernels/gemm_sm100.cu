@@ -25,6 +25,7 @@
 #include <unordered_map>
 
 #include "kernels/sm100.cuh"
+#include "kernels/swiglu.cuh"
 #include "rp/kernels.h"
 
 namespace rp {
@@ -40,7 +41,14 @@ constexpr int NUM_THREADS = 256;             // w0 TMA, w1 MMA, w2 TMEM, w4-7 ep
 constexpr int TMEM_COLS = 512;               // 2 x 256-column accumulators
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-enum Epi : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2 };
+// EPI_SWIGLU_BWD: the accumulator is dact = dL/d(silu(g)*u) [M, N]; R holds
+// gu = [g | u] ([M, 2N], pitch ldr) and D receives dgu = [dg | du] (pitch ldd)
+// EPI_SWIGLU_FWD ("dual" gate/up GEMM, pair kernel only): B = W_gu [2N, K];
+// the pair tile's two 128-row B halves are gate rows n0.. and up rows N+n0..,
+// so each TMEM row holds g (cols 0-127) and u (cols 128-255) of the same
+// outputs; the epilogue writes gu = [g | u] to D ([M, 2N]) and act =
+// silu(g) * u to D2 ([M, N])
+enum Epi : int { EPI_BF16 = 0, EPI_F32 = 1, EPI_F32_ACC = 2, EPI_SWIGLU_BWD = 3, EPI_SWIGLU_FWD = 4 };
 
 struct Params {
   int M, N, K;
@@ -50,6 +58,7 @@ struct Params {
   long long ldr;
   int vec;                 // 16-byte vector stores/loads legal for D (and R)
   int tma_out;             // fp32 D written through the TMA map (pair kernel)
+  int tma_swiglu;          // EPI_SWIGLU_BWD through the EpiMaps (pair kernel)
   // split-K of the last partial wave (pair kernel): work units [0, full) are
   // whole tiles, units beyond are the two K halves of tile full + (u-full)/2;
   // the first half parks its fp32 partial in `ws` and raises a per-warp flag
@@ -58,6 +67,14 @@ struct Params {
   float* ws;
   unsigned* flags;
   unsigned epoch;
+  void* D2;                // EPI_SWIGLU_FWD: act [M, N] bf16, pitch ldd2
+  long long ldd2;
+};
+
+// TMA maps of the SwiGLU-backward epilogue: g / u halves of gu and dg / du
+// halves of dgu, each [M, N] bf16 with a {32, 32} SWIZZLE_64B box
+struct EpiMaps {
+  CUtensorMap g, u, dg, du;
 };
 
 // Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
@@ -67,7 +84,44 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
         const int col0 = col0_;
         if (row_ok && col0 < p.N) {
         const bool full_chunk = p.vec && col0 + 32 <= p.N;
-        if (EPI == EPI_BF16) {
+        if (EPI == EPI_SWIGLU_BWD) {
+          // same arithmetic as swiglu_bwd_kernel on a bf16-rounded dact, so the
+          // fused and the two-kernel paths agree
+          const __nv_bfloat16* gr = p.R + (long long)row * p.ldr + col0;
+          const __nv_bfloat16* ur = gr + p.N;
+          __nv_bfloat16* dg = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col0;
+          __nv_bfloat16* du = dg + p.N;
+          auto one = [](float acc, float g, float u, float& og, float& ou) {
+            swiglu_bwd_elem(__bfloat162float(__float2bfloat16_rn(acc)), g, u, og, ou);
+          };
+          if (full_chunk) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              const uint4 gv = *reinterpret_cast<const uint4*>(gr + i);
+              const uint4 uv = *reinterpret_cast<const uint4*>(ur + i);
+              const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gv);
+              const __nv_bfloat16* ub = reinterpret_cast<const __nv_bfloat16*>(&uv);
+              float og[8], ou[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                one(__uint_as_float(v[i + j]), __bfloat162float(gb[j]), __bfloat162float(ub[j]),
+                    og[j], ou[j]);
+              *reinterpret_cast<uint4*>(dg + i) =
+                  make_uint4(pack_bf16x2(og[0], og[1]), pack_bf16x2(og[2], og[3]),
+                             pack_bf16x2(og[4], og[5]), pack_bf16x2(og[6], og[7]));
+              *reinterpret_cast<uint4*>(du + i) =
+                  make_uint4(pack_bf16x2(ou[0], ou[1]), pack_bf16x2(ou[2], ou[3]),
+                             pack_bf16x2(ou[4], ou[5]), pack_bf16x2(ou[6], ou[7]));
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+              float og, ou;
+              one(__uint_as_float(v[i]), __bfloat162float(gr[i]), __bfloat162float(ur[i]), og, ou);
+              dg[i] = __float2bfloat16_rn(og);
+              du[i] = __float2bfloat16_rn(ou);
+            }
+          }
+        } else if (EPI == EPI_BF16) {
           __nv_bfloat16* d = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + col0;
           float f[32];
 #pragma unroll
@@ -328,6 +382,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
         "r"(smem_u32(src)), "r"(c0), "r"(c1)
         : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -341,7 +401,8 @@ template <int A_MN, int B_MN, int EPI, int PBN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tma_a,
                      const __grid_constant__ CUtensorMap tma_b,
-                     const __grid_constant__ CUtensorMap tma_d, Params p, int n_fastest) {
+                     const __grid_constant__ CUtensorMap tma_d,
+                     const __grid_constant__ EpiMaps em, Params p, int n_fastest) {
   using Cfg = PairCfg<PBN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -351,20 +412,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* sw_bar = acc_empty + 2;       // [4 warps x 2] SwiGLU epilogue loads
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sw_bar + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + PBN - 1) / PBN;
+  constexpr bool DUAL = EPI == EPI_SWIGLU_FWD;
+  constexpr int TN = DUAL ? PBN / 2 : PBN;  // output columns per tile
+  const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + TN - 1) / TN;
   const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = (p.K + BK - 1) / BK;
   auto tile_mn = [&](int tile, int& m0, int& n0) {
     const int mt = n_fastest ? tile / n_tiles : tile % m_tiles;
     const int nt = n_fastest ? tile % n_tiles : tile / m_tiles;
     m0 = mt * 256;
-    n0 = nt * PBN;
+    n0 = nt * TN;
   };
   // work unit -> (tile, k-block range, K half: -1 whole, 0 first, 1 second)
   auto unit_info = [&](int u, int& tile, int& kb0, int& kb1, int& khalf) {
@@ -390,6 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 8);  // 4 epilogue warps x 2 CTAs
     }
+    for (int b = 0; b < 8; ++b) mbar_init(&sw_bar[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -412,7 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int tile, kb0, kb1, khalf, m0, n0;
       unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
-      const int am = m0 + 128 * rank, bn = n0 + (PBN / 2) * rank;
+      const int am = m0 + 128 * rank, bn = DUAL ? n0 + (int)rank * p.N : n0 + (PBN / 2) * rank;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE;
@@ -470,12 +535,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ---------------- epilogue (both CTAs, 128 rows each) ----------------
     const int q = warp & 3;
     uint32_t epi_chunk_no = 0;  // fp32 TMA epilogue: chunks issued by this warp
+    // SwiGLU epilogue: g/u chunks TMA-loaded into two per-warp buffers
+    // (g 2 KB | u 2 KB, SWIZZLE_64B rows of 64 B), the next chunk's load in
+    // flight while this one is computed; results overwrite the buffer in place
+    // and leave through TMA stores
+    uint32_t sw_ld = 0, sw_cs = 0;
+    const bool no_l2_prefetch = p.tma_swiglu == 2;
+    uint8_t* sw_buf = epi_smem + q * 8192;
+    auto sw_issue = [&](int col, int row) {
+      if (lane == 0) {
+        const int b = sw_ld & 1;
+        bulk_wait_read<0>();  // the store that last read this buffer
+        mbar_arrive_expect_tx(&sw_bar[q * 2 + b], 4096);
+        tma_load_2d(sw_buf + b * 4096, &em.g, &sw_bar[q * 2 + b], col, row);
+        tma_load_2d(sw_buf + b * 4096 + 2048, &em.u, &sw_bar[q * 2 + b], col, row);
+      }
+      ++sw_ld;
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < p.units; u += npairs) {
       int tile, kb0, kb1, khalf, m0, n0;
       unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
+      const bool sw_tma = EPI == EPI_SWIGLU_BWD && p.tma_swiglu && khalf != 0 &&
+                          m0 + 128 * (int)rank + q * 32 < p.M;
+      if (sw_tma) {  // needs no accumulator: start before the mainloop finishes
+        const int r0 = m0 + 128 * rank + q * 32;
+        sw_issue(n0, r0);
+        // the rest of the tile's g/u into L2, so each chunk's smem load is an
+        // L2 hit rather than a DRAM round trip (one chunk of smem look-ahead)
+        if (lane == 0 && !no_l2_prefetch)
+          for (int c = 32; c < min(PBN, p.N - n0); c += 32) {
+            tma_prefetch_l2(&em.g, n0 + c, r0);
+            tma_prefetch_l2(&em.u, n0 + c, r0);
+          }
+      }
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row0 = m0 + 128 * rank + q * 32;
@@ -518,7 +613,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       };
       if (khalf == 0) {
         // nothing to store: the partial is parked
-      } else if (EPI != EPI_BF16 && p.tma_out) {
+      } else if (EPI == EPI_SWIGLU_BWD && p.tma_swiglu) {
+        const int c_end = sw_tma ? min(PBN, p.N - n0) : 0;
+#pragma unroll 1
+        for (int c = 0; c < c_end; c += 32) {
+          if (c + 32 < c_end) sw_issue(n0 + c + 32, row0);
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
+          tmem_ld_wait();
+          add_part(c, v);
+          const int b = sw_cs & 1;
+          mbar_wait(&sw_bar[q * 2 + b], (sw_cs >> 1) & 1);
+          ++sw_cs;
+          uint8_t* gb = sw_buf + b * 4096;
+          uint8_t* ub = gb + 2048;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int off = lane * 64 + ((k ^ ((lane >> 1) & 3)) << 4);
+            const uint4 gv = *reinterpret_cast<const uint4*>(gb + off);
+            const uint4 uv = *reinterpret_cast<const uint4*>(ub + off);
+            const __nv_bfloat16* g8 = reinterpret_cast<const __nv_bfloat16*>(&gv);
+            const __nv_bfloat16* u8 = reinterpret_cast<const __nv_bfloat16*>(&uv);
+            float og[8], ou[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              swiglu_bwd_elem(__bfloat162float(__float2bfloat16_rn(__uint_as_float(v[8 * k + j]))),
+                              __bfloat162float(g8[j]), __bfloat162float(u8[j]), og[j], ou[j]);
+            }
+            *reinterpret_cast<uint4*>(gb + off) =
+                make_uint4(pack_bf16x2(og[0], og[1]), pack_bf16x2(og[2], og[3]),
+                           pack_bf16x2(og[4], og[5]), pack_bf16x2(og[6], og[7]));
+            *reinterpret_cast<uint4*>(ub + off) =
+                make_uint4(pack_bf16x2(ou[0], ou[1]), pack_bf16x2(ou[2], ou[3]),
+                           pack_bf16x2(ou[4], ou[5]), pack_bf16x2(ou[6], ou[7]));
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d<false>(&em.dg, gb, n0 + c, row0);
+            tma_store_2d<false>(&em.du, ub, n0 + c, row0);
+            bulk_commit();
+          }
+        }
+      } else if (EPI == EPI_SWIGLU_FWD) {
+        const int c_end = min(TN, p.N - n0);
+#pragma unroll 1
+        for (int c = 0; c < c_end; c += 32) {
+          uint32_t vg[32], vu[32];
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, vg);
+          tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + TN + c, vu);
+          tmem_ld_wait();
+          if (row_ok) {
+            __nv_bfloat16* dg = reinterpret_cast<__nv_bfloat16*>(p.D) + (long long)row * p.ldd + n0 + c;
+            __nv_bfloat16* du = dg + p.N;
+            __nv_bfloat16* da = reinterpret_cast<__nv_bfloat16*>(p.D2) + (long long)row * p.ldd2 + n0 + c;
+            if (p.vec && n0 + c + 32 <= p.N) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 8) {
+                uint32_t pg[4], pu[4], pa[4];
+#pragma unroll
+                for (int j = 0; j < 8; j += 2) {
+                  pg[j / 2] = pack_bf16x2(__uint_as_float(vg[i + j]), __uint_as_float(vg[i + j + 1]));
+                  pu[j / 2] = pack_bf16x2(__uint_as_float(vu[i + j]), __uint_as_float(vu[i + j + 1]));
+                  // act from the bf16-rounded g, u: what the two-kernel path reads back
+                  const __nv_bfloat162 g2 = *reinterpret_cast<const __nv_bfloat162*>(&pg[j / 2]);
+                  const __nv_bfloat162 u2 = *reinterpret_cast<const __nv_bfloat162*>(&pu[j / 2]);
+                  pa[j / 2] = pack_bf16x2(
+                      swiglu_fwd_elem(__bfloat162float(g2.x), __bfloat162float(u2.x)),
+                      swiglu_fwd_elem(__bfloat162float(g2.y), __bfloat162float(u2.y)));
+                }
+                *reinterpret_cast<uint4*>(dg + i) = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+                *reinterpret_cast<uint4*>(du + i) = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+                *reinterpret_cast<uint4*>(da + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+              }
+            } else {
+              for (int i = 0; i < 32 && n0 + c + i < p.N; ++i) {
+                const __nv_bfloat16 g = __float2bfloat16_rn(__uint_as_float(vg[i]));
+                const __nv_bfloat16 u = __float2bfloat16_rn(__uint_as_float(vu[i]));
+                dg[i] = g;
+                du[i] = u;
+                da[i] = __float2bfloat16_rn(swiglu_fwd_elem(__bfloat162float(g), __bfloat162float(u)));
+              }
+            }
+          }
+        }
+      } else if ((EPI == EPI_F32 || EPI == EPI_F32_ACC) && p.tma_out) {
         // fp32: 32x32 chunks through swizzled smem and the TMA (store or L2 add),
         // two chunk buffers per warp in flight
         uint8_t* wbuf = epi_smem + q * (2 * 4096);
@@ -560,7 +739,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive_leader(&acc_empty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (EPI != EPI_BF16 && p.tma_out && lane == 0) bulk_wait_all();
+    if (((EPI != EPI_BF16 && p.tma_out) || (EPI == EPI_SWIGLU_BWD && p.tma_swiglu)) && lane == 0)
+      bulk_wait_all();
   }
   tc_fence_before();
   cluster_sync();
@@ -621,6 +801,22 @@ bool make_map_f32(CUtensorMap* map, const void* base, long long rows, long long 
          CUDA_SUCCESS;
 }
 
+// bf16 [rows, cols] (row pitch ld elements), box {32 cols, 32 rows}, SWIZZLE_64B:
+// the SwiGLU-backward epilogue's g/u loads and dg/du stores
+bool make_map_sw64(CUtensorMap* map, const void* base, long long rows, long long cols,
+                   long long ld) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t elem[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -675,7 +871,8 @@ int pair_tile_n(int M, int N) {
 
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
-                   const Params& p, bool pair, int n_fastest, cudaStream_t stream) {
+                   const EpiMaps& em, const Params& p, bool pair, int n_fastest,
+                   cudaStream_t stream) {
   if (pair) {
     const bool narrow = pair_tile_n(p.M, p.N) == 128;
     auto kern = narrow ? gemm_pair_kernel<A_MN, B_MN, EPI, 128> : gemm_pair_kernel<A_MN, B_MN, EPI, 256>;
@@ -687,7 +884,8 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
       configured[narrow] = true;
     }
     const int pbn = narrow ? 128 : 256;
-    const int tiles = ((p.M + 255) / 256) * ((p.N + pbn - 1) / pbn);
+    const int tn = EPI == EPI_SWIGLU_FWD ? pbn / 2 : pbn;  // output columns per tile
+    const int tiles = ((p.M + 255) / 256) * ((p.N + tn - 1) / tn);
     const int npairs = num_sms() / 2;
     Params q = p;
     q.units = q.full = tiles;
@@ -698,7 +896,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     // costs about what the shorter wave saves
     const int full = (tiles / npairs) * npairs, tail = tiles - full;
     static const bool no_split = getenv("RP_GEMM_NO_SPLITK") != nullptr;
-    if (!no_split && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
+    if (!no_split && EPI != EPI_SWIGLU_BWD && EPI != EPI_SWIGLU_FWD && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
       SplitWs& w = split_ws(stream, (std::size_t)tail * 2 * 128 * pbn, (std::size_t)tail * 8);
       if (w.ws) {
         q.full = full;
@@ -709,7 +907,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
       }
     }
     const int pairs = q.units < npairs ? q.units : npairs;
-    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, q, n_fastest);
+    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, em, q, n_fastest);
     return cudaGetLastError();
   }
   auto kern = gemm_kernel<A_MN, B_MN, EPI>;
@@ -728,12 +926,24 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
 
 template <int A_MN, int B_MN>
 cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
-                         const CUtensorMap& td, const Params& p, bool pair, int n_fastest,
-                         cudaStream_t s) {
+                         const CUtensorMap& td, const EpiMaps& em, const Params& p, bool pair,
+                         int n_fastest, cudaStream_t s) {
   switch (epi) {
-    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, td, p, pair, n_fastest, s);
-    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, td, p, pair, n_fastest, s);
-    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, td, p, pair, n_fastest, s);
+    case EPI_BF16: return launch<A_MN, B_MN, EPI_BF16>(ta, tb, td, em, p, pair, n_fastest, s);
+    case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, td, em, p, pair, n_fastest, s);
+    case EPI_SWIGLU_FWD:  // pair kernel, gate/up forward layout only
+      if constexpr (A_MN == 0 && B_MN == 0) {
+        if (!pair) return cudaErrorInvalidValue;
+        return launch<A_MN, B_MN, EPI_SWIGLU_FWD>(ta, tb, td, em, p, pair, n_fastest, s);
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    case EPI_SWIGLU_BWD:  // only the down-projection dgrad layout is instantiated
+      if constexpr (A_MN == 0 && B_MN == 1)
+        return launch<A_MN, B_MN, EPI_SWIGLU_BWD>(ta, tb, td, em, p, pair, n_fastest, s);
+      else
+        return cudaErrorInvalidValue;
+    default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, td, em, p, pair, n_fastest, s);
   }
 }
 
@@ -742,8 +952,11 @@ cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
 
 using namespace rp;
 
-extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm_args_t* g,
-                                                                   void* stream) {
+// mode 0: plain GEMM; 1: SwiGLU-backward epilogue; 2: dual gate/up forward
+// with the SwiGLU epilogue (act, ld_act)
+static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act = nullptr,
+                      long long ld_act = 0) {
+  const bool swiglu_bwd = mode == 1, dual = mode == 2;
   if (!g || g->M <= 0 || g->N <= 0 || g->K <= 0 || !g->A || !g->B || !g->D) return RP_E_INPUT;
   if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
       (reinterpret_cast<uintptr_t>(g->B) & 15))
@@ -754,14 +967,16 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   bool ok = g->a_mn_major ? make_map(&ta, g->A, g->K, g->M, g->lda, 64, 64)
                           : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
   ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
-                            : make_map(&tb, g->B, g->N, g->K, g->ldb, 64,
+                            : make_map(&tb, g->B, dual ? 2LL * g->N : g->N, g->K, g->ldb, 64,
                                        pair ? pair_tile_n(g->M, g->N) / 2 : BN));
   // raster: keep the larger operand's tile hot (walk the other dimension fastest)
   const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
   if (!ok) return RP_E_CUDA;
   const int esz = g->out_f32 ? 4 : 2;
   const bool vec = (g->ldd * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
-                   (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0));
+                   (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0)) &&
+                   (!dual || ((ld_act * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(act) & 15) == 0 &&
+                              g->N % 8 == 0));
   // fp32 outputs of the pair kernel go through a TMA map (store / L2 reduce-add)
   CUtensorMap td;
   std::memset(&td, 0, sizeof(td));
@@ -769,17 +984,56 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm
   const bool tma_out = pair && g->out_f32 && !no_tma_out && (g->ldd * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                        make_map_f32(&td, g->D, g->M, g->N, g->ldd);
-  Params p{g->M, g->N, g->K, g->D, g->ldd, reinterpret_cast<const __nv_bfloat16*>(g->R), g->ldr,
-           vec ? 1 : 0, tma_out ? 1 : 0, 0, 0, nullptr, nullptr, 0};
-  const int epi = g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
+  EpiMaps em;
+  std::memset(&em, 0, sizeof(em));
+  static const bool no_tma_swiglu = getenv("RP_GEMM_NO_TMA_SWIGLU") != nullptr;
+  const auto* R16 = reinterpret_cast<const __nv_bfloat16*>(g->R);
+  auto* D16 = reinterpret_cast<__nv_bfloat16*>(g->D);
+  const bool tma_swiglu = swiglu_bwd && pair && vec && !no_tma_swiglu &&
+                          make_map_sw64(&em.g, R16, g->M, g->N, g->ldr) &&
+                          make_map_sw64(&em.u, R16 + g->N, g->M, g->N, g->ldr) &&
+                          make_map_sw64(&em.dg, D16, g->M, g->N, g->ldd) &&
+                          make_map_sw64(&em.du, D16 + g->N, g->M, g->N, g->ldd);
+  Params p{g->M, g->N, g->K, g->D, g->ldd, R16, g->ldr, vec ? 1 : 0, tma_out ? 1 : 0,
+           tma_swiglu ? (getenv("RP_GEMM_NO_L2_PREFETCH") ? 2 : 1) : 0, 0, 0, nullptr, nullptr,
+           0, act, ld_act};
+  const int epi = dual ? EPI_SWIGLU_FWD : swiglu_bwd ? EPI_SWIGLU_BWD
+                             : g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
   if (g->out_f32 && g->R) return RP_E_INPUT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (g->a_mn_major)
-    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, td, p, pair, n_fastest, s)
-                      : dispatch_epi<1, 0>(epi, ta, tb, td, p, pair, n_fastest, s);
+    e = g->b_mn_major ? dispatch_epi<1, 1>(epi, ta, tb, td, em, p, pair, n_fastest, s)
+                      : dispatch_epi<1, 0>(epi, ta, tb, td, em, p, pair, n_fastest, s);
   else
-    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, td, p, pair, n_fastest, s)
-                      : dispatch_epi<0, 0>(epi, ta, tb, td, p, pair, n_fastest, s);
+    e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, td, em, p, pair, n_fastest, s)
+                      : dispatch_epi<0, 0>(epi, ta, tb, td, em, p, pair, n_fastest, s);
   return e == cudaSuccess ? RP_OK : RP_E_CUDA;
+}
+
+extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm_args_t* g,
+                                                                   void* stream) {
+  return gemm_entry(g, stream, 0);
+}
+
+extern "C" __attribute__((visibility("default"))) int rp_gemm_swiglu_fwd(const rp_gemm_args_t* g,
+                                                                         void* act, int64_t ld_act,
+                                                                         void* stream) {
+  if (!g || !act || g->out_f32 || g->accumulate || g->R || g->N % 8 || g->a_mn_major ||
+      g->b_mn_major)
+    return RP_E_INPUT;
+  if (g->M >= 256) return gemm_entry(g, stream, 2, act, ld_act);
+  // below one pair tile: the plain GEMM into gu, then the SwiGLU kernel
+  rp_gemm_args_t a = *g;
+  a.N = 2 * g->N;
+  const int rc = gemm_entry(&a, stream, 0);
+  if (rc != RP_OK || ld_act != g->N || g->ldd != 2LL * g->N) return rc != RP_OK ? rc : RP_E_INPUT;
+  return rp_swiglu_fwd(g->D, act, g->M, g->N, stream);
+}
+
+extern "C" __attribute__((visibility("default"))) int rp_gemm_swiglu_bwd(const rp_gemm_args_t* g,
+                                                                         void* stream) {
+  if (!g || g->out_f32 || g->accumulate || !g->R || g->N % 8 || g->a_mn_major || !g->b_mn_major)
+    return RP_E_INPUT;
+  return gemm_entry(g, stream, 1);
 }

@@ -325,7 +325,7 @@ struct Runtime {
   void sync_all();
   void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
             bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_, int N_, int K_,
-            const void* Rz = nullptr, int64_t ldr = 0);
+            const void* Rz = nullptr, int64_t ldr = 0, bool swiglu_bwd = false);
   ~Runtime();
 };
 
@@ -348,7 +348,7 @@ void Runtime::d2d(void* dst, const Gpu& Gd, const void* src, const Gpu& Gs, std:
 
 void Runtime::gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B,
                    int64_t ldb, bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_,
-                   int N_, int K_, const void* Rz, int64_t ldr) {
+                   int N_, int K_, const void* Rz, int64_t ldr, bool swiglu_bwd) {
   rp_gemm_args_t a{};
   a.M = M_;
   a.N = N_;
@@ -366,7 +366,7 @@ void Runtime::gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const
   a.R = Rz;
   a.ldr = ldr;
   const int pi = prof_begin(st);
-  RP_K(rp_gemm_bf16(&a, st));
+  RP_K(swiglu_bwd ? rp_gemm_swiglu_bwd(&a, st) : rp_gemm_bf16(&a, st));
   prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)K_);
   ++kernels;
 }
@@ -718,11 +718,14 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   G.dx32[1] = static_cast<float*>(dalloc(Th * 4, 4));
   for (int b = 0; b < 2; ++b) {
     G.dx16s[b] = static_cast<uint16_t*>(dalloc(Th * 2, 4));
-    G.dgus[b] = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
     G.dqkvs[b] = static_cast<uint16_t*>(dalloc((int64_t)T * s.qkvd() * 2, 4));
     G.ev_dx16_free[b] = new_event(false);
-    G.ev_dgu_free[b] = new_event(false);
     G.ev_dqkv_free[b] = new_event(false);
+  }
+  if (const char* e = getenv("RP_DGU_BUFS")) G.n_dgu = std::max(2, std::min(3, atoi(e)));
+  for (int b = 0; b < G.n_dgu; ++b) {
+    G.dgus[b] = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
+    G.ev_dgu_free[b] = new_event(false);
   }
   G.ev_wgrad = new_event(false);
   G.dx16 = G.dx16s[0];
@@ -947,10 +950,26 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
-  gemm(st, A.h2, h, false, W + LL.gate_up.off, h, false, A.gu, 2 * s.m, false, false, T, 2 * s.m,
-       h);
-  if (lora_r) lora_fwd(st, W, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, A.gu, 2 * s.m, 2 * s.m);
-  {
+  static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
+  if (!lora_r && !unfused) {  // SwiGLU in the gate/up GEMM's epilogue (gu kept for bwd)
+    rp_gemm_args_t a{};
+    a.M = T;
+    a.N = s.m;
+    a.K = h;
+    a.A = A.h2;
+    a.lda = h;
+    a.B = W + LL.gate_up.off;
+    a.ldb = h;
+    a.D = A.gu;
+    a.ldd = 2 * s.m;
+    const int pi_ = prof_begin(st);
+    RP_K(rp_gemm_swiglu_fwd(&a, A.act, s.m, st));
+    prof_end(pi_, st, 0, 2.0 * T * 2 * s.m * (double)h);
+    ++kernels;
+  } else {
+    gemm(st, A.h2, h, false, W + LL.gate_up.off, h, false, A.gu, 2 * s.m, false, false, T,
+         2 * s.m, h);
+    if (lora_r) lora_fwd(st, W, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, A.gu, 2 * s.m, 2 * s.m);
     const int pi_ = prof_begin(st);
     RP_K(rp_swiglu_fwd(A.gu, A.act, T, s.m, st));
     prof_end(pi_, st, 2, 6.0 * T * s.m);
@@ -982,7 +1001,9 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   uint16_t* dx_b = G.dx16s[xb];
   const int p = G.bwd_par;
   G.bwd_par ^= 1;
-  uint16_t* dgu = G.dgus[p];
+  const int pg = G.dgu_i;
+  G.dgu_i = (G.dgu_i + 1) % G.n_dgu;
+  uint16_t* dgu = G.dgus[pg];
   uint16_t* dqkv = G.dqkvs[p];
   auto to_ws = [&]() {  // the wgrad stream waits for everything enqueued on compute so far
     cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
@@ -1000,13 +1021,21 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   // MLP:  x3 = x2 + act(gu(h2)) Wd^T
   to_ws();
   if (full) gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
-  gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
+  // full fine-tune: the SwiGLU backward runs in the dgrad GEMM's epilogue
+  // (dact never reaches HBM); LoRA adds the adapter term to dact first
+  static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
+  const bool fuse = full && !unfused;
+  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[pg], 0));  // wgrad n_dgu layers ago read it
+  if (fuse)
+    gemm(st, dx_a, h, false, W + LL.down.off, m, true, dgu, 2 * m, false, false, T, m, h, A.gu,
+         2 * m, true);
+  else
+    gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
   if (!full)
     lora_bwd(G, st, W, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, G.dact, m,
              first);
   RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], full ? ws : st));
-  RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[p], 0));  // wgrad two layers ago read it
-  {
+  if (!fuse) {
     const int pi_ = prof_begin(st);
     RP_K(rp_swiglu_bwd(G.dact, A.gu, dgu, T, m, st));
     prof_end(pi_, st, 2, 10.0 * T * m);
@@ -1014,7 +1043,7 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   to_ws();
   if (full)
     gemm(ws, dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
-  RP_CUDA(cudaEventRecord(G.ev_dgu_free[p], full ? ws : st));
+  RP_CUDA(cudaEventRecord(G.ev_dgu_free[pg], full ? ws : st));
   gemm(st, dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
   if (!full)
     lora_bwd(G, st, W, dW, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, dgu, 2 * m, 2 * m, G.dh, h,

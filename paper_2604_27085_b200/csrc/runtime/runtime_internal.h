@@ -137,10 +137,11 @@ struct Gpu {
   // overlap them; scratch gradients they read are double-buffered
   cudaStream_t wgrad = nullptr;
   uint16_t* dx16s[2] = {nullptr, nullptr};
-  uint16_t* dgus[2] = {nullptr, nullptr};
+  uint16_t* dgus[3] = {nullptr, nullptr, nullptr};  // ring: the fused down-dgrad
+  int n_dgu = 3, dgu_i = 0;                           // writes dgu one GEMM earlier
   uint16_t* dqkvs[2] = {nullptr, nullptr};
   cudaEvent_t ev_dx16_free[2] = {nullptr, nullptr};
-  cudaEvent_t ev_dgu_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_dgu_free[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_dqkv_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_wgrad = nullptr;  // last weight-gradient GEMM enqueued
   int bwd_par = 0;

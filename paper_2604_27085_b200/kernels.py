@@ -68,6 +68,40 @@ def gemm(A: torch.Tensor, B: torch.Tensor, D: torch.Tensor, *, a_mn_major=False,
     return D
 
 
+def gemm_swiglu_bwd(A: torch.Tensor, B: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor,
+                    stream=None):
+    """dgu = swiglu_bwd(dact = A[M,K] . B[K,N], gu) in one kernel (down-projection dgrad
+    with the SwiGLU backward in its epilogue); gu, dgu are [M, 2N] bf16."""
+    M, K = A.shape
+    Kb, N = B.shape
+    assert K == Kb and tuple(gu.shape) == (M, 2 * N) and tuple(dgu.shape) == (M, 2 * N)
+    for t in (A, B, gu, dgu):
+        assert t.is_cuda and t.stride(1) == 1 and t.dtype == torch.bfloat16
+    args = GemmArgs(M, N, K, _ptr(A), A.stride(0), 0, _ptr(B), B.stride(0), 1,
+                    _ptr(dgu), dgu.stride(0), 0, 0, _ptr(gu), gu.stride(0))
+    f = _lib().rp_gemm_swiglu_bwd
+    f.restype = C.c_int
+    _check(f(C.byref(args), _stream(stream)))
+    return dgu
+
+
+def gemm_swiglu_fwd(A: torch.Tensor, W_gu: torch.Tensor, gu: torch.Tensor, act: torch.Tensor,
+                    stream=None):
+    """gu = A[M,K] . W_gu[2N,K]^T and act = silu(gu[:, :N]) * gu[:, N:] in one kernel."""
+    M, K = A.shape
+    N2, Kb = W_gu.shape
+    N = N2 // 2
+    assert K == Kb and N2 == 2 * N and tuple(gu.shape) == (M, N2) and tuple(act.shape) == (M, N)
+    for t in (A, W_gu, gu, act):
+        assert t.is_cuda and t.stride(1) == 1 and t.dtype == torch.bfloat16
+    args = GemmArgs(M, N, K, _ptr(A), A.stride(0), 0, _ptr(W_gu), W_gu.stride(0), 0,
+                    _ptr(gu), gu.stride(0), 0, 0, None, 0)
+    f = _lib().rp_gemm_swiglu_fwd
+    f.restype = C.c_int
+    _check(f(C.byref(args), _ptr(act), I64(act.stride(0)), _stream(stream)))
+    return act
+
+
 class AdamHParams(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
                 ("eps", C.c_float), ("weight_decay", C.c_float), ("grad_scale", C.c_float)]

@@ -114,3 +114,52 @@ def test_gemm_split_k_last_wave(M, N, K, a_mn, b_mn):
     kernels.gemm(Aop, Bop, D32, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn), accumulate=True)
     torch.cuda.synchronize()
     assert _rel(D32, 2 * ref) < 3e-5  # fp32 summation order over K up to 12288
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 1536, 256), (128, 256, 64), (300, 1000, 192),
+                                   (4096, 3072, 1024)])
+def test_gemm_swiglu_bwd_epilogue(M, N, K):
+    """Down-projection dgrad with the SwiGLU backward fused into the epilogue equals
+    the two-kernel path (GEMM into a bf16 dact, then rp_swiglu_bwd) up to FMA
+    contraction, and the fp32 autograd reference within bf16 rounding."""
+    from paper_2604_27085_b200 import kernels
+    dy = _mk(M, K, 21)
+    Wd = _mk(K, N, 22)  # [h, m] row-major: the MN-major B operand
+    gu = _mk(M, 2 * N, 23)
+    dgu = torch.empty(M, 2 * N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm_swiglu_bwd(dy, Wd, gu, dgu)
+    dact = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm(dy, Wd, dact, b_mn_major=True)
+    two = torch.empty_like(dgu)
+    kernels.swiglu_bwd(dact, gu, two)
+    torch.cuda.synchronize()
+    diff = (dgu.float() - two.float()).abs()
+    assert (diff <= two.float().abs() * 2 ** -7 + 1e-30).all()
+    assert (diff == 0).float().mean().item() > 0.95
+    x = gu.float().requires_grad_(True)
+    (torch.nn.functional.silu(x[:, :N]) * x[:, N:]).backward(dy.float() @ Wd.float())
+    assert _rel(dgu, x.grad) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 1536, 256), (300, 1000, 192), (128, 256, 64),
+                                   (4096, 3072, 1024)])
+def test_gemm_swiglu_fwd_epilogue(M, N, K):
+    """Gate/up GEMM with the SwiGLU forward in its epilogue (pair tiles whose two
+    B halves are matching gate and up rows) equals the plain GEMM into gu followed
+    by rp_swiglu_fwd; M < 256 takes the two-kernel route inside the entry point."""
+    from paper_2604_27085_b200 import kernels
+    X = _mk(M, K, 31)
+    Wgu = _mk(2 * N, K, 32)
+    gu = torch.empty(M, 2 * N, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm_swiglu_fwd(X, Wgu, gu, act)
+    gu2 = torch.empty_like(gu)
+    kernels.gemm(X, Wgu, gu2)
+    act2 = torch.empty_like(act)
+    kernels.swiglu_fwd(gu2, act2)
+    torch.cuda.synchronize()
+    assert _rel(gu, gu2) < 1e-6
+    assert _rel(act, act2) < 1e-6
+    ref = X.float() @ Wgu.float().t()
+    assert _rel(gu, ref) < 8e-3
+    assert _rel(act, torch.nn.functional.silu(ref[:, :N]) * ref[:, N:]) < 2e-2

@@ -19,7 +19,32 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn, out_f32/acc)
     "gu_wgrad": (24576, 4096, T, 1, 1, 1),
     "down_wgrad": (4096, 12288, T, 1, 1, 1),
     "head_fwd_chunk": (1024, 151936, 4096, 0, 0, 0),
+    "down_dgrad": (T, 12288, 4096, 0, 1, 0),
 }
+
+
+def swiglu_case():
+    """down dgrad + SwiGLU backward: fused epilogue vs GEMM then rp_swiglu_bwd"""
+    m, h = 12288, 4096
+    dy = torch.randn(T, h, device="cuda").to(torch.bfloat16)
+    Wd = torch.randn(h, m, device="cuda").to(torch.bfloat16)
+    gu = torch.randn(T, 2 * m, device="cuda").to(torch.bfloat16)
+    dgu = torch.empty_like(gu)
+    dact = torch.empty(T, m, device="cuda", dtype=torch.bfloat16)
+    fused = bench(lambda: kernels.gemm_swiglu_bwd(dy, Wd, gu, dgu))
+    gemm_only = bench(lambda: kernels.gemm(dy, Wd, dact, b_mn_major=True))
+    two = bench(lambda: (kernels.gemm(dy, Wd, dact, b_mn_major=True),
+                         kernels.swiglu_bwd(dact, gu, dgu)))
+    X = torch.randn(T, h, device="cuda").to(torch.bfloat16)
+    Wgu = torch.randn(2 * m, h, device="cuda").to(torch.bfloat16)
+    act = torch.empty(T, m, device="cuda", dtype=torch.bfloat16)
+    ffused = bench(lambda: kernels.gemm_swiglu_fwd(X, Wgu, gu, act))
+    fgemm = bench(lambda: kernels.gemm(X, Wgu, gu))
+    ftwo = bench(lambda: (kernels.gemm(X, Wgu, gu), kernels.swiglu_fwd(gu, act)))
+    print(json.dumps({"gemm": "gu_fwd_swiglu", "fused_ms": round(ffused, 4),
+                      "gemm_only_ms": round(fgemm, 4), "two_kernel_ms": round(ftwo, 4)}))
+    print(json.dumps({"gemm": "down_dgrad_swiglu", "fused_ms": round(fused, 4),
+                      "gemm_only_ms": round(gemm_only, 4), "two_kernel_ms": round(two, 4)}))
 
 
 def bench(fn, iters=20, warm=5):
@@ -38,6 +63,9 @@ def bench(fn, iters=20, warm=5):
 def main():
     names = sys.argv[1:] or list(SHAPES)
     for name in names:
+        if name == "swiglu":
+            swiglu_case()
+            continue
         M, N, K, a_mn, b_mn, f32 = SHAPES[name]
         A = torch.randn(*((K, M) if a_mn else (M, K)), device="cuda").to(torch.bfloat16)
         B = torch.randn(*((K, N) if b_mn else (N, K)), device="cuda").to(torch.bfloat16)
