@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libroundpipe_b200.so")
+# RP_LIB: an alternative build of the same library (same-box A/B measurements)
+LIB_PATH = os.environ.get("RP_LIB") or os.path.join(_HERE, "libroundpipe_b200.so")
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
 

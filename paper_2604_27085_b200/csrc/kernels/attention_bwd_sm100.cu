@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kb = blockIdx.x, hq = blockIdx.y;
+  const int kb = causal_block(blockIdx.y, T / A_BK, seq / A_BK, false), hq = blockIdx.x;
   const int kvh = hq / (nq / nk);
   const int k0 = kb * A_BK;
   const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kb = blockIdx.x, ha = 2 * (int)blockIdx.y;
+  const int kb = causal_block(blockIdx.y, T / A_BK, seq / A_BK, false), ha = 2 * (int)blockIdx.x;
   const int kvh = ha / (nq / nk);
   const int k0 = kb * A_BK;
   const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kb = blockIdx.x, ha = 2 * (int)blockIdx.y;
+  const int kb = causal_block(blockIdx.y, T / A_BK, seq / A_BK, false), ha = 2 * (int)blockIdx.x;
   const int kvh = ha / (nq / nk);
   const int k0 = kb * A_BK;
   const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
@@ -787,8 +787,8 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / B_Q;
-  const int qb = qblocks - 1 - blockIdx.x;
-  const int h = blockIdx.y, kvh = h / (nq / nk);
+  const int qb = causal_block(blockIdx.y, qblocks, seq / B_Q, true);
+  const int h = blockIdx.x, kvh = h / (nq / nk);
   const int q0 = qb * B_Q;
   const int s0 = (q0 / seq) * seq;
   const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
@@ -999,8 +999,8 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / B_Q;
-  const int qb = qblocks - 1 - (int)blockIdx.x;
-  const int ha = 2 * (int)blockIdx.y, kvh = ha / (nq / nk);
+  const int qb = causal_block(blockIdx.y, qblocks, seq / B_Q, true);
+  const int ha = 2 * (int)blockIdx.x, kvh = ha / (nq / nk);
   const int q0 = qb * B_Q;
   const int s0 = (q0 / seq) * seq;
   const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
@@ -1208,8 +1208,8 @@ __global__ void __launch_bounds__(384, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / B_Q;
-  const int qb = qblocks - 1 - (int)blockIdx.x;
-  const int h = blockIdx.y, kvh = h / (nq / nk);
+  const int qb = causal_block(blockIdx.y, qblocks, seq / B_Q, true);
+  const int h = blockIdx.x, kvh = h / (nq / nk);
   const int q0 = qb * B_Q;
   const int s0 = (q0 / seq) * seq;
   const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
@@ -1497,7 +1497,7 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       if (!set_smem(attn_bwd_dkv3_kernel<HD>, Dkv3Smem<HD>::BYTES)) return RP_E_CUDA;
       cfg5 = true;
     }
-    attn_bwd_dkv3_kernel<HD><<<dim3(T / A_BK, nq / 2), 384, Dkv3Smem<HD>::BYTES, s>>>(
+    attn_bwd_dkv3_kernel<HD><<<dim3(nq / 2, T / A_BK), 384, Dkv3Smem<HD>::BYTES, s>>>(
         (const bf16*)k, ldk, (const bf16*)v, ldv, mq32, mdo32, lse, delta, dkv_acc,
         dkv_acc + acc_n, T, seq, nq, nk, scale);
   } else if ((nq / nk) % 2 == 0 && !v1) {  // two heads of one KV group per CTA
@@ -1506,10 +1506,10 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       if (!set_smem(attn_bwd_dkv_pp_kernel<HD>, Dkv2Smem<HD>::BYTES)) return RP_E_CUDA;
       cfg2 = true;
     }
-    attn_bwd_dkv_pp_kernel<HD><<<dim3(T / A_BK, nq / 2), A2_THREADS, Dkv2Smem<HD>::BYTES, s>>>(
+    attn_bwd_dkv_pp_kernel<HD><<<dim3(nq / 2, T / A_BK), A2_THREADS, Dkv2Smem<HD>::BYTES, s>>>(
         mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
   } else {
-    attn_bwd_dkv_kernel<HD><<<dim3(T / A_BK, nq), 384, DkvSmem<HD>::BYTES, s>>>(
+    attn_bwd_dkv_kernel<HD><<<dim3(nq, T / A_BK), 384, DkvSmem<HD>::BYTES, s>>>(
         mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
   }
   dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
@@ -1525,7 +1525,7 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       if (!set_smem(attn_bwd_dq3_kernel<HD>, Dq3Smem<HD>::BYTES)) return RP_E_CUDA;
       cfg4 = true;
     }
-    attn_bwd_dq3_kernel<HD><<<dim3(T / B_Q, nq), 384, Dq3Smem<HD>::BYTES, s>>>(
+    attn_bwd_dq3_kernel<HD><<<dim3(nq, T / B_Q), 384, Dq3Smem<HD>::BYTES, s>>>(
         (const bf16*)q, ldq, (const bf16*)dout, lddo, mk64, mv64, lse, delta, (bf16*)dq, lddq, T,
         seq, nq, nk, scale);
   } else if ((nq / nk) % 2 == 0 && !v1) {
@@ -1534,10 +1534,10 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       if (!set_smem(attn_bwd_dq_pp_kernel<HD>, Dq2Smem<HD>::BYTES)) return RP_E_CUDA;
       cfg3 = true;
     }
-    attn_bwd_dq_pp_kernel<HD><<<dim3(T / B_Q, nq / 2), 384, Dq2Smem<HD>::BYTES, s>>>(
+    attn_bwd_dq_pp_kernel<HD><<<dim3(nq / 2, T / B_Q), 384, Dq2Smem<HD>::BYTES, s>>>(
         mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
   } else {
-    attn_bwd_dq_kernel<HD><<<dim3(T / B_Q, nq), 384, DqSmem<HD>::BYTES, s>>>(
+    attn_bwd_dq_kernel<HD><<<dim3(nq, T / B_Q), 384, DqSmem<HD>::BYTES, s>>>(
         mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
   }
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;

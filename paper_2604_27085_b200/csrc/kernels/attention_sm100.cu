@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / TILE;
-  const int qb = qblocks - 1 - blockIdx.x;  // heaviest tiles first
-  const int h = blockIdx.y, kvh = h / (nq / nk);
+  const int qb = causal_block(blockIdx.y, qblocks, seq / TILE, true);  // heaviest first
+  const int h = blockIdx.x, kvh = h / (nq / nk);
   const int q0 = qb * TILE;
   const int s0 = (q0 / seq) * seq;
   const int ntiles = (q0 - s0) / TILE + 1;
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qblocks = T / TILE;
-  const int qb = qblocks - 1 - (int)blockIdx.x;  // heaviest tiles first
-  const int h0 = 2 * (int)blockIdx.y;            // heads h0, h0+1 share a KV head
+  const int qb = causal_block(blockIdx.y, qblocks, seq / TILE, true);  // heaviest first
+  const int h0 = 2 * (int)blockIdx.x;  // heads h0, h0+1 share a KV head
   const int kvh = h0 / (nq / nk);
   const int q0 = qb * TILE;
   const int s0 = (q0 / seq) * seq;
@@ -629,7 +629,7 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
         return RP_E_CUDA;
       cfg_pp = true;
     }
-    dim3 grid(T / TILE, nq / 2);
+    dim3 grid(nq / 2, T / TILE);
     kern<<<grid, PP_THREADS, bytes, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);
     return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
   }
@@ -641,7 +641,7 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       return RP_E_CUDA;
     cfg = true;
   }
-  dim3 grid(T / TILE, nq);
+  dim3 grid(nq, T / TILE);
   kern<<<grid, 192, FwdSmem<HD>::BYTES, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
 }

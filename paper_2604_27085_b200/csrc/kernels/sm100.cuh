@@ -65,6 +65,17 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ---- causal-attention CTA order -----------------------------------------------
+// CTAs are dispatched in linear block order with blockIdx.x fastest, so the
+// attention grids put the heads on x and the (query or key) block on y, and
+// map y to blocks in decreasing-work order: a longest-first list schedule
+// over the SMs (work of a query block grows with its position in the
+// sequence, that of a key block shrinks). nb blocks of which sb per sequence.
+__device__ __forceinline__ int causal_block(int y, int nb, int sb, bool late_heavy) {
+  const int nseq = nb / sb;
+  const int pos = y / nseq, sq = y % nseq;
+  return sq * sb + (late_heavy ? sb - 1 - pos : pos);
+}
 // ---- TMA ------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
