@@ -104,10 +104,13 @@ int rp_attn_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const vo
 int rp_attn_fwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
                    int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
-/* Backward on the 5th-gen tensor cores: a key-major dK/dV kernel (one CTA per
- * key block and query head, GQA partials summed in fp32) and a query-major
- * dQ kernel (recomputes S and dP; no dQ atomics). Workspaces: delta fp32
- * [nq, T]; dkv_acc fp32 [2, T, nk*head_dim]. Layouts as rp_attn_bwd. */
+/* Backward on the 5th-gen tensor cores. head_dim 128, even GQA groups: one
+ * key-major kernel per (key block, query-head pair) forms dK, dV and dQ
+ * (dQ^T = K^T dS^T reduce-added into an internal fp32 accumulator in L2).
+ * Otherwise (or RP_ATTN_SPLIT=1): a dK/dV kernel plus a query-major dQ
+ * kernel that recomputes S and dP. GQA partials of dK/dV are summed in fp32.
+ * Workspaces: delta fp32 [nq, T]; dkv_acc fp32 [2, T, nk*head_dim].
+ * Layouts as rp_attn_bwd. */
 int rp_attn_bwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
                    const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,

@@ -15,7 +15,13 @@
 //      dS to double-buffered smem -> dQ += dS K (M128 N=hd K64, K as an
 //      MN-major operand). Epilogue: dQ*scale -> bf16.
 // (B) recomputes S and dP instead of reducing dQ partials through atomics.
+// Default for head_dim 128 with even GQA groups: (A4) below, one kernel that
+// also forms dQ^T = K^T dS^T per tile and reduce-adds it (TMA, fp32, in L2)
+// — no S/dP recompute; (A)+(B) stay as the RP_ATTN_SPLIT=1 path.
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -501,6 +507,337 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
         atomicAdd(reinterpret_cast<float4*>(dst + c + i),
+                  make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
+                              __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ============================================================ (A4) dK / dV / dQ in one kernel
+// The ping-pong dK/dV kernel (A2) plus dQ: after the softmax pass P^T and
+// dS^T (bf16) sit in the first 64 TMEM columns of the head's S^T|dP^T block,
+// so the last 64 hold dQ^T = K^T dS^T (M = head_dim, N = 64 queries; K^T is
+// the MN-major view of the resident K tile, dS^T a bf16 copy in shared
+// memory). The softmax warpgroup drains dQ^T (thread = head-dim lane), stages
+// it [dim][query] and adds it into a d-major fp32 dQ^T accumulator with TMA
+// reduce-adds (cp.reduce.async.bulk .add.f32, performed in L2). This removes
+// the dQ kernel's recompute of S and dP (2 of its 3 MMA units) and its exp
+// pass. Tensor-core order per query tile j:
+//   dV,dK,dQ_a(j) | S/dP_a(j+1) | dV,dK,dQ_b(j) | S/dP_b(j+1) | ...
+constexpr int A4_NST = 3;
+
+template <int HD>
+struct Dkv4Smem {
+  static constexpr int NSUB = HD / 64;
+  static constexpr int K = 0;
+  static constexpr int V = K + NSUB * SUB128;
+  static constexpr int R0 = V + NSUB * SUB128;     // ring slot s at R0 + s*STAGE
+  static constexpr int STAGE = 2 * NSUB * SUB64;   // Q + dO of one (tile, head)
+  static constexpr int DO_OFF = NSUB * SUB64;
+  static constexpr int DST = R0 + A4_NST * STAGE;  // [2] dS^T [128 keys][64 q] bf16, SW128
+  static constexpr int STG = DST + 2 * A_BK * A_BQ * 2;  // [2 wg][4 warps] 4 KB dQ staging
+  static constexpr int LD = STG + 8 * 4096;        // [A4_NST][2][A_BQ] lse, delta
+  static constexpr int BAR = LD + A4_NST * 2 * A_BQ * 4;
+  static constexpr int BYTES = BAR + 256 + 1024;
+  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
+};
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src,
+                                                  int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::
+          "l"(reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit_grp() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_done_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(A2_THREADS, 1)
+    attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v,
+                          const __grid_constant__ CUtensorMap tm_q,
+                          const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_dq,
+                          const float* __restrict__ lse, const float* __restrict__ delta,
+                          float* __restrict__ dk_acc, float* __restrict__ dv_acc, int T, int seq,
+                          int nq, int nk, float scale) {
+  using L = Dkv4Smem<HD>;
+  constexpr int NSUB = L::NSUB;
+  constexpr int NS = A4_NST;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* st_full = bar + 1;             // [NS]
+  uint64_t* st_empty = bar + 1 + NS;       // [NS]
+  uint64_t* sd_full = bar + 1 + 2 * NS;    // [2] per head
+  uint64_t* ps_full = sd_full + 2;         // [2]
+  uint64_t* dq_full = ps_full + 2;         // [2]
+  uint64_t* dq_free = dq_full + 2;         // [2]
+  uint64_t* acc_done = dq_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kb = causal_block(blockIdx.y, T / A_BK, seq / A_BK, false), ha = 2 * (int)blockIdx.x;
+  const int kvh = ha / (nq / nk);
+  const int k0 = kb * A_BK;
+  const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
+  const int nqt = (s_end - k0) / A_BQ;  // query tiles at/after the diagonal
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_k);
+    tma_prefetch(&tm_v);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_dq);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&st_full[i], 1);
+      mbar_init(&st_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sd_full[i], 1);
+      mbar_init(&ps_full[i], 4);
+      mbar_init(&dq_full[i], 1);
+      mbar_init(&dq_free[i], 4);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM per head w: S^T at w*128 (64 cols), dP^T at w*128 + 64; after the
+  // softmax pass P^T (bf16 pairs) at w*128 + [0, 32), dS^T at w*128 + [32, 64)
+  // and dQ^T (fp32, lane = head dim) at w*128 + [64, 128). dV at 256, dK at 384.
+  const uint32_t TM_DV = 256, TM_DK = 384;
+
+  if (warp == 0 && lane == 0) {
+    mbar_arrive_expect_tx(kv_full, 2 * NSUB * SUB128);
+    for (int sub = 0; sub < NSUB; ++sub) {
+      tma_load_2d(sm + L::K + sub * SUB128, &tm_k, kv_full, kvh * HD + 64 * sub, k0);
+      tma_load_2d(sm + L::V + sub * SUB128, &tm_v, kv_full, kvh * HD + 64 * sub, k0);
+    }
+    for (int idx = 0; idx < 2 * nqt; ++idx) {
+      const int s = idx % NS, w = idx & 1, hq = ha + w;
+      mbar_wait(&st_empty[s], ((idx / NS) & 1) ^ 1);
+      const int qs = k0 + (idx >> 1) * A_BQ;
+      uint8_t* qd = sm + L::R0 + s * L::STAGE;
+      mbar_arrive_expect_tx(&st_full[s], L::STAGE + 2 * A_BQ * 4);
+      for (int sub = 0; sub < NSUB; ++sub) {
+        tma_load_2d(qd + sub * SUB64, &tm_q, &st_full[s], hq * HD + 64 * sub, qs);
+        tma_load_2d(qd + L::DO_OFF + sub * SUB64, &tm_do, &st_full[s], hq * HD + 64 * sub, qs);
+      }
+      float* ld = reinterpret_cast<float*>(sm + L::LD) + s * 2 * A_BQ;
+      bulk_load_1d(ld, lse + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
+      bulk_load_1d(ld + A_BQ, delta + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
+    }
+  } else if (warp == 1) {  // whole warp: uniform descriptors, elected issue
+    constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A_BQ, 0, 0);  // K-major x K-major
+    constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);    // TMEM A x MN-major
+    constexpr uint32_t idesc_q = umma_idesc_bf16(HD, A_BQ, 1, 1);    // MN-major x MN-major
+    const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
+    auto stage = [&](int idx) { return smem_u32(sm + L::R0 + (idx % NS) * L::STAGE); };
+    auto issue_sdp = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&st_full[idx % NS], (idx / NS) & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
+          const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
+          umma_f16(tmem + w * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
+                   umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
+          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
+                   umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+        }
+        umma_commit(&sd_full[w]);
+      }
+      __syncwarp();
+    };
+    auto issue_gq = [&](int j, int w) {
+      const int idx = 2 * j + w;
+      mbar_wait(&ps_full[w], j & 1);
+      tc_fence_after();
+      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+      const uint32_t ds_addr = smem_u32(sm + L::DST + w * (A_BK * A_BQ * 2));
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < A_BQ / 16; ++kk) {
+          const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
+          const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
+          umma_f16_ts(tmem + TM_DV, tmem + w * 128 + kk * 8, ob, idesc_g, (idx | kk) != 0);
+          umma_f16_ts(tmem + TM_DK, tmem + w * 128 + 32 + kk * 8, qb, idesc_g, (idx | kk) != 0);
+        }
+        umma_commit(&st_empty[idx % NS]);
+        // dQ^T = K^T dS^T over the 128 keys of this block
+#pragma unroll
+        for (int kk = 0; kk < A_BK / 16; ++kk)
+          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(k_addr + kk * 2048, SUB128, 1024),
+                   umma_desc_sw128(ds_addr + kk * 2048, 8192, 1024), idesc_q, kk != 0);
+        umma_commit(&dq_full[w]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    issue_sdp(0, 0);
+    issue_sdp(0, 1);
+    // gq_a(j) | S/dP_a(j+1) | gq_b(j) | S/dP_b(j+1): each warpgroup's softmax
+    // hides behind the other head's gq + S/dP; the tensor core only waits for
+    // the short dQ^T drain (TMEM -> registers) between a gq and the same
+    // head's next S/dP
+    for (int j = 0; j < nqt; ++j) {
+#pragma unroll
+      for (int w = 0; w < 2; ++w) {
+        issue_gq(j, w);
+        if (j + 1 < nqt) {
+          mbar_wait(&dq_free[w], j & 1);  // warpgroup w drained dQ^T_w(j)
+          tc_fence_after();
+          issue_sdp(j + 1, w);
+        }
+      }
+    }
+    if (elect_one()) umma_commit(acc_done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    // two softmax warpgroups: w = head slot, thread = key row (softmax) or
+    // head-dim lane (dQ drain)
+    const int w = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int key = k0 + r;
+    const int hq = ha + w;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const float sl2 = scale * kLog2e;
+    uint8_t* dst = sm + L::DST + w * (A_BK * A_BQ * 2);  // this head's dS^T
+    uint8_t* stg0 = sm + L::STG + (w * 4 + quarter) * 4096;
+    uint8_t* stg1 = dst + quarter * 4096;  // this warp's rows of dS^T, free after dQ^T
+    for (int j = 0; j < nqt; ++j) {
+      const int idx = 2 * j + w, s = idx % NS;
+      const int qs = k0 + j * A_BQ;
+      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + s * 2 * A_BQ;
+      const float* del_t = lse_t + A_BQ;
+      mbar_wait(&st_full[s], (idx / NS) & 1);  // lse/delta visibility (already complete)
+      mbar_wait(&sd_full[w], j & 1);
+      tc_fence_after();
+      const bool diag = qs < k0 + A_BK;  // tile overlaps this key block's diagonal
+      uint32_t pk[32], dk2[32];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t sv[32], dpv[32];
+        tmem_ld_32x32b_x32(lane_base + w * 128 + half * 32, sv);
+        tmem_ld_32x32b_x32(lane_base + w * 128 + 64 + half * 32, dpv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int c = half * 32 + i;
+          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c] * kLog2e));
+          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1] * kLog2e));
+          if (diag) {
+            if (qs + c < key) p0 = 0.f;
+            if (qs + c + 1 < key) p1 = 0.f;
+          }
+          const float d0 = p0 * (__uint_as_float(dpv[i]) - del_t[c]);
+          const float d1 = p1 * (__uint_as_float(dpv[i + 1]) - del_t[c + 1]);
+          pk[c / 2] = pack_bf16x2(p0, p1);
+          dk2[c / 2] = pack_bf16x2(d0, d1);
+        }
+      }
+      // every S^T / dP^T column of this thread has been read: P^T -> [0, 32),
+      // dS^T -> [32, 64)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t a[16], b[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          a[i] = pk[h * 16 + i];
+          b[i] = dk2[h * 16 + i];
+        }
+        tmem_st_32x32b_x16(lane_base + w * 128 + h * 16, a);
+        tmem_st_32x32b_x16(lane_base + w * 128 + 32 + h * 16, b);
+      }
+      // dS^T (bf16) into shared memory for dQ^T = K^T dS^T: row = key (128 B),
+      // SWIZZLE_128B. These rows were the staging buffer of the previous
+      // tile's second dQ half: its TMA reduce must have read them.
+      if (lane == 0) bulk_wait_read_all();
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) << 4)) =
+            make_uint4(dk2[4 * c], dk2[4 * c + 1], dk2[4 * c + 2], dk2[4 * c + 3]);
+      fence_proxy_async();
+      tmem_st_wait_all();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps_full[w]);
+      // drain dQ^T (lane = head dim d = r), queries 0-31 and 32-63
+      mbar_wait(&dq_full[w], j & 1);
+      tc_fence_after();
+      uint32_t q0v[32], q1v[32];
+      tmem_ld_32x32b_x32(lane_base + w * 128 + 64, q0v);
+      tmem_ld_32x32b_x32(lane_base + w * 128 + 96, q1v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_free[w]);
+      // stage [32 dims][32 queries] fp32 (this thread's dim = one SWIZZLE_128B
+      // row) and add into the d-major dQ^T accumulator
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint8_t* buf = half ? stg1 : stg0;
+        if (half == 0) {
+          if (lane == 0) bulk_wait_read_all();  // previous tile's stores from stg0
+          __syncwarp();
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* v = half ? q1v : q0v;
+          *reinterpret_cast<uint4*>(buf + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+              make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&tm_dq, buf, qs + half * 32, hq * HD + quarter * 32);
+          bulk_commit_grp();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_done_all();
+    // epilogue: warpgroup a -> dK (scaled), warpgroup b -> dV; fp32 atomics
+    // reduce the G/2 head pairs of the KV group
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    float* dst_acc = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
+    const uint32_t col = w == 0 ? TM_DK : TM_DV;
+    const float f = w == 0 ? scale : 1.f;
+#pragma unroll 1
+    for (int c = 0; c < HD; c += 32) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(lane_base + col + c, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        atomicAdd(reinterpret_cast<float4*>(dst_acc + c + i),
                   make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
                               __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
     }
@@ -1424,6 +1761,37 @@ __global__ void dkv_cast_kernel(const float* __restrict__ dka, const float* __re
   }
 }
 
+// dq[t, c] (bf16, strided) = scale * acc[c, t]: transpose of the d-major fp32
+// accumulator through a 32 x 33 shared tile (block 32 x 8)
+__global__ void dq_cast_kernel(const float* __restrict__ acc, bf16* __restrict__ dq, long long lddq,
+                               int T, int cols, float scale) {
+  __shared__ float tile[32][33];
+  const int t0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = 0; i < 32; i += 8) tile[ty + i][tx] = acc[(long long)(c0 + ty + i) * T + t0 + tx];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 32; i += 8)
+    dq[(long long)(t0 + ty + i) * lddq + c0 + tx] = __float2bfloat16_rn(tile[tx][ty + i] * scale);
+}
+
+// per-stream fp32 dQ accumulator of the fused backward (grown on demand)
+float* dq_workspace(cudaStream_t s, size_t floats) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> ws;
+  std::lock_guard<std::mutex> g(mu);
+  auto& e = ws[s];
+  if (e.second < floats) {
+    if (e.first) cudaFree(e.first);
+    e.first = nullptr;
+    e.second = 0;
+    if (cudaMalloc(&e.first, floats * sizeof(float)) != cudaSuccess) return nullptr;
+    e.second = floats;
+  }
+  return e.first;
+}
+
 // ---- host ------------------------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1446,6 +1814,18 @@ bool map2d(CUtensorMap* m, const void* base, long long rows, long long cols, lon
   cuuint32_t es[2] = {1, 1};
   EncodeFn fn = encode_fn();
   return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                   CUDA_SUCCESS;
+}
+
+bool map_f32(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  EncodeFn fn = encode_fn();
+  return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
                    CUDA_SUCCESS;
@@ -1487,6 +1867,31 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   // opt-in: K/V-in-TMEM variant with 32-query tiles — correct, but measured
   // 2 % slower than the 64-query ping-pong kernel below (0.596 vs 0.586 ms)
   static const bool dkv3 = getenv("RP_ATTN_DKV3") != nullptr;
+  // default: dK/dV/dQ in one kernel (A4); RP_ATTN_SPLIT=1 selects the
+  // two-kernel path (dK/dV kernel + dQ kernel that recomputes S and dP)
+  static const bool split =
+      getenv("RP_ATTN_SPLIT") != nullptr || getenv("RP_ATTN_DQ_PP") != nullptr;
+  if (HD == 128 && (nq / nk) % 2 == 0 && !v1 && !dkv3 && !split) {  // dK/dV/dQ in one kernel
+    const long long qn = (long long)T * nq * HD;
+    float* dq_acc = dq_workspace(s, (size_t)qn);
+    CUtensorMap mdq;
+    if (!dq_acc || !map_f32(&mdq, dq_acc, (long long)nq * HD, T, T))  // d-major [nq*HD, T]
+      return RP_E_CUDA;
+    if (cudaMemsetAsync(dq_acc, 0, sizeof(float) * qn, s) != cudaSuccess) return RP_E_CUDA;
+    static bool cfg6 = false;
+    if (!cfg6) {
+      if (!set_smem(attn_bwd_fused_kernel<HD>, Dkv4Smem<HD>::BYTES)) return RP_E_CUDA;
+      cfg6 = true;
+    }
+    attn_bwd_fused_kernel<HD><<<dim3(nq / 2, T / A_BK), A2_THREADS, Dkv4Smem<HD>::BYTES, s>>>(
+        mk128, mv128, mq64, mdo64, mdq, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk,
+        scale);
+    dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
+                                            lddv, T, nk * HD);
+    dq_cast_kernel<<<dim3(T / 32, nq * HD / 32), dim3(32, 8), 0, s>>>(dq_acc, (bf16*)dq, lddq, T,
+                                                                      nq * HD, scale);
+    return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
+  }
   if ((nq / nk) % 2 == 0 && !v1 && dkv3) {  // K/V in TMEM, two heads, 32-query tiles
     CUtensorMap mq32, mdo32;
     if (!map2d(&mq32, q, T, (long long)nq * HD, ldq, A3_BQ) ||
@@ -1547,7 +1952,9 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
 }  // namespace rp
 
 // tcgen05 backward: dq/dk/dv (bf16) from q/k/v/o/dO/lse; `delta` is an fp32
-// [nq, T] workspace. Deterministic (no atomics). Same layouts as rp_attn_bwd.
+// [nq, T] workspace, dkv_acc an fp32 [2, T, nk*head_dim] one. dK/dV (and, on
+// the default fused path, dQ) are reduced in fp32 through L2 atomics / TMA
+// reduce-adds, so bits can vary run to run. Same layouts as rp_attn_bwd.
 extern "C" __attribute__((visibility("default"))) int rp_attn_bwd_tc(
     const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
     const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse, void* dq,

@@ -277,3 +277,16 @@ def test_flash_attention_bwd_dkv3_variant():
                         "test_flash_attention_bwd_tcgen05", "-p", "no:cacheprovider"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_flash_attention_bwd_split_path():
+    """The two-kernel backward (RP_ATTN_SPLIT=1: dK/dV kernel + dQ kernel that
+    recomputes S and dP) still matches torch; the default is the fused kernel
+    (own process: the knob is read once per process)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, RP_ATTN_SPLIT="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "test_flash_attention_bwd_tcgen05", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
