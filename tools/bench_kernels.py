@@ -77,6 +77,11 @@ def main():
     rq, rk = torch.empty(T, nq, device="cuda"), torch.empty(T, nk, device="cuda")
     ms = bench(lambda: K.qk_norm_rope_fwd(qkv, nq, nk, hd, w[:hd], w[:hd], cs, seq, qo, ko, rq, rk))
     out.append({"kernel": "qk_norm_rope_fwd", "ms": ms, "gbs": T * (nq + nk) * hd * 4 / ms / 1e6})
+    dqk = torch.empty_like(qkv)
+    dqw, dkw = torch.zeros(hd, device="cuda"), torch.zeros(hd, device="cuda")
+    ms = bench(lambda: K.qk_norm_rope_bwd(qo, ko, qkv, nq, nk, hd, w[:hd], w[:hd], rq, rk, cs, seq,
+                                          dqk, dqw, dkw))
+    out.append({"kernel": "qk_norm_rope_bwd", "ms": ms, "gbs": T * (nq + nk) * hd * 6 / ms / 1e6})
     rows = 1024
     z = torch.randn(rows, V, device="cuda").to(torch.bfloat16)
     labels = torch.randint(0, V, (rows,), device="cuda", dtype=torch.int32)
