@@ -26,6 +26,12 @@ typedef struct {
   const void* R; int64_t ldr;
 } rp_gemm_args_t;
 int rp_gemm_bf16(const rp_gemm_args_t* args, void* stream);
+/* D = A . B^T + A2 . B2^T (+ R / accumulate as in rp_gemm_bf16): a second K
+ * segment of K2 columns with the same majors as A and B (A2 [M,K2] or [K2,M],
+ * B2 [N,K2] or [K2,N]). Used for LoRA: X W^T + U B^T and dY W + dU A in one
+ * GEMM. */
+int rp_gemm_bf16_2seg(const rp_gemm_args_t* args, const void* A2, int64_t lda2, const void* B2,
+                      int64_t ldb2, int32_t K2, void* stream);
 /* Down-projection dgrad fused with the SwiGLU backward: acc = A . B^T is
  * dact [M,N] (A [M,K] K-major, B [K,N] MN-major); R = gu = [g | u] [M,2N]
  * (pitch ldr), D = dgu = [dg | du] [M,2N] bf16 (pitch ldd); dact is never

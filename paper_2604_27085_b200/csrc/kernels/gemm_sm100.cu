@@ -59,6 +59,7 @@ struct Params {
   int vec;                 // 16-byte vector stores/loads legal for D (and R)
   int tma_out;             // fp32 D written through the TMA map (pair kernel)
   int tma_swiglu;          // EPI_SWIGLU_BWD through the EpiMaps (pair kernel)
+  int trans;               // store D transposed: element (m, n) -> D[n * ldd + m] (skinny swap)
   // split-K of the last partial wave (pair kernel): work units [0, full) are
   // whole tiles, units beyond are the two K halves of tile full + (u-full)/2;
   // the first half parks its fp32 partial in `ws` and raises a per-warp flag
@@ -69,12 +70,14 @@ struct Params {
   unsigned epoch;
   void* D2;                // EPI_SWIGLU_FWD: act [M, N] bf16, pitch ldd2
   long long ldd2;
+  int kb2;                 // k-blocks of the second K segment (0: none)
 };
 
 // TMA maps of the SwiGLU-backward epilogue: g / u halves of gu and dg / du
 // halves of dgu, each [M, N] bf16 with a {32, 32} SWIZZLE_64B box
 struct EpiMaps {
   CUtensorMap g, u, dg, du;
+  CUtensorMap a2, b2;  // second K segment (pair kernel): D = A B^T + A2 B2^T
 };
 
 // Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
@@ -82,6 +85,20 @@ template <int EPI>
 __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok, int col0_,
                                           const uint32_t (&v)[32]) {
         const int col0 = col0_;
+        if (p.trans) {  // D^T of a swapped skinny GEMM: per column, the warp's 32 rows are contiguous
+          if (row_ok)
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+              const long long o = (long long)(col0 + i) * p.ldd + row;
+              const float f = __uint_as_float(v[i]);
+              if (EPI == EPI_BF16) {
+                reinterpret_cast<__nv_bfloat16*>(p.D)[o] = __float2bfloat16_rn(f);
+              } else {
+                float* d = reinterpret_cast<float*>(p.D) + o;
+                *d = (EPI == EPI_F32_ACC ? *d : 0.f) + f;
+              }
+            }
+          return;
+        }
         if (row_ok && col0 < p.N) {
         const bool full_chunk = p.vec && col0 + 32 <= p.N;
         if (EPI == EPI_SWIGLU_BWD) {
@@ -174,10 +191,26 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
         }
 }
 
-template <int A_MN, int B_MN, int EPI>
+// Single-CTA kernel geometry. TBN = 256 is the general tile; TBN = 32 serves
+// the skinny GEMMs of LoRA adapters (one of M / N is the rank): a 128 x 32
+// tile keeps every MMA column useful and deepens the ring so one CTA streams
+// its long K fast enough (the big operand is read once, HBM-bound).
+template <int TBN, int B_MN>
+struct SingleCfg {
+  static constexpr int B_ROWS = B_MN && TBN < 64 ? 64 : TBN;  // MN-major boxes are 64 wide
+  static constexpr int STAGE = A_STAGE_BYTES + B_ROWS * BK * 2;
+  static constexpr int STAGES = TBN == 256 ? 4 : 8;
+  static constexpr int TMEM = TBN == 256 ? 512 : 64;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(SMEM <= 232448, "single-CTA GEMM shared memory");
+};
+
+template <int A_MN, int B_MN, int EPI, int TBN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                 const __grid_constant__ CUtensorMap tma_b, Params p) {
+  using Cfg = SingleCfg<TBN, B_MN>;
+  constexpr int BN = TBN, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE, TMEM_COLS = Cfg::TMEM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -231,7 +264,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (B_MN) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+          for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
+            tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
         } else {
           tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
         }
@@ -423,7 +457,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   constexpr int TN = DUAL ? PBN / 2 : PBN;  // output columns per tile
   const int m_tiles = (p.M + 255) / 256, n_tiles = (p.N + TN - 1) / TN;
   const int num_tiles = m_tiles * n_tiles;
-  const int k_blocks = (p.K + BK - 1) / BK;
+  const int kb_main = (p.K + BK - 1) / BK;  // segment 1; segment 2 follows
+  const int k_blocks = kb_main + p.kb2;
   auto tile_mn = [&](int tile, int& m0, int& n0) {
     const int mt = n_fastest ? tile / n_tiles : tile % m_tiles;
     const int nt = n_fastest ? tile % n_tiles : tile / m_tiles;
@@ -483,18 +518,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint8_t* sa = smem + stage * Cfg::STAGE;
         uint8_t* sb = sa + P_A_BYTES;
         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
-        const int k0 = kb * BK;
+        const bool seg2 = kb >= kb_main;  // LoRA: [X | U] . [W | B]^T without a concat
+        const int k0 = (seg2 ? kb - kb_main : kb) * BK;
+        const CUtensorMap* ma = seg2 ? &em.a2 : &tma_a;
+        const CUtensorMap* mb = seg2 ? &em.b2 : &tma_b;
         if (A_MN) {
-          tma_load_2d_pair(sa, &tma_a, &full[stage], am, k0);
-          tma_load_2d_pair(sa + 8192, &tma_a, &full[stage], am + 64, k0);
+          tma_load_2d_pair(sa, ma, &full[stage], am, k0);
+          tma_load_2d_pair(sa + 8192, ma, &full[stage], am + 64, k0);
         } else {
-          tma_load_2d_pair(sa, &tma_a, &full[stage], k0, am);
+          tma_load_2d_pair(sa, ma, &full[stage], k0, am);
         }
         if (B_MN) {
-          tma_load_2d_pair(sb, &tma_b, &full[stage], bn, k0);
-          if (PBN == 256) tma_load_2d_pair(sb + 8192, &tma_b, &full[stage], bn + 64, k0);
+          tma_load_2d_pair(sb, mb, &full[stage], bn, k0);
+          if (PBN == 256) tma_load_2d_pair(sb + 8192, mb, &full[stage], bn + 64, k0);
         } else {
-          tma_load_2d_pair(sb, &tma_b, &full[stage], k0, bn);
+          tma_load_2d_pair(sb, mb, &full[stage], k0, bn);
         }
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
@@ -910,17 +948,19 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, em, q, n_fastest);
     return cudaGetLastError();
   }
-  auto kern = gemm_kernel<A_MN, B_MN, EPI>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
+  const bool skinny = p.N <= 32;
+  auto kern = skinny ? gemm_kernel<A_MN, B_MN, EPI, 32> : gemm_kernel<A_MN, B_MN, EPI, 256>;
+  const int smem = skinny ? SingleCfg<32, B_MN>::SMEM : SingleCfg<256, B_MN>::SMEM;
+  static bool configured[2] = {false, false};
+  if (!configured[skinny]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured[skinny] = true;
   }
-  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  const int tbn = skinny ? 32 : BN;
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  kern<<<grid, NUM_THREADS, smem, stream>>>(ta, tb, p);
   return cudaGetLastError();
 }
 
@@ -954,21 +994,51 @@ using namespace rp;
 
 // mode 0: plain GEMM; 1: SwiGLU-backward epilogue; 2: dual gate/up forward
 // with the SwiGLU epilogue (act, ld_act)
+struct Seg2 {
+  const void* A2 = nullptr;
+  long long lda2 = 0;
+  const void* B2 = nullptr;
+  long long ldb2 = 0;
+  int K2 = 0;
+};
+
 static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act = nullptr,
-                      long long ld_act = 0) {
+                      long long ld_act = 0, const Seg2& s2 = Seg2()) {
   const bool swiglu_bwd = mode == 1, dual = mode == 2;
+  // M <= 32 (e.g. a LoRA A-gradient, M = rank): compute D^T = B A^T with the
+  // roles swapped — its N is the small side, served by 128 x 32 tiles — and
+  // store it transposed
+  bool trans = false;
+  rp_gemm_args_t sw;
+  if (mode == 0 && g && g->M <= 32 && g->N > 32 && !g->R && !s2.K2) {
+    sw = *g;
+    sw.M = g->N;
+    sw.N = g->M;
+    sw.A = g->B;
+    sw.lda = g->ldb;
+    sw.a_mn_major = g->b_mn_major;
+    sw.B = g->A;
+    sw.ldb = g->lda;
+    sw.b_mn_major = g->a_mn_major;
+    g = &sw;
+    trans = true;
+  }
   if (!g || g->M <= 0 || g->N <= 0 || g->K <= 0 || !g->A || !g->B || !g->D) return RP_E_INPUT;
   if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
       (reinterpret_cast<uintptr_t>(g->B) & 15))
     return RP_E_INPUT;
   // CTA pairs (cta_group::2, 256-row tiles) whenever M fills a pair tile
-  const bool pair = g->M >= 256;
+  // N <= 32 (LoRA rank side): 128 x 32 single-CTA tiles, except few row tiles
+  // with a long K, where the pair kernel measured faster (dU = dY B, K = 24576)
+  const bool skinny = mode == 0 && g->N <= 32 && !(g->M / 128 < num_sms() && g->K > 8192);
+  const bool pair = g->M >= 256 && !skinny;
   CUtensorMap ta, tb;
   bool ok = g->a_mn_major ? make_map(&ta, g->A, g->K, g->M, g->lda, 64, 64)
                           : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
   ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
                             : make_map(&tb, g->B, dual ? 2LL * g->N : g->N, g->K, g->ldb, 64,
-                                       pair ? pair_tile_n(g->M, g->N) / 2 : BN));
+                                       pair ? pair_tile_n(g->M, g->N) / 2
+                                            : g->N <= 32 ? 32 : BN));  // = launch()'s tile
   // raster: keep the larger operand's tile hot (walk the other dimension fastest)
   const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
   if (!ok) return RP_E_CUDA;
@@ -994,9 +1064,19 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                           make_map_sw64(&em.u, R16 + g->N, g->M, g->N, g->ldr) &&
                           make_map_sw64(&em.dg, D16, g->M, g->N, g->ldd) &&
                           make_map_sw64(&em.du, D16 + g->N, g->M, g->N, g->ldd);
+  if (s2.K2 > 0) {  // second K segment: same majors and boxes as A / B
+    if (!pair) return RP_E_INPUT;
+    const bool ok2 =
+        (g->a_mn_major ? make_map(&em.a2, s2.A2, s2.K2, g->M, s2.lda2, 64, 64)
+                       : make_map(&em.a2, s2.A2, g->M, s2.K2, s2.lda2, 64, BM)) &&
+        (g->b_mn_major ? make_map(&em.b2, s2.B2, s2.K2, g->N, s2.ldb2, 64, 64)
+                       : make_map(&em.b2, s2.B2, dual ? 2LL * g->N : g->N, s2.K2, s2.ldb2, 64,
+                                  pair_tile_n(g->M, g->N) / 2));
+    if (!ok2) return RP_E_CUDA;
+  }
   Params p{g->M, g->N, g->K, g->D, g->ldd, R16, g->ldr, vec ? 1 : 0, tma_out ? 1 : 0,
-           tma_swiglu ? (getenv("RP_GEMM_NO_L2_PREFETCH") ? 2 : 1) : 0, 0, 0, nullptr, nullptr,
-           0, act, ld_act};
+           tma_swiglu ? (getenv("RP_GEMM_NO_L2_PREFETCH") ? 2 : 1) : 0, trans ? 1 : 0, 0, 0,
+           nullptr, nullptr, 0, act, ld_act, (s2.K2 + BK - 1) / BK};
   const int epi = dual ? EPI_SWIGLU_FWD : swiglu_bwd ? EPI_SWIGLU_BWD
                              : g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;
   if (g->out_f32 && g->R) return RP_E_INPUT;
@@ -1036,4 +1116,39 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_swiglu_bwd(const r
   if (!g || g->out_f32 || g->accumulate || !g->R || g->N % 8 || g->a_mn_major || !g->b_mn_major)
     return RP_E_INPUT;
   return gemm_entry(g, stream, 1);
+}
+
+// D = A B^T + A2 B2^T (+ R): a second K segment with the same majors, read by
+// the producer after A / B's k-blocks — the LoRA up-projection folded into the
+// base GEMM without materialising [X | U] or [W | B]. Pair tiles only (M >= 256).
+extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16_2seg(
+    const rp_gemm_args_t* g, const void* A2, int64_t lda2, const void* B2, int64_t ldb2,
+    int32_t K2, void* stream) {
+  if (!g || !A2 || !B2 || K2 <= 0 || (lda2 * 2) % 16 || (ldb2 * 2) % 16 ||
+      (reinterpret_cast<uintptr_t>(A2) & 15) || (reinterpret_cast<uintptr_t>(B2) & 15))
+    return RP_E_INPUT;
+  if (g->M < 256 || g->N <= 32) {  // below a pair tile: two GEMMs, the second adds into D
+    int rc = gemm_entry(g, stream, 0);
+    if (rc != RP_OK) return rc;
+    rp_gemm_args_t b = *g;
+    b.A = A2;
+    b.lda = lda2;
+    b.B = B2;
+    b.ldb = ldb2;
+    b.K = K2;
+    if (g->out_f32) {
+      b.accumulate = 1;
+    } else {
+      b.R = g->D;
+      b.ldr = g->ldd;
+    }
+    return gemm_entry(&b, stream, 0);
+  }
+  Seg2 s2;
+  s2.A2 = A2;
+  s2.lda2 = lda2;
+  s2.B2 = B2;
+  s2.ldb2 = ldb2;
+  s2.K2 = K2;
+  return gemm_entry(g, stream, 0, nullptr, 0, s2);
 }

@@ -293,27 +293,48 @@ struct Runtime {
   float lora_scale = 0.f;  // alpha / r
   bool trainable(int g) const { return host[g].tn() > 0; }
   // LoRA: Y += s (X A^T) B^T; keeps Us = s X A^T (T x r) for the backward
-  void lora_fwd(cudaStream_t st, const uint16_t* W, const Tensor& Ta, const Tensor& Tb,
-                const uint16_t* X, int64_t ldx, int in, uint16_t* Us, uint16_t* Y, int64_t ldy,
-                int out) {
+  // One linear layer's forward, Y = X W^T (+ R). LoRA: Us = s X A^T first, then
+  // Y = X W^T + Us B^T (+ R) as ONE GEMM with a second K segment (no rank-r
+  // update pass over Y).
+  void lin_fwd(cudaStream_t st, const uint16_t* W, const Tensor& Tw, const Tensor* Ta,
+               const Tensor* Tb, const uint16_t* X, int64_t ldx, int in, uint16_t* Us,
+               uint16_t* Y, int64_t ldy, int out, const void* R = nullptr, int64_t ldr = 0) {
+    if (!lora_r) {
+      gemm(st, X, ldx, false, W + Tw.off, in, false, Y, ldy, false, false, T, out, in, R, ldr);
+      return;
+    }
     const int r = lora_r;
-    gemm(st, X, ldx, false, W + Ta.off, in, false, Us, r, false, false, T, r, in);
+    gemm(st, X, ldx, false, W + Ta->off, in, false, Us, r, false, false, T, r, in);
     RP_K(rp_scale_bf16(Us, (int64_t)T * r, lora_scale, st));
-    gemm(st, Us, r, false, W + Tb.off, r, false, Y, ldy, false, false, T, out, r, Y, ldy);
+    gemm2(st, X, ldx, false, W + Tw.off, in, false, Y, ldy, T, out, in, R, ldr, Us, r,
+          W + Tb->off, r, r);
     kernels += 1;
   }
-  // LoRA backward of one linear (base dgrad dX already in place):
-  // dB += dY^T Us, dU = s dY B, dA += dU^T X, dX += dU A
-  void lora_bwd(Gpu& G, cudaStream_t st, const uint16_t* W, float* dW, const Tensor& Ta,
-                const Tensor& Tb, const uint16_t* X, int64_t ldx, int in, const uint16_t* Us,
-                const uint16_t* dY, int64_t ldy, int out, uint16_t* dX, int64_t lddx, bool first) {
+  // One linear layer's input gradient, dX = dY W. LoRA: dUs = s dY B first,
+  // then dX = dY W + dUs A as one two-segment GEMM; lora_wgrad() afterwards.
+  void lin_dgrad(Gpu& G, cudaStream_t st, const uint16_t* W, const Tensor& Tw, const Tensor* Ta,
+                 const Tensor* Tb, const uint16_t* dY, int64_t ldy, int out, uint16_t* dX,
+                 int64_t lddx, int in, bool swiglu_bwd = false, const void* gu = nullptr) {
+    if (!lora_r) {
+      gemm(st, dY, ldy, false, W + Tw.off, in, true, dX, lddx, false, false, T, in, out,
+           swiglu_bwd ? gu : nullptr, swiglu_bwd ? lddx : 0, swiglu_bwd);
+      return;
+    }
+    const int r = lora_r;
+    gemm(st, dY, ldy, false, W + Tb->off, r, true, G.du, r, false, false, T, r, out);
+    RP_K(rp_scale_bf16(G.du, (int64_t)T * r, lora_scale, st));
+    gemm2(st, dY, ldy, false, W + Tw.off, in, true, dX, lddx, T, in, out, nullptr, 0, G.du, r,
+          W + Ta->off, in, r);
+    kernels += 1;
+  }
+  // LoRA adapter gradients of one linear (after lin_dgrad): dB += dY^T Us,
+  // dA += dUs^T X
+  void lora_wgrad(Gpu& G, cudaStream_t st, float* dW, const Tensor& Ta, const Tensor& Tb,
+                  const uint16_t* X, int64_t ldx, int in, const uint16_t* Us, const uint16_t* dY,
+                  int64_t ldy, int out, bool first) {
     const int r = lora_r;
     gemm(st, dY, ldy, true, Us, r, true, dW + Tb.off, r, true, !first, out, r, T);
-    gemm(st, dY, ldy, false, W + Tb.off, r, true, G.du, r, false, false, T, r, out);
-    RP_K(rp_scale_bf16(G.du, (int64_t)T * r, lora_scale, st));
     gemm(st, G.du, r, true, X, ldx, true, dW + Ta.off, in, true, !first, r, in, T);
-    gemm(st, G.du, r, false, W + Ta.off, in, true, dX, lddx, false, false, T, in, r, dX, lddx);
-    kernels += 1;
   }
   // before the first grad write of an HBM-resident group g in an iteration:
   // AdamW of the previous iteration has consumed its single grad buffer (edge 4)
@@ -326,6 +347,9 @@ struct Runtime {
   void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
             bool b_mn, void* D, int64_t ldd, bool f32, bool acc, int M_, int N_, int K_,
             const void* Rz = nullptr, int64_t ldr = 0, bool swiglu_bwd = false);
+  void gemm2(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
+             bool b_mn, void* D, int64_t ldd, int M_, int N_, int K_, const void* Rz, int64_t ldr,
+             const void* A2, int64_t lda2, const void* B2, int64_t ldb2, int K2);
   ~Runtime();
 };
 
@@ -368,6 +392,30 @@ void Runtime::gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const
   const int pi = prof_begin(st);
   RP_K(swiglu_bwd ? rp_gemm_swiglu_bwd(&a, st) : rp_gemm_bf16(&a, st));
   prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)K_);
+  ++kernels;
+}
+
+void Runtime::gemm2(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B,
+                    int64_t ldb, bool b_mn, void* D, int64_t ldd, int M_, int N_, int K_,
+                    const void* Rz, int64_t ldr, const void* A2, int64_t lda2, const void* B2,
+                    int64_t ldb2, int K2) {
+  rp_gemm_args_t a{};
+  a.M = M_;
+  a.N = N_;
+  a.K = K_;
+  a.A = A;
+  a.lda = lda;
+  a.a_mn_major = a_mn;
+  a.B = B;
+  a.ldb = ldb;
+  a.b_mn_major = b_mn;
+  a.D = D;
+  a.ldd = ldd;
+  a.R = Rz;
+  a.ldr = ldr;
+  const int pi = prof_begin(st);
+  RP_K(rp_gemm_bf16_2seg(&a, A2, lda2, B2, ldb2, K2, st));
+  prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)(K_ + K2));
   ++kernels;
 }
 
@@ -928,8 +976,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     RP_K(rp_rmsnorm_fwd(x, h, W + LL.in_norm.off, A.h1, h, A.rstd1, T, h, (float)s.eps, st));
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
-  gemm(st, A.h1, h, false, W + LL.qkv.off, h, false, A.qkv, qkvd, false, false, T, qkvd, h);
-  if (lora_r) lora_fwd(st, W, LL.qkv_A, LL.qkv_B, A.h1, h, h, A.u_qkv, A.qkv, qkvd, qkvd);
+  lin_fwd(st, W, LL.qkv, &LL.qkv_A, &LL.qkv_B, A.h1, h, h, A.u_qkv, A.qkv, qkvd, qkvd);
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_qk_norm_rope_fwd(A.qkv, qkvd, s.nq, s.nk, s.hd, W + LL.q_norm.off, W + LL.k_norm.off,
@@ -943,8 +990,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
                    s.nk, s.hd, 1.0f / std::sqrt((float)s.hd), st));
     prof_end(pi_, st, 1, 2.0 * s.nq * s.hd * (double)T * cfg.seq_len);
   }
-  gemm(st, A.o, qd, false, W + LL.o.off, qd, false, A.x2, h, false, false, T, h, qd, x, h);
-  if (lora_r) lora_fwd(st, W, LL.o_A, LL.o_B, A.o, qd, qd, A.u_o, A.x2, h, h);
+  lin_fwd(st, W, LL.o, &LL.o_A, &LL.o_B, A.o, qd, qd, A.u_o, A.x2, h, h, x, h);
   {
     const int pi_ = prof_begin(st);
     RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
@@ -967,16 +1013,13 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     prof_end(pi_, st, 0, 2.0 * T * 2 * s.m * (double)h);
     ++kernels;
   } else {
-    gemm(st, A.h2, h, false, W + LL.gate_up.off, h, false, A.gu, 2 * s.m, false, false, T,
-         2 * s.m, h);
-    if (lora_r) lora_fwd(st, W, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, A.gu, 2 * s.m, 2 * s.m);
+    lin_fwd(st, W, LL.gate_up, &LL.gu_A, &LL.gu_B, A.h2, h, h, A.u_gu, A.gu, 2 * s.m, 2 * s.m);
     const int pi_ = prof_begin(st);
     RP_K(rp_swiglu_fwd(A.gu, A.act, T, s.m, st));
     prof_end(pi_, st, 2, 6.0 * T * s.m);
   }
-  gemm(st, A.act, s.m, false, W + LL.down.off, s.m, false, x_out, h, false, false, T, h, s.m,
-       A.x2, h);
-  if (lora_r) lora_fwd(st, W, LL.down_A, LL.down_B, A.act, s.m, s.m, A.u_down, x_out, h, h);
+  lin_fwd(st, W, LL.down, &LL.down_A, &LL.down_B, A.act, s.m, s.m, A.u_down, x_out, h, h, A.x2,
+          h);
   kernels += 5;
 }
 
@@ -1026,14 +1069,15 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
   const bool fuse = full && !unfused;
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[pg], 0));  // wgrad n_dgu layers ago read it
-  if (fuse)
+  if (fuse) {
     gemm(st, dx_a, h, false, W + LL.down.off, m, true, dgu, 2 * m, false, false, T, m, h, A.gu,
          2 * m, true);
-  else
+  } else if (full) {
     gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
-  if (!full)
-    lora_bwd(G, st, W, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, G.dact, m,
-             first);
+  } else {
+    lin_dgrad(G, st, W, LL.down, &LL.down_A, &LL.down_B, dx_a, h, h, G.dact, m, m);
+    lora_wgrad(G, st, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, first);
+  }
   RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], full ? ws : st));
   if (!fuse) {
     const int pi_ = prof_begin(st);
@@ -1044,10 +1088,12 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   if (full)
     gemm(ws, dgu, 2 * m, true, A.h2, h, true, dW + LL.gate_up.off, h, true, !first, 2 * m, h, T);
   RP_CUDA(cudaEventRecord(G.ev_dgu_free[pg], full ? ws : st));
-  gemm(st, dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
-  if (!full)
-    lora_bwd(G, st, W, dW, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, dgu, 2 * m, 2 * m, G.dh, h,
-             first);
+  if (full) {
+    gemm(st, dgu, 2 * m, false, W + LL.gate_up.off, h, true, G.dh, h, false, false, T, h, 2 * m);
+  } else {
+    lin_dgrad(G, st, W, LL.gate_up, &LL.gu_A, &LL.gu_B, dgu, 2 * m, 2 * m, G.dh, h, h);
+    lora_wgrad(G, st, dW, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, dgu, 2 * m, 2 * m, first);
+  }
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xb], 0));
   {
     const int pi_ = prof_begin(st);
@@ -1058,9 +1104,12 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   // attention:  x2 = x + attn(qkv(h1)) Wo^T
   to_ws();
   if (full) gemm(ws, dx_b, h, true, A.o, qd, true, dW + LL.o.off, qd, true, !first, h, qd, T);
-  gemm(st, dx_b, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
-  if (!full)
-    lora_bwd(G, st, W, dW, LL.o_A, LL.o_B, A.o, qd, qd, A.u_o, dx_b, h, h, G.dattn, qd, first);
+  if (full) {
+    gemm(st, dx_b, h, false, W + LL.o.off, qd, true, G.dattn, qd, false, false, T, qd, h);
+  } else {
+    lin_dgrad(G, st, W, LL.o, &LL.o_A, &LL.o_B, dx_b, h, h, G.dattn, qd, qd);
+    lora_wgrad(G, st, dW, LL.o_A, LL.o_B, A.o, qd, qd, A.u_o, dx_b, h, h, first);
+  }
   RP_CUDA(cudaEventRecord(G.ev_dx16_free[xb], full ? ws : st));
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dqkv_free[p], 0));
   {
@@ -1084,10 +1133,12 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   RP_CUDA(cudaEventRecord(G.ev_dqkv_free[p], ws));
   RP_CUDA(cudaEventRecord(A.ev_free, ws));  // act / h2 / o / h1 no longer needed
   RP_CUDA(cudaEventRecord(G.ev_wgrad, ws));
-  gemm(st, dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
-  if (!full)
-    lora_bwd(G, st, W, dW, LL.qkv_A, LL.qkv_B, A.h1, h, h, A.u_qkv, dqkv, qkvd, qkvd, G.dh, h,
-             first);
+  if (full) {
+    gemm(st, dqkv, qkvd, false, W + LL.qkv.off, h, true, G.dh, h, false, false, T, h, qkvd);
+  } else {
+    lin_dgrad(G, st, W, LL.qkv, &LL.qkv_A, &LL.qkv_B, dqkv, qkvd, qkvd, G.dh, h, h);
+    lora_wgrad(G, st, dW, LL.qkv_A, LL.qkv_B, A.h1, h, h, A.u_qkv, dqkv, qkvd, qkvd, first);
+  }
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xa], 0));  // wgrad(down) read dx_a
   {
     const int pi_ = prof_begin(st);

@@ -68,6 +68,23 @@ def gemm(A: torch.Tensor, B: torch.Tensor, D: torch.Tensor, *, a_mn_major=False,
     return D
 
 
+def gemm_2seg(A, B, A2, B2, D, *, b_mn_major=False, residual=None, stream=None):
+    """D = A[M,K] . op(B)^T + A2[M,K2] . op(B2)^T (+ residual): one GEMM with a second
+    K segment (A, A2 K-major; B [N,K] / B2 [N,K2], or [K,N] / [K2,N] when b_mn_major)."""
+    M, K = A.shape
+    M2, K2 = A2.shape
+    N = B.shape[1] if b_mn_major else B.shape[0]
+    assert M2 == M and tuple(D.shape) == (M, N)
+    args = GemmArgs(M, N, K, _ptr(A), A.stride(0), 0, _ptr(B), B.stride(0), int(b_mn_major),
+                    _ptr(D), D.stride(0), int(D.dtype == torch.float32), 0,
+                    _ptr(residual), residual.stride(0) if residual is not None else 0)
+    f = _lib().rp_gemm_bf16_2seg
+    f.restype = C.c_int
+    _check(f(C.byref(args), _ptr(A2), I64(A2.stride(0)), _ptr(B2), I64(B2.stride(0)), I32(K2),
+             _stream(stream)))
+    return D
+
+
 def gemm_swiglu_bwd(A: torch.Tensor, B: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor,
                     stream=None):
     """dgu = swiglu_bwd(dact = A[M,K] . B[K,N], gu) in one kernel (down-projection dgrad

@@ -19,7 +19,10 @@ def _mk(rows, cols, seed):
 
 
 SHAPES = [(128, 256, 64), (256, 512, 128), (384, 768, 1024), (200, 300, 320),
-          (4096, 1024, 4096), (1000, 2000, 192), (128, 16, 64), (640, 6144, 256)]
+          (4096, 1024, 4096), (1000, 2000, 192), (128, 16, 64), (640, 6144, 256),
+          # skinny (LoRA adapter) shapes: N <= 32 -> 128x32 tiles; M <= 32 -> swapped
+          # roles with a transposed store
+          (4096, 32, 1024), (32, 2048, 512), (200, 24, 320), (16, 296, 128), (2048, 32, 4096)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -163,3 +166,23 @@ def test_gemm_swiglu_fwd_epilogue(M, N, K):
     ref = X.float() @ Wgu.float().t()
     assert _rel(gu, ref) < 8e-3
     assert _rel(act, torch.nn.functional.silu(ref[:, :N]) * ref[:, N:]) < 2e-2
+
+
+@pytest.mark.parametrize("M,N,K,K2", [(512, 1024, 256, 32), (4096, 6144, 1024, 32),
+                                      (128, 256, 64, 32), (300, 1000, 192, 48)])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_gemm_second_k_segment(M, N, K, K2, b_mn):
+    """D = A B^T + A2 B2^T (+ R) in one GEMM (LoRA's base + adapter product); below
+    a pair tile the entry point runs two GEMMs, the second adding into D."""
+    from paper_2604_27085_b200 import kernels
+    if b_mn and N % 8:
+        pytest.skip("MN-major rows need 16-byte pitch")
+    A, B, A2, B2 = _mk(M, K, 51), _mk(N, K, 52), _mk(M, K2, 53), _mk(N, K2, 54)
+    R = _mk(M, N, 55)
+    Bop = B.t().contiguous() if b_mn else B
+    B2op = B2.t().contiguous() if b_mn else B2
+    D = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm_2seg(A, Bop, A2, B2op, D, b_mn_major=bool(b_mn), residual=R)
+    ref = A.float() @ B.float().t() + A2.float() @ B2.float().t() + R.float()
+    torch.cuda.synchronize()
+    assert _rel(D, ref) < 8e-3

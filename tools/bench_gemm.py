@@ -20,6 +20,12 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn, out_f32/acc)
     "down_wgrad": (4096, 12288, T, 1, 1, 1),
     "head_fwd_chunk": (1024, 151936, 4096, 0, 0, 0),
     "down_dgrad": (T, 12288, 4096, 0, 1, 0),
+    # LoRA r=32 adapter GEMMs (gate/up linear: in 4096, out 24576)
+    "lora_u": (T, 32, 4096, 0, 0, 0),          # U = X A^T
+    "lora_du": (T, 32, 24576, 0, 1, 0),        # dU = dY B
+    "lora_db": (24576, 32, T, 1, 1, 1),        # dB += dY^T U
+    "lora_da": (32, 4096, T, 1, 1, 1),         # dA += dU^T X
+    "lora_upd": (T, 24576, 32, 0, 0, 0),       # Y += U B^T (rank-r update)
 }
 
 

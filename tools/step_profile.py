@@ -29,10 +29,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--mode", default="async")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--lora-rank", type=int, default=0)
     a = ap.parse_args()
     import torch
     rt = RoundPipe(a.model, seq_len=a.seq, micro_batch=1, micro_batches=a.micro_batches,
-                   num_gpus=a.gpus, async_optimizer=a.mode == "async", adam=AdamW(lr=1e-5))
+                   num_gpus=a.gpus, async_optimizer=a.mode == "async", adam=AdamW(lr=1e-5),
+                   **({"lora_rank": a.lora_rank, "lora_alpha": 2.0 * a.lora_rank}
+                      if a.lora_rank else {}))
     V = {"qwen3-8b": 151936, "qwen3-1.7b": 151936, "tiny": 32768}[a.model]
     g = torch.Generator().manual_seed(1234)
     ids = torch.randint(0, V, (a.micro_batches, 1, a.seq + 1), generator=g)
