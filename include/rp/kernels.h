@@ -44,6 +44,13 @@ int rp_gemm_swiglu_bwd(const rp_gemm_args_t* args, void* stream);
  * (pitch ld_act). args->N is N (half of W_gu's rows); R unused. Equals
  * rp_gemm_bf16 into gu followed by rp_swiglu_fwd. N % 8 == 0. */
 int rp_gemm_swiglu_fwd(const rp_gemm_args_t* args, void* act, int64_t ld_act, void* stream);
+/* Every GEMM epilogue with an optional second K segment: epilogue 0 =
+ * rp_gemm_bf16, 1 = rp_gemm_swiglu_bwd, 2 = rp_gemm_swiglu_fwd (act, ld_act);
+ * K2 > 0 adds A2 . B2^T as rp_gemm_bf16_2seg does (for the SwiGLU epilogues
+ * M >= 256). LoRA runs its gate/up and down linears through this. */
+int rp_gemm_ex(const rp_gemm_args_t* args, int32_t epilogue, void* act, int64_t ld_act,
+               const void* A2, int64_t lda2, const void* B2, int64_t ldb2, int32_t K2,
+               void* stream);
 
 /* AdamW hyper-parameters (decoupled weight decay), fp32. */
 typedef struct {

@@ -1152,3 +1152,31 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16_2seg(
   s2.K2 = K2;
   return gemm_entry(g, stream, 0, nullptr, 0, s2);
 }
+
+// One entry for every epilogue with an optional second K segment:
+// epilogue 0 = rp_gemm_bf16, 1 = rp_gemm_swiglu_bwd, 2 = rp_gemm_swiglu_fwd
+// (act / ld_act); K2 > 0 adds A2 . B2^T as in rp_gemm_bf16_2seg. The fused
+// SwiGLU epilogues with a second segment need M >= 256 (pair tiles).
+extern "C" __attribute__((visibility("default"))) int rp_gemm_ex(
+    const rp_gemm_args_t* g, int32_t epilogue, void* act, int64_t ld_act, const void* A2,
+    int64_t lda2, const void* B2, int64_t ldb2, int32_t K2, void* stream) {
+  if (!g || epilogue < 0 || epilogue > 2) return RP_E_INPUT;
+  if (K2 <= 0) {
+    if (epilogue == 0) return rp_gemm_bf16(g, stream);
+    if (epilogue == 1) return rp_gemm_swiglu_bwd(g, stream);
+    return rp_gemm_swiglu_fwd(g, act, ld_act, stream);
+  }
+  if (epilogue == 0) return rp_gemm_bf16_2seg(g, A2, lda2, B2, ldb2, K2, stream);
+  if (g->M < 256 || !A2 || !B2 || (lda2 * 2) % 16 || (ldb2 * 2) % 16 || g->out_f32 ||
+      g->accumulate || g->N % 8)
+    return RP_E_INPUT;
+  if (epilogue == 1 && (!g->R || g->a_mn_major || !g->b_mn_major)) return RP_E_INPUT;
+  if (epilogue == 2 && (!act || g->R || g->a_mn_major || g->b_mn_major)) return RP_E_INPUT;
+  Seg2 s2;
+  s2.A2 = A2;
+  s2.lda2 = lda2;
+  s2.B2 = B2;
+  s2.ldb2 = ldb2;
+  s2.K2 = K2;
+  return gemm_entry(g, stream, epilogue, act, ld_act, s2);
+}

@@ -997,7 +997,25 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
   static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
-  if (!lora_r && !unfused) {  // SwiGLU in the gate/up GEMM's epilogue (gu kept for bwd)
+  if (lora_r && !unfused && T >= 256) {  // LoRA: Us first, then the dual GEMM with [X | Us]
+    const int r = lora_r;
+    gemm(st, A.h2, h, false, W + LL.gu_A.off, h, false, A.u_gu, r, false, false, T, r, h);
+    RP_K(rp_scale_bf16(A.u_gu, (int64_t)T * r, lora_scale, st));
+    rp_gemm_args_t a{};
+    a.M = T;
+    a.N = s.m;
+    a.K = h;
+    a.A = A.h2;
+    a.lda = h;
+    a.B = W + LL.gate_up.off;
+    a.ldb = h;
+    a.D = A.gu;
+    a.ldd = 2 * s.m;
+    const int pi_ = prof_begin(st);
+    RP_K(rp_gemm_ex(&a, 2, A.act, s.m, A.u_gu, r, W + LL.gu_B.off, r, r, st));
+    prof_end(pi_, st, 0, 2.0 * T * 2 * s.m * (double)(h + r));
+    kernels += 2;
+  } else if (!lora_r && !unfused) {  // SwiGLU in the gate/up GEMM's epilogue (gu kept for bwd)
     rp_gemm_args_t a{};
     a.M = T;
     a.N = s.m;
@@ -1068,18 +1086,41 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   // (dact never reaches HBM); LoRA adds the adapter term to dact first
   static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
   const bool fuse = full && !unfused;
+  const bool lora_fuse = !full && !unfused && T >= 256;
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[pg], 0));  // wgrad n_dgu layers ago read it
   if (fuse) {
     gemm(st, dx_a, h, false, W + LL.down.off, m, true, dgu, 2 * m, false, false, T, m, h, A.gu,
          2 * m, true);
   } else if (full) {
     gemm(st, dx_a, h, false, W + LL.down.off, m, true, G.dact, m, false, false, T, m, h);
+  } else if (lora_fuse) {  // dUs = s dY B, then dgu from [dY | dUs] [Wd ; A] in one GEMM
+    const int r = lora_r;
+    gemm(st, dx_a, h, false, W + LL.down_B.off, r, true, G.du, r, false, false, T, r, h);
+    RP_K(rp_scale_bf16(G.du, (int64_t)T * r, lora_scale, st));
+    rp_gemm_args_t a{};
+    a.M = T;
+    a.N = m;
+    a.K = h;
+    a.A = dx_a;
+    a.lda = h;
+    a.B = W + LL.down.off;
+    a.ldb = m;
+    a.b_mn_major = 1;
+    a.D = dgu;
+    a.ldd = 2 * m;
+    a.R = A.gu;
+    a.ldr = 2 * m;
+    const int pi_ = prof_begin(st);
+    RP_K(rp_gemm_ex(&a, 1, nullptr, 0, G.du, r, W + LL.down_A.off, m, r, st));
+    prof_end(pi_, st, 0, 2.0 * T * m * (double)(h + r));
+    kernels += 2;
+    lora_wgrad(G, st, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, first);
   } else {
     lin_dgrad(G, st, W, LL.down, &LL.down_A, &LL.down_B, dx_a, h, h, G.dact, m, m);
     lora_wgrad(G, st, dW, LL.down_A, LL.down_B, A.act, m, m, A.u_down, dx_a, h, h, first);
   }
   RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], full ? ws : st));
-  if (!fuse) {
+  if (!fuse && !lora_fuse) {
     const int pi_ = prof_begin(st);
     RP_K(rp_swiglu_bwd(G.dact, A.gu, dgu, T, m, st));
     prof_end(pi_, st, 2, 10.0 * T * m);
