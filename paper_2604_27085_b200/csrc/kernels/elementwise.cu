@@ -132,12 +132,17 @@ __global__ void __launch_bounds__(RN_THREADS)
   for (int row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1) {
     const long long off = (long long)row * h;
     uint4 av[VPT], bv[VPT];
+    float4 rv[VPT][2];  // the residual gradient, loaded with dy / x (not after the reduction)
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
       const int c = (threadIdx.x + j * RN_THREADS) * 8;
       if (c < h) {
         av[j] = *reinterpret_cast<const uint4*>(dy + off + c);
         bv[j] = *reinterpret_cast<const uint4*>(x + off + c);
+        if (dres) {
+          rv[j][0] = *reinterpret_cast<const float4*>(dres + off + c);
+          rv[j][1] = *reinterpret_cast<const float4*>(dres + off + c + 4);
+        }
       } else {
         av[j] = bv[j] = make_uint4(0, 0, 0, 0);
       }
@@ -175,8 +180,7 @@ __global__ void __launch_bounds__(RN_THREADS)
         dwa[j][i] += a[i] * xh;
       }
       if (dres) {
-        const float4 d0 = *reinterpret_cast<const float4*>(dres + off + c);
-        const float4 d1 = *reinterpret_cast<const float4*>(dres + off + c + 4);
+        const float4 d0 = rv[j][0], d1 = rv[j][1];
         o[0] += d0.x; o[1] += d0.y; o[2] += d0.z; o[3] += d0.w;
         o[4] += d1.x; o[5] += d1.y; o[6] += d1.z; o[7] += d1.w;
       }
@@ -624,9 +628,23 @@ RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const fl
                               (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
                               dw, rows, h);
   };
-  rn_dispatch(h, go, rmsnorm_bwd_kernel<128, 1>, rmsnorm_bwd_kernel<128, 2>,
-              rmsnorm_bwd_kernel<128, 3>, rmsnorm_bwd_kernel<128, 4>,
-              rmsnorm_bwd_kernel<256, 3>, rmsnorm_bwd_kernel<256, 4>);
+  // 256 threads above h = 1024: the row's dy / x / dres and the dw partials
+  // live in registers, so fewer columns per thread keep occupancy up
+  static const bool narrow = getenv("RP_RMSNORM_BWD_128") != nullptr;  // A/B knob
+  if (narrow)
+    rn_dispatch(h, go, rmsnorm_bwd_kernel<128, 1>, rmsnorm_bwd_kernel<128, 2>,
+                rmsnorm_bwd_kernel<128, 3>, rmsnorm_bwd_kernel<128, 4>,
+                rmsnorm_bwd_kernel<256, 3>, rmsnorm_bwd_kernel<256, 4>);
+  else if (h <= 1024)
+    go(rmsnorm_bwd_kernel<128, 1>, 128);
+  else if (h <= 2048)
+    go(rmsnorm_bwd_kernel<256, 1>, 256);
+  else if (h <= 4096)
+    go(rmsnorm_bwd_kernel<256, 2>, 256);
+  else if (h <= 6144)
+    go(rmsnorm_bwd_kernel<256, 3>, 256);
+  else
+    go(rmsnorm_bwd_kernel<256, 4>, 256);
   return status();
 }
 
