@@ -371,6 +371,11 @@ def run_ours(args):
                             "note": "fp32 AdamW state of the largest groups that fit in free HBM "
                                     "stays resident (single device); the rest streams from "
                                     "pinned host memory every step"},
+        # the runtime's device allocations by category (all workers), GB
+        "hbm_gb": {k: round(v / 1e9, 2) for k, v in zip(
+            ("weights_2_versions", "grads", "pending_adamw_out", "activations",
+             "scratch", "resident_optimizer_state", "optimizer_chunk_ring"),
+            st1["device_bytes"][:7])},
     }
     if not args.no_cpu_baseline:
         try:
