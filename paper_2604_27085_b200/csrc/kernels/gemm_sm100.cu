@@ -71,6 +71,7 @@ struct Params {
   void* D2;                // EPI_SWIGLU_FWD: act [M, N] bf16, pitch ldd2
   long long ldd2;
   int kb2;                 // k-blocks of the second K segment (0: none)
+  int nsplit;              // units beyond `full` are N halves (256 x PBN/2) instead of K halves
 };
 
 // TMA maps of the SwiGLU-backward epilogue: g / u halves of gu and dg / du
@@ -78,6 +79,7 @@ struct Params {
 struct EpiMaps {
   CUtensorMap g, u, dg, du;
   CUtensorMap a2, b2;  // second K segment (pair kernel): D = A B^T + A2 B2^T
+  CUtensorMap bh;      // K-major B with PBN/4-row boxes: N-half units of the last wave
 };
 
 // Store one 32-column TMEM chunk of a tile row (bf16 [+ residual] / fp32 [+=]).
@@ -465,10 +467,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     m0 = mt * 256;
     n0 = nt * TN;
   };
-  // work unit -> (tile, k-block range, K half: -1 whole, 0 first, 1 second)
+  // work unit -> (tile, k-block range, K half: -1 whole, 0 first, 1 second,
+  // N half: -1 whole, 0 / 1 = columns [0, PBN/2) / [PBN/2, PBN) of the tile).
+  // The last partial wave is split in two along K (long K) or along N.
+  int nh_ = -1;
   auto unit_info = [&](int u, int& tile, int& kb0, int& kb1, int& khalf) {
+    nh_ = -1;
     if (u < p.full) {
       tile = u, kb0 = 0, kb1 = k_blocks, khalf = -1;
+    } else if (p.nsplit) {
+      tile = p.full + ((u - p.full) >> 1);
+      nh_ = (u - p.full) & 1;
+      kb0 = 0, kb1 = k_blocks, khalf = -1;
     } else {
       const int mid = k_blocks / 2;
       tile = p.full + ((u - p.full) >> 1);
@@ -512,12 +522,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int tile, kb0, kb1, khalf, m0, n0;
       unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
-      const int am = m0 + 128 * rank, bn = DUAL ? n0 + (int)rank * p.N : n0 + (PBN / 2) * rank;
+      const bool half = nh_ >= 0;  // N-half unit: each CTA loads PBN/4 rows of B
+      if (half) n0 += nh_ * (PBN / 2);
+      const int am = m0 + 128 * rank;
+      const int bn = DUAL ? n0 + (int)rank * p.N : n0 + (half ? PBN / 4 : PBN / 2) * rank;
+      const uint32_t stage_tx = half ? Cfg::STAGE - Cfg::B_BYTES / 2 : Cfg::STAGE;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * Cfg::STAGE;
         uint8_t* sb = sa + P_A_BYTES;
-        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE);
+        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_tx);
         const bool seg2 = kb >= kb_main;  // LoRA: [X | U] . [W | B]^T without a concat
         const int k0 = (seg2 ? kb - kb_main : kb) * BK;
         const CUtensorMap* ma = seg2 ? &em.a2 : &tma_a;
@@ -530,16 +544,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         if (B_MN) {
           tma_load_2d_pair(sb, mb, &full[stage], bn, k0);
-          if (PBN == 256) tma_load_2d_pair(sb + 8192, mb, &full[stage], bn + 64, k0);
+          if (PBN == 256 && !half) tma_load_2d_pair(sb + 8192, mb, &full[stage], bn + 64, k0);
         } else {
-          tma_load_2d_pair(sb, mb, &full[stage], k0, bn);
+          tma_load_2d_pair(sb, half ? &em.bh : mb, &full[stage], k0, bn);
         }
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1 && lane == 0 && leader) {
     // ---------------- MMA issuer (leader only) ----------------
-    constexpr uint32_t idesc = umma_idesc_bf16(256, PBN, A_MN, B_MN);
+    constexpr uint32_t idesc_full = umma_idesc_bf16(256, PBN, A_MN, B_MN);
+    constexpr uint32_t idesc_half = umma_idesc_bf16(256, PBN / 2, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -547,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int u = pair; u < p.units; u += npairs) {
       int tile, kb0, kb1, khalf;
       unit_info(u, tile, kb0, kb1, khalf);
+      const uint32_t idesc = nh_ >= 0 ? idesc_half : idesc_full;
       mbar_wait(&acc_empty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * PBN;
@@ -596,6 +612,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int tile, kb0, kb1, khalf, m0, n0;
       unit_info(u, tile, kb0, kb1, khalf);
       tile_mn(tile, m0, n0);
+      const int cw = nh_ >= 0 ? PBN / 2 : PBN;  // accumulator columns of this unit
+      if (nh_ >= 0) n0 += nh_ * (PBN / 2);
       const bool sw_tma = EPI == EPI_SWIGLU_BWD && p.tma_swiglu && khalf != 0 &&
                           m0 + 128 * (int)rank + q * 32 < p.M;
       if (sw_tma) {  // needs no accumulator: start before the mainloop finishes
@@ -741,7 +759,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint8_t* wbuf = epi_smem + q * (2 * 4096);
         // chunks wholly outside D are skipped (warp-uniform), so every written
         // buffer belongs to a committed store and "two chunks ago" holds
-        const int c_end = min(PBN, p.N - n0);
+        const int c_end = min(cw, p.N - n0);
 #pragma unroll 1
         for (int c = 0; c < c_end && row0 < p.M; c += 32) {
           uint32_t v[32];
@@ -764,7 +782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < PBN; c += 32) {
+        for (int c = 0; c < cw; c += 32) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + acc * PBN + c, v);
           tmem_ld_wait();
@@ -913,6 +931,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
                    cudaStream_t stream) {
   if (pair) {
     const bool narrow = pair_tile_n(p.M, p.N) == 128;
+    const bool PBN_OK = !narrow;  // N halves of 256-wide tiles (em.bh built for K-major B)
     auto kern = narrow ? gemm_pair_kernel<A_MN, B_MN, EPI, 128> : gemm_pair_kernel<A_MN, B_MN, EPI, 256>;
     const int smem = narrow ? PairCfg<128>::SMEM : PairCfg<256>::SMEM;
     static bool configured[2] = {false, false};
@@ -934,7 +953,15 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     // costs about what the shorter wave saves
     const int full = (tiles / npairs) * npairs, tail = tiles - full;
     static const bool no_split = getenv("RP_GEMM_NO_SPLITK") != nullptr;
-    if (!no_split && EPI != EPI_SWIGLU_BWD && EPI != EPI_SWIGLU_FWD && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
+    static const bool no_nsplit = getenv("RP_GEMM_NO_NSPLIT") != nullptr;
+    // a short last wave at moderate K: its tiles become two 256 x PBN/2 halves
+    // (no partials to reduce, unlike the K split); plain epilogues only
+    if (!no_nsplit && (EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_F32_ACC) && PBN_OK &&
+        q.kb2 == 0 && tail > 0 && 2 * tail <= npairs && p.K < 8192) {
+      q.full = full;
+      q.units = full + 2 * tail;
+      q.nsplit = 1;
+    } else if (!no_split && EPI != EPI_SWIGLU_BWD && EPI != EPI_SWIGLU_FWD && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
       SplitWs& w = split_ws(stream, (std::size_t)tail * 2 * 128 * pbn, (std::size_t)tail * 8);
       if (w.ws) {
         q.full = full;
@@ -1064,6 +1091,9 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                           make_map_sw64(&em.u, R16 + g->N, g->M, g->N, g->ldr) &&
                           make_map_sw64(&em.dg, D16, g->M, g->N, g->ldd) &&
                           make_map_sw64(&em.du, D16 + g->N, g->M, g->N, g->ldd);
+  if (pair && !g->b_mn_major && !dual &&
+      !make_map(&em.bh, g->B, g->N, g->K, g->ldb, 64, pair_tile_n(g->M, g->N) / 4))
+    return RP_E_CUDA;
   if (s2.K2 > 0) {  // second K segment: same majors and boxes as A / B
     if (!pair) return RP_E_INPUT;
     const bool ok2 =

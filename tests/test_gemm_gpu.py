@@ -22,7 +22,9 @@ SHAPES = [(128, 256, 64), (256, 512, 128), (384, 768, 1024), (200, 300, 320),
           (4096, 1024, 4096), (1000, 2000, 192), (128, 16, 64), (640, 6144, 256),
           # skinny (LoRA adapter) shapes: N <= 32 -> 128x32 tiles; M <= 32 -> swapped
           # roles with a transposed store
-          (4096, 32, 1024), (32, 2048, 512), (200, 24, 320), (16, 296, 128), (2048, 32, 4096)]
+          (4096, 32, 1024), (32, 2048, 512), (200, 24, 320), (16, 296, 128), (2048, 32, 4096),
+          # short last wave split into 256 x 128 N-halves (256 and 384 tiles on 74 pairs)
+          (4096, 4096, 512), (4096, 6144, 256), (4000, 4000, 320)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
