@@ -566,7 +566,13 @@ __device__ __forceinline__ void bulk_wait_done_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-template <int HD>
+// GQA reduction of dK/dV over the G/2 head pairs of a KV group (CL):
+//   0: fp32 atomics into dk_acc / dv_acc (+ a cast kernel), any G
+//   1: G = 2, one CTA per group: bf16 straight from TMEM into dk / dv
+//   2: G = 4, the two CTAs of a group form a cluster: rank 1 ships its fp32
+//      dK/dV rows into rank 0's (then idle) shared memory over DSMEM, rank 0
+//      adds them to its own and writes bf16 — no atomics, memset or cast
+template <int HD, int CL>
 __global__ void __launch_bounds__(A2_THREADS, 1)
     attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v,
@@ -574,8 +580,9 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
                           const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_dq,
                           const float* __restrict__ lse, const float* __restrict__ delta,
-                          float* __restrict__ dk_acc, float* __restrict__ dv_acc, int T, int seq,
-                          int nq, int nk, float scale) {
+                          float* __restrict__ dk_acc, float* __restrict__ dv_acc,
+                          bf16* __restrict__ dk, long long lddk, bf16* __restrict__ dv,
+                          long long lddv, int T, int seq, int nq, int nk, float scale) {
   using L = Dkv4Smem<HD>;
   constexpr int NSUB = L::NSUB;
   constexpr int NS = A4_NST;
@@ -823,23 +830,93 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_done_all();
-    // epilogue: warpgroup a -> dK (scaled), warpgroup b -> dV; fp32 atomics
-    // reduce the G/2 head pairs of the KV group
+    // epilogue: warpgroup a -> dK (scaled), warpgroup b -> dV
     mbar_wait(acc_done, 0);
     tc_fence_after();
-    float* dst_acc = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
-    const uint32_t col = w == 0 ? TM_DK : TM_DV;
-    const float f = w == 0 ? scale : 1.f;
+    if (CL == 0) {  // fp32 atomics reduce the G/2 head pairs of the KV group
+      float* dst_acc = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
+      const uint32_t col = w == 0 ? TM_DK : TM_DV;
+      const float f = w == 0 ? scale : 1.f;
 #pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t a[32];
-      tmem_ld_32x32b_x32(lane_base + col + c, a);
-      tmem_ld_wait();
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t a[32];
+        tmem_ld_32x32b_x32(lane_base + col + c, a);
+        tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        atomicAdd(reinterpret_cast<float4*>(dst_acc + c + i),
-                  make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
-                              __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
+        for (int i = 0; i < 32; i += 4)
+          atomicAdd(reinterpret_cast<float4*>(dst_acc + c + i),
+                    make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
+                                __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (CL >= 1) {
+    // dK / dV rows of this key block: thread = key row, HD fp32 per row; the
+    // partner's rows arrive in this CTA's ring + dS^T region (2 x 128 x HD fp32,
+    // 16-byte chunks XOR-swizzled by row so 32 rows hit 32 different banks)
+    uint32_t rank = 0;
+    if (CL == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int w = (warp - 4) >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int key = k0 + r;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    const uint32_t col = w == 0 ? TM_DK : TM_DV;
+    constexpr int CH = HD / 4;  // 16-byte chunks per row
+    float* xbuf = reinterpret_cast<float*>(sm + L::R0) + (size_t)w * A_BK * HD + (size_t)r * HD;
+    auto chunk = [&](int c4) { return ((c4 ^ (r & (CH - 1))) * 4); };
+    if (CL == 2) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                       : "memory");  // rank 0's ring / dS^T shared memory is free
+      if (rank == 1 && warp >= 4) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(xbuf)));
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t a[32];
+          tmem_ld_32x32b_x32(lane_base + col + c, a);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             remote + chunk((c + i) / 4) * 4),
+                         "f"(__uint_as_float(a[i])), "f"(__uint_as_float(a[i + 1])),
+                         "f"(__uint_as_float(a[i + 2])), "f"(__uint_as_float(a[i + 3]))
+                         : "memory");
+        }
+      }
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                       : "memory");
+    }
+    if (warp >= 4 && rank == 0) {
+      bf16* dst = (w == 0 ? dk + (long long)key * lddk : dv + (long long)key * lddv) +
+                  (long long)kvh * HD;
+      const float f = w == 0 ? scale : 1.f;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t a[32];
+        tmem_ld_32x32b_x32(lane_base + col + c, a);
+        tmem_ld_wait();
+        float o[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = __uint_as_float(a[i]);
+        if (CL == 2) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = *reinterpret_cast<const float4*>(xbuf + chunk((c + i) / 4));
+            o[i] += b.x;
+            o[i + 1] += b.y;
+            o[i + 2] += b.z;
+            o[i + 3] += b.w;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+          *reinterpret_cast<uint4*>(dst + c + i) =
+              make_uint4(pack_bf16x2(o[i] * f, o[i + 1] * f), pack_bf16x2(o[i + 2] * f, o[i + 3] * f),
+                         pack_bf16x2(o[i + 4] * f, o[i + 5] * f), pack_bf16x2(o[i + 6] * f, o[i + 7] * f));
+      }
     }
   }
   tc_fence_before();
@@ -1862,7 +1939,6 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
     cfg = true;
   }
   const long long acc_n = (long long)T * nk * HD;
-  if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
   static const bool v1 = getenv("RP_ATTN_BWD_V1") != nullptr;
   // opt-in: K/V-in-TMEM variant with 32-query tiles — correct, but measured
   // 2 % slower than the 64-query ping-pong kernel below (0.596 vs 0.586 ms)
@@ -1878,20 +1954,46 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
     if (!dq_acc || !map_f32(&mdq, dq_acc, (long long)nq * HD, T, T))  // d-major [nq*HD, T]
       return RP_E_CUDA;
     if (cudaMemsetAsync(dq_acc, 0, sizeof(float) * qn, s) != cudaSuccess) return RP_E_CUDA;
-    static bool cfg6 = false;
-    if (!cfg6) {
-      if (!set_smem(attn_bwd_fused_kernel<HD>, Dkv4Smem<HD>::BYTES)) return RP_E_CUDA;
-      cfg6 = true;
-    }
-    attn_bwd_fused_kernel<HD><<<dim3(nq / 2, T / A_BK), A2_THREADS, Dkv4Smem<HD>::BYTES, s>>>(
-        mk128, mv128, mq64, mdo64, mdq, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk,
-        scale);
-    dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
-                                            lddv, T, nk * HD);
+    static const bool atomics = getenv("RP_ATTN_DKV_ATOMICS") != nullptr;  // A/B knob
+    const int G = nq / nk;
+    const int cl = atomics ? 0 : G == 2 ? 1 : G == 4 ? 2 : 0;
+    static bool smem_set[3] = {false, false, false};  // per CL variant (same pointer type)
+    auto go = [&](auto kern, int cluster) -> cudaError_t {
+      if (!smem_set[cl]) {
+        if (!set_smem(kern, Dkv4Smem<HD>::BYTES)) return cudaErrorInvalidValue;
+        smem_set[cl] = true;
+      }
+      cudaLaunchConfig_t c = {};
+      c.gridDim = dim3(nq / 2, T / A_BK, 1);
+      c.blockDim = dim3(A2_THREADS, 1, 1);
+      c.dynamicSmemBytes = Dkv4Smem<HD>::BYTES;
+      c.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      c.attrs = at;
+      c.numAttrs = 1;
+      return cudaLaunchKernelEx(&c, kern, mk128, mv128, mq64, mdo64, mdq, lse, (const float*)delta,
+                                dkv_acc, dkv_acc + acc_n, (bf16*)dk, (long long)lddk, (bf16*)dv,
+                                (long long)lddv, T, seq, nq, nk, scale);
+    };
+    if (cl == 0 &&
+        cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess)
+      return RP_E_CUDA;
+    cudaError_t e = cl == 2   ? go(attn_bwd_fused_kernel<HD, 2>, 2)
+                    : cl == 1 ? go(attn_bwd_fused_kernel<HD, 1>, 1)
+                              : go(attn_bwd_fused_kernel<HD, 0>, 1);
+    if (e != cudaSuccess) return RP_E_CUDA;
+    if (cl == 0)
+      dkv_cast_kernel<<<148 * 8, 256, 0, s>>>(dkv_acc, dkv_acc + acc_n, (bf16*)dk, lddk, (bf16*)dv,
+                                              lddv, T, nk * HD);
     dq_cast_kernel<<<dim3(T / 32, nq * HD / 32), dim3(32, 8), 0, s>>>(dq_acc, (bf16*)dq, lddq, T,
                                                                       nq * HD, scale);
     return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
   }
+  if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
   if ((nq / nk) % 2 == 0 && !v1 && dkv3) {  // K/V in TMEM, two heads, 32-query tiles
     CUtensorMap mq32, mdo32;
     if (!map2d(&mq32, q, T, (long long)nq * HD, ldq, A3_BQ) ||
