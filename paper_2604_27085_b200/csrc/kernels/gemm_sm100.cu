@@ -88,8 +88,9 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
                                           const uint32_t (&v)[32]) {
         const int col0 = col0_;
         if (p.trans) {  // D^T of a swapped skinny GEMM: per column, the warp's 32 rows are contiguous
-          if (row_ok)
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+          if (row_ok) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) if (col0 + i < p.N) {
               const long long o = (long long)(col0 + i) * p.ldd + row;
               const float f = __uint_as_float(v[i]);
               if (EPI == EPI_BF16) {
@@ -99,6 +100,7 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
                 *d = (EPI == EPI_F32_ACC ? *d : 0.f) + f;
               }
             }
+          }
           return;
         }
         if (row_ok && col0 < p.N) {
@@ -133,7 +135,8 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
                              pack_bf16x2(ou[4], ou[5]), pack_bf16x2(ou[6], ou[7]));
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) if (col0 + i < p.N) {
               float og, ou;
               one(__uint_as_float(v[i]), __bfloat162float(gr[i]), __bfloat162float(ur[i]), og, ou);
               dg[i] = __float2bfloat16_rn(og);
@@ -156,7 +159,8 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
                 for (int j = 0; j < 8; ++j) f[i + j] += __bfloat162float(rb[j]);
               }
             } else {
-              for (int i = 0; i < 32 && col0 + i < p.N; ++i) f[i] += __bfloat162float(r[i]);
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) if (col0 + i < p.N) f[i] += __bfloat162float(r[i]);
             }
           }
           if (full_chunk) {
@@ -170,7 +174,8 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
               *reinterpret_cast<uint4*>(d + i) = o;
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) d[i] = __float2bfloat16_rn(f[i]);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) if (col0 + i < p.N) d[i] = __float2bfloat16_rn(f[i]);
           }
         } else {
           float* d = reinterpret_cast<float*>(p.D) + (long long)row * p.ldd + col0;
@@ -186,7 +191,8 @@ __device__ __forceinline__ void epi_chunk(const Params& p, int row, bool row_ok,
               *reinterpret_cast<float4*>(d + i) = o;
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+#pragma unroll
+            for (int i = 0; i < 32; ++i) if (col0 + i < p.N)
               d[i] = (EPI == EPI_F32_ACC ? d[i] : 0.f) + __uint_as_float(v[i]);
           }
         }
@@ -534,19 +540,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * stage_tx);
         const bool seg2 = kb >= kb_main;  // LoRA: [X | U] . [W | B]^T without a concat
         const int k0 = (seg2 ? kb - kb_main : kb) * BK;
-        const CUtensorMap* ma = seg2 ? &em.a2 : &tma_a;
-        const CUtensorMap* mb = seg2 ? &em.b2 : &tma_b;
-        if (A_MN) {
-          tma_load_2d_pair(sa, ma, &full[stage], am, k0);
-          tma_load_2d_pair(sa + 8192, ma, &full[stage], am + 64, k0);
+        // every TMA names its tensor map directly: selecting between
+        // __grid_constant__ maps through a pointer makes the compiler copy
+        // them to the stack (measured: gate/up fwd 92.6 -> 83.7 % tensor-active)
+        auto load_a = [&](const CUtensorMap* m) {
+          if (A_MN) {
+            tma_load_2d_pair(sa, m, &full[stage], am, k0);
+            tma_load_2d_pair(sa + 8192, m, &full[stage], am + 64, k0);
+          } else {
+            tma_load_2d_pair(sa, m, &full[stage], k0, am);
+          }
+        };
+        auto load_b = [&](const CUtensorMap* m) {
+          if (B_MN) {
+            tma_load_2d_pair(sb, m, &full[stage], bn, k0);
+            if (PBN == 256 && !half) tma_load_2d_pair(sb + 8192, m, &full[stage], bn + 64, k0);
+          } else {
+            tma_load_2d_pair(sb, m, &full[stage], k0, bn);
+          }
+        };
+        if (!seg2) {
+          load_a(&tma_a);
+          if (B_MN || !half) load_b(&tma_b);
+          else load_b(&em.bh);
         } else {
-          tma_load_2d_pair(sa, ma, &full[stage], k0, am);
-        }
-        if (B_MN) {
-          tma_load_2d_pair(sb, mb, &full[stage], bn, k0);
-          if (PBN == 256 && !half) tma_load_2d_pair(sb + 8192, mb, &full[stage], bn + 64, k0);
-        } else {
-          tma_load_2d_pair(sb, half ? &em.bh : mb, &full[stage], k0, bn);
+          load_a(&em.a2);
+          load_b(&em.b2);
         }
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
@@ -743,7 +762,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 *reinterpret_cast<uint4*>(da + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
               }
             } else {
-              for (int i = 0; i < 32 && n0 + c + i < p.N; ++i) {
+  #pragma unroll
+              for (int i = 0; i < 32; ++i) if (n0 + c + i < p.N) {
                 const __nv_bfloat16 g = __float2bfloat16_rn(__uint_as_float(vg[i]));
                 const __nv_bfloat16 u = __float2bfloat16_rn(__uint_as_float(vu[i]));
                 dg[i] = g;
