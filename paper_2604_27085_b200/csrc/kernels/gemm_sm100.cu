@@ -355,12 +355,16 @@ constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB (this CTA's 128 rows of A)
 // fp32 epilogue staging for TMA store / reduce-add: per epilogue warp two
 // 32 x 32 fp32 chunks (SWIZZLE_128B rows of 128 B)
 constexpr int P_EPI_BYTES = 4 * 2 * 32 * 32 * 4;  // 32 KB
-template <int PBN>
+template <int PBN, int EPI_>
 struct PairCfg {
+  // epilogues that store straight from registers (bf16, dual SwiGLU) need no
+  // staging buffer: its 32 KB becomes one more operand stage
+  static constexpr bool STAGED = EPI_ != 0 && EPI_ != 4;
   static constexpr int B_BYTES = (PBN / 2) * BK * 2;       // this CTA's half of B
   static constexpr int STAGE = P_A_BYTES + B_BYTES;
-  static constexpr int STAGES = PBN == 256 ? 6 : 8;
-  static constexpr int SMEM = STAGES * STAGE + P_EPI_BYTES + 1024 + 256;
+  static constexpr int EPI_BYTES = STAGED ? P_EPI_BYTES : 0;
+  static constexpr int STAGES = (PBN == 256 ? 6 : 8) + (STAGED ? 0 : (PBN == 256 ? 1 : 1));
+  static constexpr int SMEM = STAGES * STAGE + EPI_BYTES + 1024 + 256;
   static_assert(SMEM <= 232448, "pair GEMM shared memory");
 };
 
@@ -445,12 +449,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                      const __grid_constant__ CUtensorMap tma_b,
                      const __grid_constant__ CUtensorMap tma_d,
                      const __grid_constant__ EpiMaps em, Params p, int n_fastest) {
-  using Cfg = PairCfg<PBN>;
+  using Cfg = PairCfg<PBN, EPI>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_smem = smem + Cfg::STAGES * Cfg::STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + P_EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::EPI_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* acc_full = empty + Cfg::STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;     // [2] (leader's copy is the one used)
@@ -953,7 +957,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     const bool narrow = pair_tile_n(p.M, p.N) == 128;
     const bool PBN_OK = !narrow;  // N halves of 256-wide tiles (em.bh built for K-major B)
     auto kern = narrow ? gemm_pair_kernel<A_MN, B_MN, EPI, 128> : gemm_pair_kernel<A_MN, B_MN, EPI, 256>;
-    const int smem = narrow ? PairCfg<128>::SMEM : PairCfg<256>::SMEM;
+    const int smem = narrow ? PairCfg<128, EPI>::SMEM : PairCfg<256, EPI>::SMEM;
     static bool configured[2] = {false, false};
     if (!configured[narrow]) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
