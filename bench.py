@@ -245,7 +245,8 @@ def run_ours(args):
     t_setup = time.time()
     rt = RoundPipe(args.model, seq_len=args.seq, micro_batch=1, micro_batches=args.micro_batches,
                    num_gpus=args.gpus, async_optimizer=args.mode == "async", adam=AdamW(lr=1e-5),
-                   record_timeline=True, lora_rank=args.lora_rank, lora_alpha=args.lora_alpha)
+                   record_timeline=True, lora_rank=args.lora_rank, lora_alpha=args.lora_alpha,
+                   resident_state_gb=0.0 if args.host_optimizer else -1.0)
     setup_s = time.time() - t_setup
     d = MODEL_DIMS[args.model]
     g = torch.Generator().manual_seed(1234)
@@ -412,8 +413,6 @@ def main():
                          "(no HBM-resident groups): the strict host-offloaded configuration")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    if args.host_optimizer:
-        os.environ["RP_RESIDENT_GB"] = "0"  # read by the runtime at construction
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:

@@ -105,37 +105,27 @@ int rp_scale_bf16(void* a, int64_t n, float f, void* stream);
 int rp_init_normal(float* f32, void* b16, int64_t n, uint64_t seed, float std, void* stream);
 int rp_fill(float* f32, void* b16, int64_t n, float value, void* stream);
 
-/* Causal GQA flash attention, head_dim 64 or 128, bf16 in/out.
+/* Causal GQA flash attention forward on the 5th-gen tensor cores (tcgen05 +
+ * TMEM + TMA), head_dim 64 or 128, bf16 in/out.
  * q [T, nq, hd] (row pitch ldq), k/v [T, nk, hd] (pitch ldk/ldv), o [T, nq, hd];
  * lse [nq, T] fp32 (natural log). Sequences are packed: T = batch * seq and
- * attention never crosses a seq boundary. */
-int rp_attn_fwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
-                int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
-                int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
-/* Same contract, on the 5th-gen tensor cores (tcgen05 + TMEM + TMA); needs
- * 16-byte aligned base pointers and pitches. */
+ * attention never crosses a seq boundary. 16-byte aligned base pointers and
+ * pitches. */
 int rp_attn_fwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, void* o, int64_t ldo, float* lse, int32_t T, int32_t seq,
                    int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
-/* Backward on the 5th-gen tensor cores. head_dim 128, even GQA groups: one
- * key-major kernel per (key block, query-head pair) forms dK, dV and dQ
- * (dQ^T = K^T dS^T reduce-added into an internal fp32 accumulator in L2).
- * Otherwise (or RP_ATTN_SPLIT=1): a dK/dV kernel plus a query-major dQ
- * kernel that recomputes S and dP. GQA partials of dK/dV are summed in fp32.
- * Workspaces: delta fp32 [nq, T]; dkv_acc fp32 [2, T, nk*head_dim].
- * Layouts as rp_attn_bwd. */
+/* Backward on the 5th-gen tensor cores; dq/dk/dv bf16 with the layouts of
+ * q/k/v (own pitches). head_dim 128 with an even GQA group: one key-major
+ * kernel per (key block, query-head pair) forms dK, dV and dQ (dQ^T = K^T
+ * dS^T reduce-added into a per-stream fp32 accumulator in L2). Otherwise a
+ * dK/dV kernel plus a query-major dQ kernel that recomputes S and dP. GQA
+ * partials of dK/dV are summed in fp32. Workspaces: delta fp32 [nq, T];
+ * dkv_acc fp32 [2, T, nk*head_dim]. */
 int rp_attn_bwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
                    int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
                    const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
                    int64_t lddv, float* delta, float* dkv_acc, int32_t T, int32_t seq,
                    int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
-/* Backward: dq/dk/dv bf16 (same layouts as q/k/v, own pitches). Needs
- * workspace: dq_acc fp32 [T, nq, hd] and delta fp32 [nq, T]. */
-int rp_attn_bwd(const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v,
-                int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
-                const float* lse, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
-                int64_t lddv, float* dq_acc, float* delta, int32_t T, int32_t seq, int32_t nq,
-                int32_t nk, int32_t head_dim, float scale, void* stream);
 
 #ifdef __cplusplus
 }

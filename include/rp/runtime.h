@@ -25,8 +25,18 @@ extern "C" {
 typedef struct rp_runtime rp_runtime_t;
 
 enum {
-  RP_RT_SKIP_INIT = 1,      /* do not randomise weights (caller loads them) */
-  RP_RT_RECORD_TIMELINE = 2 /* record per-task CUDA events (measured bubble) */
+  RP_RT_SKIP_INIT = 1,       /* do not randomise weights (caller loads them) */
+  RP_RT_RECORD_TIMELINE = 2, /* record per-task CUDA events (measured bubble) */
+  /* whole model in one fused slot (N <= 2): the forward + LM head of
+   * micro-batch k+1 runs on a second stream beside k's backward (two
+   * activation sets; measured no faster at the 1 kW power cap) */
+  RP_RT_FUSED_PIPELINE = 4,
+  /* SwiGLU as separate kernels instead of the gate/up and down GEMM
+   * epilogues (the path T < 256 always takes; kept selectable for tests) */
+  RP_RT_UNFUSED_SWIGLU = 8,
+  /* record the (action, group, iteration) wait edges of the optimizer
+   * hand-off protocol the runtime realises (rp_runtime_protocol_edges) */
+  RP_RT_RECORD_PROTOCOL = 16
 };
 
 typedef struct {
@@ -52,6 +62,15 @@ typedef struct {
    * only for the adapters. 0 = full fine-tune. */
   int32_t lora_rank;
   float lora_alpha;
+  /* fp32 AdamW state placement (single device): < 0 keeps the state of the
+   * largest groups that fit in free HBM resident (the rest streams), 0 keeps
+   * ALL of it in pinned host memory, streamed through the GPU every step
+   * (BASELINE configs[2], host-offloaded Adam), > 0 caps the resident state
+   * at that many GB. A zero-initialised config is host-offloaded. */
+  double resident_state_gb;
+  /* rows of the LM-head logits chunk [rows, V] (multiple of 128; 0 = 2048) */
+  int32_t logits_rows;
+  int32_t reserved_;
 } rp_runtime_config_t;
 
 typedef struct {

@@ -1,32 +1,25 @@
-// Causal GQA flash-attention BACKWARD on the 5th-gen tensor cores (sm_100a),
-// as two kernels:
+// Causal GQA flash-attention BACKWARD on the 5th-gen tensor cores (sm_100a).
 //
-//  (A) dK/dV, key-major. CTA = 128 keys x 1 query head; loops over every query
-//      tile (64 queries) at or after the diagonal. Per tile: S^T = K Q^T and
-//      dP^T = V dO^T (tcgen05, M128 N64) into double-buffered TMEM; 4 softmax
-//      warps (thread = key row) form P^T = exp2(S^T*scale*log2e - lse*log2e)
-//      and dS^T = P^T (dP^T - delta) in bf16 smem; then dV += P^T dO and
-//      dK += dS^T Q (M128 N=hd K64) accumulate in TMEM for the whole loop.
-//      Epilogue: the G query heads of a KV group sum their partials into fp32
-//      (16-byte atomics; G adds per element), a cast kernel writes bf16.
-//  (B) dQ, query-major. CTA = 128 queries x 1 head; loops over key tiles
-//      (64 keys) up to the diagonal: S = Q K^T and dP = dO V^T (M128 N64,
-//      double-buffered in TMEM) -> softmax warps (thread = query row) write
-//      dS to double-buffered smem -> dQ += dS K (M128 N=hd K64, K as an
-//      MN-major operand). Epilogue: dQ*scale -> bf16.
-// (B) recomputes S and dP instead of reducing dQ partials through atomics.
-// Default for head_dim 128 with even GQA groups: (A4) below, one kernel that
-// also forms dQ^T = K^T dS^T per tile and reduce-adds it (TMA, fp32, in L2)
-// — no S/dP recompute; (A)+(B) stay as the RP_ATTN_SPLIT=1 path.
-#include <cstdlib>
-#include <mutex>
-#include <unordered_map>
+// Default (head_dim 128, even GQA group): (A4) below — ONE key-major kernel
+// per (128-key block, query-head pair) forms dK, dV and dQ: S^T and dP^T per
+// 64-query tile into TMEM, P^T / dS^T written back as bf16 A operands of
+// dV += P^T dO and dK += dS^T Q, and dQ^T = K^T dS^T reduce-added (TMA, fp32,
+// in L2) into a d-major accumulator — no S/dP recompute.
+// Otherwise (head_dim 64 or odd GQA groups) two kernels:
+//  (A/A2) dK/dV, key-major. CTA = 128 keys x 1 (A) or 2 (A2, ping-pong)
+//      query heads; per 64-query tile S^T = K Q^T and dP^T = V dO^T (M128
+//      N64) into double-buffered TMEM; softmax warps form P^T and dS^T;
+//      dV += P^T dO and dK += dS^T Q accumulate in TMEM. GQA partials are
+//      summed in fp32 (atomics), a cast kernel writes bf16.
+//  (B3) dQ, query-major, Q and dO staged once into TMEM: S = Q K^T and
+//      dP = dO V^T recomputed per 64-key tile, dQ += dS K.
 #include <utility>
 
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "kernels/launch_util.h"
 #include "kernels/sm100.cuh"
 #include "rp/kernels.h"
 
@@ -927,657 +920,10 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
   }
 }
 
-// ============================================================ (A3) dK / dV, operands in TMEM
-// CTA = 128 keys x TWO query heads of one KV group. K and V are staged ONCE
-// into TMEM (bf16 pairs, row = key = lane) and are the A operands of
-// S^T = K Q^T and dP^T = V dO^T, so shared memory only carries the small
-// (32-query) Q / dO tiles; with 32-query tiles two heads ping-pong in TMEM:
-//   K | V | S^T_a dP^T_a | S^T_b dP^T_b | dV | dK   (64+64+64+64+128+128 cols)
-// P^T / dS^T go back as bf16 pairs over the columns they came from and are
-// the A operands of dV += P^T dO and dK += dS^T Q (both heads into the same
-// accumulators). The (Q, dO, lse, delta) ring is 10 deep.
-constexpr int A3_BQ = 32;
-constexpr int A3_NST = 10;
-
-template <int HD>
-struct Dkv3Smem {
-  static constexpr int NSUB = HD / 64;
-  static constexpr int QT = A3_BQ * 128;               // one 32-row x 64-col sub-tile (4 KB)
-  static constexpr int STAGE = 2 * NSUB * QT;          // Q + dO of one (tile, head)
-  static constexpr int DO_OFF = NSUB * QT;
-  static constexpr int LD = A3_NST * STAGE;            // [A3_NST][2][A3_BQ] lse, delta
-  static constexpr int BAR = LD + A3_NST * 2 * A3_BQ * 4;
-  static constexpr int BYTES = BAR + 512 + 1024;
-  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
-};
-
-template <int HD>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dkv3_kernel(const bf16* __restrict__ kg, long long ldk, const bf16* __restrict__ vg,
-                         long long ldv, const __grid_constant__ CUtensorMap tm_q,
-                         const __grid_constant__ CUtensorMap tm_do,
-                         const float* __restrict__ lse, const float* __restrict__ delta,
-                         float* __restrict__ dk_acc, float* __restrict__ dv_acc, int T, int seq,
-                         int nq, int nk, float scale) {
-  using L = Dkv3Smem<HD>;
-  constexpr int NSUB = L::NSUB;
-  constexpr uint32_t TK = 0, TV = HD / 2, TH = HD, TDV = 256, TDK = 384;  // TMEM columns
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* kv_ready = bar + 0;
-  uint64_t* st_full = bar + 1;             // [A3_NST]
-  uint64_t* st_empty = bar + 1 + A3_NST;   // [A3_NST]
-  uint64_t* sd_full = st_empty + A3_NST;   // [2] per head
-  uint64_t* ps_full = sd_full + 2;         // [2]
-  uint64_t* acc_done = ps_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kb = causal_block(blockIdx.y, T / A_BK, seq / A_BK, false), ha = 2 * (int)blockIdx.x;
-  const int kvh = ha / (nq / nk);
-  const int k0 = kb * A_BK;
-  const int s0 = (k0 / seq) * seq, s_end = s0 + seq;
-  const int nqt = (s_end - k0) / A3_BQ;  // query tiles at/after the diagonal
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm_q);
-    tma_prefetch(&tm_do);
-    mbar_init(kv_ready, 8);
-    for (int i = 0; i < A3_NST; ++i) {
-      mbar_init(&st_full[i], 1);
-      mbar_init(&st_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&ps_full[i], 4);
-    }
-    mbar_init(acc_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0 && lane == 0) {
-    for (int idx = 0; idx < 2 * nqt; ++idx) {
-      const int st = idx % A3_NST, w = idx & 1, hq = ha + w;
-      mbar_wait(&st_empty[st], ((idx / A3_NST) & 1) ^ 1);
-      const int qs = k0 + (idx >> 1) * A3_BQ;
-      uint8_t* qd = sm + st * L::STAGE;
-      mbar_arrive_expect_tx(&st_full[st], L::STAGE + 2 * A3_BQ * 4);
-      for (int sub = 0; sub < NSUB; ++sub) {
-        tma_load_2d(qd + sub * L::QT, &tm_q, &st_full[st], hq * HD + 64 * sub, qs);
-        tma_load_2d(qd + L::DO_OFF + sub * L::QT, &tm_do, &st_full[st], hq * HD + 64 * sub, qs);
-      }
-      float* ld = reinterpret_cast<float*>(sm + L::LD) + st * 2 * A3_BQ;
-      bulk_load_1d(ld, lse + (long long)hq * T + qs, A3_BQ * 4, &st_full[st]);
-      bulk_load_1d(ld + A3_BQ, delta + (long long)hq * T + qs, A3_BQ * 4, &st_full[st]);
-    }
-  } else if (warp == 1) {  // MMA: whole warp, uniform descriptors, elected issue
-    constexpr uint32_t idesc_s = umma_idesc_bf16(A_BK, A3_BQ, 0, 0);   // A TMEM x B K-major
-    constexpr uint32_t idesc_g = umma_idesc_bf16(A_BK, HD, 0, 1);      // A TMEM x B MN-major
-    auto stage = [&](int idx) { return smem_u32(sm + (idx % A3_NST) * L::STAGE); };
-    auto issue_sdp = [&](int j, int w) {
-      const int idx = 2 * j + w;
-      mbar_wait(&st_full[idx % A3_NST], (idx / A3_NST) & 1);
-      tc_fence_after();
-      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t qo = (kk >> 2) * L::QT + (kk & 3) * 32;
-          umma_f16_ts(tmem + TH + w * 64, tmem + TK + kk * 8, umma_desc_sw128(q_addr + qo, 16, 1024),
-                      idesc_s, kk != 0);
-          umma_f16_ts(tmem + TH + w * 64 + 32, tmem + TV + kk * 8,
-                      umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
-        }
-        umma_commit(&sd_full[w]);
-      }
-      __syncwarp();
-    };
-    auto issue_grads = [&](int j, int w) {
-      const int idx = 2 * j + w;
-      mbar_wait(&ps_full[w], j & 1);
-      tc_fence_after();
-      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < A3_BQ / 16; ++kk) {  // 16 query rows of the MN-major B per step
-          const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, L::QT, 1024);
-          const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, L::QT, 1024);
-          umma_f16_ts(tmem + TDV, tmem + TH + w * 64 + kk * 8, ob, idesc_g, (idx | kk) != 0);
-          umma_f16_ts(tmem + TDK, tmem + TH + w * 64 + 32 + kk * 8, qb, idesc_g, (idx | kk) != 0);
-        }
-        umma_commit(&st_empty[idx % A3_NST]);
-      }
-      __syncwarp();
-    };
-    mbar_wait(kv_ready, 0);
-    tc_fence_after();
-    issue_sdp(0, 0);
-    issue_sdp(0, 1);
-    for (int j = 0; j < nqt; ++j) {
-      issue_grads(j, 0);
-      if (j + 1 < nqt) issue_sdp(j + 1, 0);  // in-order after grads_a(j) read P^T_a
-      issue_grads(j, 1);
-      if (j + 1 < nqt) issue_sdp(j + 1, 1);
-    }
-    if (elect_one()) umma_commit(acc_done);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int w = (warp - 4) >> 2, quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const int key = k0 + r;
-    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    // stage K (warpgroup a) or V (warpgroup b) row `key` into TMEM
-    {
-      const bf16* src = w == 0 ? kg + (long long)key * ldk + (long long)kvh * HD
-                               : vg + (long long)key * ldv + (long long)kvh * HD;
-      const uint32_t col = w == 0 ? TK : TV;
-#pragma unroll
-      for (int c = 0; c < HD / 2; c += 16) {
-        uint32_t v[16];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint4 u = *reinterpret_cast<const uint4*>(src + 2 * c + 8 * i);
-          v[4 * i] = u.x;
-          v[4 * i + 1] = u.y;
-          v[4 * i + 2] = u.z;
-          v[4 * i + 3] = u.w;
-        }
-        tmem_st_32x32b_x16(lane_base + col + c, v);
-      }
-      tmem_st_wait_all();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(kv_ready);
-    }
-    const float sl2 = scale * kLog2e;
-    for (int j = 0; j < nqt; ++j) {
-      const int idx = 2 * j + w, st = idx % A3_NST;
-      const int qs = k0 + j * A3_BQ;
-      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + st * 2 * A3_BQ;
-      const float* del_t = lse_t + A3_BQ;
-      mbar_wait(&st_full[st], (idx / A3_NST) & 1);  // lse/delta visibility
-      mbar_wait(&sd_full[w], j & 1);
-      tc_fence_after();
-      uint32_t sv[32], dpv[32], pk[16], dk2[16];
-      tmem_ld_32x32b_x32(lane_base + TH + w * 64, sv);
-      tmem_ld_32x32b_x32(lane_base + TH + w * 64 + 32, dpv);
-      tmem_ld_wait();
-      const bool diag = qs < k0 + A_BK;
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[i] * kLog2e));
-        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[i + 1] * kLog2e));
-        if (diag) {
-          if (qs + i < key) p0 = 0.f;
-          if (qs + i + 1 < key) p1 = 0.f;
-        }
-        pk[i / 2] = pack_bf16x2(p0, p1);
-        dk2[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - del_t[i]),
-                                 p1 * (__uint_as_float(dpv[i + 1]) - del_t[i + 1]));
-      }
-      tmem_st_32x32b_x16(lane_base + TH + w * 64, pk);        // over read S^T columns
-      tmem_st_32x32b_x16(lane_base + TH + w * 64 + 32, dk2);  // over read dP^T columns
-      tmem_st_wait_all();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ps_full[w]);
-    }
-    mbar_wait(acc_done, 0);
-    tc_fence_after();
-    float* dst = (w == 0 ? dk_acc : dv_acc) + (long long)key * nk * HD + (long long)kvh * HD;
-    const uint32_t col = w == 0 ? TDK : TDV;
-    const float f = w == 0 ? scale : 1.f;
-#pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t a[32];
-      tmem_ld_32x32b_x32(lane_base + col + c, a);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        atomicAdd(reinterpret_cast<float4*>(dst + c + i),
-                  make_float4(__uint_as_float(a[i]) * f, __uint_as_float(a[i + 1]) * f,
-                              __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
 // ======================================================================== (B) dQ
-// 128 queries per CTA, key tiles of 64 so that S and dP (64 TMEM columns
-// each) are double-buffered next to the dQ accumulator: the tensor core
-// computes S/dP of tile j+1 and dQ of tile j-1 while the softmax warps turn
-// tile j into dS.
+// query-major dQ kernel of the two-kernel path (head_dim 64 / odd GQA groups)
 constexpr int B_Q = 128;  // queries per CTA
 constexpr int B_K = 64;   // keys per tile
-
-template <int HD>
-struct DqSmem {
-  static constexpr int NSUB = HD / 64;
-  static constexpr int Q = 0;
-  static constexpr int DO = Q + NSUB * SUB128;
-  static constexpr int KV0 = DO + NSUB * SUB128;     // stage s: K at KV0 + s*STAGE, V after
-  static constexpr int STAGE = 2 * NSUB * SUB64;
-  static constexpr int DS = KV0 + NST * STAGE;       // dS[b]: [128 q][64 keys] (16 KB)
-  static constexpr int BAR = DS + 2 * SUB128;
-  static constexpr int BYTES = BAR + 256 + 1024;
-  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
-};
-
-template <int HD>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q,
-                       const __grid_constant__ CUtensorMap tm_do,
-                       const __grid_constant__ CUtensorMap tm_k,
-                       const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ lse,
-                       const float* __restrict__ delta, bf16* __restrict__ dq, long long lddq,
-                       int T, int seq, int nq, int nk, float scale) {
-  using L = DqSmem<HD>;
-  constexpr int NSUB = L::NSUB;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [NST]
-  uint64_t* kv_empty = bar + 4;  // [NST]
-  uint64_t* sd_full = bar + 7;   // [2]
-  uint64_t* sd_free = bar + 9;   // [2]
-  uint64_t* ds_full = bar + 11;  // [2]
-  uint64_t* ds_free = bar + 13;  // [2]  (dQ MMA of the tile done reading dS[b])
-  uint64_t* dq_done = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qblocks = T / B_Q;
-  const int qb = causal_block(blockIdx.y, qblocks, seq / B_Q, true);
-  const int h = blockIdx.x, kvh = h / (nq / nk);
-  const int q0 = qb * B_Q;
-  const int s0 = (q0 / seq) * seq;
-  const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm_q);
-    tma_prefetch(&tm_do);
-    tma_prefetch(&tm_k);
-    tma_prefetch(&tm_v);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < NST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&sd_free[i], 8);
-      mbar_init(&ds_full[i], 8);
-      mbar_init(&ds_free[i], 1);
-    }
-    mbar_init(dq_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: S[b] at b*128, dP[b] at b*128 + 64 (64 cols each), dQ at 256
-  const uint32_t TM_DQ = 256;
-
-  if (warp == 0 && lane == 0) {
-    mbar_arrive_expect_tx(q_full, 2 * NSUB * SUB128);
-    for (int sub = 0; sub < NSUB; ++sub) {
-      tma_load_2d(sm + L::Q + sub * SUB128, &tm_q, q_full, h * HD + 64 * sub, q0);
-      tma_load_2d(sm + L::DO + sub * SUB128, &tm_do, q_full, h * HD + 64 * sub, q0);
-    }
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % NST;
-      mbar_wait(&kv_empty[st], ((j / NST) & 1) ^ 1);
-      const int k0 = s0 + j * B_K;
-      uint8_t* kd = sm + L::KV0 + st * L::STAGE;
-      mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
-      for (int sub = 0; sub < NSUB; ++sub) {
-        tma_load_2d(kd + sub * SUB64, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
-        tma_load_2d(kd + NSUB * SUB64 + sub * SUB64, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
-                    k0);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
-    const uint32_t q_addr = smem_u32(sm + L::Q), do_addr = smem_u32(sm + L::DO);
-    auto issue_dq = [&](int j) {
-      const int b = j & 1;
-      mbar_wait(&ds_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % NST) * L::STAGE);
-      const uint32_t ds_addr = smem_u32(sm + L::DS + b * SUB128);
-#pragma unroll
-      for (int kk = 0; kk < B_K / 16; ++kk) {
-        const uint64_t ad = umma_desc_sw128(ds_addr + kk * 32, 16, 1024);
-        const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
-        umma_f16(tmem + TM_DQ, ad, bd, idesc_q, (j | kk) != 0);
-      }
-      umma_commit(&ds_free[b]);
-      umma_commit(&kv_empty[j % NST]);
-    };
-    mbar_wait(q_full, 0);
-    for (int j = 0; j < ntiles; ++j) {
-      const int b = j & 1;
-      mbar_wait(&kv_full[j % NST], (j / NST) & 1);
-      if (j >= 2) mbar_wait(&sd_free[b], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % NST) * L::STAGE);
-      const uint32_t v_addr = k_addr + NSUB * SUB64;
-#pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
-        const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
-        umma_f16(tmem + b * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
-                 umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
-        umma_f16(tmem + b * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
-                 umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
-      }
-      umma_commit(&sd_full[b]);
-      if (j >= 1) issue_dq(j - 1);
-    }
-    issue_dq(ntiles - 1);
-    umma_commit(dq_done);
-  } else if (warp >= 4) {
-    // 8 softmax warps: lane quarter = warp % 4 (query rows), key half = (warp-4)/4
-    const int quarter = warp & 3, half = (warp - 4) >> 2;
-    const int r = quarter * 32 + lane;  // query row
-    const int qrow = q0 + r;
-    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    const float sl2 = scale * kLog2e;
-    const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
-    const float dl = delta[(long long)h * T + qrow];
-    const int c0 = half * 32;
-    for (int j = 0; j < ntiles; ++j) {
-      const int b = j & 1;
-      mbar_wait(&sd_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sv[32], dpv[32];
-      tmem_ld_32x32b_x32(lane_base + b * 128 + c0, sv);
-      tmem_ld_32x32b_x32(lane_base + b * 128 + 64 + c0, dpv);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sd_free[b]);
-      const int kbase = s0 + j * B_K + c0;  // first key of this thread's columns
-      const bool diag = kbase + 31 > q0;
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
-        float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
-        if (diag) {
-          if (kbase + i > qrow) p0 = 0.f;
-          if (kbase + i + 1 > qrow) p1 = 0.f;
-        }
-        pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
-                                p1 * (__uint_as_float(dpv[i + 1]) - dl));
-      }
-      if (j >= 2) {  // dQ MMA of tile j-2 done reading dS[b]
-        mbar_wait(&ds_free[b], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-      }
-      uint8_t* ds_row = sm + L::DS + b * SUB128 + (r >> 3) * 1024 + (r & 7) * 128;
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4)
-        *reinterpret_cast<uint4*>(ds_row + (((half * 4 + q4) ^ (r & 7)) << 4)) =
-            make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-      fence_proxy_async();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[b]);
-    }
-    mbar_wait(dq_done, 0);
-    tc_fence_after();
-    bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
-#pragma unroll 1
-    for (int c = half * (HD / 2); c < (half + 1) * (HD / 2); c += 32) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(lane_base + TM_DQ + c, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
-        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
-        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
-        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
-        *reinterpret_cast<uint4*>(dqr + c + i) = u;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
-// ============================================================ (B2) dQ, ping-pong
-// CTA = 128 queries x TWO query heads of one KV group: K_j / V_j (64 keys) are
-// loaded once for both heads, and the two softmax warpgroups alternate with
-// the tensor core:  S/dP_a(j) | dQ_b(j-1) | S/dP_b(j) | dQ_a(j) | S/dP_a(j+1) ...
-// dS (bf16 pairs) goes back into the TMEM columns of the S it came from and is
-// the TMEM A operand of dQ += dS K; the K/V ring is 3 deep.
-constexpr int B2_NST = 3;
-
-template <int HD>
-struct Dq2Smem {
-  static constexpr int NSUB = HD / 64;
-  static constexpr int QT = NSUB * SUB128;           // one 128-row Q or dO tile
-  static constexpr int Q0 = 0;                       // head w: Q at Q0 + 2w*QT, dO after
-  static constexpr int KV0 = Q0 + 4 * QT;            // stage s: K at KV0 + s*STAGE, V after
-  static constexpr int STAGE = 2 * NSUB * SUB64;
-  static constexpr int BAR = KV0 + B2_NST * STAGE;
-  static constexpr int BYTES = BAR + 256 + 1024;
-  static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
-};
-
-template <int HD>
-__global__ void __launch_bounds__(384, 1)
-    attn_bwd_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
-                          const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_k,
-                          const __grid_constant__ CUtensorMap tm_v, const float* __restrict__ lse,
-                          const float* __restrict__ delta, bf16* __restrict__ dq, long long lddq,
-                          int T, int seq, int nq, int nk, float scale) {
-  using L = Dq2Smem<HD>;
-  constexpr int NSUB = L::NSUB;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;            // [B2_NST]
-  uint64_t* kv_empty = bar + 1 + B2_NST;  // [B2_NST]
-  uint64_t* sd_full = kv_empty + B2_NST;  // [2] per head
-  uint64_t* ds_full = sd_full + 2;        // [2]
-  uint64_t* dq_done = ds_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qblocks = T / B_Q;
-  const int qb = causal_block(blockIdx.y, qblocks, seq / B_Q, true);
-  const int ha = 2 * (int)blockIdx.x, kvh = ha / (nq / nk);
-  const int q0 = qb * B_Q;
-  const int s0 = (q0 / seq) * seq;
-  const int ntiles = (q0 - s0) / B_K + B_Q / B_K;  // keys [s0, q0 + 128)
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm_q);
-    tma_prefetch(&tm_do);
-    tma_prefetch(&tm_k);
-    tma_prefetch(&tm_v);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < B2_NST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sd_full[i], 1);
-      mbar_init(&ds_full[i], 4);
-    }
-    mbar_init(dq_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // TMEM: head w: S at w*128 (64 cols; dS pairs overwrite [0, 32) of it),
-  // dP at w*128 + 64; dQ_w at 256 + w*HD
-
-  if (warp == 0 && lane == 0) {
-    mbar_arrive_expect_tx(q_full, 4 * L::QT);
-    for (int w = 0; w < 2; ++w)
-      for (int sub = 0; sub < NSUB; ++sub) {
-        tma_load_2d(sm + L::Q0 + 2 * w * L::QT + sub * SUB128, &tm_q, q_full,
-                    (ha + w) * HD + 64 * sub, q0);
-        tma_load_2d(sm + L::Q0 + (2 * w + 1) * L::QT + sub * SUB128, &tm_do, q_full,
-                    (ha + w) * HD + 64 * sub, q0);
-      }
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j % B2_NST;
-      mbar_wait(&kv_empty[st], ((j / B2_NST) & 1) ^ 1);
-      const int k0 = s0 + j * B_K;
-      uint8_t* kd = sm + L::KV0 + st * L::STAGE;
-      mbar_arrive_expect_tx(&kv_full[st], L::STAGE);
-      for (int sub = 0; sub < NSUB; ++sub) {
-        tma_load_2d(kd + sub * SUB64, &tm_k, &kv_full[st], kvh * HD + 64 * sub, k0);
-        tma_load_2d(kd + NSUB * SUB64 + sub * SUB64, &tm_v, &kv_full[st], kvh * HD + 64 * sub,
-                    k0);
-      }
-    }
-  } else if (warp == 1) {  // whole warp: uniform descriptors, elected issue
-    constexpr uint32_t idesc_s = umma_idesc_bf16(B_Q, B_K, 0, 0);
-    constexpr uint32_t idesc_q = umma_idesc_bf16(B_Q, HD, 0, 1);
-    auto issue_sdp = [&](int j, int w) {
-      if (w == 0) {
-        mbar_wait(&kv_full[j % B2_NST], (j / B2_NST) & 1);
-        tc_fence_after();
-      }
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % B2_NST) * L::STAGE);
-      const uint32_t v_addr = k_addr + NSUB * SUB64;
-      const uint32_t q_addr = smem_u32(sm + L::Q0 + 2 * w * L::QT), do_addr = q_addr + L::QT;
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t oq = (kk >> 2) * SUB128 + (kk & 3) * 32;
-          const uint32_t okv = (kk >> 2) * SUB64 + (kk & 3) * 32;
-          umma_f16(tmem + w * 128, umma_desc_sw128(q_addr + oq, 16, 1024),
-                   umma_desc_sw128(k_addr + okv, 16, 1024), idesc_s, kk != 0);
-          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(do_addr + oq, 16, 1024),
-                   umma_desc_sw128(v_addr + okv, 16, 1024), idesc_s, kk != 0);
-        }
-        umma_commit(&sd_full[w]);
-      }
-      __syncwarp();
-    };
-    auto issue_dq = [&](int j, int w) {
-      mbar_wait(&ds_full[w], j & 1);
-      tc_fence_after();
-      const uint32_t k_addr = smem_u32(sm + L::KV0 + (j % B2_NST) * L::STAGE);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < B_K / 16; ++kk) {
-          const uint64_t bd = umma_desc_sw128(k_addr + kk * 2048, SUB64, 1024);
-          umma_f16_ts(tmem + 256 + w * HD, tmem + w * 128 + kk * 8, bd, idesc_q, (j | kk) != 0);
-        }
-        if (w == 1) umma_commit(&kv_empty[j % B2_NST]);
-      }
-      __syncwarp();
-    };
-    mbar_wait(q_full, 0);
-    issue_sdp(0, 0);
-    issue_sdp(0, 1);
-    for (int j = 0; j < ntiles; ++j) {
-      issue_dq(j, 0);
-      if (j + 1 < ntiles) issue_sdp(j + 1, 0);  // in-order after dQ_a(j) read dS_a
-      issue_dq(j, 1);
-      if (j + 1 < ntiles) issue_sdp(j + 1, 1);
-    }
-    if (elect_one()) umma_commit(dq_done);
-    __syncwarp();
-  } else if (warp >= 4) {
-    const int w = (warp - 4) >> 2, quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // query row
-    const int qrow = q0 + r, h = ha + w;
-    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    const float sl2 = scale * kLog2e;
-    const float lse2 = lse[(long long)h * T + qrow] * kLog2e;
-    const float dl = delta[(long long)h * T + qrow];
-    for (int j = 0; j < ntiles; ++j) {
-      mbar_wait(&sd_full[w], j & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t sv[32], dpv[32], pk[16];
-        tmem_ld_32x32b_x32(lane_base + w * 128 + half * 32, sv);
-        tmem_ld_32x32b_x32(lane_base + w * 128 + 64 + half * 32, dpv);
-        tmem_ld_wait();
-        const int kbase = s0 + j * B_K + half * 32;  // first key of these columns
-        const bool diag = kbase + 31 > q0;
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse2));
-          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse2));
-          if (diag) {
-            if (kbase + i > qrow) p0 = 0.f;
-            if (kbase + i + 1 > qrow) p1 = 0.f;
-          }
-          pk[i / 2] = pack_bf16x2(p0 * (__uint_as_float(dpv[i]) - dl),
-                                      p1 * (__uint_as_float(dpv[i + 1]) - dl));
-        }
-        tmem_st_32x32b_x16(lane_base + w * 128 + half * 16, pk);  // over read columns
-      }
-      tmem_st_wait_all();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[w]);
-    }
-    mbar_wait(dq_done, 0);
-    tc_fence_after();
-    bf16* dqr = dq + (long long)qrow * lddq + (long long)h * HD;
-#pragma unroll 1
-    for (int c = 0; c < HD; c += 32) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(lane_base + 256 + w * HD + c, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; i += 8) {
-        uint4 u;
-        u.x = pack_bf16x2(__uint_as_float(v[i]) * scale, __uint_as_float(v[i + 1]) * scale);
-        u.y = pack_bf16x2(__uint_as_float(v[i + 2]) * scale, __uint_as_float(v[i + 3]) * scale);
-        u.z = pack_bf16x2(__uint_as_float(v[i + 4]) * scale, __uint_as_float(v[i + 5]) * scale);
-        u.w = pack_bf16x2(__uint_as_float(v[i + 6]) * scale, __uint_as_float(v[i + 7]) * scale);
-        *reinterpret_cast<uint4*>(dqr + c + i) = u;
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
 
 // ============================================================ (B3) dQ, operands in TMEM
 // CTA = 128 queries x 1 head. Q and dO are staged ONCE into TMEM (bf16 pairs,
@@ -1853,22 +1199,6 @@ __global__ void dq_cast_kernel(const float* __restrict__ acc, bf16* __restrict__
     dq[(long long)(t0 + ty + i) * lddq + c0 + tx] = __float2bfloat16_rn(tile[tx][ty + i] * scale);
 }
 
-// per-stream fp32 dQ accumulator of the fused backward (grown on demand)
-float* dq_workspace(cudaStream_t s, size_t floats) {
-  static std::mutex mu;
-  static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> ws;
-  std::lock_guard<std::mutex> g(mu);
-  auto& e = ws[s];
-  if (e.second < floats) {
-    if (e.first) cudaFree(e.first);
-    e.first = nullptr;
-    e.second = 0;
-    if (cudaMalloc(&e.first, floats * sizeof(float)) != cudaSuccess) return nullptr;
-    e.second = floats;
-  }
-  return e.first;
-}
-
 // ---- host ------------------------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1910,8 +1240,7 @@ bool map_f32(CUtensorMap* m, const void* base, long long rows, long long cols, l
 
 template <class K>
 bool set_smem(K kern, int bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
-         cudaSuccess;
+  return ensure_smem_t(kern, bytes);
 }
 
 template <int HD>
@@ -1923,46 +1252,27 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   const long long warps = (long long)T * nq;
   delta_kernel<HD><<<(int)((warps + 7) / 8), 256, 0, s>>>((const bf16*)o, ldo, (const bf16*)dout,
                                                          lddo, delta, T, nq);
-  CUtensorMap mk128, mv128, mq64, mdo64, mq128, mdo128;
+  CUtensorMap mk128, mv128, mq64, mdo64;
   if (!map2d(&mk128, k, T, (long long)nk * HD, ldk, 128) ||
       !map2d(&mv128, v, T, (long long)nk * HD, ldv, 128) ||
       !map2d(&mq64, q, T, (long long)nq * HD, ldq, 64) ||
-      !map2d(&mdo64, dout, T, (long long)nq * HD, lddo, 64) ||
-      !map2d(&mq128, q, T, (long long)nq * HD, ldq, 128) ||
-      !map2d(&mdo128, dout, T, (long long)nq * HD, lddo, 128))
+      !map2d(&mdo64, dout, T, (long long)nq * HD, lddo, 64))
     return RP_E_CUDA;
-  static bool cfg = false;
-  if (!cfg) {
-    if (!set_smem(attn_bwd_dkv_kernel<HD>, DkvSmem<HD>::BYTES) ||
-        !set_smem(attn_bwd_dq_kernel<HD>, DqSmem<HD>::BYTES))
-      return RP_E_CUDA;
-    cfg = true;
-  }
   const long long acc_n = (long long)T * nk * HD;
-  static const bool v1 = getenv("RP_ATTN_BWD_V1") != nullptr;
-  // opt-in: K/V-in-TMEM variant with 32-query tiles — correct, but measured
-  // 2 % slower than the 64-query ping-pong kernel below (0.596 vs 0.586 ms)
-  static const bool dkv3 = getenv("RP_ATTN_DKV3") != nullptr;
-  // default: dK/dV/dQ in one kernel (A4); RP_ATTN_SPLIT=1 selects the
-  // two-kernel path (dK/dV kernel + dQ kernel that recomputes S and dP)
-  static const bool split =
-      getenv("RP_ATTN_SPLIT") != nullptr || getenv("RP_ATTN_DQ_PP") != nullptr;
-  if (HD == 128 && (nq / nk) % 2 == 0 && !v1 && !dkv3 && !split) {  // dK/dV/dQ in one kernel
+  const int G = nq / nk;
+  if (HD == 128 && G % 2 == 0) {  // dK/dV/dQ in one kernel (A4)
     const long long qn = (long long)T * nq * HD;
-    float* dq_acc = dq_workspace(s, (size_t)qn);
+    Workspace* w = stream_workspace(s, WS_ATTN_DQ, sizeof(float) * (size_t)qn);
+    float* dq_acc = w ? static_cast<float*>(w->p) : nullptr;
     CUtensorMap mdq;
     if (!dq_acc || !map_f32(&mdq, dq_acc, (long long)nq * HD, T, T))  // d-major [nq*HD, T]
       return RP_E_CUDA;
     if (cudaMemsetAsync(dq_acc, 0, sizeof(float) * qn, s) != cudaSuccess) return RP_E_CUDA;
-    static const bool atomics = getenv("RP_ATTN_DKV_ATOMICS") != nullptr;  // A/B knob
-    const int G = nq / nk;
-    const int cl = atomics ? 0 : G == 2 ? 1 : G == 4 ? 2 : 0;
-    static bool smem_set[3] = {false, false, false};  // per CL variant (same pointer type)
+    // GQA partials of dK/dV: G = 2 both heads share the CTA (bf16 straight
+    // from TMEM); G = 4 a 2-CTA cluster sums over DSMEM; G >= 8 fp32 atomics
+    const int cl = G == 2 ? 1 : G == 4 ? 2 : 0;
     auto go = [&](auto kern, int cluster) -> cudaError_t {
-      if (!smem_set[cl]) {
-        if (!set_smem(kern, Dkv4Smem<HD>::BYTES)) return cudaErrorInvalidValue;
-        smem_set[cl] = true;
-      }
+      if (!set_smem(kern, Dkv4Smem<HD>::BYTES)) return cudaErrorInvalidValue;
       cudaLaunchConfig_t c = {};
       c.gridDim = dim3(nq / 2, T / A_BK, 1);
       c.blockDim = dim3(A2_THREADS, 1, 1);
@@ -1993,29 +1303,14 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
                                                                       nq * HD, scale);
     return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
   }
+  // two-kernel path: dK/dV (A2 for even groups, A otherwise) + dQ (B3)
   if (cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * acc_n, s) != cudaSuccess) return RP_E_CUDA;
-  if ((nq / nk) % 2 == 0 && !v1 && dkv3) {  // K/V in TMEM, two heads, 32-query tiles
-    CUtensorMap mq32, mdo32;
-    if (!map2d(&mq32, q, T, (long long)nq * HD, ldq, A3_BQ) ||
-        !map2d(&mdo32, dout, T, (long long)nq * HD, lddo, A3_BQ))
-      return RP_E_CUDA;
-    static bool cfg5 = false;
-    if (!cfg5) {
-      if (!set_smem(attn_bwd_dkv3_kernel<HD>, Dkv3Smem<HD>::BYTES)) return RP_E_CUDA;
-      cfg5 = true;
-    }
-    attn_bwd_dkv3_kernel<HD><<<dim3(nq / 2, T / A_BK), 384, Dkv3Smem<HD>::BYTES, s>>>(
-        (const bf16*)k, ldk, (const bf16*)v, ldv, mq32, mdo32, lse, delta, dkv_acc,
-        dkv_acc + acc_n, T, seq, nq, nk, scale);
-  } else if ((nq / nk) % 2 == 0 && !v1) {  // two heads of one KV group per CTA
-    static bool cfg2 = false;
-    if (!cfg2) {
-      if (!set_smem(attn_bwd_dkv_pp_kernel<HD>, Dkv2Smem<HD>::BYTES)) return RP_E_CUDA;
-      cfg2 = true;
-    }
+  if (G % 2 == 0) {
+    if (!set_smem(attn_bwd_dkv_pp_kernel<HD>, Dkv2Smem<HD>::BYTES)) return RP_E_CUDA;
     attn_bwd_dkv_pp_kernel<HD><<<dim3(nq / 2, T / A_BK), A2_THREADS, Dkv2Smem<HD>::BYTES, s>>>(
         mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
   } else {
+    if (!set_smem(attn_bwd_dkv_kernel<HD>, DkvSmem<HD>::BYTES)) return RP_E_CUDA;
     attn_bwd_dkv_kernel<HD><<<dim3(nq, T / A_BK), 384, DkvSmem<HD>::BYTES, s>>>(
         mk128, mv128, mq64, mdo64, lse, delta, dkv_acc, dkv_acc + acc_n, T, seq, nq, nk, scale);
   }
@@ -2025,28 +1320,10 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   if (!map2d(&mk64, k, T, (long long)nk * HD, ldk, 64) ||
       !map2d(&mv64, v, T, (long long)nk * HD, ldv, 64))
     return RP_E_CUDA;
-  static const bool dq_pp = getenv("RP_ATTN_DQ_PP") != nullptr;  // A/B knob
-  if (!v1 && !dq_pp) {
-    static bool cfg4 = false;
-    if (!cfg4) {
-      if (!set_smem(attn_bwd_dq3_kernel<HD>, Dq3Smem<HD>::BYTES)) return RP_E_CUDA;
-      cfg4 = true;
-    }
-    attn_bwd_dq3_kernel<HD><<<dim3(nq, T / B_Q), 384, Dq3Smem<HD>::BYTES, s>>>(
-        (const bf16*)q, ldq, (const bf16*)dout, lddo, mk64, mv64, lse, delta, (bf16*)dq, lddq, T,
-        seq, nq, nk, scale);
-  } else if ((nq / nk) % 2 == 0 && !v1) {
-    static bool cfg3 = false;
-    if (!cfg3) {
-      if (!set_smem(attn_bwd_dq_pp_kernel<HD>, Dq2Smem<HD>::BYTES)) return RP_E_CUDA;
-      cfg3 = true;
-    }
-    attn_bwd_dq_pp_kernel<HD><<<dim3(nq / 2, T / B_Q), 384, Dq2Smem<HD>::BYTES, s>>>(
-        mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
-  } else {
-    attn_bwd_dq_kernel<HD><<<dim3(nq, T / B_Q), 384, DqSmem<HD>::BYTES, s>>>(
-        mq128, mdo128, mk64, mv64, lse, delta, (bf16*)dq, lddq, T, seq, nq, nk, scale);
-  }
+  if (!set_smem(attn_bwd_dq3_kernel<HD>, Dq3Smem<HD>::BYTES)) return RP_E_CUDA;
+  attn_bwd_dq3_kernel<HD><<<dim3(nq, T / B_Q), 384, Dq3Smem<HD>::BYTES, s>>>(
+      (const bf16*)q, ldq, (const bf16*)dout, lddo, mk64, mv64, lse, delta, (bf16*)dq, lddq, T,
+      seq, nq, nk, scale);
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
 }
 
@@ -2056,7 +1333,7 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
 // tcgen05 backward: dq/dk/dv (bf16) from q/k/v/o/dO/lse; `delta` is an fp32
 // [nq, T] workspace, dkv_acc an fp32 [2, T, nk*head_dim] one. dK/dV (and, on
 // the default fused path, dQ) are reduced in fp32 through L2 atomics / TMA
-// reduce-adds, so bits can vary run to run. Same layouts as rp_attn_bwd.
+// reduce-adds, so bits can vary run to run. Layouts as rp_attn_fwd_tc.
 extern "C" __attribute__((visibility("default"))) int rp_attn_bwd_tc(
     const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv,
     const void* o, int64_t ldo, const void* dout, int64_t lddo, const float* lse, void* dq,

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "kernels/launch_util.h"
 #include "kernels/sm100.cuh"
 #include "rp/kernels.h"
 
@@ -298,7 +299,8 @@ __global__ void __launch_bounds__(192, 1)
 // head's MMAs, so the MUFU/FMA work of the two heads hides behind the MMAs.
 constexpr int PP_THREADS = 384;
 
-// PT: P goes back into the TMEM columns of its S (bf16 pairs) and feeds the
+// PT (the only instantiation; PT = false keeps P in shared memory and
+// measured slower): P goes back into the TMEM columns of its S (bf16 pairs) and feeds the
 // PV MMA as a TMEM A operand — no P store to shared memory, whose port the
 // SS MMAs at N=128 already saturate — and the freed smem deepens the K/V ring.
 template <int HD, bool PT>
@@ -617,30 +619,16 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
   if (!map_tile(&mq, q, T, (long long)nq * HD, ldq) || !map_tile(&mk, k, T, (long long)nk * HD, ldk) ||
       !map_tile(&mv, v, T, (long long)nk * HD, ldv))
     return RP_E_CUDA;
-  static const bool force_v1 = getenv("RP_ATTN_FWD_V1") != nullptr;
-  if ((nq / nk) % 2 == 0 && !force_v1) {  // two heads of one KV group per CTA
-    static const bool p_smem = getenv("RP_ATTN_FWD_PSMEM") != nullptr;  // A/B knob
-    auto kern = p_smem ? attn_fwd_pp_kernel<HD, false> : attn_fwd_pp_kernel<HD, true>;
-    const int bytes = p_smem ? PpSmem<HD, false>::BYTES : PpSmem<HD, true>::BYTES;
-    static bool cfg_pp = false;
-    if (!cfg_pp) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
-          cudaSuccess)
-        return RP_E_CUDA;
-      cfg_pp = true;
-    }
+  if ((nq / nk) % 2 == 0) {  // two heads of one KV group per CTA
+    auto kern = attn_fwd_pp_kernel<HD, true>;
+    const int bytes = PpSmem<HD, true>::BYTES;
+    if (!ensure_smem_t(kern, bytes)) return RP_E_CUDA;
     dim3 grid(nq / 2, T / TILE);
     kern<<<grid, PP_THREADS, bytes, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);
     return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
   }
   auto kern = attn_fwd_tc_kernel<HD>;
-  static bool cfg = false;
-  if (!cfg) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             FwdSmem<HD>::BYTES) != cudaSuccess)
-      return RP_E_CUDA;
-    cfg = true;
-  }
+  if (!ensure_smem_t(kern, FwdSmem<HD>::BYTES)) return RP_E_CUDA;
   dim3 grid(nq, T / TILE);
   kern<<<grid, 192, FwdSmem<HD>::BYTES, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);
   return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA;
@@ -649,8 +637,8 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
 }  // namespace
 }  // namespace rp
 
-// tcgen05 forward; same contract as rp_attn_fwd (include/rp/kernels.h) plus
-// 16-byte aligned q/k/v/o base pointers and pitches.
+// tcgen05 forward (include/rp/kernels.h): 16-byte aligned q/k/v/o base
+// pointers and pitches.
 extern "C" __attribute__((visibility("default"))) int rp_attn_fwd_tc(
     const void* q, int64_t ldq, const void* k, int64_t ldk, const void* v, int64_t ldv, void* o,
     int64_t ldo, float* lse, int32_t T, int32_t seq, int32_t nq, int32_t nk, int32_t head_dim,

@@ -630,12 +630,7 @@ RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const fl
   };
   // 256 threads above h = 1024: the row's dy / x / dres and the dw partials
   // live in registers, so fewer columns per thread keep occupancy up
-  static const bool narrow = getenv("RP_RMSNORM_BWD_128") != nullptr;  // A/B knob
-  if (narrow)
-    rn_dispatch(h, go, rmsnorm_bwd_kernel<128, 1>, rmsnorm_bwd_kernel<128, 2>,
-                rmsnorm_bwd_kernel<128, 3>, rmsnorm_bwd_kernel<128, 4>,
-                rmsnorm_bwd_kernel<256, 3>, rmsnorm_bwd_kernel<256, 4>);
-  else if (h <= 1024)
+  if (h <= 1024)
     go(rmsnorm_bwd_kernel<128, 1>, 128);
   else if (h <= 2048)
     go(rmsnorm_bwd_kernel<256, 1>, 256);

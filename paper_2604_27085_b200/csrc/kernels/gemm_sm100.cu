@@ -21,9 +21,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <mutex>
-#include <unordered_map>
 
+#include "kernels/launch_util.h"
 #include "kernels/sm100.cuh"
 #include "kernels/swiglu.cuh"
 #include "rp/kernels.h"
@@ -350,7 +349,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // and each CTA's TMEM receives its 128 rows. Both CTAs' TMA loads complete on
 // the leader's full barrier; MMA commits multicast to both CTAs' barriers;
 // epilogue warps of both CTAs release the accumulator on the leader's barrier.
-// Tile N is 256 (PBN; 128 is an opt-in variant, see pair_tile_n).
+// Tile N is 256 (PBN).
 constexpr int P_A_BYTES = 128 * BK * 2;     // 16 KB (this CTA's 128 rows of A)
 // fp32 epilogue staging for TMA store / reduce-add: per epilogue warp two
 // 32 x 32 fp32 chunks (SWIZZLE_128B rows of 128 B)
@@ -617,7 +616,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // flight while this one is computed; results overwrite the buffer in place
     // and leave through TMA stores
     uint32_t sw_ld = 0, sw_cs = 0;
-    const bool no_l2_prefetch = p.tma_swiglu == 2;
     uint8_t* sw_buf = epi_smem + q * 8192;
     auto sw_issue = [&](int col, int row) {
       if (lane == 0) {
@@ -644,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         sw_issue(n0, r0);
         // the rest of the tile's g/u into L2, so each chunk's smem load is an
         // L2 hit rather than a DRAM round trip (one chunk of smem look-ahead)
-        if (lane == 0 && !no_l2_prefetch)
+        if (lane == 0)
           for (int c = 32; c < min(PBN, p.N - n0); c += 32) {
             tma_prefetch_l2(&em.g, n0 + c, r0);
             tma_prefetch_l2(&em.u, n0 + c, r0);
@@ -907,64 +905,36 @@ int num_sms() {
   return n;
 }
 
-// Split-K workspace per stream (GEMMs on the compute and weight-gradient
+// Split-K scratch per stream (GEMMs on the compute and weight-gradient
 // streams may run concurrently): fp32 partial slabs + per-warp flags that
 // carry a launch epoch, so they never need resetting.
 struct SplitWs {
   float* ws = nullptr;
   unsigned* flags = nullptr;
-  std::size_t ws_elems = 0, n_flags = 0;
   unsigned epoch = 0;
 };
-SplitWs& split_ws(cudaStream_t st, std::size_t elems, std::size_t flags) {
-  static std::unordered_map<cudaStream_t, SplitWs> pool;
-  SplitWs& w = pool[st];
-  if (w.ws_elems < elems || w.n_flags < flags) {
-    if (w.ws) cudaFree(w.ws);
-    if (w.flags) cudaFree(w.flags);
-    w.ws_elems = std::max<std::size_t>(elems, (std::size_t)37 * 2 * 128 * 256);
-    w.n_flags = std::max<std::size_t>(flags, 37 * 8);
-    if (cudaMalloc(&w.ws, w.ws_elems * 4) != cudaSuccess ||
-        cudaMalloc(&w.flags, w.n_flags * 4) != cudaSuccess ||
-        cudaMemset(w.flags, 0, w.n_flags * 4) != cudaSuccess) {
-      cudaGetLastError();
-      w = SplitWs{};
-    }
-    w.epoch = 0;
-  }
-  return w;
+SplitWs split_ws(cudaStream_t st, std::size_t elems, std::size_t flags) {
+  Workspace* a = stream_workspace(st, WS_SPLITK_PARTIALS,
+                                  4 * std::max<std::size_t>(elems, (std::size_t)37 * 2 * 128 * 256));
+  Workspace* f = stream_workspace(st, WS_SPLITK_FLAGS, 4 * std::max<std::size_t>(flags, 37 * 8));
+  if (!a || !f) return SplitWs{};
+  return SplitWs{static_cast<float*>(a->p), static_cast<unsigned*>(f->p), ++f->epoch};
 }
 
-// Tile N for the CTA-pair kernel: 256. (256x128 pair tiles would fill the 74
-// pairs' last wave better for 4096-wide GEMMs, but measured at ~1.0 PF/s vs
-// ~1.35 for 256x256 on B200 — half-size MMAs double the per-k-block pipeline
-// overhead; RP_GEMM_TILE_N=128 keeps the variant selectable for study.)
-int pair_tile_n(int M, int N) {
-  (void)M;
-  (void)N;
-  static const int forced = [] {
-    const char* e = getenv("RP_GEMM_TILE_N");
-    return e ? atoi(e) : 0;
-  }();
-  return forced == 128 ? 128 : 256;
-}
+// Pair tiles are 256 x 256 (256 x 128 pair tiles would fill the 74 pairs'
+// last wave better for 4096-wide GEMMs, but measured ~1.0 PF/s vs ~1.35 on
+// B200: half-size MMAs double the per-k-block pipeline overhead).
+constexpr int PBN = 256;
 
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                    const EpiMaps& em, const Params& p, bool pair, int n_fastest,
                    cudaStream_t stream) {
   if (pair) {
-    const bool narrow = pair_tile_n(p.M, p.N) == 128;
-    const bool PBN_OK = !narrow;  // N halves of 256-wide tiles (em.bh built for K-major B)
-    auto kern = narrow ? gemm_pair_kernel<A_MN, B_MN, EPI, 128> : gemm_pair_kernel<A_MN, B_MN, EPI, 256>;
-    const int smem = narrow ? PairCfg<128, EPI>::SMEM : PairCfg<256, EPI>::SMEM;
-    static bool configured[2] = {false, false};
-    if (!configured[narrow]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      configured[narrow] = true;
-    }
-    const int pbn = narrow ? 128 : 256;
+    auto kern = gemm_pair_kernel<A_MN, B_MN, EPI, PBN>;
+    const int smem = PairCfg<PBN, EPI>::SMEM;
+    if (!ensure_smem_t(kern, smem)) return cudaErrorInvalidValue;
+    const int pbn = PBN;
     const int tn = EPI == EPI_SWIGLU_FWD ? pbn / 2 : pbn;  // output columns per tile
     const int tiles = ((p.M + 255) / 256) * ((p.N + tn - 1) / tn);
     const int npairs = num_sms() / 2;
@@ -976,23 +946,21 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     // K = 4096, where parking and re-reading the 128 KB fp32 partial per CTA
     // costs about what the shorter wave saves
     const int full = (tiles / npairs) * npairs, tail = tiles - full;
-    static const bool no_split = getenv("RP_GEMM_NO_SPLITK") != nullptr;
-    static const bool no_nsplit = getenv("RP_GEMM_NO_NSPLIT") != nullptr;
     // a short last wave at moderate K: its tiles become two 256 x PBN/2 halves
     // (no partials to reduce, unlike the K split); plain epilogues only
-    if (!no_nsplit && (EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_F32_ACC) && PBN_OK &&
+    if ((EPI == EPI_BF16 || EPI == EPI_F32 || EPI == EPI_F32_ACC) &&
         q.kb2 == 0 && tail > 0 && 2 * tail <= npairs && p.K < 8192) {
       q.full = full;
       q.units = full + 2 * tail;
       q.nsplit = 1;
-    } else if (!no_split && EPI != EPI_SWIGLU_BWD && EPI != EPI_SWIGLU_FWD && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
-      SplitWs& w = split_ws(stream, (std::size_t)tail * 2 * 128 * pbn, (std::size_t)tail * 8);
+    } else if (EPI != EPI_SWIGLU_BWD && EPI != EPI_SWIGLU_FWD && tail > 0 && 2 * tail <= npairs && p.K >= 8192) {
+      const SplitWs w = split_ws(stream, (std::size_t)tail * 2 * 128 * pbn, (std::size_t)tail * 8);
       if (w.ws) {
         q.full = full;
         q.units = full + 2 * tail;
         q.ws = w.ws;
         q.flags = w.flags;
-        q.epoch = ++w.epoch;
+        q.epoch = w.epoch;
       }
     }
     const int pairs = q.units < npairs ? q.units : npairs;
@@ -1002,12 +970,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   const bool skinny = p.N <= 32;
   auto kern = skinny ? gemm_kernel<A_MN, B_MN, EPI, 32> : gemm_kernel<A_MN, B_MN, EPI, 256>;
   const int smem = skinny ? SingleCfg<32, B_MN>::SMEM : SingleCfg<256, B_MN>::SMEM;
-  static bool configured[2] = {false, false};
-  if (!configured[skinny]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured[skinny] = true;
-  }
+  if (!ensure_smem_t(kern, smem)) return cudaErrorInvalidValue;
   const int tbn = skinny ? 32 : BN;
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
   const int grid = tiles < num_sms() ? tiles : num_sms();
@@ -1088,7 +1051,7 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                           : make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
   ok = ok && (g->b_mn_major ? make_map(&tb, g->B, g->K, g->N, g->ldb, 64, 64)
                             : make_map(&tb, g->B, dual ? 2LL * g->N : g->N, g->K, g->ldb, 64,
-                                       pair ? pair_tile_n(g->M, g->N) / 2
+                                       pair ? PBN / 2
                                             : g->N <= 32 ? 32 : BN));  // = launch()'s tile
   // raster: keep the larger operand's tile hot (walk the other dimension fastest)
   const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
@@ -1101,22 +1064,20 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
   // fp32 outputs of the pair kernel go through a TMA map (store / L2 reduce-add)
   CUtensorMap td;
   std::memset(&td, 0, sizeof(td));
-  static const bool no_tma_out = getenv("RP_GEMM_NO_TMA_EPI") != nullptr;
-  const bool tma_out = pair && g->out_f32 && !no_tma_out && (g->ldd * 4) % 16 == 0 &&
+  const bool tma_out = pair && g->out_f32 && (g->ldd * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                        make_map_f32(&td, g->D, g->M, g->N, g->ldd);
   EpiMaps em;
   std::memset(&em, 0, sizeof(em));
-  static const bool no_tma_swiglu = getenv("RP_GEMM_NO_TMA_SWIGLU") != nullptr;
   const auto* R16 = reinterpret_cast<const __nv_bfloat16*>(g->R);
   auto* D16 = reinterpret_cast<__nv_bfloat16*>(g->D);
-  const bool tma_swiglu = swiglu_bwd && pair && vec && !no_tma_swiglu &&
+  const bool tma_swiglu = swiglu_bwd && pair && vec &&
                           make_map_sw64(&em.g, R16, g->M, g->N, g->ldr) &&
                           make_map_sw64(&em.u, R16 + g->N, g->M, g->N, g->ldr) &&
                           make_map_sw64(&em.dg, D16, g->M, g->N, g->ldd) &&
                           make_map_sw64(&em.du, D16 + g->N, g->M, g->N, g->ldd);
   if (pair && !g->b_mn_major && !dual &&
-      !make_map(&em.bh, g->B, g->N, g->K, g->ldb, 64, pair_tile_n(g->M, g->N) / 4))
+      !make_map(&em.bh, g->B, g->N, g->K, g->ldb, 64, PBN / 4))
     return RP_E_CUDA;
   if (s2.K2 > 0) {  // second K segment: same majors and boxes as A / B
     if (!pair) return RP_E_INPUT;
@@ -1125,11 +1086,11 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                        : make_map(&em.a2, s2.A2, g->M, s2.K2, s2.lda2, 64, BM)) &&
         (g->b_mn_major ? make_map(&em.b2, s2.B2, s2.K2, g->N, s2.ldb2, 64, 64)
                        : make_map(&em.b2, s2.B2, dual ? 2LL * g->N : g->N, s2.K2, s2.ldb2, 64,
-                                  pair_tile_n(g->M, g->N) / 2));
+                                  PBN / 2));
     if (!ok2) return RP_E_CUDA;
   }
   Params p{g->M, g->N, g->K, g->D, g->ldd, R16, g->ldr, vec ? 1 : 0, tma_out ? 1 : 0,
-           tma_swiglu ? (getenv("RP_GEMM_NO_L2_PREFETCH") ? 2 : 1) : 0, trans ? 1 : 0, 0, 0,
+           tma_swiglu ? 1 : 0, trans ? 1 : 0, 0, 0,
            nullptr, nullptr, 0, act, ld_act, (s2.K2 + BK - 1) / BK};
   const int epi = dual ? EPI_SWIGLU_FWD : swiglu_bwd ? EPI_SWIGLU_BWD
                              : g->out_f32 ? (g->accumulate ? EPI_F32_ACC : EPI_F32) : EPI_BF16;

@@ -36,6 +36,7 @@
 #include <cstring>
 #include <thread>
 
+#include "kernels/launch_util.h"
 #include "runtime/runtime_internal.h"
 
 namespace rp {
@@ -267,6 +268,36 @@ struct Runtime {
   void init_weights();
   cudaEvent_t new_event(bool timing);
   void set_dev(const Gpu& G) { RP_CUDA(cudaSetDevice(G.dev)); }
+  // device memory of worker G (current device = G.dev), tracked for ~Runtime
+  void* dalloc(Gpu& G, std::size_t bytes, int cat) {
+    void* p = nullptr;
+    RP_CUDA(cudaMalloc(&p, std::max<std::size_t>(bytes, 256)));
+    G.allocated[cat] += bytes;
+    G.owned.push_back(p);
+    return p;
+  }
+  void dfree(Gpu& G, void* p) {
+    auto it = std::find(G.owned.begin(), G.owned.end(), p);
+    if (it == G.owned.end()) throw RtError(RP_E_INTERNAL, "freeing an untracked device buffer");
+    G.owned.erase(it);
+    RP_CUDA(cudaFree(p));
+  }
+  // stream `to` waits for everything enqueued on `from` so far (both on
+  // worker G's device); the fork events are reused round-robin (a wait
+  // captures the event's state when it is enqueued)
+  void join(Gpu& G, cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
+    if (!e) e = new_event(false);
+    RP_CUDA(cudaEventRecord(e, from));
+    RP_CUDA(cudaStreamWaitEvent(to, e, 0));
+  }
+  // producer P finished writing hand-off / checkpoint buffer b on stream st
+  void mark_ready(Slotbuf& b, const Gpu& P, cudaStream_t st) {
+    cudaEvent_t& e = b.ready_dev[P.dev];
+    if (!e) e = new_event(false);  // created on the producer's device (current)
+    RP_CUDA(cudaEventRecord(e, st));
+    b.ready = e;
+  }
   void d2d(void* dst, const Gpu& Gd, const void* src, const Gpu& Gs, std::size_t bytes,
            cudaStream_t st);
 
@@ -461,9 +492,10 @@ void Runtime::init(const rp_runtime_config_t& c) {
   lora_scale = lora_r > 0 ? (cfg.lora_alpha > 0 ? cfg.lora_alpha : (float)lora_r) / lora_r : 0.f;
   LL = make_layer_layout(s, lora_r);
   HL = make_head_layout(s);
-  if (const char* e = getenv("RP_LOGITS_ROWS")) {  // LM-head chunk rows (study knob)
-    const int r = atoi(e);
-    if (r >= 128 && r % 128 == 0) logits_rows = r;
+  if (cfg.logits_rows) {  // LM-head chunk rows
+    if (cfg.logits_rows < 128 || cfg.logits_rows % 128)
+      throw RtError(RP_E_INPUT, "logits_rows must be a positive multiple of 128");
+    logits_rows = cfg.logits_rows;
   }
   if (!(cfg.residency_factor > 0)) cfg.residency_factor = 2.0;
   if (cfg.adam.lr == 0.f && cfg.adam.beta1 == 0.f) {
@@ -517,17 +549,19 @@ void Runtime::init(const rp_runtime_config_t& c) {
 // Optimizer state in free HBM (single device only: with N devices a group's
 // grads land on a different device every iteration). Greedy over groups,
 // largest first, until the free memory minus a reserve is used; the rest
-// streams from pinned host memory as before. RP_RESIDENT_GB caps it (0 = off).
+// streams from pinned host memory. cfg.resident_state_gb: < 0 no cap, 0 off
+// (every group host-offloaded: BASELINE configs[2]), > 0 cap in GB.
 void Runtime::place_resident_state() {
   if (ndev != 1) return;
-  double cap_gb = 1e9;
-  if (const char* e = getenv("RP_RESIDENT_GB")) cap_gb = atof(e);
+  const double cap_gb = cfg.resident_state_gb < 0 ? 1e9 : cfg.resident_state_gb;
   if (cap_gb <= 0) return;
   set_dev(gpus[0]);
   std::size_t free_b = 0, total_b = 0;
   RP_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const std::size_t reserve = std::size_t(6) << 30;  // allocator, cuBLAS-free kernels, slack
-  int64_t budget = (int64_t)std::min<double>((double)free_b - (double)reserve, cap_gb * 1e9);
+  int64_t budget = (int64_t)free_b - (int64_t)reserve;  // device memory
+  const int64_t cap = (int64_t)std::min(cap_gb * 1e9, 9.0e18);  // resident state bytes
+  int64_t placed = 0;
   std::vector<int> order(ngroups());
   for (int g = 0; g < ngroups(); ++g) order[g] = g;
   std::stable_sort(order.begin(), order.end(),
@@ -541,14 +575,14 @@ void Runtime::place_resident_state() {
     if (n == 0) continue;  // frozen group
     const bool direct = N == 1;  // publish straight into the device weights
     const int64_t freed = n * 4 * (int64_t)gpus.size() + (direct ? host[g].n * 2 : 0);
-    if (n * 12 > budget + freed) continue;
+    if (n * 12 > budget + freed || placed + n * 12 > cap) continue;
     for (Gpu& G : gpus) {
       DevGroup& D = G.groups[g];
-      RP_CUDA(cudaFree(D.grad[1] + o));
+      dfree(G, D.grad[1] + o);
       D.grad[1] = D.grad[0];
       G.allocated[1] -= (std::size_t)n * 4;
       if (direct) {
-        RP_CUDA(cudaFree(D.pend));
+        dfree(G, D.pend);
         D.pend = nullptr;
         G.allocated[2] -= (std::size_t)host[g].n * 2;
       }
@@ -560,17 +594,15 @@ void Runtime::place_resident_state() {
       cudaGetLastError();
       for (Gpu& G : gpus) {  // undo: back to two buffers (and a pend buffer)
         DevGroup& D = G.groups[g];
-        float* q = nullptr;
-        RP_CUDA(cudaMalloc(&q, (std::size_t)n * 4));
-        D.grad[1] = q - o;
-        G.allocated[1] += (std::size_t)n * 4;
-        if (!D.pend) RP_CUDA(cudaMalloc(&D.pend, (std::size_t)host[g].n * 2));
+        D.grad[1] = static_cast<float*>(dalloc(G, (std::size_t)n * 4, 1)) - o;
+        if (!D.pend) D.pend = static_cast<uint16_t*>(dalloc(G, (std::size_t)host[g].n * 2, 2));
       }
       host[g].direct = false;
       break;
     }
     host[g].d_state = static_cast<float*>(p);
     budget -= n * 12;
+    placed += n * 12;
     resident_params += n;
     gpus[0].allocated[5] += (std::size_t)(n * 12);
     push_resident(g);
@@ -592,14 +624,16 @@ void Runtime::pull_w16(int g) {
   HostGroup& H = host[g];
   if (!H.direct || !H.w16_stale) return;
   DevGroup& D = gpus[0].groups[g];
-  for (int b = 0; b < 2; ++b)
-    if (D.loaded[b] == iter) {  // the version the next iteration computes with
-      set_dev(gpus[0]);
-      RP_CUDA(cudaMemcpy(H.w16 + H.t_off, D.w[b] + H.t_off, H.tn() * 2, cudaMemcpyDeviceToHost));
-      H.w16_stale = false;
-      return;
-    }
-  throw RtError(RP_E_INTERNAL, "direct group: next iteration's weights not on the device");
+  // the version the next iteration computes with: the newest one not beyond
+  // it (a pending staleness-1 update, version iter+1, is not published yet;
+  // without step() calls in between, the newest version is older than iter)
+  int b = -1;
+  for (int c = 0; c < 2; ++c)
+    if (D.loaded[c] >= 0 && D.loaded[c] <= iter && (b < 0 || D.loaded[c] > D.loaded[b])) b = c;
+  if (b < 0) throw RtError(RP_E_INTERNAL, "direct group: no current weights on the device");
+  set_dev(gpus[0]);
+  RP_CUDA(cudaMemcpy(H.w16 + H.t_off, D.w[b] + H.t_off, H.tn() * 2, cudaMemcpyDeviceToHost));
+  H.w16_stale = false;
 }
 
 void Runtime::pull_resident(int g) {
@@ -690,12 +724,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   mk(&G.opt_comp, lo);
   mk(&G.opt_res, lo);
   G.allocated.assign(8, 0);
-  auto dalloc = [&](std::size_t bytes, int cat) -> void* {
-    void* p = nullptr;
-    RP_CUDA(cudaMalloc(&p, std::max<std::size_t>(bytes, 256)));
-    G.allocated[cat] += bytes;
-    return p;
-  };
+  auto dalloc = [&](std::size_t bytes, int cat) -> void* { return this->dalloc(G, bytes, cat); };
   const int64_t Th = (int64_t)T * s.h;
   G.groups.resize(ngroups());
   for (int g = 0; g < ngroups(); ++g) {
@@ -721,8 +750,8 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   // step runs at the 1 kW power cap (the overlap lowers SM clocks instead),
   // while the second activation set costs 20.6 GB of HBM that otherwise holds
   // optimizer state
-  const char* pe = getenv("RP_FUSED_PIPELINE");
-  const bool pipe = plan.fused_stage.first == 0 && MR >= 2 && pe && pe[0] == '1';
+  const bool pipe =
+      plan.fused_stage.first == 0 && MR >= 2 && (cfg.flags & RP_RT_FUSED_PIPELINE);
   if (pipe) G.acts2.resize(nsets);
   for (auto* set : {&G.acts, &G.acts2})
   for (auto& A : *set) {
@@ -770,7 +799,6 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     G.ev_dx16_free[b] = new_event(false);
     G.ev_dqkv_free[b] = new_event(false);
   }
-  if (const char* e = getenv("RP_DGU_BUFS")) G.n_dgu = std::max(2, std::min(3, atoi(e)));
   for (int b = 0; b < G.n_dgu; ++b) {
     G.dgus[b] = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
     G.ev_dgu_free[b] = new_event(false);
@@ -816,7 +844,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     auto mkbuf = [&](std::size_t bytes, int cat) {
       Slotbuf b;
       b.p = dalloc(bytes, cat);
-      b.ready = new_event(false);
+      b.ready_dev.assign(ndev, nullptr);
       b.read = new_event(false);
       return b;
     };
@@ -996,7 +1024,7 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
-  static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
+  const bool unfused = cfg.flags & RP_RT_UNFUSED_SWIGLU;
   if (lora_r && !unfused && T >= 256) {  // LoRA: Us first, then the dual GEMM with [X | Us]
     const int r = lora_r;
     gemm(st, A.h2, h, false, W + LL.gu_A.off, h, false, A.u_gu, r, false, false, T, r, h);
@@ -1066,12 +1094,7 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   G.dgu_i = (G.dgu_i + 1) % G.n_dgu;
   uint16_t* dgu = G.dgus[pg];
   uint16_t* dqkv = G.dqkvs[p];
-  auto to_ws = [&]() {  // the wgrad stream waits for everything enqueued on compute so far
-    cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
-    if (!e) e = new_event(false);
-    RP_CUDA(cudaEventRecord(e, st));
-    RP_CUDA(cudaStreamWaitEvent(ws, e, 0));
-  };
+  auto to_ws = [&]() { join(G, st, ws); };  // wgrad waits for everything on compute so far
   const bool full = lora_r == 0;  // LoRA: base weights frozen, adapters trained
   if (first) {
     grad_free(G, l + 1, st);
@@ -1084,7 +1107,7 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   if (full) gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
   // full fine-tune: the SwiGLU backward runs in the dgrad GEMM's epilogue
   // (dact never reaches HBM); LoRA adds the adapter term to dact first
-  static const bool unfused = getenv("RP_NO_SWIGLU_FUSION") != nullptr;
+  const bool unfused = cfg.flags & RP_RT_UNFUSED_SWIGLU;
   const bool fuse = full && !unfused;
   const bool lora_fuse = !full && !unfused && T >= 256;
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[pg], 0));  // wgrad n_dgu layers ago read it
@@ -1285,12 +1308,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
   // Profiled steps run the plain order so kernel times stay their own.
   if (ss.kind == StageKind::Fused && a == 0 && !G.acts2.empty() && !prof_on) {
     cudaStream_t F = G.fwd2;
-    {
-      cudaEvent_t& e = G.fork_ev[G.fork_i++ & 63];
-      if (!e) e = new_event(false);
-      RP_CUDA(cudaEventRecord(e, st));  // uploads, tokens, edge-4 waits so far
-      RP_CUDA(cudaStreamWaitEvent(F, e, 0));
-    }
+    join(G, st, F);  // uploads, tokens, edge-4 waits so far
     auto wait_on = [&](cudaStream_t q, int g) {
       RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_upload[it & 1], 0));
     };
@@ -1386,12 +1404,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         // checkpoint x_l for the backward slot that recomputes layer l
         Gpu& O = gpus[worker_of(round, bwd_slot_of[l])];
         Slotbuf& ck = O.ckpt[((std::size_t)par * s.L + l) * MR + mb];
-        cudaEvent_t xr = new_event(false);
-        RP_CUDA(cudaEventRecord(xr, st));
-        RP_CUDA(cudaStreamWaitEvent(G.act, xr, 0));
+        join(G, st, G.act);
         RP_CUDA(cudaStreamWaitEvent(G.act, ck.read, 0));
         d2d(ck.p, O, x, G, Th2, G.act);
-        RP_CUDA(cudaEventRecord(ck.ready, G.act));
+        mark_ready(ck, G, G.act);
         wait_group(l + 1);
         uint16_t* out = x == G.xbuf[0] ? G.xbuf[1] : G.xbuf[0];
         RP_CUDA(cudaStreamWaitEvent(st, ck.ready, 0));  // x_l is overwritten next layer
@@ -1402,12 +1418,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
       if (in_buf) RP_CUDA(cudaEventRecord(in_buf->read, st));
       // hand x_{b+1} to the next slot
       Slotbuf& nb = next->hand_act[hb];
-      cudaEvent_t xr = new_event(false);
-      RP_CUDA(cudaEventRecord(xr, st));
-      RP_CUDA(cudaStreamWaitEvent(G.act, xr, 0));
+      join(G, st, G.act);
       RP_CUDA(cudaStreamWaitEvent(G.act, nb.read, 0));
       d2d(nb.p, *next, x, G, Th2, G.act);
-      RP_CUDA(cudaEventRecord(nb.ready, G.act));
+      mark_ready(nb, G, G.act);
       RP_CUDA(cudaStreamWaitEvent(st, nb.ready, 0));  // xbuf reuse
     } else if (ss.kind == StageKind::Fused) {
       const int nl = s.L - a;  // decoder layers inside the fused stage
@@ -1461,12 +1475,10 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         }
       } else {  // hand dL/dx_a to the next (backward) slot
         Slotbuf& nb = next->hand_grad[hb];
-        cudaEvent_t gr = new_event(false);
-        RP_CUDA(cudaEventRecord(gr, st));
-        RP_CUDA(cudaStreamWaitEvent(G.act, gr, 0));
+        join(G, st, G.act);
         RP_CUDA(cudaStreamWaitEvent(G.act, nb.read, 0));
         d2d(nb.p, *next, G.dx32[0], G, Th4, G.act);
-        RP_CUDA(cudaEventRecord(nb.ready, G.act));
+        mark_ready(nb, G, G.act);
         RP_CUDA(cudaStreamWaitEvent(st, nb.ready, 0));  // dx32 reuse
       }
     }
@@ -1500,13 +1512,20 @@ void Runtime::forward_backward(const int32_t* tokens, const int32_t* labels, flo
 // non-blocking form of forward_backward: with S=1 plans on N>1 GPUs the next
 // iteration runs on another GPU while this one finishes).
 void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
+  // ids index the embedding table and the logits row: validate them before
+  // anything is enqueued (an out-of-range id would make the gather /
+  // scatter-add kernels touch memory outside the table); labels < 0 are ignored
+  int64_t n_valid = 0;
+  for (int64_t i = 0; i < (int64_t)M * T; ++i) {
+    if (tokens[i] < 0 || tokens[i] >= s.V || labels[i] >= s.V)
+      throw RtError(RP_E_INPUT, "token id / label out of range at index " + std::to_string(i));
+    n_valid += labels[i] >= 0;
+  }
   const int it = iter++;
   last_iter = it;
   exec_iter = it;
   ensure_horizon(it);
   const int par = it & 1;
-  int64_t n_valid = 0;
-  for (int64_t i = 0; i < (int64_t)M * T; ++i) n_valid += labels[i] >= 0;
   const float grad_scale = n_valid > 0 ? 1.0f / (float)n_valid : 0.f;
   fused_worker.assign(N, 0);
   for (Gpu& G : gpus) {
@@ -1596,6 +1615,9 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     cudaStream_t q = G.opt_res;
     RP_CUDA(cudaStreamWaitEvent(q, D.ev_gradwrite, 0));  // edge (3)
     RP_CUDA(cudaStreamWaitEvent(q, D.ev_pcopy, 0));      // pend free again
+    // the shared d_state was last updated by another logical worker's
+    // optimizer stream (grads land on a different worker each iteration)
+    if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(q, state_ev[g], 0));
     cudaEvent_t xa = xfer_begin(q);
     const int pi_ = prof_begin(q);
     const int64_t tn = H.tn(), to = H.t_off;
@@ -1617,6 +1639,9 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     prof_end(pi_, q, 3, 30.0 * tn);
     ++kernels;
     RP_CUDA(cudaEventRecord(D.ev_adam[parity], q));
+    if (!D.ev_state) D.ev_state = new_event(false);
+    RP_CUDA(cudaEventRecord(D.ev_state, q));
+    state_ev[g] = D.ev_state;
     xfer_end(xa, q, 2, g - 1, last_iter, G.id);
     H.host_stale = true;
     if (H.direct) {  // published in place: no p_copy, no upload
@@ -1641,17 +1666,13 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     RP_CUDA(cudaMemcpyAsync(buf[1], H.m + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
     RP_CUDA(cudaMemcpyAsync(buf[2], H.v + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
     h2d_bytes += n * 12;
-    cudaEvent_t ev_in = new_event(false);
-    RP_CUDA(cudaEventRecord(ev_in, G.opt_h2d));
-    RP_CUDA(cudaStreamWaitEvent(G.opt_comp, ev_in, 0));
+    join(G, G.opt_h2d, G.opt_comp);
     const int pi_ = prof_begin(G.opt_comp);
     RP_K(rp_adamw(buf[0], buf[1], buf[2], D.grad[parity] + off, D.pend + off, n, &cfg.adam,
                   step_no, G.opt_comp));
     prof_end(pi_, G.opt_comp, 3, 30.0 * n);
     ++kernels;
-    cudaEvent_t ev_out = new_event(false);
-    RP_CUDA(cudaEventRecord(ev_out, G.opt_comp));
-    RP_CUDA(cudaStreamWaitEvent(G.opt_d2h, ev_out, 0));
+    join(G, G.opt_comp, G.opt_d2h);
     RP_CUDA(cudaMemcpyAsync(H.master + off, buf[0], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
     RP_CUDA(cudaMemcpyAsync(H.m + off, buf[1], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
     RP_CUDA(cudaMemcpyAsync(H.v + off, buf[2], n * 4, cudaMemcpyDeviceToHost, G.opt_d2h));
@@ -1694,6 +1715,10 @@ void Runtime::sync_all() {
   }
 }
 
+// Releases every device allocation (weights, grads, activations, hand-off
+// and checkpoint buffers, scratch, the optimizer ring, resident state), the
+// per-stream kernel workspaces, events and streams, so a new runtime in the
+// same process (e.g. a re-plan on measured costs) starts from a clean device.
 Runtime::~Runtime() {
   for (Gpu& G : gpus) {
     cudaSetDevice(G.dev);
@@ -1704,9 +1729,15 @@ Runtime::~Runtime() {
     cudaSetDevice(G.dev);
     for (cudaStream_t st : {G.compute, G.act, G.wgrad, G.w_h2d, G.opt_h2d, G.opt_d2h, G.opt_comp,
                             G.opt_res, G.fwd2})
-      if (st) cudaStreamDestroy(st);
+      if (st) {
+        release_stream_workspaces(st);
+        cudaStreamDestroy(st);
+      }
+    for (void* p : G.owned) cudaFree(p);
+    G.owned.clear();
   }
   if (loss_host) cudaFreeHost(loss_host);
+  if (!gpus.empty()) cudaSetDevice(gpus[0].dev);
   for (auto& H : host)
     if (H.d_state) cudaFree(H.d_state);
 }
@@ -1869,6 +1900,11 @@ RP_API int rp_set_params(rp_runtime_t* p, int32_t group, const float* values, in
     H.w16_stale = false;
     rt->push_resident(g);
     for (auto& G : rt->gpus) G.groups[g].loaded[0] = G.groups[g].loaded[1] = -1;
+    // a pending staleness-1 update was computed from the old values: drop it
+    // (pending gradients stay and are applied by the next step(), as an
+    // optimizer applies .grad to whatever the parameters hold)
+    rt->pend_owner[g] = -1;
+    rt->uploaders[g].clear();
   });
 }
 

@@ -117,11 +117,17 @@ struct LayerActs {
   cudaEvent_t ev_chain_free = nullptr;  // the dgrad chain done with this layer's activations
 };
 
-// A hand-off / checkpoint buffer with its producer and consumer events.
+// A hand-off / checkpoint buffer with its producer and consumer events. The
+// producer records `ready` on ITS stream after the write; cudaEventRecord
+// needs an event of the stream's device, and the producer of a checkpoint
+// buffer changes with the round, so there is one ready event per producer
+// device (created there on first use). The consumer (this buffer's device)
+// records `read` after its last read; cross-device waits on either are legal.
 struct Slotbuf {
   void* p = nullptr;
-  cudaEvent_t ready = nullptr;  // recorded by the producer after the write
-  cudaEvent_t read = nullptr;   // recorded by the consumer after the last read
+  std::vector<cudaEvent_t> ready_dev;  // by producer device
+  cudaEvent_t ready = nullptr;         // the one last recorded (what consumers wait on)
+  cudaEvent_t read = nullptr;
 };
 
 // One logical RoundPipe worker ("stateless GPU"). Workers map onto physical
@@ -138,7 +144,8 @@ struct Gpu {
   cudaStream_t wgrad = nullptr;
   uint16_t* dx16s[2] = {nullptr, nullptr};
   uint16_t* dgus[3] = {nullptr, nullptr, nullptr};  // ring: the fused down-dgrad
-  int n_dgu = 3, dgu_i = 0;                           // writes dgu one GEMM earlier
+  static constexpr int n_dgu = 3;                     // writes dgu one GEMM earlier
+  int dgu_i = 0;
   uint16_t* dqkvs[2] = {nullptr, nullptr};
   cudaEvent_t ev_dx16_free[2] = {nullptr, nullptr};
   cudaEvent_t ev_dgu_free[3] = {nullptr, nullptr, nullptr};
@@ -185,6 +192,7 @@ struct Gpu {
   cudaEvent_t anchor = nullptr;
   cudaEvent_t ev_tokens = nullptr;
   std::vector<std::size_t> allocated;
+  std::vector<void*> owned;  // every device allocation of this worker (freed by ~Runtime)
 };
 
 struct TaskRecord {

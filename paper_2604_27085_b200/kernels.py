@@ -195,14 +195,6 @@ def adamw(master, m, v, grad, w16, step, lr=1e-4, beta1=0.9, beta2=0.95, eps=1e-
           I64(master.numel()), C.byref(hp), I32(step), _stream(stream))
 
 
-def attn_fwd(q, k, v, o, lse, seq, nq, nk, hd, scale=None, stream=None):
-    T = q.shape[0]
-    scale = scale if scale is not None else hd ** -0.5
-    _call("rp_attn_fwd", _ptr(q), I64(q.stride(0)), _ptr(k), I64(k.stride(0)), _ptr(v),
-          I64(v.stride(0)), _ptr(o), I64(o.stride(0)), _ptr(lse), I32(T), I32(seq), I32(nq),
-          I32(nk), I32(hd), F(scale), _stream(stream))
-
-
 def attn_fwd_tc(q, k, v, o, lse, seq, nq, nk, hd, scale=None, stream=None):
     T = q.shape[0]
     scale = scale if scale is not None else hd ** -0.5
@@ -221,17 +213,6 @@ def attn_bwd_tc(q, k, v, o, do, lse, dq, dk, dv, delta, seq, nq, nk, hd, scale=N
           I64(v.stride(0)), _ptr(o), I64(o.stride(0)), _ptr(do), I64(do.stride(0)), _ptr(lse),
           _ptr(dq), I64(dq.stride(0)), _ptr(dk), I64(dk.stride(0)), _ptr(dv), I64(dv.stride(0)),
           _ptr(delta), _ptr(dkv_acc), I32(T), I32(seq), I32(nq), I32(nk), I32(hd), F(scale),
-          _stream(stream))
-
-
-def attn_bwd(q, k, v, o, do, lse, dq, dk, dv, dq_acc, delta, seq, nq, nk, hd, scale=None,
-             stream=None):
-    T = q.shape[0]
-    scale = scale if scale is not None else hd ** -0.5
-    _call("rp_attn_bwd", _ptr(q), I64(q.stride(0)), _ptr(k), I64(k.stride(0)), _ptr(v),
-          I64(v.stride(0)), _ptr(o), I64(o.stride(0)), _ptr(do), I64(do.stride(0)), _ptr(lse),
-          _ptr(dq), I64(dq.stride(0)), _ptr(dk), I64(dk.stride(0)), _ptr(dv), I64(dv.stride(0)),
-          _ptr(dq_acc), _ptr(delta), I32(T), I32(seq), I32(nq), I32(nk), I32(hd), F(scale),
           _stream(stream))
 
 

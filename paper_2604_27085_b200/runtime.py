@@ -20,6 +20,9 @@ P = C.POINTER
 
 RP_RT_SKIP_INIT = 1
 RP_RT_RECORD_TIMELINE = 2
+RP_RT_FUSED_PIPELINE = 4
+RP_RT_UNFUSED_SWIGLU = 8
+RP_RT_RECORD_PROTOCOL = 16
 
 
 class AdamC(C.Structure):
@@ -32,7 +35,8 @@ class RuntimeConfigC(C.Structure):
                 ("micro_batches", I32), ("round_micro_batches", I32), ("num_gpus", I32),
                 ("async_optimizer", I32), ("mem_limit_bytes", I64), ("residency_factor", F64),
                 ("costs", VP), ("n_costs", I32), ("adam", AdamC), ("init_seed", C.c_uint64),
-                ("init_std", F32), ("flags", I32), ("lora_rank", I32), ("lora_alpha", F32)]
+                ("init_std", F32), ("flags", I32), ("lora_rank", I32), ("lora_alpha", F32),
+                ("resident_state_gb", F64), ("logits_rows", I32), ("reserved_", I32)]
 
 
 class StatsC(C.Structure):
@@ -64,7 +68,13 @@ class RoundPipe:
                  num_gpus=1, round_micro_batches=0, async_optimizer=True, adam=AdamW(),
                  costs=None, mem_limit_bytes=0, residency_factor=2.0, init_seed=0,
                  init_std=0.02, skip_init=False, record_timeline=False, lora_rank=0,
-                 lora_alpha=0.0):
+                 lora_alpha=0.0, resident_state_gb=-1.0, logits_rows=0, fused_pipeline=False,
+                 unfused_swiglu=False, record_protocol=False):
+        """resident_state_gb: fp32 AdamW state placement on a single device —
+        < 0 keeps the groups that fit in free HBM resident (default), 0 keeps
+        all of it in pinned host memory (host-offloaded Adam, BASELINE
+        configs[2]), > 0 caps the resident part in GB. logits_rows: LM-head
+        chunk rows (0 = 2048)."""
         self.lib = _native.load()
         self._costs = None
         if costs is not None:
@@ -77,8 +87,11 @@ class RoundPipe:
             len(self._costs) if self._costs is not None else 0,
             AdamC(adam.lr, adam.betas[0], adam.betas[1], adam.eps, adam.weight_decay, 1.0),
             init_seed, init_std,
-            (RP_RT_SKIP_INIT if skip_init else 0) | (RP_RT_RECORD_TIMELINE if record_timeline else 0),
-            lora_rank, lora_alpha)
+            (RP_RT_SKIP_INIT if skip_init else 0) | (RP_RT_RECORD_TIMELINE if record_timeline else 0)
+            | (RP_RT_FUSED_PIPELINE if fused_pipeline else 0)
+            | (RP_RT_UNFUSED_SWIGLU if unfused_swiglu else 0)
+            | (RP_RT_RECORD_PROTOCOL if record_protocol else 0),
+            lora_rank, lora_alpha, float(resident_state_gb), int(logits_rows), 0)
         self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.h = VP()
         self._call("rp_runtime_create", C.byref(cfg), C.byref(self.h))
@@ -201,7 +214,10 @@ class RoundPipe:
     def forward_backward(self, tokens: np.ndarray, labels: np.ndarray) -> float:
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         labels = np.ascontiguousarray(labels, dtype=np.int32)
-        assert tokens.size == self.micro_batches * self.micro_batch * self.seq_len
+        n = self.micro_batches * self.micro_batch * self.seq_len
+        if tokens.size != n or labels.size != n:
+            raise ValueError(f"tokens/labels need {n} entries ([M, b, s]), got "
+                             f"{tokens.size} / {labels.size}")
         loss = F32()
         self._call("rp_forward_backward", self.h, tokens.ctypes.data_as(P(I32)),
                    labels.ctypes.data_as(P(I32)), C.byref(loss))
@@ -212,7 +228,10 @@ class RoundPipe:
         host buffers may be reused at once. Read the loss with loss(it)."""
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         labels = np.ascontiguousarray(labels, dtype=np.int32)
-        assert tokens.size == self.micro_batches * self.micro_batch * self.seq_len
+        n = self.micro_batches * self.micro_batch * self.seq_len
+        if tokens.size != n or labels.size != n:
+            raise ValueError(f"tokens/labels need {n} entries ([M, b, s]), got "
+                             f"{tokens.size} / {labels.size}")
         it = I32()
         self._call("rp_forward_backward_async", self.h, tokens.ctypes.data_as(P(I32)),
                    labels.ctypes.data_as(P(I32)), C.byref(it))

@@ -99,3 +99,16 @@ def test_gemm_and_elementwise_kernels_use_no_local_memory():
     if not found:
         pytest.skip("no in-tree build logs")
     assert not bad, bad
+
+
+def test_product_sources_have_no_env_knobs():
+    """Runtime options are fields of rp_runtime_config_t; the product library
+    reads no environment variables (round-1 A/B knobs removed)."""
+    csrc = os.path.join(ROOT, "paper_2604_27085_b200", "csrc")
+    hits = []
+    for d, _, files in os.walk(csrc):
+        for f in files:
+            if f.endswith((".cu", ".cpp", ".cuh", ".h", ".inc")):
+                text = open(os.path.join(d, f)).read()
+                hits += [f"{f}: {m}" for m in re.findall(r"getenv\([^)]*\)", text)]
+    assert not hits, hits

@@ -99,7 +99,7 @@ def test_gemm_split_k_last_wave(M, N, K, a_mn, b_mn):
     """Shapes whose last wave over the 74 CTA pairs is short (e.g. 256 tiles =
     3 waves + 34) run that wave as split-K halves: bf16, bf16+residual, fp32
     and fp32-accumulate epilogues all match torch, repeated launches (epochs)
-    included; RP_GEMM_NO_SPLITK would disable it."""
+    included."""
     from paper_2604_27085_b200 import kernels
     A, B, R = _mk(M, K, 11), _mk(N, K, 12), _mk(M, N, 13)
     Aop = A.t().contiguous() if a_mn else A

@@ -200,11 +200,6 @@ def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
     torch.cuda.synchronize()
     assert rel(o, oref) < 2e-2
     assert (lse - lref).abs().max().item() < 2e-2
-    o2 = torch.empty_like(o)
-    lse2 = torch.empty_like(lse)
-    K.attn_fwd(q, k, v, o2, lse2, seq, nq, nk, hd)
-    torch.cuda.synchronize()
-    assert rel(o, o2) < 1e-2
 
 
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
@@ -234,59 +229,3 @@ def test_flash_attention_bwd_tcgen05(T, seq, nq, nk, hd):
     assert rel(dq, qf.grad) < 2e-2
     assert rel(dk, kf.grad) < 2e-2
     assert rel(dv, vf.grad) < 2e-2
-
-
-@pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
-                                            (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64)])
-def test_flash_attention_fwd_bwd(T, seq, nq, nk, hd):
-    from paper_2604_27085_b200 import kernels as K
-    qkv = rnd(T, (nq + 2 * nk) * hd, seed=20)
-    q = qkv[:, : nq * hd]
-    k = qkv[:, nq * hd:(nq + nk) * hd]
-    v = qkv[:, (nq + nk) * hd:]
-    o = torch.empty(T, nq * hd, device="cuda", dtype=torch.bfloat16)
-    lse = torch.empty(nq, T, device="cuda")
-    K.attn_fwd(q, k, v, o, lse, seq, nq, nk, hd)
-    qf = q.float().requires_grad_(True)
-    kf = k.float().requires_grad_(True)
-    vf = v.float().requires_grad_(True)
-    oref, lref = _attn_ref(qf, kf, vf, seq, nq, nk, hd)
-    torch.cuda.synchronize()
-    assert rel(o, oref) < 2e-2
-    assert (lse - lref).abs().max().item() < 2e-2
-    do = rnd(T, nq * hd, seed=21)
-    oref.backward(do.float())
-    dqkv = torch.zeros_like(qkv)
-    dq, dk, dv = dqkv[:, : nq * hd], dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:]
-    dq_acc = torch.empty(T, nq * hd, device="cuda")
-    delta = torch.empty(nq, T, device="cuda")
-    K.attn_bwd(q, k, v, o, do, lse, dq, dk, dv, dq_acc, delta, seq, nq, nk, hd)
-    torch.cuda.synchronize()
-    assert rel(dq, qf.grad) < 2e-2
-    assert rel(dk, kf.grad) < 2e-2
-    assert rel(dv, vf.grad) < 2e-2
-
-
-def test_flash_attention_bwd_dkv3_variant():
-    """The opt-in K/V-in-TMEM dK/dV kernel (RP_ATTN_DKV3=1) matches torch too
-    (own process: the knob is read once per process)."""
-    import subprocess
-    import sys
-    env = dict(os.environ, RP_ATTN_DKV3="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
-                        "test_flash_attention_bwd_tcgen05", "-p", "no:cacheprovider"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-
-
-def test_flash_attention_bwd_split_path():
-    """The two-kernel backward (RP_ATTN_SPLIT=1: dK/dV kernel + dQ kernel that
-    recomputes S and dP) still matches torch; the default is the fused kernel
-    (own process: the knob is read once per process)."""
-    import subprocess
-    import sys
-    env = dict(os.environ, RP_ATTN_SPLIT="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
-                        "test_flash_attention_bwd_tcgen05", "-p", "no:cacheprovider"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -9,7 +9,7 @@ seed 1234, AdamW lr 1e-3 betas (0.9, 0.95) wd 0. Sync and async
     [3], fused [4], bwd [3], [2], [1], [0]) so the dispatcher, hand-offs,
     checkpoints and recompute all run; workers share the one B200.
 Tolerances (bf16 compute vs fp32 oracle):
-  loss rel <= 2e-3; per-tensor grads rel-L2 <= 3e-2 and cosine >= 0.999
+  loss rel <= 2e-3; per-tensor grads rel-L2 <= 2e-2 and cosine >= 0.999
   (tensors with norm > 1e-6); fp32 master after 3 steps rel-L2 <= 1e-2 and
   cosine(dW_gpu, dW_oracle) >= 0.98 for the accumulated update dW of every
   weight matrix (rel-L2 only for the 64..4096-element norm vectors). (AdamW
@@ -41,7 +41,7 @@ def uniform_costs(L1):
     return c
 
 
-def run_case(mode, N, costs=None, steps=3, timeline=False):
+def run_case(mode, N, costs=None, steps=3, timeline=False, **rt_kw):
     from paper_2604_27085_b200.runtime import AdamW, RoundPipe
     s = O.Shape.from_config("tiny")
     params = O.init_params(s, seed=0)
@@ -49,7 +49,7 @@ def run_case(mode, N, costs=None, steps=3, timeline=False):
     rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=N,
                    async_optimizer=(mode == "async"),
                    adam=AdamW(HP["lr"], HP["betas"], HP["eps"], HP["weight_decay"]),
-                   costs=costs, skip_init=True, record_timeline=timeline)
+                   costs=costs, skip_init=True, record_timeline=timeline, **rt_kw)
     rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
     losses, grads0 = [], None
     for it in range(steps):
@@ -102,7 +102,7 @@ def check(mode, losses, grads0, master):
         rel = (g - ref).norm().item() / rn
         cos = torch.nn.functional.cosine_similarity(g.flatten(), ref.flatten(), dim=0).item()
         gworst = max(gworst, (k, rel), key=lambda kv: kv[1])
-        assert rel < 3e-2 and cos > 0.999, (k, rel, cos)
+        assert rel < 2e-2 and cos > 0.999, (k, rel, cos)
     print(mode, "worst grad rel-L2", gworst)
     worst, cosd = {}, {}
     init = O.init_params(O.Shape.from_config("tiny"), seed=0)
@@ -115,7 +115,7 @@ def check(mode, losses, grads0, master):
     print(mode, "losses", losses, "oracle", ol)
     print(mode, "worst master rel-L2", max(worst.items(), key=lambda kv: kv[1]),
           "worst update cosine", min(cosd.items(), key=lambda kv: kv[1]))
-    assert max(worst.values()) < 2e-2, max(worst.items(), key=lambda kv: kv[1])
+    assert max(worst.values()) < 1e-2, max(worst.items(), key=lambda kv: kv[1])
     assert min(cosd.values()) > 0.98, min(cosd.items(), key=lambda kv: kv[1])
 
 
@@ -134,17 +134,21 @@ def test_multi_worker_grads_match_single_fused_stage():
     assert worst[1] < 1e-2, worst
 
 
-@pytest.mark.parametrize("variant", ["hbm", "streamed", "pipelined"])
+VARIANTS = {"hbm": {}, "streamed": {"resident_state_gb": 0.0},
+            "pipelined": {"fused_pipeline": True},
+            # LM head in 128-row chunks: the multi-chunk logits loop (wgrad
+            # accumulation across chunks) and the unfused SwiGLU kernels
+            "chunked_head": {"logits_rows": 128, "unfused_swiglu": True}}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("mode", ["sync", "async"])
-def test_step_parity_single_fused_stage(mode, variant, monkeypatch):
+def test_step_parity_single_fused_stage(mode, variant):
     """Single fused stage; the fp32 optimizer state either resident in free HBM
     (single-device default) or streamed from pinned host memory every step;
-    'pipelined' runs micro-batch k+1's forward beside k's backward."""
-    if variant == "streamed":
-        monkeypatch.setenv("RP_RESIDENT_GB", "0")
-    if variant == "pipelined":
-        monkeypatch.setenv("RP_FUSED_PIPELINE", "1")
-    losses, g0, master, _, (plan, durs) = run_case(mode, 1)
+    'pipelined' runs micro-batch k+1's forward beside k's backward;
+    'chunked_head' runs the LM head + CE over two 128-row logits chunks."""
+    losses, g0, master, _, (plan, durs) = run_case(mode, 1, **VARIANTS[variant])
     assert plan.num_slots() == 1 and plan.fused_stage.first == 0
     check(mode, losses, g0, master)
 
@@ -171,13 +175,11 @@ def test_step_parity_four_workers_seven_slots(mode):
 
 @pytest.mark.parametrize("resident", ["hbm", "streamed"])
 @pytest.mark.parametrize("mode", ["async", "sync"])
-def test_checkpoint_resume(mode, resident, tmp_path, monkeypatch):
+def test_checkpoint_resume(mode, resident, tmp_path):
     """Host-state checkpoint (SURVEY 8(f)3): save after 2 steps, continue 2;
     a fresh runtime resumed from the file reproduces steps 3-4 (losses and the
     fp32 master), including async mode's unpublished staleness-1 update."""
     from paper_2604_27085_b200.runtime import AdamW, RoundPipe
-    if resident == "streamed":
-        monkeypatch.setenv("RP_RESIDENT_GB", "0")
     s = O.Shape.from_config("tiny")
     params = O.init_params(s, seed=0)
     tok, lab = O.synthetic_batch(s, 4, 1, 256)
@@ -186,7 +188,7 @@ def test_checkpoint_resume(mode, resident, tmp_path, monkeypatch):
         rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=1,
                        async_optimizer=(mode == "async"),
                        adam=AdamW(HP["lr"], HP["betas"], HP["eps"], HP["weight_decay"]),
-                       skip_init=True)
+                       skip_init=True, resident_state_gb=0.0 if resident == "streamed" else -1.0)
         return rt
 
     rt = make()
@@ -375,3 +377,86 @@ def test_lora_step_parity(N):
                                   params[k].numpy().reshape(-1)), k
     assert np.array_equal(np.asarray(w["head.lm_head"]).reshape(-1),
                           params["head.lm_head"].numpy().reshape(-1))
+
+
+def test_sync_direct_group_reads_after_repeated_forward(tmp_path):
+    """Sync mode, single device, HBM-resident groups publishing in place:
+    forward_backward twice without step() in between, then read weights,
+    grads and a checkpoint (the bf16 readback wanted version ==
+    iter and threw). The bf16 weights read back are bf16(fp32 master)."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    params = O.init_params(s, seed=0)
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=1,
+                   async_optimizer=False, adam=AdamW(**HP), skip_init=True)
+    rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+    assert rt.stats()["resident_params"] > 0
+    rt.forward_backward(tok.numpy(), lab.numpy())
+    rt.step()
+    rt.forward_backward(tok.numpy(), lab.numpy())
+    rt.forward_backward(tok.numpy(), lab.numpy())  # no step() in between
+    g = rt.read_state(s.layers, which=2)
+    w16 = rt.read_state(s.layers, which=1)
+    m32 = rt.read_state(s.layers, which=0)
+    rt.save(str(tmp_path / "ck.rpck"))
+    rt.close()
+    assert np.isfinite(g["layers.0.qkv"]).all() and np.abs(g["layers.0.qkv"]).sum() > 0
+    for k in ("layers.0.qkv", "head.lm_head", "embed"):
+        ref = torch.from_numpy(np.asarray(m32[k])).to(torch.bfloat16).float().numpy()
+        assert np.array_equal(np.asarray(w16[k]), ref), k
+
+
+def test_out_of_range_ids_are_rejected():
+    """Token ids outside [0, V) and labels >= V are rejected before anything
+    is enqueued (ADVICE r01: they reached the gather / scatter-add kernels);
+    the runtime stays usable afterwards."""
+    from paper_2604_27085_b200._native import NativeError
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=1,
+                   async_optimizer=False, adam=AdamW(**HP))
+    bad = tok.numpy().copy()
+    bad[1, 0, 7] = s.vocab
+    with pytest.raises(NativeError):
+        rt.forward_backward(bad, lab.numpy())
+    bad = tok.numpy().copy()
+    bad[0, 0, 0] = -1
+    with pytest.raises(NativeError):
+        rt.forward_backward(bad, lab.numpy())
+    badl = lab.numpy().copy()
+    badl[3, 0, 255] = s.vocab + 5
+    with pytest.raises(NativeError):
+        rt.forward_backward(tok.numpy(), badl)
+    with pytest.raises(ValueError):
+        rt.forward_backward(tok.numpy(), lab.numpy()[:2])
+    loss = rt.forward_backward(tok.numpy(), lab.numpy())
+    rt.close()
+    assert np.isfinite(loss) and abs(loss - np.log(s.vocab)) < 0.5
+
+
+@pytest.mark.parametrize("N", [1, 4])
+def test_destroy_releases_device_memory(N):
+    """rp_runtime_destroy frees every device allocation of every worker
+    (only the resident state was freed), so creating and
+    destroying runtimes in one process does not leak HBM."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    torch.cuda.synchronize()
+
+    def cycle():
+        rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=N,
+                       async_optimizer=True, adam=AdamW(**HP),
+                       costs=uniform_costs(5) if N == 4 else None)
+        rt.forward_backward(tok.numpy(), lab.numpy())
+        rt.step()
+        rt.sync()
+        rt.close()
+    cycle()  # first cycle: kernel workspaces, module loading
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(3):
+        cycle()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < (64 << 20), (free0, free1)

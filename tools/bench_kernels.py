@@ -31,18 +31,11 @@ def main():
     o = torch.empty(T, nq * hd, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(nq, T, device="cuda")
     flops = 4.0 * nq * hd * seq * seq / 2 * (T // seq)  # causal
-    ms = bench(lambda: K.attn_fwd(q, k, v, o, lse, seq, nq, nk, hd))
-    out.append({"kernel": "attn_fwd", "ms": ms, "tflops": flops / ms / 1e9})
     ms = bench(lambda: K.attn_fwd_tc(q, k, v, o, lse, seq, nq, nk, hd))
     out.append({"kernel": "attn_fwd_tc", "ms": ms, "tflops": flops / ms / 1e9})
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
-    dq_acc = torch.empty(T, nq * hd, device="cuda")
     delta = torch.empty(nq, T, device="cuda")
-    ms = bench(lambda: K.attn_bwd(q, k, v, o, do, lse, dqkv[:, :nq * hd],
-                                  dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:],
-                                  dq_acc, delta, seq, nq, nk, hd))
-    out.append({"kernel": "attn_bwd", "ms": ms, "tflops": 2.5 * flops / ms / 1e9})
     ms = bench(lambda: K.attn_bwd_tc(q, k, v, o, do, lse, dqkv[:, :nq * hd],
                                      dqkv[:, nq * hd:(nq + nk) * hd], dqkv[:, (nq + nk) * hd:],
                                      delta, seq, nq, nk, hd))
