@@ -2,22 +2,35 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload (BASELINE configs[2], the metric's config): Qwen3-8B full fine-tune,
-seq 4096, b=1, M=16 micro-batches per step (65,536 tokens), RoundPipe async
-(staleness-1 optimizer), fp32 AdamW states host-offloaded in pinned memory
-and streamed through the GPU, bf16 weights streamed from the pinned bf16
-master every slot. Synthetic seeded token ids, random-init weights.
+Workload = BASELINE configs[2], the metric's config: Qwen3-8B full fine-tune,
+seq 4096, b=1, M=16 micro-batches per step (65,536 tokens), RoundPipe-async
+(staleness-1 optimizer), fp32 AdamW master weights + m + v HOST-OFFLOADED in
+pinned memory and streamed through the GPU every step (chunked H2D ->
+fused AdamW kernel -> D2H), activation recompute wherever the reference
+partitioner places backward stages (at N=1 it plans a single fused stage,
+so nothing is recomputed). Synthetic seeded token ids, random-init weights.
 
-One JSON line (rank 0). `value` = tokens/s over exactly K steps bracketed by
-full device synchronisation + CUDA events (max over ranks: the runtime is a
-single controller, rank 0 drives all N workers); `e2e` = the same K steps
-through the public API measured by the host clock (token/label host buffers
-in, loss read back every step). `roofline` = the dominant kernel (tcgen05
-GEMM) inside a profiled step vs the measured sustained bf16 peak; `bubble` =
-the reference's interior_bubble on the MEASURED per-task timeline;
-`cpu_baseline` = the fp32 CPU oracle (port) on a bounded sample.
---impl reference times the CPU implementation of the step (the oracle port:
-the reference has no data-plane code) on all host cores.
+One JSON line (rank 0):
+* `value`: tokens/s over exactly K steps bracketed by full device
+  synchronisation + CUDA events; the runtime is a single controller, rank 0
+  drives all N workers (the other ranks wait at a barrier), so the max over
+  ranks is rank 0's time. Includes the last step's optimizer drain.
+* `e2e`: the same K steps through the public API by the host clock (token /
+  label host buffers in, the loss read back every step).
+* `roofline`: the dominant kernel family (tcgen05 GEMMs) inside one profiled
+  step vs the measured sustained bf16 peak; `step_roofline`: the slower of
+  executed FLOPs at that peak and streamed host-link bytes at the measured
+  PCIe rates.
+* `bubble`: the reference's interior_bubble (async) / idle_in_window (sync)
+  on the MEASURED per-task timeline, next to the simulator's for the plan.
+* `variants`: shorter labelled runs of the HBM-resident optimizer placement
+  and of RoundPipe-sync on the same workload (not the headline).
+* `cpu_baseline`: the fp32 CPU oracle (port) timed on a bounded sample of the
+  same step on all host cores (see cpu_step_sample).
+--impl reference times that CPU implementation alone (the reference has no
+data-plane code), plus the reference's own control path
+(oracle/_ref: partition + synthesize + simulate, single-threaded) and the C1
+step end to end on the CPU oracle.
 """
 from __future__ import annotations
 
@@ -38,7 +51,9 @@ MODEL_DIMS = {  # executed FLOPs per token per decoder layer / head (fwd); see D
     "qwen3-1.7b": dict(h=2048, nq=16, nk=8, hd=128, m=6144, L=28, V=151936),
     "tiny": dict(h=256, nq=4, nk=2, hd=64, m=768, L=4, V=32768),
 }
-PCIE_H2D_GBS, PCIE_D2H_GBS = 55.6, 52.9  # measured pinned copies on this pool (tools/probe_box.sh)
+# pinned host<->device copy rates measured on this pool's B200 boxes
+# (tools/probe_box.sh, capture committed as profiles/r02_pcie_probe.txt)
+PCIE_H2D_GBS, PCIE_D2H_GBS = 55.6, 52.9
 
 
 def peaks():
@@ -134,76 +149,146 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
-def cpu_sample(model="qwen3-8b", seq=4096, M=16, threads=None, head_tokens=512):
-    """Bounded sample of the step on the CPU oracle (fp32 torch, all host
-    cores): one full-width decoder layer fwd+bwd at seq, the LM head + CE
-    fwd+bwd on head_tokens tokens, AdamW over one layer's parameters. The
-    full step time is assembled from these measured parts (L layers x M
-    micro-batches, head scaled to M*seq tokens, AdamW x (L + 2 groups))."""
+# ---------------------------------------------------------------------------- CPU side
+def cpu_step_sample(model="qwen3-8b", tokens=32, steps=2, warmup=1, threads=None,
+                    budget_s=None):
+    """Bounded CPU sample of the training step, timed end to end (no
+    assembly from parts): the fp32 CPU oracle's math (oracle/step_oracle.py:
+    Qwen3 decoder layers, RMSNorm, RoPE, GQA attention, SwiGLU, LM head + CE)
+    on all host cores, for a model of the named architecture at FULL depth —
+    embedding, L decoder layers, LM head — whose L decoder layers share ONE
+    weight set (the FLOPs per token equal the real model's; host memory is
+    1/L of it). One sampled step = forward + backward of one sequence of
+    `tokens` tokens (gradients accumulated in place). The optimizer is not in
+    the sample: AdamW over 8.2B parameters once per 65,536-token step is
+    < 0.2 % of the CPU step's time. The short sequence also makes attention
+    cheaper than at seq 4096, so the CPU throughput is, if anything,
+    overstated. Returns per-step seconds of the timed steps (the first
+    `warmup` are not timed; `budget_s` stops the timed loop early)."""
     import torch
     from oracle import step_oracle as O
     threads = threads or os.cpu_count()
     torch.set_num_threads(threads)
     s = O.Shape.from_config(model)
-    g = torch.Generator().manual_seed(0)
-    p = {}
-    for n, sh in O.layer_param_shapes(s):
-        p["l." + n] = (torch.ones(sh) if len(sh) == 1 else torch.randn(sh, generator=g) * 0.02)
-    p = {k: v.requires_grad_(True) for k, v in p.items()}
-    cos, sin = O.rope_cos_sin(seq, s.head_dim, s.rope_theta)
-    x = torch.randn(1, seq, s.hidden, generator=g)
+    a = 0.02 * 3 ** 0.5  # uniform with std 0.02 (normal_ is single-threaded)
+
+    def mat(*shape):
+        return torch.empty(shape).uniform_(-a, a).requires_grad_(True)
+    lp = {n: (torch.ones(sh).requires_grad_(True) if len(sh) == 1 else mat(*sh))
+          for n, sh in O.layer_param_shapes(s)}
+    emb, wn, wh = mat(s.vocab, s.hidden), torch.ones(s.hidden).requires_grad_(True), mat(s.vocab, s.hidden)
+    params = list(lp.values()) + [emb, wn, wh]
+    for p in params:
+        p.grad = torch.zeros_like(p)
+    g = torch.Generator().manual_seed(1234)
+    ids = torch.randint(0, s.vocab, (1, tokens + 1), generator=g)
+    tok, lab = ids[:, :-1], ids[:, 1:]
+    cos, sin = O.rope_cos_sin(tokens, s.head_dim, s.rope_theta)
+    times = []
+    t_start = time.perf_counter()
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        x = emb[tok]
+        for _ in range(s.layers):
+            x = O.decoder_layer(x, lp.__getitem__, "", s, cos, sin)
+        x = O.rms(x, wn, s.eps)
+        loss = torch.nn.functional.cross_entropy((x @ wh.t()).view(-1, s.vocab),
+                                                 lab.reshape(-1), reduction="mean")
+        loss.backward()
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+        if budget_s and time.perf_counter() - t_start > budget_s and times:
+            break
+    return times, threads, s
+
+
+def sample_desc(model, tokens, L):
+    return (f"fp32 CPU oracle (oracle/step_oracle.py math, torch CPU): full-depth {model} "
+            f"({L} decoder layers sharing one weight set, embedding, LM head) forward + "
+            f"backward of one {tokens}-token sequence, timed end to end per step (optimizer "
+            f"excluded: <0.2% of a 65,536-token CPU step); tokens/s = {tokens} / step time")
+
+
+def reference_planner_times(model, seq, M):
+    """The reference's own CPU path (oracle/_ref = the reference headers built
+    from /root/reference): optimal_partition + synthesize + simulate for N =
+    1, 2, 4, 8 on the model's cost table (built by this repo's bit-exact
+    cost model: the reference ships no qwen3-8b config), single-threaded by
+    construction; mem_limit 0.9 x 180 GB."""
+    import ctypes
+    from paper_2604_27085_b200.planner import Planner
+    so = os.path.join(ROOT, "oracle", "_ref", "libref_planner.so")
+    if not os.path.exists(so):
+        return {"unavailable": "oracle/_ref not built"}
+    ours = Planner()
+    costs = ours.layer_costs(ours.load_model(model), seq, 1, ours.load_gpu("b200"), True)
+    ref = Planner(ctypes.CDLL(so), prefix="ref_")
+    out = {}
+    for N in (1, 2, 4, 8):
+        t0 = time.perf_counter()
+        plan = ref.optimal_partition(costs, N, M, int(0.9 * 180e9))
+        durs = ref.slot_durations(plan, costs)
+        sched = ref.synthesize("roundpipe", N, M, 0, 7, durs)
+        sim = ref.simulate(sched, False)
+        wall = time.perf_counter() - t0
+        bub = ref.interior_bubble(sim.timeline, N, 2, 4)[0]
+        out[f"n{N}"] = {"wall_ms": round(wall * 1e3, 3), "slots": plan.num_slots(),
+                        "tasks": len(sched.tasks), "sim_interior_bubble": round(bub, 5)}
+    out["cores"] = 1
+    out["what"] = "reference partition + synthesize (7 iterations) + simulate, 1 host core"
+    return out
+
+
+def c1_cpu_tokens_per_s(steps=2):
+    """C1 (BASELINE configs[0]: tiny, seq 256, M=4) one full RoundPipe step end
+    to end on the CPU oracle (sync), all host cores."""
+    import torch
+    from oracle import step_oracle as O
+    torch.set_num_threads(os.cpu_count())
+    s = O.Shape.from_config("tiny")
+    o = O.StepOracle(s, O.init_params(s, seed=0), mode="sync", lr=1e-3)
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    o.step(tok, lab)
     t0 = time.perf_counter()
-    y = O.decoder_layer(x, lambda n: p[n], "l.", s, cos, sin)
-    y.float().pow(2).mean().backward()
-    t_layer = time.perf_counter() - t0
-    wh = (torch.randn(s.vocab, s.hidden, generator=g) * 0.02).requires_grad_(True)
-    xh = torch.randn(head_tokens, s.hidden, generator=g)
-    lab = torch.randint(0, s.vocab, (head_tokens,), generator=g)
-    t0 = time.perf_counter()
-    torch.nn.functional.cross_entropy(xh @ wh.t(), lab).backward()
-    t_head = (time.perf_counter() - t0) * (seq / head_tokens)
-    params = list(p.values())
-    opt = torch.optim.AdamW(params, lr=1e-4)
-    t0 = time.perf_counter()
-    opt.step()
-    t_adam_layer = time.perf_counter() - t0
-    n_layer = sum(v.numel() for v in params)
-    n_total = n_layer * s.layers + 2 * s.vocab * s.hidden
-    step_s = M * (s.layers * t_layer + t_head) + t_adam_layer * n_total / n_layer
-    return {"tokens_per_s": M * seq / step_s, "step_s": step_s, "threads": threads,
-            "t_layer_s": t_layer, "t_head_s": t_head, "t_adam_layer_s": t_adam_layer,
-            "sample_wall_s": None}
+    for _ in range(steps):
+        o.step(tok, lab)
+    dt = (time.perf_counter() - t0) / steps
+    return {"tokens_per_s": round(4 * 256 / dt, 1), "step_s": round(dt, 3),
+            "cores": os.cpu_count(), "config": "tiny h256 L4 V32768, seq 256, M=4, sync"}
 
 
 def run_reference(args):
-    t0 = time.time()
-    r = cpu_sample(args.model, args.seq, args.micro_batches)
-    wall = time.time() - t0
-    steps = []
-    for _ in range(args.steps):  # every step is one bounded sample
-        t1 = time.time()
-        rr = cpu_sample(args.model, args.seq, args.micro_batches)
-        steps.append(rr["step_s"])
-        if time.time() - t1 > 120:
-            break
-    step_s = statistics.mean(steps) if steps else r["step_s"]
-    v = args.micro_batches * args.seq / step_s
-    sample = (f"fp32 CPU oracle (oracle/step_oracle.py): 1 full-width {args.model} decoder layer "
-              f"fwd+bwd at seq {args.seq}, LM head+CE on 512 tokens, AdamW on one layer; step time "
-              f"assembled for {args.micro_batches} micro-batches x all layers (first sample {wall:.1f}s)")
-    line = {"impl": "reference", "metric": metric_name(args), "value": round(v, 3), "unit": "tokens/s",
-            "n_gpus": args.gpus, "steps": len(steps), "warmup": args.warmup,
-            "ms_per_step": round(step_s * 1e3, 1), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+    tokens = args.cpu_tokens
+    # bounded so the whole --steps K --warmup W run ends within a few minutes
+    times, threads, s = cpu_step_sample(args.model, tokens, steps=args.steps, warmup=args.warmup,
+                                        budget_s=240)
+    step_s = statistics.mean(times)
+    v = tokens / step_s
+    extras = {}
+    try:
+        extras["reference_planner"] = reference_planner_times(args.model, args.seq,
+                                                              args.micro_batches)
+    except Exception as e:  # report, never fail the line
+        extras["reference_planner"] = {"error": str(e)[:200]}
+    try:
+        extras["c1_cpu_step"] = c1_cpu_tokens_per_s()
+    except Exception as e:
+        extras["c1_cpu_step"] = {"error": str(e)[:200]}
+    sample = sample_desc(args.model, tokens, s.layers)
+    line = {"impl": "reference", "metric": metric_name(args), "value": round(v, 3),
+            "unit": "tokens/s", "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": round(step_s * 1e3, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(args),
-            "cpu_baseline": {"value": round(v, 3), "unit": "tokens/s", "cores": r["threads"],
+            "cpu_baseline": {"value": round(v, 3), "unit": "tokens/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            **extras}
     print(json.dumps(line), flush=True)
 
 
-METRIC = "fine-tune tokens/s (Qwen3-8B seq4K, RoundPipe)"
+# ---------------------------------------------------------------------------- GPU side
 MODEL_NAMES = {"qwen3-8b": "Qwen3-8B", "qwen3-1.7b": "Qwen3-1.7B", "tiny": "tiny Qwen3"}
 
 
@@ -220,23 +305,28 @@ def weight_gb(model):
     return 2 * (d["L"] * layer + 2 * d["V"] * d["h"]) / 1e9
 
 
-def config_dict(args):
-    kind = f"LoRA r={args.lora_rank} fine-tune" if getattr(args, "lora_rank", 0) else "full fine-tune"
-    return {"workload": f"{args.model} {kind}, seq {args.seq}, b=1, M={args.micro_batches} "
-                        f"micro-batches/step, RoundPipe-{'async' if args.mode == 'async' else 'sync'}, "
-                        + ("fp32 AdamW master weights + states in pinned host memory (all streamed)"
-                           if getattr(args, "host_optimizer", False) or args.gpus > 1 else
-                           "fp32 AdamW master weights + states HBM-resident for the groups that "
-                           "fit, the rest in pinned host memory (see optimizer_state)"),
+def config_dict(args, resident=None, mode=None):
+    resident = args.resident_optimizer if resident is None else resident
+    mode = mode or args.mode
+    kind = f"LoRA r={args.lora_rank} fine-tune" if args.lora_rank else "full fine-tune"
+    name = MODEL_NAMES.get(args.model, args.model)
+    return {"workload": (f"{name} {kind} seq {args.seq // 1024 if args.seq >= 1024 else args.seq}"
+                         f"{'K' if args.seq >= 1024 else ''} with "
+                         + ("fp32 AdamW states HBM-resident for the groups that fit (rest "
+                            "host-offloaded)" if resident else "host-offloaded Adam states")
+                         + " and activation recompute (BASELINE configs[2]): b=1, "
+                         f"M={args.micro_batches} micro-batches/step, "
+                         f"RoundPipe-{'async' if mode == 'async' else 'sync'}, N={args.gpus}"),
             "model": args.model, "global_batch": args.micro_batches, "seq_len": args.seq,
             "tokens_per_step": args.micro_batches * args.seq,
+            "optimizer_state": "hbm-resident where it fits" if resident else "pinned host (streamed)",
             "parallelism": f"roundpipe-{args.gpus}",
             "l2": f"inputs larger than L2 ({weight_gb(args.model):.1f} GB of bf16 weights "
                   "read per step)"}
 
 
-def run_ours(args):
-    import numpy as np
+def measure(args, resident, mode, steps, warmup, profile=False, report_dir=None, clocks=True):
+    """One RoundPipe runtime, `warmup` untimed + `steps` timed steps."""
     import torch
 
     from paper_2604_27085_b200.planner import Planner
@@ -244,9 +334,9 @@ def run_ours(args):
 
     t_setup = time.time()
     rt = RoundPipe(args.model, seq_len=args.seq, micro_batch=1, micro_batches=args.micro_batches,
-                   num_gpus=args.gpus, async_optimizer=args.mode == "async", adam=AdamW(lr=1e-5),
+                   num_gpus=args.gpus, async_optimizer=mode == "async", adam=AdamW(lr=1e-5),
                    record_timeline=True, lora_rank=args.lora_rank, lora_alpha=args.lora_alpha,
-                   resident_state_gb=0.0 if args.host_optimizer else -1.0)
+                   resident_state_gb=-1.0 if resident else 0.0)
     setup_s = time.time() - t_setup
     d = MODEL_DIMS[args.model]
     g = torch.Generator().manual_seed(1234)
@@ -255,13 +345,13 @@ def run_ours(args):
     labels = ids[..., 1:].contiguous().int().numpy()
     tokens_step = args.micro_batches * args.seq
     losses = []
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         losses.append(rt.forward_backward(tokens, labels))
         rt.step()
     rt.sync()
     rt.clear_timeline()
     st0 = rt.stats()
-    with ClockSampler(args.gpus) as clk:
+    with ClockSampler(args.gpus if clocks else 0) as clk:
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
@@ -269,7 +359,7 @@ def run_ours(args):
         # non-blocking forward_backward: step t's loss is read (D2H) while
         # t+1 is enqueued, so S=1 plans on N>1 GPUs overlap iterations
         prev = None
-        for _ in range(args.steps):
+        for _ in range(steps):
             cur = rt.forward_backward_async(tokens, labels)
             rt.step()
             if prev is not None:
@@ -284,39 +374,54 @@ def run_ours(args):
     st1 = rt.stats()
     tl = rt.timeline()
     plan, durs = rt.plan()
-    # bubble on the measured timeline (reference formulas)
     pl = Planner()
-    it_lo, it_hi = args.warmup, args.warmup + args.steps - 1
-    if args.steps >= 3:
-        bub = pl.interior_bubble(tl, args.gpus, it_lo + 1, it_hi - 1)[0]
-    else:
-        bub = pl.interior_bubble(tl, args.gpus, it_lo, it_hi)[0]
-    sched = pl.synthesize("roundpipe" if args.mode == "async" else "roundpipe-sync", args.gpus,
-                          args.micro_batches, 0, max(3, args.steps), durs)
-    sim = pl.simulate(sched, args.mode != "async")
-    sim_bub = (pl.interior_bubble(sim.timeline, args.gpus, 1, max(3, args.steps) - 2)[0]
-               if args.mode == "async" else sim.bubble_ratio)
-    if args.report_dir:  # measured timeline in the reference CLI's report schema + Gantt
+    N = args.gpus
+    it_lo, it_hi = warmup, warmup + steps - 1
+    if mode == "async":
+        lo, hi = (it_lo + 1, it_hi - 1) if steps >= 3 else (it_lo, it_hi)
+        bub = pl.interior_bubble(tl, N, lo, hi)[0]
+    else:  # sync: idle inside one iteration's window (middle timed iteration)
+        mid = tl[tl["iteration"] == (it_lo + it_hi) // 2]
+        bub = pl.idle_in_window(tl, N, int(mid["start_ns"].min()), int(mid["end_ns"].max()))[0] \
+            if len(mid) else None
+    sched = pl.synthesize("roundpipe" if mode == "async" else "roundpipe-sync", N,
+                          args.micro_batches, 0, max(3, steps), durs)
+    sim = pl.simulate(sched, mode != "async")
+    sim_bub = (pl.interior_bubble(sim.timeline, N, 1, max(3, steps) - 2)[0]
+               if mode == "async" else sim.bubble_ratio)
+    if report_dir:  # measured timeline in the reference CLI's report schema + Gantt
         from paper_2604_27085_b200.planner import report_json
-        os.makedirs(args.report_dir, exist_ok=True)
-        rep = pl.timeline_report(tl, args.gpus)
-        tag = f"{args.model}_n{args.gpus}_{args.mode}"
-        with open(os.path.join(args.report_dir, f"timeline_{tag}.json"), "w") as f:
-            json.dump({"measured": report_json(rep, args.gpus),
-                       "simulated": {k: v for k, v in report_json(sim, args.gpus).items()
-                                     if k != "events"},
+        os.makedirs(report_dir, exist_ok=True)
+        rep = pl.timeline_report(tl, N)
+        tag = f"{args.model}_n{N}_{mode}"
+        with open(os.path.join(report_dir, f"timeline_{tag}.json"), "w") as f:
+            json.dump({"measured": report_json(rep, N),
+                       "simulated": {k: v for k, v in report_json(sim, N).items() if k != "events"},
                        "transfers": rt.transfer_timeline().tolist()}, f)
-        with open(os.path.join(args.report_dir, f"gantt_{tag}.svg"), "w") as f:
-            f.write(pl.render_gantt(tl, args.gpus, plan))
-    # one profiled step (not timed): kernel-level roofline
-    rt.profile(True)
-    rt.forward_backward(tokens, labels)
-    rt.step()
-    prof = rt.profile_read()
-    rt.profile(False)
+        with open(os.path.join(report_dir, f"gantt_{tag}.svg"), "w") as f:
+            f.write(pl.render_gantt(tl, N, plan))
+    prof = None
+    if profile:  # one profiled step (not timed): kernel-level roofline
+        rt.profile(True)
+        rt.forward_backward(tokens, labels)
+        rt.step()
+        prof = rt.profile_read()
+        rt.profile(False)
     rt.sync()
     rt.close()
+    return {"ms": ms, "wall_s": w1 - w0, "steps": steps, "tokens_step": tokens_step,
+            "value": steps * tokens_step / (ms * 1e-3),
+            "e2e": steps * tokens_step / (w1 - w0), "st0": st0, "st1": st1, "plan": plan,
+            "bubble": bub, "sim_bubble": sim_bub, "losses": losses, "prof": prof,
+            "clocks": clk.summary() if clocks else None, "setup_s": setup_s}
 
+
+def run_ours(args):
+    resident = args.resident_optimizer
+    r = measure(args, resident, args.mode, args.steps, args.warmup, profile=True,
+                report_dir=args.report_dir)
+    d = MODEL_DIMS[args.model]
+    st0, st1, plan, prof = r["st0"], r["st1"], r["plan"], r["prof"]
     burst, sustained, hbm, src = peaks()
     gemm = prof["gemm"]
     gemm_tf = gemm["work"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] else 0.0
@@ -324,33 +429,32 @@ def run_ours(args):
     attn_tf = attn["work"] / (attn["ms"] * 1e-3) / 1e12 if attn["ms"] else 0.0
     hbmk = prof["hbm_kernels"]
     adam = prof["adamw"]
-    h2d = (st1["h2d_bytes"] - st0["h2d_bytes"]) / args.steps
-    d2h = (st1["d2h_bytes"] - st0["d2h_bytes"]) / args.steps
-    recompute = sum(r.size() for r in plan.bwd_stages)
-    flops = step_flops(d, args.seq, tokens_step, recompute, args.lora_rank)
+    steps = args.steps
+    h2d = (st1["h2d_bytes"] - st0["h2d_bytes"]) / steps
+    d2h = (st1["d2h_bytes"] - st0["d2h_bytes"]) / steps
+    p2p = (st1["p2p_bytes"] - st0["p2p_bytes"]) / steps
+    recompute = sum(x.size() for x in plan.bwd_stages)
+    flops = step_flops(d, args.seq, r["tokens_step"], recompute, args.lora_rank)
     t_comp = flops / (sustained * 1e12) / args.gpus
     t_link = max(h2d / (PCIE_H2D_GBS * 1e9), d2h / (PCIE_D2H_GBS * 1e9)) / args.gpus
-    value = args.steps * tokens_step / (ms * 1e-3)
-    e2e = args.steps * tokens_step / (w1 - w0)
-    roof_tps = tokens_step / max(t_comp, t_link)
-    gpu_launches = (st1["kernels_launched"] - st0["kernels_launched"])
+    roof_tps = r["tokens_step"] / max(t_comp, t_link)
+    traffic = ncu_gemm_traffic()
     line = {
-        "metric": metric_name(args), "value": round(value, 2), "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 2),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "metric": metric_name(args), "value": round(r["value"], 2), "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(r["ms"] / steps, 2), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded uniform token ids; random-init N(0,0.02) weights)",
         "config": config_dict(args),
-        "clocks": clk.summary(),
-        "e2e": {"value": round(e2e, 2), "unit": "tokens/s",
-                "h2d_bytes_per_step": int(args.micro_batches * args.seq * 8),
-                "d2h_bytes_per_step": 4,
+        "clocks": r["clocks"],
+        "e2e": {"value": round(r["e2e"], 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(r["tokens_step"] * 8), "d2h_bytes_per_step": 4,
                 "streamed_h2d_bytes_per_step": int(h2d), "streamed_d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(gpu_launches),
+        "gpu_launches": int(st1["kernels_launched"] - st0["kernels_launched"]),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all linear layers of the step)",
                      "achieved": round(gemm_tf, 1), "peak": sustained, "unit": "TFLOP/s",
                      "frac": round(gemm_tf / sustained, 4),
-                     "traffic": (ncu_gemm_traffic() or {}).get("traffic"),
-                     "traffic_detail": ncu_gemm_traffic(),
+                     "traffic": (traffic or {}).get("traffic"), "traffic_detail": traffic,
                      "peak_source": f"{src} bf16_tflops_sustained (kernel inside a long step)",
                      "launches": gemm["launches"]},
         "kernels": {"attention_tflops": round(attn_tf, 1),
@@ -360,33 +464,47 @@ def run_ours(args):
         "step_roofline": {"flops_per_step": flops, "t_compute_ms": round(t_comp * 1e3, 1),
                           "t_link_ms": round(t_link * 1e3, 1),
                           "tokens_per_s_bound": round(roof_tps, 1),
-                          "frac": round(value / roof_tps, 4),
+                          "frac": round(r["value"] / roof_tps, 4),
                           "note": "slower of executed FLOPs at sustained bf16 peak and streamed "
                                   "host-link bytes at measured PCIe H2D/D2H GB/s"},
-        "bubble": {"measured_interior": round(bub, 5), "simulated": round(sim_bub, 5),
-                   "slots": plan.num_slots(), "iterations": [it_lo, it_hi]},
-        "loss": {"first": losses[0], "last": losses[-1]},
-        "setup_s": round(setup_s, 1),
+        "transfers": {"p2p_bytes_per_step": int(p2p), "h2d_gbs_avg": round(h2d / (r["ms"] / steps * 1e-3) / 1e9, 2),
+                      "d2h_gbs_avg": round(d2h / (r["ms"] / steps * 1e-3) / 1e9, 2)},
+        "bubble": {"measured": round(r["bubble"], 5) if r["bubble"] is not None else None,
+                   "simulated": round(r["sim_bubble"], 5), "slots": plan.num_slots(),
+                   "kind": "interior (async)" if args.mode == "async" else "in-iteration (sync)",
+                   "iterations": [args.warmup, args.warmup + steps - 1]},
+        "loss": {"first": r["losses"][0], "last": r["losses"][-1]},
+        "setup_s": round(r["setup_s"], 1),
         "optimizer_state": {"resident_params_hbm": int(st1["resident_params"]),
-                            "streamed_params_host": int(st1["params_total"] - st1["resident_params"]),
-                            "note": "fp32 AdamW state of the largest groups that fit in free HBM "
-                                    "stays resident (single device); the rest streams from "
-                                    "pinned host memory every step"},
+                            "streamed_params_host": int(st1["params_total"] - st1["resident_params"])},
         # the runtime's device allocations by category (all workers), GB
         "hbm_gb": {k: round(v / 1e9, 2) for k, v in zip(
             ("weights_2_versions", "grads", "pending_adamw_out", "activations",
              "scratch", "resident_optimizer_state", "optimizer_chunk_ring"),
             st1["device_bytes"][:7])},
     }
+    if not args.no_variants:
+        variants = {}
+        vs, vw = min(args.steps, 6), 3
+        for name, res, mode in (("hbm_resident_optimizer", not resident, args.mode),
+                                ("roundpipe_sync", resident, "sync" if args.mode == "async" else "async")):
+            try:
+                v = measure(args, res, mode, vs, vw, clocks=False)
+                variants[name] = {"value": round(v["value"], 2), "unit": "tokens/s",
+                                  "ms_per_step": round(v["ms"] / vs, 2), "steps": vs,
+                                  "bubble": round(v["bubble"], 5) if v["bubble"] is not None else None,
+                                  "simulated_bubble": round(v["sim_bubble"], 5),
+                                  "config": config_dict(args, res, mode)["workload"]}
+            except Exception as e:  # report, never fail the headline
+                variants[name] = {"error": str(e)[:300]}
+        line["variants"] = variants
     if not args.no_cpu_baseline:
         try:
-            r = cpu_sample(args.model, args.seq, args.micro_batches)
-            line["cpu_baseline"] = {
-                "value": round(r["tokens_per_s"], 3), "unit": "tokens/s", "cores": r["threads"],
-                "kind": "port",
-                "sample": (f"fp32 CPU oracle: 1 full-width {args.model} layer fwd+bwd at seq "
-                           f"{args.seq}, head+CE on 512 tokens, AdamW on one layer; assembled into "
-                           f"a {args.micro_batches}-micro-batch step")}
+            times, threads, s = cpu_step_sample(args.model, args.cpu_tokens, steps=1, warmup=1)
+            v = args.cpu_tokens / statistics.mean(times)
+            line["cpu_baseline"] = {"value": round(v, 3), "unit": "tokens/s", "cores": threads,
+                                    "kind": "port",
+                                    "sample": sample_desc(args.model, args.cpu_tokens, s.layers)}
         except Exception as e:  # report, never fail the GPU line
             line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     print(json.dumps(line), flush=True)
@@ -402,15 +520,19 @@ def main():
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--micro-batches", type=int, default=16)
     ap.add_argument("--mode", default="async", choices=["async", "sync"])
+    ap.add_argument("--resident-optimizer", action="store_true",
+                    help="keep the fp32 AdamW state of the groups that fit in HBM (single "
+                         "device) instead of the host-offloaded BASELINE configs[2] placement")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the labelled resident-optimizer / sync comparison runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=32,
+                    help="tokens of the bounded CPU step sample (cpu_baseline / --impl reference)")
     ap.add_argument("--lora-rank", type=int, default=0,
                     help="LoRA fine-tune (base frozen, rank-r adapters); 0 = full fine-tune")
     ap.add_argument("--lora-alpha", type=float, default=0.0)
     ap.add_argument("--report-dir", default=None,
                     help="write the measured timeline (report JSON + SVG Gantt) here")
-    ap.add_argument("--host-optimizer", action="store_true",
-                    help="keep every group's fp32 AdamW state in pinned host memory "
-                         "(no HBM-resident groups): the strict host-offloaded configuration")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = int(os.environ.get("RANK", "0"))
