@@ -36,7 +36,11 @@ enum {
   RP_RT_UNFUSED_SWIGLU = 8,
   /* record the (action, group, iteration) wait edges of the optimizer
    * hand-off protocol the runtime realises (rp_runtime_protocol_edges) */
-  RP_RT_RECORD_PROTOCOL = 16
+  RP_RT_RECORD_PROTOCOL = 16,
+  /* one worker: publish every AdamW result through the pinned bf16 master
+   * (p_copy, then upload) as with several workers, instead of writing the
+   * HBM-resident groups' new weights in place (keeps the host master current) */
+  RP_RT_HOST_PUBLISH = 32
 };
 
 typedef struct {
@@ -160,6 +164,23 @@ typedef struct {
  * kernel ns of one micro-batch's forward (t_fwd) and forward+backward
  * (t_bwd); bytes from the cost model. Feed back as rp_runtime_config_t.costs
  * (or to rp_partition) to re-plan on measured costs. */
+/* Realised optimizer hand-off edges (needs RP_RT_RECORD_PROTOCOL): every
+ * protocol wait the controller enqueued — (kind, group, iteration) of the
+ * action waited on -> of the waiting action; kinds as consistency.hpp
+ * ActionKind (0 param upload, 1 grad write, 2 opt step, 3 p_copy, 4
+ * g_copy); group -1 = embedding, 0..L-1 layers, L = head. Compare with
+ * rp_build_protocol(L+1, T, event-per-layer) (tests/test_protocol_gpu.py). */
+typedef struct {
+  int32_t before_kind, before_group, before_iteration;
+  int32_t after_kind, after_group, after_iteration;
+} rp_protocol_edge_rec_t;
+int rp_runtime_protocol_edges(rp_runtime_t* rt, rp_protocol_edge_rec_t* out, int64_t cap,
+                              int64_t* n);
+/* Host-mapped flag words, read without synchronising: the latest p_copy
+ * (ParamCopy index) published for `group` (-1 none) and the latest iteration
+ * whose loss is on the host. */
+int rp_runtime_progress(rp_runtime_t* rt, int32_t group, int32_t* published,
+                        int32_t* loss_iteration);
 int rp_runtime_measured_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
 int rp_runtime_profile_records(rp_runtime_t* rt, rp_prof_record_t* out, int64_t cap, int64_t* n);
 

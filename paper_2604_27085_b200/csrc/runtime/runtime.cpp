@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -37,6 +38,7 @@
 #include <thread>
 
 #include "kernels/launch_util.h"
+#include "runtime/flags.h"
 #include "runtime/runtime_internal.h"
 
 namespace rp {
@@ -168,7 +170,26 @@ struct Runtime {
   std::vector<Gpu> gpus;             // logical workers
   std::vector<int> grad_owner;       // g -> worker holding this iteration's grads
   std::vector<int> pend_owner;       // g -> worker holding pending AdamW output (-1 none)
-  std::vector<cudaEvent_t> pcopy_ev; // g -> event of the latest p_copy (publication)
+  // optimizer hand-off protocol state (consistency.hpp:122-135): per group
+  // the ParamCopy index of the latest p_copy (-1 none) and the newest
+  // iteration whose weights were uploaded; flag words: pub(g) = latest
+  // published ParamCopy index + 1, loss(w) = latest iteration + 1 whose loss
+  // worker w has copied to the host
+  std::vector<int> pcopy_idx, upload_ver;
+  FlagWords flags;
+  int flag_pub(int g) const { return g; }
+  int flag_loss(int w) const { return ngroups() + w; }
+  // realised protocol edges (RP_RT_RECORD_PROTOCOL): (kind, group, iteration)
+  // of the action waited on -> of the waiting action
+  struct ProtoEdge {
+    int bk, bg, bi, ak, ag, ai;
+  };
+  std::vector<ProtoEdge> proto;
+  void proto_edge(roundpipe::ActionKind bk, int bg, int bi, roundpipe::ActionKind ak, int ag,
+                  int ai) {
+    if ((cfg.flags & RP_RT_RECORD_PROTOCOL) && bi >= 0)
+      proto.push_back({(int)bk, bg, bi, (int)ak, ag, ai});
+  }
   std::vector<cudaEvent_t> state_ev; // g -> event of the latest fp32 state write-back
   std::vector<std::vector<int>> uploaders;  // g -> workers that uploaded this version
   std::vector<char> fused_worker;    // worker ran a fused task this iteration
@@ -369,10 +390,16 @@ struct Runtime {
   }
   // before the first grad write of an HBM-resident group g in an iteration:
   // AdamW of the previous iteration has consumed its single grad buffer (edge 4)
+  // (the latest AdamW on this worker's buffer: resident AdamW passes of a
+  // group are chained through state_ev, so it implies every earlier one)
   void grad_free(Gpu& G, int g, cudaStream_t q) {
     if (!host[g].d_state) return;  // streamed groups: two buffers, waited at slot start
-    RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_adam[0], 0));
-    RP_CUDA(cudaStreamWaitEvent(q, G.groups[g].ev_adam[1], 0));
+    DevGroup& D = G.groups[g];
+    const int p = D.adam_iter[0] >= D.adam_iter[1] ? 0 : 1;
+    if (D.adam_iter[p] < 0) return;
+    RP_CUDA(cudaStreamWaitEvent(q, D.ev_adam[p], 0));  // edge (4)
+    proto_edge(roundpipe::ActionKind::GradCopy, g, D.adam_iter[p],
+               roundpipe::ActionKind::GradWrite, g, exec_iter);
   }
   void sync_all();
   void gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
@@ -530,10 +557,13 @@ void Runtime::init(const rp_runtime_config_t& c) {
   arena.commit();
   grad_owner.assign(ngroups(), 0);
   pend_owner.assign(ngroups(), -1);
-  pcopy_ev.assign(ngroups(), nullptr);
+  pcopy_idx.assign(ngroups(), -1);
+  upload_ver.assign(ngroups(), -1);
   state_ev.assign(ngroups(), nullptr);
   uploaders.assign(ngroups(), {});
   RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N * 2));
+  RP_CUDA(cudaSetDevice(0));
+  flags.init(ngroups() + N);
   gpus.resize(N);
   for (int w = 0; w < N; ++w) alloc_worker(gpus[w], w);
   ev_loss.resize(N);
@@ -573,7 +603,9 @@ void Runtime::place_resident_state() {
   for (int g : order) {
     const int64_t n = host[g].tn(), o = host[g].t_off;
     if (n == 0) continue;  // frozen group
-    const bool direct = N == 1;  // publish straight into the device weights
+    // publish straight into the device weights (unless asked to go through
+    // the pinned bf16 master as with several workers)
+    const bool direct = N == 1 && !(cfg.flags & RP_RT_HOST_PUBLISH);
     const int64_t freed = n * 4 * (int64_t)gpus.size() + (direct ? host[g].n * 2 : 0);
     if (n * 12 > budget + freed || placed + n * 12 > cap) continue;
     for (Gpu& G : gpus) {
@@ -924,9 +956,14 @@ void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
     RP_CUDA(cudaEventRecord(D.ev_upload[b], G.w_h2d));
     D.loaded[b] = it;
   }
+  upload_ver[g] = std::max(upload_ver[g], it);
   if (D.loaded[b] != it) {
     set_dev(G);
-    if (pcopy_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.w_h2d, pcopy_ev[g], 0));  // edge (2)
+    if (pcopy_idx[g] >= 0) {  // edge (2): the host master holds the published version
+      flags.wait_geq(G.w_h2d, flag_pub(g), (uint32_t)pcopy_idx[g] + 1);
+      proto_edge(roundpipe::ActionKind::ParamCopy, g, pcopy_idx[g],
+                 roundpipe::ActionKind::ParamUpload, g, it);
+    }
     RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse[b], 0));               // WAR (t-2)
     cudaEvent_t xa = xfer_begin(G.w_h2d);
     RP_CUDA(cudaMemcpyAsync(D.w[b], H.w16, H.n * 2, cudaMemcpyHostToDevice, G.w_h2d));
@@ -975,8 +1012,13 @@ void Runtime::p_copy(int g) {
   set_dev(O);
   DevGroup& D = O.groups[g];
   HostGroup& H = host[g];
-  for (int wb : uploaders[g])
+  // ParamCopy index = the version whose uploads this publication follows
+  const int idx = upload_ver[g];
+  for (int wb : uploaders[g])  // edge (1)
     RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, gpus[wb / 2].groups[g].ev_upload[wb % 2], 0));
+  if (!uploaders[g].empty())
+    proto_edge(roundpipe::ActionKind::ParamUpload, g, idx, roundpipe::ActionKind::ParamCopy, g,
+               idx);
   uploaders[g].clear();
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[0], 0));
   RP_CUDA(cudaStreamWaitEvent(O.opt_d2h, D.ev_adam[1], 0));
@@ -986,7 +1028,8 @@ void Runtime::p_copy(int g) {
   xfer_end(xa, O.opt_d2h, 1, g - 1, H.step, O.id);
   d2h_bytes += H.tn() * 2;
   RP_CUDA(cudaEventRecord(D.ev_pcopy, O.opt_d2h));
-  pcopy_ev[g] = D.ev_pcopy;
+  flags.set(O.opt_d2h, flag_pub(g), (uint32_t)idx + 1);
+  pcopy_idx[g] = idx;
   pend_owner[g] = -1;
 }
 
@@ -1296,8 +1339,13 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     // HBM-resident groups keep ONE grad buffer: they wait last iteration's
     // AdamW right before their first grad write instead (grad_free), so the
     // slot does not stall on the whole resident optimizer pass
-    for (int g : grad_groups)
-      if (!host[g].d_state) RP_CUDA(cudaStreamWaitEvent(st, G.groups[g].ev_adam[it & 1], 0));
+    for (int g : grad_groups) {
+      DevGroup& D = G.groups[g];
+      if (host[g].d_state || D.adam_iter[it & 1] < 0) continue;
+      RP_CUDA(cudaStreamWaitEvent(st, D.ev_adam[it & 1], 0));  // edge (4), parity buffers
+      proto_edge(roundpipe::ActionKind::GradCopy, g, D.adam_iter[it & 1],
+                 roundpipe::ActionKind::GradWrite, g, it);
+    }
   }
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_tokens, 0));
   const bool want_tl = cfg.flags & RP_RT_RECORD_TIMELINE;
@@ -1577,6 +1625,7 @@ void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
       RP_CUDA(cudaMemcpyAsync(loss_host + par * N + G.id, G.loss_dev, 4, cudaMemcpyDeviceToHost,
                               G.act));
       RP_CUDA(cudaEventRecord(G.ev_loss_par[par], G.act));
+      flags.set(G.act, flag_loss(G.id), (uint32_t)it + 1);  // loss of `it` is on the host
     }
   }
   fused_par[par] = fused_worker;
@@ -1590,12 +1639,22 @@ float Runtime::wait_loss(int it) {
   const int par = it & 1;
   if (it < 0 || iter_par[par] != it)
     throw RtError(RP_E_INPUT, "loss of iteration " + std::to_string(it) + " is no longer held");
+  // early return: the controller polls the workers' loss flag
+  // words instead of blocking in the driver; every ~1K polls it checks the
+  // loss event for a device error so a failed step cannot spin forever
   double total = 0.0;
   for (Gpu& G : gpus) {
     if (!fused_par[par][G.id]) continue;
-    set_dev(G);
-    RP_CUDA(cudaEventSynchronize(G.ev_loss_par[par]));
-    total += loss_host[par * N + G.id];
+    for (long spins = 0; flags.read(flag_loss(G.id)) < (uint32_t)it + 1; ++spins) {
+      if (spins % 1024 == 1023) {
+        set_dev(G);
+        const cudaError_t e = cudaEventQuery(G.ev_loss_par[par]);
+        if (e != cudaSuccess && e != cudaErrorNotReady) RP_CUDA(e);
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    total += static_cast<volatile float*>(loss_host)[par * N + G.id];
   }
   return (float)(total * grad_scale_par[par]);
 }
@@ -1610,6 +1669,9 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   HostGroup& H = host[g];
   const int step_no = ++H.step;
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_gradwrite, 0));  // edge (3)
+  proto_edge(roundpipe::ActionKind::GradWrite, g, last_iter, roundpipe::ActionKind::GradCopy, g,
+             last_iter);
+  D.adam_iter[parity] = last_iter;
   RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_pcopy, 0));      // pend free again
   if (H.d_state) {  // HBM-resident fp32 state: one fused pass, no PCIe
     cudaStream_t q = G.opt_res;
@@ -1646,6 +1708,7 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     H.host_stale = true;
     if (H.direct) {  // published in place: no p_copy, no upload
       RP_CUDA(cudaEventRecord(D.ev_upload[b], q));
+      flags.set(q, flag_pub(g), (uint32_t)ver);  // = the ParamCopy index (ver - 1) + 1
       D.loaded[b] = ver;
       H.w16_stale = true;
       return;
@@ -2270,6 +2333,40 @@ RP_API int rp_runtime_profile_records(rp_runtime_t* p, rp_prof_record_t* out, in
       out[i] = rp_prof_record_t{r.cat, r.worker, r.lane, 0,
                                 (int64_t)std::llround((double)a * 1e6),
                                 (int64_t)std::llround((double)b * 1e6), r.work};
+    }
+  });
+}
+
+// Realised optimizer hand-off edges (RP_RT_RECORD_PROTOCOL): every
+// protocol wait the controller enqueued, as (kind, group, iteration) of the
+// action waited on -> of the waiting action (ActionKind numbering of
+// consistency.hpp; group -1 = embedding, L = head).
+RP_API int rp_runtime_protocol_edges(rp_runtime_t* p, rp_protocol_edge_rec_t* out, int64_t cap,
+                                     int64_t* n) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    *n = (int64_t)rt->proto.size();
+    if (*n > cap) throw RtError(RP_E_TOOSMALL, "protocol edge capacity");
+    for (int64_t i = 0; i < *n; ++i) {
+      const auto& e = rt->proto[(std::size_t)i];
+      out[i] = rp_protocol_edge_rec_t{e.bk, e.bg - 1, e.bi, e.ak, e.ag - 1, e.ai};
+    }
+  });
+}
+
+// Host-side view of the flag words (no synchronisation): the latest
+// ParamCopy index published for a group (-1: none since creation / load) and
+// the latest iteration whose loss is on the host.
+RP_API int rp_runtime_progress(rp_runtime_t* p, int32_t group, int32_t* published,
+                               int32_t* loss_iteration) {
+  return rt_guard([&] {
+    Runtime* rt = R(p);
+    const int g = gidx(rt, group);
+    if (published) *published = (int32_t)rt->flags.read(rt->flag_pub(g)) - 1;
+    if (loss_iteration) {
+      uint32_t m = 0;
+      for (int w = 0; w < rt->N; ++w) m = std::max(m, rt->flags.read(rt->flag_loss(w)));
+      *loss_iteration = (int32_t)m - 1;
     }
   });
 }

@@ -103,6 +103,7 @@ struct DevGroup {
   cudaEvent_t ev_lastuse[2] = {nullptr, nullptr};  // last compute read of w[b] (WAR)
   cudaEvent_t ev_gradwrite = nullptr;     // GradWrite(l, t)           GPU lane
   cudaEvent_t ev_adam[2] = {nullptr, nullptr};  // g_copy: AdamW consumed grad[p]
+  int adam_iter[2] = {-1, -1};            // iteration whose grads that AdamW consumed
   cudaEvent_t ev_pcopy = nullptr;         // p_copy(l, t)              optimizer lane
   cudaEvent_t ev_state = nullptr;         // fp32 state written back to host
 };

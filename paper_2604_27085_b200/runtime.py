@@ -23,6 +23,7 @@ RP_RT_RECORD_TIMELINE = 2
 RP_RT_FUSED_PIPELINE = 4
 RP_RT_UNFUSED_SWIGLU = 8
 RP_RT_RECORD_PROTOCOL = 16
+RP_RT_HOST_PUBLISH = 32
 
 
 class AdamC(C.Structure):
@@ -69,7 +70,7 @@ class RoundPipe:
                  costs=None, mem_limit_bytes=0, residency_factor=2.0, init_seed=0,
                  init_std=0.02, skip_init=False, record_timeline=False, lora_rank=0,
                  lora_alpha=0.0, resident_state_gb=-1.0, logits_rows=0, fused_pipeline=False,
-                 unfused_swiglu=False, record_protocol=False):
+                 unfused_swiglu=False, record_protocol=False, host_publish=False):
         """resident_state_gb: fp32 AdamW state placement on a single device —
         < 0 keeps the groups that fit in free HBM resident (default), 0 keeps
         all of it in pinned host memory (host-offloaded Adam, BASELINE
@@ -90,7 +91,8 @@ class RoundPipe:
             (RP_RT_SKIP_INIT if skip_init else 0) | (RP_RT_RECORD_TIMELINE if record_timeline else 0)
             | (RP_RT_FUSED_PIPELINE if fused_pipeline else 0)
             | (RP_RT_UNFUSED_SWIGLU if unfused_swiglu else 0)
-            | (RP_RT_RECORD_PROTOCOL if record_protocol else 0),
+            | (RP_RT_RECORD_PROTOCOL if record_protocol else 0)
+            | (RP_RT_HOST_PUBLISH if host_publish else 0),
             lora_rank, lora_alpha, float(resident_state_gb), int(logits_rows), 0)
         self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.h = VP()
@@ -258,6 +260,26 @@ class RoundPipe:
 
     def clear_timeline(self):
         self._call("rp_timeline_clear", self.h)
+
+    PROTO_DTYPE = np.dtype([("before_kind", "<i4"), ("before_group", "<i4"),
+                            ("before_iteration", "<i4"), ("after_kind", "<i4"),
+                            ("after_group", "<i4"), ("after_iteration", "<i4")])
+
+    def protocol_edges(self) -> np.ndarray:
+        """Realised hand-off edges (record_protocol=True): (kind, group,
+        iteration) waited on -> waiting; kinds as consistency.hpp ActionKind."""
+        cap = 1 << 20
+        ev = np.zeros(cap, dtype=self.PROTO_DTYPE)
+        n = I64()
+        self._call("rp_runtime_protocol_edges", self.h, ev.ctypes.data_as(VP), I64(cap), C.byref(n))
+        return ev[: n.value].copy()
+
+    def progress(self, group: int = -1) -> tuple:
+        """(latest p_copy index published for `group`, latest iteration whose
+        loss is on the host), read from the host-mapped flag words."""
+        pub, it = I32(), I32()
+        self._call("rp_runtime_progress", self.h, I32(group), C.byref(pub), C.byref(it))
+        return pub.value, it.value
 
     XFER_DTYPE = np.dtype([("kind", "<i4"), ("group", "<i4"), ("iteration", "<i4"),
                            ("worker", "<i4"), ("start_ns", "<i8"), ("end_ns", "<i8")])

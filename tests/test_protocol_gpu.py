@@ -1,0 +1,149 @@
+"""The optimizer hand-off protocol the runtime REALISES, against the
+reference's (consistency.hpp:84-162 build_protocol, EventPerLayer edges
+(1)-(4)).
+
+The runtime records every protocol wait it enqueues (record_protocol=True)
+as (kind, group, iteration) waited on -> waiting action. Groups map to the
+protocol's layers as embedding -> 0 (it lives in layer 0's slots), decoder
+layer l -> l, head -> L, so the model is build_protocol(L+1, T).
+
+* N=1, HBM-resident optimizer state published through the pinned bf16
+  master (host_publish): ONE grad buffer per group, exactly the paper's
+  setting -> the realised cross-lane edge set EQUALS the reference's
+  EventPerLayer set (minus ParamCopy(., 0): nothing is published before the
+  first step, so the runtime issues no copy), and the reference checker
+  proves that set safe in every interleaving.
+* Host-offloaded state (two fp32 grad buffers by iteration parity) and N=4
+  logical workers (grads stay on the worker that produced them): edges
+  (1)-(3) are the reference's exactly; edge (4) protects each PHYSICAL grad
+  buffer — GradCopy of the last iteration that wrote the same (worker,
+  parity) buffer -> GradWrite(t). The test derives those from the dispatch
+  list and demands equality. (With a single master buffer, dropping edge (4)
+  is unsafe — the reference checker finds the witness — which is why every
+  buffer reuse carries it.)
+"""
+import numpy as np
+import pytest
+
+from oracle import step_oracle as O
+
+pytestmark = pytest.mark.gpu
+UP, GW, OS, PC, GC = 0, 1, 2, 3, 4
+T = 4
+
+
+def uniform_costs(L1):
+    from paper_2604_27085_b200.planner import COST_DTYPE
+    c = np.zeros(L1, dtype=COST_DTYPE)
+    c["t_fwd_ns"], c["t_bwd_ns"], c["param_bytes"] = 1000, 3000, 1
+    c["act_ckpt_bytes"] = 1
+    return c
+
+
+def realised(N, resident, host_publish=False):
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=N,
+                   async_optimizer=True, adam=AdamW(lr=1e-4),
+                   costs=uniform_costs(s.layers + 1) if N > 1 else None,
+                   resident_state_gb=-1.0 if resident else 0.0, record_protocol=True,
+                   host_publish=host_publish)
+    for _ in range(T):
+        rt.forward_backward(tok.numpy(), lab.numpy())
+        rt.step()
+    rt.sync()
+    pub, loss_it = rt.progress(s.layers)  # host-mapped flag words
+    e = rt.protocol_edges()
+    plan, durs = rt.plan()
+    st = rt.stats()
+    rt.close()
+    assert loss_it == T - 1
+    edges = set()
+    for r in e:
+        if r["after_iteration"] >= T:  # uploads of iteration T (prefetched) are outside the model
+            continue
+        edges.add((int(r["before_kind"]), max(int(r["before_group"]), 0), int(r["before_iteration"]),
+                   int(r["after_kind"]), max(int(r["after_group"]), 0), int(r["after_iteration"])))
+    return edges, plan, durs, st, pub
+
+
+def reference_edges(L1):
+    from paper_2604_27085_b200.planner import Planner
+    p = Planner().build_protocol(L1, T, "event-per-layer")
+    out = set()
+    for a, b in p.edges:
+        if (a < p.gpu_actions) == (b < p.gpu_actions):
+            continue  # lane order, not a protocol wait
+        ka, la, ia = p.actions[a]
+        kb, lb, ib = p.actions[b]
+        if (ka == PC and ia == 0) or (kb == PC and ib == 0):
+            continue  # ParamCopy(., 0): nothing to publish before the first step
+        out.add((ka, la, ia, kb, lb, ib))
+    return out
+
+
+def by_kind(edges, pair):
+    return {e for e in edges if (e[0], e[3]) == pair}
+
+
+def grad_workers(plan, durs, N, L):
+    """worker that produces the grads of protocol layer l in iteration t
+    (reference dispatcher: slot i of round r runs on (r*S + i) mod N)."""
+    from paper_2604_27085_b200.planner import Planner
+    sched = Planner().synthesize("roundpipe", N, 4, 4, T, durs)
+    S = plan.num_slots()
+    nf = len(plan.fwd_stages)
+    grad_slot = {}
+    for i, r in enumerate(plan.bwd_stages):
+        for l in range(r.first, r.last + 1):
+            grad_slot[l] = nf + 1 + i
+    for l in range(plan.fused_stage.first, plan.fused_stage.last + 1):
+        grad_slot[l] = nf
+    w = {}
+    for t in sched.tasks:
+        for l, sl in grad_slot.items():
+            if t["slot"] == sl and t["mb"] == 0:
+                w[(l, int(t["iteration"]))] = int(t["gpu"])
+    assert len(w) == (L + 1) * T and S == len(durs), len(w)
+    return w
+
+
+def expected_edge4(w, L1, parity_buffers):
+    out = set()
+    for l in range(L1):
+        for t in range(T):
+            prev = [u for u in range(t) if w[(l, u)] == w[(l, t)]
+                    and (not parity_buffers or u % 2 == t % 2)]
+            if prev:
+                out.add((GC, l, max(prev), GW, l, t))
+    return out
+
+
+def test_single_buffer_edges_equal_reference_event_per_layer():
+    from paper_2604_27085_b200.planner import Planner
+    L = O.Shape.from_config("tiny").layers
+    got, plan, durs, st, pub = realised(1, resident=True, host_publish=True)
+    assert st["resident_params"] == st["params_total"]
+    ref = reference_edges(L + 1)
+    assert got == ref, (sorted(got - ref)[:8], sorted(ref - got)[:8])
+    assert Planner().check_all_interleavings(L + 1, T, "event-per-layer").ok
+    v = Planner().check_all_interleavings(L + 1, T, "event-per-layer", drop_edge=4)
+    assert not v.ok and v.violated_constraint == 4  # why every buffer reuse carries edge (4)
+    assert pub == T - 1  # the last publication (ParamCopy(T-1)) reached the flag word
+
+
+@pytest.mark.parametrize("N,resident", [(1, False), (4, True), (4, False)])
+def test_per_buffer_edges(N, resident):
+    L = O.Shape.from_config("tiny").layers
+    got, plan, durs, st, pub = realised(N, resident)
+    ref = reference_edges(L + 1)
+    for pair in ((UP, PC), (PC, UP), (GW, GC)):  # (1), (2), (3): global, exactly the reference's
+        assert by_kind(got, pair) == by_kind(ref, pair), pair
+    if N == 1:
+        w = {(l, t): 0 for l in range(L + 1) for t in range(T)}
+    else:
+        w = grad_workers(plan, durs, N, L)
+    exp4 = expected_edge4(w, L + 1, parity_buffers=not resident)
+    assert by_kind(got, (GC, GW)) == exp4, (sorted(by_kind(got, (GC, GW)) ^ exp4)[:8])
+    assert got == by_kind(got, (UP, PC)) | by_kind(got, (PC, UP)) | by_kind(got, (GW, GC)) | exp4
