@@ -31,6 +31,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <deque>
+#include <unordered_map>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -325,7 +327,25 @@ struct Runtime {
   void forward_backward(const int32_t* tokens, const int32_t* labels, float* loss);
   void run_slot(Gpu& G, int it, int round, int slot, int first_round, float grad_scale);
   void upload(Gpu& G, int g, int it, bool last_use);
+  bool upload_reserve(Gpu& G, int g, int it);
+  void upload_chunk(Gpu& G, int g, int it, int64_t off, int64_t len);
+  void upload_done(Gpu& G, int g, int it);
   void prefetch(int it, bool reverse = false);
+  // LPT-windowed uploads of the next iteration (async), released one window
+  // per micro-batch start of the worker's compute
+  struct UpChunk {
+    int g;
+    int64_t off, len;  // bytes within the group's bf16 buffer
+  };
+  struct UpWindow {
+    int it = 0;
+    std::vector<UpChunk> chunks;
+  };
+  std::vector<std::deque<UpWindow>> upq;   // per worker
+  std::vector<std::vector<int>> up_left;   // per worker, per group: chunks not yet enqueued
+  void plan_upload_windows(int it_next);
+  void release_window(Gpu& G);
+  void flush_windows();
   std::vector<int> slot_groups(const roundpipe::StageSlot& ss) const;
   int exec_iter = 0;  // iteration whose compute is being enqueued
   void p_copy(int g);
@@ -559,6 +579,8 @@ void Runtime::init(const rp_runtime_config_t& c) {
   pend_owner.assign(ngroups(), -1);
   pcopy_idx.assign(ngroups(), -1);
   upload_ver.assign(ngroups(), -1);
+  upq.assign(N, {});
+  up_left.assign(N, std::vector<int>(ngroups(), 0));
   state_ev.assign(ngroups(), nullptr);
   uploaders.assign(ngroups(), {});
   RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N * 2));
@@ -943,6 +965,18 @@ void Runtime::init_weights() {
 // group in the iteration, the pending AdamW result may be published
 // (p_copy, edge 1) — async mode only.
 void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
+  if (upload_reserve(G, g, it)) {
+    upload_chunk(G, g, it, 0, host[g].n * 2);
+    upload_done(G, g, it);
+  }
+  if (last_use && cfg.async_optimizer && pend_owner[g] >= 0) p_copy(g);
+  set_dev(G);
+}
+
+// The upload of (g, it) into w[it%2] of worker G is now the runtime's job:
+// returns true when a host copy is needed (the caller then enqueues its
+// chunks and upload_done); false when the worker already holds version it.
+bool Runtime::upload_reserve(Gpu& G, int g, int it) {
   DevGroup& D = G.groups[g];
   HostGroup& H = host[g];
   const int b = it & 1;
@@ -957,24 +991,131 @@ void Runtime::upload(Gpu& G, int g, int it, bool last_use) {
     D.loaded[b] = it;
   }
   upload_ver[g] = std::max(upload_ver[g], it);
-  if (D.loaded[b] != it) {
-    set_dev(G);
+  if (D.loaded[b] == it) return false;
+  D.loaded[b] = it;  // reserved: the chunks follow (possibly window by window)
+  D.up_started = false;
+  return true;
+}
+
+// One chunk [off, off+len) bytes of group g's bf16 weights, pinned host
+// master -> worker G, on the low-priority H2D stream. The first chunk of an
+// upload carries its waits: edge (2) — the group's published-version flag
+// word — and the WAR wait on the buffer's previous version.
+void Runtime::upload_chunk(Gpu& G, int g, int it, int64_t off, int64_t len) {
+  DevGroup& D = G.groups[g];
+  HostGroup& H = host[g];
+  const int b = it & 1;
+  set_dev(G);
+  if (!D.up_started) {
     if (pcopy_idx[g] >= 0) {  // edge (2): the host master holds the published version
       flags.wait_geq(G.w_h2d, flag_pub(g), (uint32_t)pcopy_idx[g] + 1);
       proto_edge(roundpipe::ActionKind::ParamCopy, g, pcopy_idx[g],
                  roundpipe::ActionKind::ParamUpload, g, it);
     }
-    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse[b], 0));               // WAR (t-2)
-    cudaEvent_t xa = xfer_begin(G.w_h2d);
-    RP_CUDA(cudaMemcpyAsync(D.w[b], H.w16, H.n * 2, cudaMemcpyHostToDevice, G.w_h2d));
-    xfer_end(xa, G.w_h2d, 0, g - 1, it, G.id);
-    h2d_bytes += H.n * 2;
-    RP_CUDA(cudaEventRecord(D.ev_upload[b], G.w_h2d));
-    D.loaded[b] = it;
-    uploaders[g].push_back(G.id * 2 + b);
+    RP_CUDA(cudaStreamWaitEvent(G.w_h2d, D.ev_lastuse[b], 0));  // WAR (t-2)
+    D.up_xa = xfer_begin(G.w_h2d);
+    D.up_started = true;
   }
-  if (last_use && cfg.async_optimizer && pend_owner[g] >= 0) p_copy(g);
+  RP_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(D.w[b]) + off,
+                          reinterpret_cast<const uint8_t*>(H.w16) + off, (std::size_t)len,
+                          cudaMemcpyHostToDevice, G.w_h2d));
+  h2d_bytes += len;
+}
+
+void Runtime::upload_done(Gpu& G, int g, int it) {
+  DevGroup& D = G.groups[g];
+  const int b = it & 1;
   set_dev(G);
+  xfer_end(D.up_xa, G.w_h2d, 0, g - 1, it, G.id);
+  RP_CUDA(cudaEventRecord(D.ev_upload[b], G.w_h2d));
+  uploaders[g].push_back(G.id * 2 + b);
+}
+
+// LPT transfer windows: the uploads of iteration it+1 are
+// cut with the reference transfer planner (transfer_planner::plan: tensors
+// sorted by size, chunked to ceil(total/W), each chunk to the least-loaded
+// window) into one window per micro-batch task worker G runs in iteration
+// it; window k is released onto the low-priority H2D stream when G's compute
+// starts its k-th micro-batch, so parameter traffic is paced by compute and
+// spread over the iteration instead of queued in one burst. A worker without
+// tasks in iteration it gets everything at once.
+void Runtime::plan_upload_windows(int it_next) {
+  ensure_horizon(it_next);
+  std::vector<std::vector<int>> todo(N);  // per worker, groups in use order
+  std::vector<int> wins(N, 0);
+  for (std::size_t i = 0; i < sched.tasks.size();) {
+    const roundpipe::Task& t = sched.tasks[i];
+    if (t.iteration > it_next) break;
+    if (t.iteration == it_next - 1) wins[t.gpu] += MR;
+    if (t.iteration == it_next)
+      for (int g : slot_groups(slots[t.slot])) todo[t.gpu].push_back(g);
+    i += MR;
+  }
+  for (int w = 0; w < N; ++w) {
+    Gpu& G = gpus[w];
+    std::vector<roundpipe::TransferItem> items;
+    std::vector<std::pair<int, int64_t>> tensor;  // item -> (group, byte offset)
+    for (int g : todo[w]) {
+      if (!upload_reserve(G, g, it_next)) continue;
+      // the group's tensors (weights of one layer / the head / the table)
+      std::vector<Tensor> ts;
+      if (g == 0) ts = {Tensor{0, s.V, s.h}};
+      else if (g == s.L + 1) ts = {HL.final_norm, HL.lm_head};
+      else ts = {LL.in_norm, LL.qkv, LL.q_norm, LL.k_norm, LL.o, LL.post_norm, LL.gate_up, LL.down};
+      const int64_t end = host[g].n * 2;
+      for (std::size_t k = 0; k < ts.size(); ++k) {  // tensor k spans to the next tensor's offset
+        const int64_t a = ts[k].off * 2;
+        const int64_t z = k + 1 < ts.size() ? ts[k + 1].off * 2 : end;
+        items.push_back({"g" + std::to_string(g) + "." + std::to_string(k), z - a,
+                         roundpipe::TransferDirection::Upload, 0});
+        tensor.push_back({g, a});
+      }
+    }
+    if (items.empty()) continue;
+    std::unordered_map<std::string, std::size_t> idx;
+    for (std::size_t k = 0; k < items.size(); ++k) idx[items[k].tensor_id] = k;
+    auto& left = up_left[w];
+    if (wins[w] == 0) {  // no compute to pace against: all now
+      for (std::size_t k = 0; k < items.size(); ++k) ++left[tensor[k].first];
+      for (std::size_t k = 0; k < items.size(); ++k) {
+        const int g = tensor[k].first;
+        upload_chunk(G, g, it_next, tensor[k].second, items[k].bytes);
+        if (--left[g] == 0) upload_done(G, g, it_next);
+      }
+      continue;
+    }
+    const int64_t max_chunk = roundpipe::transfer_planner::default_max_chunk(items, wins[w]);
+    const auto plan = roundpipe::transfer_planner::plan(items, wins[w], max_chunk);
+    for (const auto& win : plan.windows) {
+      UpWindow uw;
+      uw.it = it_next;
+      for (const auto& c : win.items) {
+        const auto [g, base] = tensor[idx.at(c.tensor_id)];
+        uw.chunks.push_back({g, base + (int64_t)c.chunk_index * max_chunk, c.bytes});
+        ++left[g];
+      }
+      upq[w].push_back(std::move(uw));
+    }
+  }
+}
+
+// Worker G's compute is about to start a micro-batch: release the next
+// upload window onto the H2D stream behind that point of the compute stream.
+void Runtime::release_window(Gpu& G) {
+  if (upq[G.id].empty()) return;
+  UpWindow uw = std::move(upq[G.id].front());
+  upq[G.id].pop_front();
+  if (!uw.chunks.empty()) join(G, G.compute, G.w_h2d);
+  auto& left = up_left[G.id];
+  for (const auto& c : uw.chunks) {
+    upload_chunk(G, c.g, uw.it, c.off, c.len);
+    if (--left[c.g] == 0) upload_done(G, c.g, uw.it);
+  }
+}
+
+void Runtime::flush_windows() {
+  for (Gpu& G : gpus)
+    while (!upq[G.id].empty()) release_window(G);
 }
 
 // Enqueue iteration it's weight uploads ahead of time (into the other
@@ -1365,6 +1506,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
       const int gmb = rin * MR + mb;
       const bool first = rin == 0 && mb == 0;
       LayerActs* acts = (mb & 1) ? G.acts2.data() : G.acts.data();
+      release_window(G);  // next iteration's weights, paced by this micro-batch
       TaskRecord rec{};
       if (want_tl) {
         rec.task = roundpipe::Task{it, round, slot, mb, G.id, ss.dur_ns};
@@ -1421,6 +1563,7 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     const int gmb = rin * MR + mb;
     const bool first = rin == 0 && mb == 0;
     const int hb = par * MR + mb;  // hand-off buffer index
+    release_window(G);  // next iteration's weights, paced by this micro-batch
     TaskRecord rec{};
     if (want_tl) {
       rec.task = roundpipe::Task{it, round, slot, mb, G.id, ss.dur_ns};
@@ -1600,7 +1743,7 @@ void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
   if (cfg.async_optimizer) {
     for (int g = 0; g < ngroups(); ++g)
       if (pend_owner[g] >= 0) p_copy(g);
-    prefetch(it + 1);
+    plan_upload_windows(it + 1);
   }
   // walk the dispatch list of this iteration in emission order
   int first_round = -1;
@@ -1617,6 +1760,7 @@ void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
     run_slot(G, it, t.round, t.slot, first_round, grad_scale);
     i += MR;  // a (round, slot) is MR consecutive tasks on one worker
   }
+  flush_windows();  // every upload of it+1 is enqueued before p_copy(it+1) (edge 1)
   for (Gpu& G : gpus) {  // this parity's buffers are free once `compute` gets here
     set_dev(G);
     RP_CUDA(cudaEventRecord(G.ev_iter_done[par], G.compute));

@@ -106,6 +106,8 @@ struct DevGroup {
   int adam_iter[2] = {-1, -1};            // iteration whose grads that AdamW consumed
   cudaEvent_t ev_pcopy = nullptr;         // p_copy(l, t)              optimizer lane
   cudaEvent_t ev_state = nullptr;         // fp32 state written back to host
+  bool up_started = false;                // windowed upload: first chunk enqueued
+  cudaEvent_t up_xa = nullptr;            // its transfer-timeline start event
 };
 
 // Activations of one decoder layer for one micro-batch.
