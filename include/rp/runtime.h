@@ -40,7 +40,12 @@ enum {
   /* one worker: publish every AdamW result through the pinned bf16 master
    * (p_copy, then upload) as with several workers, instead of writing the
    * HBM-resident groups' new weights in place (keeps the host master current) */
-  RP_RT_HOST_PUBLISH = 32
+  RP_RT_HOST_PUBLISH = 32,
+  /* N > 1: each worker allocates weights / grads / AdamW output / checkpoints
+   * on demand from a per-worker pool and returns them after their last use
+   * (its footprint is its working set, not the model). Automatic when one
+   * buffer per group and worker would not fit in HBM. */
+  RP_RT_POOLED = 64
 };
 
 typedef struct {
@@ -88,6 +93,8 @@ typedef struct {
   int32_t kernels_launched;    /* cumulative count of this library's kernel launches */
   int32_t pad_;
   int64_t resident_params;     /* params whose fp32 AdamW state lives in HBM (1 device) */
+  int64_t pool_peak_bytes;     /* pooled workers: max over workers of the peak bytes in use */
+  int64_t pool_bytes;          /* pooled workers: slab bytes allocated, all workers */
 } rp_runtime_stats_t;
 
 int rp_runtime_create(const rp_runtime_config_t* cfg, rp_runtime_t** out);
@@ -183,6 +190,24 @@ int rp_runtime_progress(rp_runtime_t* rt, int32_t group, int32_t* published,
                         int32_t* loss_iteration);
 int rp_runtime_measured_costs(rp_runtime_t* rt, rp_layer_cost_t* out, int32_t cap, int32_t* n);
 int rp_runtime_profile_records(rp_runtime_t* rt, rp_prof_record_t* out, int64_t cap, int64_t* n);
+
+/* Device-memory plan of a configuration for one worker, computed on the
+ * host without a GPU: the activation-aware stage plan the runtime would use
+ * (mem_limit_bytes = 90 % of hbm_bytes minus the fixed per-worker buffers
+ * unless cfg->mem_limit_bytes is set), the fixed buffers, the bytes of one
+ * buffer per parameter group (2 weight versions, 2 grad buffers, AdamW
+ * output, checkpoints), and for pooled workers the peak of the worst worker
+ * replayed over the dispatch list. pooled = 1 if the runtime would pool. */
+typedef struct {
+  int32_t num_slots, pooled;
+  int32_t pool_worker, pad_;
+  int64_t mem_limit_bytes;
+  int64_t activations, scratch, handoff, optimizer_ring, workspace;
+  int64_t static_groups;
+  int64_t pool_peak, pool_weights, pool_grads, pool_pend, pool_checkpoints;
+  int64_t total_static, total_pooled;
+} rp_memory_plan_t;
+int rp_memory_plan(const rp_runtime_config_t* cfg, int64_t hbm_bytes, rp_memory_plan_t* out);
 
 #ifdef __cplusplus
 }

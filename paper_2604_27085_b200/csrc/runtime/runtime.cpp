@@ -277,6 +277,16 @@ struct Runtime {
   }
 
   int ngroups() const { return s.L + 2; }
+  // device bytes of one worker's per-group buffers without pooling: two bf16
+  // weight versions, two fp32 grad buffers, the AdamW output, checkpoints
+  std::size_t static_bytes_per_worker() const {
+    std::size_t b = 0;
+    for (int g = 0; g < ngroups(); ++g)
+      b += (std::size_t)host[g].n * 2 * 3 + (std::size_t)host[g].tn() * 4 * 2;
+    const int lck = std::max(0, plan.fused_stage.first);
+    if (S > 1) b += (std::size_t)parities * lck * MR * T * s.h * 2;
+    return b;
+  }
   int64_t group_numel(int g) const {
     if (g == 0) return (int64_t)s.V * s.h;
     if (g == s.L + 1) return HL.total;
@@ -314,6 +324,61 @@ struct Runtime {
     RP_CUDA(cudaEventRecord(e, from));
     RP_CUDA(cudaStreamWaitEvent(to, e, 0));
   }
+  // ---- per-worker buffer pools (N > 1: "stateless" workers) -------------------
+  // A worker holds weights only for the versions it is about to use or using,
+  // grads only until the optimizer consumed them, AdamW output until p_copy,
+  // checkpoints until the recomputing slot read them — so its HBM footprint
+  // is its working set, not the model (a Qwen3-32B at N=8 would need ~0.4 TB
+  // per worker with one buffer per group). Slabs are exact-size, allocated
+  // on first need and reused through their free events.
+  bool pooled = false;
+  int slab_acquire(Gpu& G, std::size_t bytes, int cat, cudaStream_t user) {
+    int cur = 0;
+    RP_CUDA(cudaGetDevice(&cur));
+    RP_CUDA(cudaSetDevice(G.dev));
+    int idx = -1;
+    for (int i = 0; i < (int)G.slabs.size(); ++i)
+      if (!G.slabs[i].busy && G.slabs[i].bytes == bytes) {
+        idx = i;
+        break;
+      }
+    if (idx < 0) {
+      Slab sl;
+      sl.bytes = bytes;
+      sl.p = dalloc(G, bytes, cat);
+      sl.free_ev = new_event(false);
+      G.slabs.push_back(sl);
+      G.pool_bytes += bytes;
+      idx = (int)G.slabs.size() - 1;
+    }
+    Slab& sl = G.slabs[idx];
+    if (sl.recorded) RP_CUDA(cudaStreamWaitEvent(user, sl.free_ev, 0));  // previous user done
+    sl.busy = true;
+    sl.cat = cat;
+    G.pool_busy += bytes;
+    G.pool_peak = std::max(G.pool_peak, G.pool_busy);
+    RP_CUDA(cudaSetDevice(cur));
+    return idx;
+  }
+  // the slab's last access was enqueued on `st` (a stream of G's device)
+  void slab_release(Gpu& G, int idx, cudaStream_t st, int tag_kind = -1, int tag_group = -1,
+                    int tag_iter = -1) {
+    Slab& sl = G.slabs.at(idx);
+    if (!sl.busy) throw RtError(RP_E_INTERNAL, "releasing a free slab");
+    int cur = 0;
+    RP_CUDA(cudaGetDevice(&cur));
+    RP_CUDA(cudaSetDevice(G.dev));
+    RP_CUDA(cudaEventRecord(sl.free_ev, st));
+    RP_CUDA(cudaSetDevice(cur));
+    sl.recorded = true;
+    sl.busy = false;
+    sl.tag_kind = tag_kind;
+    sl.tag_group = tag_group;
+    sl.tag_iter = tag_iter;
+    G.pool_busy -= sl.bytes;
+  }
+  // (worker, group) -> (round, slot) of its last use in the iteration being enqueued
+  std::unordered_map<int64_t, int64_t> last_use_task;
   // producer P finished writing hand-off / checkpoint buffer b on stream st
   void mark_ready(Slotbuf& b, const Gpu& P, cudaStream_t st) {
     cudaEvent_t& e = b.ready_dev[P.dev];
@@ -362,6 +427,7 @@ struct Runtime {
   void pull_w16(int g);             // direct groups: device bf16 of the next iteration -> host
   int64_t resident_params = 0;
   int lora_r = 0;          // LoRA rank (0 = full fine-tune)
+  int64_t partition_limit = 0;  // memory limit the partitioner planned with
   float lora_scale = 0.f;  // alpha / r
   bool trainable(int g) const { return host[g].tn() > 0; }
   // LoRA: Y += s (X A^T) B^T; keeps Us = s X A^T (T x r) for the backward
@@ -501,18 +567,7 @@ void Runtime::init(const rp_runtime_config_t& c) {
   cfg = c;
   model = c.model ? c.model : "qwen3-8b";
   cfg.model = nullptr;
-  const auto shape = roundpipe::config_io::load_shape(model);
-  s.h = (int)shape.cfg.hidden_dim;
-  s.nq = shape.cfg.num_heads;
-  s.nk = shape.cfg.num_kv_heads;
-  s.hd = shape.head_dim;
-  s.m = (int)shape.cfg.intermediate_dim;
-  s.L = shape.cfg.num_layers;
-  s.V = shape.vocab_size;
-  s.theta = shape.rope_theta;
-  s.eps = shape.rms_norm_eps;
-  if (shape.cfg.total_experts != 1)
-    throw RtError(RP_E_INPUT, "MoE models are not supported by the executor yet");
+  s = load_shape(model);
   if (c.seq_len < 128 || c.seq_len % 128 || c.micro_batch < 1 || c.micro_batches < 1 ||
       c.num_gpus < 1)
     throw RtError(RP_E_INPUT, "need seq_len % 128 == 0, b >= 1, M >= 1, N >= 1");
@@ -586,6 +641,14 @@ void Runtime::init(const rp_runtime_config_t& c) {
   RP_CUDA(cudaMallocHost(&loss_host, sizeof(float) * N * 2));
   RP_CUDA(cudaSetDevice(0));
   flags.init(ngroups() + N);
+  // pooled workers: requested, or one-buffer-per-group would not fit
+  if (N > 1) {
+    cudaDeviceProp prop;
+    RP_CUDA(cudaGetDeviceProperties(&prop, 0));
+    const int per_dev = (N + ndev - 1) / ndev;
+    const double need = (double)per_dev * (double)static_bytes_per_worker();
+    pooled = (cfg.flags & RP_RT_POOLED) || need > 0.6 * (double)prop.totalGlobalMem;
+  }
   gpus.resize(N);
   for (int w = 0; w < N; ++w) alloc_worker(gpus[w], w);
   ev_loss.resize(N);
@@ -604,7 +667,7 @@ void Runtime::init(const rp_runtime_config_t& c) {
 // streams from pinned host memory. cfg.resident_state_gb: < 0 no cap, 0 off
 // (every group host-offloaded: BASELINE configs[2]), > 0 cap in GB.
 void Runtime::place_resident_state() {
-  if (ndev != 1) return;
+  if (ndev != 1 || pooled) return;
   const double cap_gb = cfg.resident_state_gb < 0 ? 1e9 : cfg.resident_state_gb;
   if (cap_gb <= 0) return;
   set_dev(gpus[0]);
@@ -702,38 +765,14 @@ void Runtime::pull_resident(int g) {
 }
 
 void Runtime::build_plan() {
-  if (cfg.costs && cfg.n_costs > 0) {
-    if (cfg.n_costs != s.L + 1) throw RtError(RP_E_INPUT, "cost table must have L+1 rows");
-    for (int i = 0; i < cfg.n_costs; ++i) {
-      roundpipe::LayerCost lc;
-      lc.t_fwd_ns = cfg.costs[i].t_fwd_ns;
-      lc.t_bwd_ns = cfg.costs[i].t_bwd_ns;
-      lc.param_bytes = cfg.costs[i].param_bytes;
-      lc.act_ckpt_bytes = cfg.costs[i].act_ckpt_bytes;
-      lc.act_full_bytes = cfg.costs[i].act_full_bytes;
-      costs.push_back(lc);
-    }
-    cfg.costs = nullptr;
-  } else {
-    const auto mc = roundpipe::config_io::load_model(model);
-    const auto gpu = roundpipe::config_io::load_gpu("b200");
-    costs = roundpipe::cost_model::layer_costs(
-        mc, roundpipe::Workload{cfg.seq_len, cfg.micro_batch}, gpu, true);
-  }
-  roundpipe::PartitionProblem p;
-  p.costs = costs;
-  p.num_gpus = cfg.num_gpus;
-  p.micro_batches = cfg.micro_batches;
-  p.residency_factor = cfg.residency_factor;
-  if (cfg.mem_limit_bytes > 0) {
-    p.mem_limit_bytes = cfg.mem_limit_bytes;
-  } else {
-    cudaDeviceProp prop;
-    RP_CUDA(cudaGetDeviceProperties(&prop, 0));
-    p.mem_limit_bytes = (int64_t)(0.9 * (double)prop.totalGlobalMem);
-  }
-  plan = roundpipe::partitioner::optimal_partition(p);
-  slots = roundpipe::scheduler::slot_table_from_plan(plan, costs);
+  cudaDeviceProp prop;
+  RP_CUDA(cudaGetDeviceProperties(&prop, 0));
+  PlanChoice pc = choose_plan(cfg, s, model, (int64_t)prop.totalGlobalMem, logits_rows, chunk_elems);
+  cfg.costs = nullptr;  // the caller's table was copied
+  costs = std::move(pc.costs);
+  plan = pc.plan;
+  slots = std::move(pc.slots);
+  partition_limit = pc.mem_limit;
   S = (int)slots.size();
   bwd_slot_of.assign(s.L, -1);
   for (const auto& sl : slots)
@@ -785,14 +824,16 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     DevGroup& D = G.groups[g];
     const int64_t n = group_numel(g);
     for (int b = 0; b < 2; ++b) {
-      D.w[b] = static_cast<uint16_t*>(dalloc(n * 2, 0));
+      if (!pooled) D.w[b] = static_cast<uint16_t*>(dalloc(n * 2, 0));
       D.ev_upload[b] = new_event(false);
       D.ev_lastuse[b] = new_event(false);
     }
     const int64_t tn = host[g].tn(), to = host[g].t_off;  // trainable region only
-    D.grad[0] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
-    D.grad[1] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
-    D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
+    if (!pooled) {
+      D.grad[0] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
+      D.grad[1] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
+      D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
+    }
     D.ev_gradwrite = new_event(false);
     D.ev_adam[0] = new_event(false);
     D.ev_adam[1] = new_event(false);
@@ -895,9 +936,9 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     RP_CUDA(cudaMemcpy(G.cos_sin, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
   }
   if (S > 1) {  // hand-off and checkpoint buffers
-    auto mkbuf = [&](std::size_t bytes, int cat) {
+    auto mkbuf = [&](std::size_t bytes, int cat) {  // cat < 0: pooled (bound on demand)
       Slotbuf b;
-      b.p = dalloc(bytes, cat);
+      b.p = cat < 0 ? nullptr : dalloc(bytes, cat);
       b.ready_dev.assign(ndev, nullptr);
       b.read = new_event(false);
       return b;
@@ -911,7 +952,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     for (int p = 0; p < parities; ++p)
       for (int l = 0; l < plan.fused_stage.first && l < s.L; ++l)
         for (int mb = 0; mb < MR; ++mb)
-          G.ckpt[((std::size_t)p * s.L + l) * MR + mb] = mkbuf(Th * 2, 5);
+          G.ckpt[((std::size_t)p * s.L + l) * MR + mb] = mkbuf(Th * 2, pooled ? -1 : 5);
   }
   for (int b = 0; b < 2; ++b)
     for (int j = 0; j < 3; ++j)
@@ -929,12 +970,13 @@ void Runtime::init_weights() {
   const float std_ = cfg.init_std > 0 ? cfg.init_std : 0.02f;
   int64_t nmax = 0;
   for (int g = 0; g < ngroups(); ++g) nmax = std::max(nmax, host[g].n);
-  float* f32 = nullptr;  // fp32 scratch of the largest group
+  float* f32 = nullptr;  // fp32 + bf16 scratch of the largest group
+  uint16_t* b16 = nullptr;
   RP_CUDA(cudaMalloc(&f32, (std::size_t)nmax * 4));
+  RP_CUDA(cudaMalloc(&b16, (std::size_t)nmax * 2));
   for (int g = 0; g < ngroups(); ++g) {
     HostGroup& H = host[g];
-    DevGroup& D = G.groups[g];
-    RP_K(rp_init_normal(f32, D.w[0], H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_,
+    RP_K(rp_init_normal(f32, b16, H.n, cfg.init_seed * 1000003ull + (uint64_t)g, std_,
                         G.compute));
     std::vector<std::pair<int64_t, int64_t>> ones, zeros;
     if (g >= 1 && g <= s.L) {
@@ -946,15 +988,16 @@ void Runtime::init_weights() {
     } else if (g == s.L + 1) {
       ones = {{HL.final_norm.off, s.h}};
     }
-    for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, D.w[0] + off, n, 1.0f, G.compute));
-    for (auto [off, n] : zeros) RP_K(rp_fill(f32 + off, D.w[0] + off, n, 0.0f, G.compute));
+    for (auto [off, n] : ones) RP_K(rp_fill(f32 + off, b16 + off, n, 1.0f, G.compute));
+    for (auto [off, n] : zeros) RP_K(rp_fill(f32 + off, b16 + off, n, 0.0f, G.compute));
     if (H.tn() > 0)
       RP_CUDA(cudaMemcpyAsync(H.master + H.t_off, f32 + H.t_off, H.tn() * 4,
                               cudaMemcpyDeviceToHost, G.compute));
-    RP_CUDA(cudaMemcpyAsync(H.w16, D.w[0], H.n * 2, cudaMemcpyDeviceToHost, G.compute));
+    RP_CUDA(cudaMemcpyAsync(H.w16, b16, H.n * 2, cudaMemcpyDeviceToHost, G.compute));
     RP_CUDA(cudaStreamSynchronize(G.compute));
   }
   RP_CUDA(cudaFree(f32));
+  RP_CUDA(cudaFree(b16));
 }
 
 // ---- GPU lane: weight upload ----------------------------------------------------------
@@ -992,6 +1035,10 @@ bool Runtime::upload_reserve(Gpu& G, int g, int it) {
   }
   upload_ver[g] = std::max(upload_ver[g], it);
   if (D.loaded[b] == it) return false;
+  if (pooled && !D.w[b]) {  // a slab of the worker's pool for this version
+    D.w_slab[b] = slab_acquire(G, (std::size_t)H.n * 2, 0, G.w_h2d);
+    D.w[b] = static_cast<uint16_t*>(G.slabs[D.w_slab[b]].p);
+  }
   D.loaded[b] = it;  // reserved: the chunks follow (possibly window by window)
   D.up_started = false;
   return true;
@@ -1170,6 +1217,11 @@ void Runtime::p_copy(int g) {
   d2h_bytes += H.tn() * 2;
   RP_CUDA(cudaEventRecord(D.ev_pcopy, O.opt_d2h));
   flags.set(O.opt_d2h, flag_pub(g), (uint32_t)idx + 1);
+  if (pooled && D.pend_slab >= 0) {
+    slab_release(O, D.pend_slab, O.opt_d2h);
+    D.pend_slab = -1;
+    D.pend = nullptr;
+  }
   pcopy_idx[g] = idx;
   pend_owner[g] = -1;
 }
@@ -1482,6 +1534,18 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
     // slot does not stall on the whole resident optimizer pass
     for (int g : grad_groups) {
       DevGroup& D = G.groups[g];
+      if (pooled) {  // a fresh slab for this iteration's grads (edge (4) = its free event)
+        if (rin > 0) continue;
+        const int p = it & 1;
+        if (D.grad_slab[p] >= 0) throw RtError(RP_E_INTERNAL, "grad slab still bound");
+        D.grad_slab[p] = slab_acquire(G, (std::size_t)host[g].tn() * 4, 1, st);
+        const Slab& sl = G.slabs[D.grad_slab[p]];
+        D.grad[p] = static_cast<float*>(sl.p) - host[g].t_off;
+        if (sl.tag_kind == (int)roundpipe::ActionKind::GradCopy)
+          proto_edge(roundpipe::ActionKind::GradCopy, sl.tag_group, sl.tag_iter,
+                     roundpipe::ActionKind::GradWrite, g, it);
+        continue;
+      }
       if (host[g].d_state || D.adam_iter[it & 1] < 0) continue;
       RP_CUDA(cudaStreamWaitEvent(st, D.ev_adam[it & 1], 0));  // edge (4), parity buffers
       proto_edge(roundpipe::ActionKind::GradCopy, g, D.adam_iter[it & 1],
@@ -1595,6 +1659,11 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         // checkpoint x_l for the backward slot that recomputes layer l
         Gpu& O = gpus[worker_of(round, bwd_slot_of[l])];
         Slotbuf& ck = O.ckpt[((std::size_t)par * s.L + l) * MR + mb];
+        if (pooled) {  // a slab of the consumer's pool until the recomputing slot read it
+          if (ck.slab >= 0) throw RtError(RP_E_INTERNAL, "checkpoint slab still bound");
+          ck.slab = slab_acquire(O, Th2, 5, G.act);
+          ck.p = O.slabs[ck.slab].p;
+        }
         join(G, st, G.act);
         RP_CUDA(cudaStreamWaitEvent(G.act, ck.read, 0));
         d2d(ck.p, O, x, G, Th2, G.act);
@@ -1651,6 +1720,11 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
         prof_unit(l, 1);
         layer_bwd(G, l, A, first);
         RP_CUDA(cudaEventRecord(ck.read, st));
+        if (pooled) {
+          slab_release(G, ck.slab, st);
+          ck.slab = -1;
+          ck.p = nullptr;
+        }
       }
     }
     if (has_grads) {
@@ -1681,6 +1755,18 @@ void Runtime::run_slot(Gpu& G, int it, int round, int slot, int first_round, flo
   // last compute read of the slot's weights; grads complete (GradWrite) once
   // the weight-gradient stream has drained into `compute`
   for (int g : gs) RP_CUDA(cudaEventRecord(G.groups[g].ev_lastuse[it & 1], st));
+  if (pooled)  // the worker's last use of this version: its slab goes back to the pool
+    for (int g : gs) {
+      const auto lu = last_use_task.find((int64_t)G.id * 1000003 + g);
+      if (lu == last_use_task.end() || lu->second != (int64_t)round * 1000003 + slot) continue;
+      DevGroup& D = G.groups[g];
+      const int b = it & 1;
+      if (D.w_slab[b] < 0) continue;
+      slab_release(G, D.w_slab[b], st);
+      D.w_slab[b] = -1;
+      D.w[b] = nullptr;
+      D.loaded[b] = -1;
+    }
   if (has_grads) RP_CUDA(cudaStreamWaitEvent(st, G.ev_wgrad, 0));
   if (has_grads && rin == R - 1)
     for (int g : grad_groups) {
@@ -1744,6 +1830,15 @@ void Runtime::enqueue_iteration(const int32_t* tokens, const int32_t* labels) {
     for (int g = 0; g < ngroups(); ++g)
       if (pend_owner[g] >= 0) p_copy(g);
     plan_upload_windows(it + 1);
+  }
+  if (pooled) {  // each worker's last use of each group in this iteration
+    last_use_task.clear();
+    for (std::size_t i = 0; i < sched.tasks.size(); i += MR) {
+      const roundpipe::Task& t = sched.tasks[i];
+      if (t.iteration != it) continue;
+      for (int g : slot_groups(slots[t.slot]))
+        last_use_task[(int64_t)t.gpu * 1000003 + g] = (int64_t)t.round * 1000003 + t.slot;
+    }
   }
   // walk the dispatch list of this iteration in emission order
   int first_round = -1;
@@ -1861,6 +1956,10 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     if (!cfg.async_optimizer) p_copy(g);
     return;
   }
+  if (pooled && !D.pend) {  // AdamW output slab until p_copy publishes it
+    D.pend_slab = slab_acquire(G, (std::size_t)H.n * 2, 2, G.opt_comp);
+    D.pend = static_cast<uint16_t*>(G.slabs[D.pend_slab].p);
+  }
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
   cudaEvent_t xa = xfer_begin(G.opt_h2d);
   for (int64_t off = H.t_off; off < H.n; off += chunk_elems) {  // trainable region
@@ -1887,6 +1986,12 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     RP_CUDA(cudaEventRecord(G.opt_free[sl], G.opt_d2h));
   }
   RP_CUDA(cudaEventRecord(D.ev_adam[parity], G.opt_comp));  // g_copy(l, t) complete
+  if (pooled) {  // grads consumed: the slab goes back to the pool
+    slab_release(G, D.grad_slab[parity], G.opt_comp, (int)roundpipe::ActionKind::GradCopy, g,
+                 last_iter);
+    D.grad_slab[parity] = -1;
+    D.grad[parity] = nullptr;
+  }
   if (!D.ev_state) D.ev_state = new_event(false);
   RP_CUDA(cudaEventRecord(D.ev_state, G.opt_d2h));
   xfer_end(xa, G.opt_d2h, 2, g - 1, last_iter, G.id);
@@ -2140,6 +2245,8 @@ RP_API int rp_get_params(rp_runtime_t* p, int32_t group, int32_t which, float* o
         if (n > o) {
           rp::rt::Gpu& G = rt->gpus[rt->grad_owner[g]];
           rt->set_dev(G);
+          if (!G.groups[g].grad[rt->last_iter & 1])
+            throw RtError(RP_E_INPUT, "gradients already consumed by step() (pooled workers)");
           RP_CUDA(cudaMemcpy(out + o, G.groups[g].grad[rt->last_iter & 1] + o, (n - o) * 4,
                              cudaMemcpyDeviceToHost));
         }
@@ -2280,6 +2387,10 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
         D.loaded[b] = rt->iter + 1;
         continue;
       }
+      if (rt->pooled && !G.groups[g].pend) {
+        G.groups[g].pend_slab = rt->slab_acquire(G, (std::size_t)H.n * 2, 2, G.opt_d2h);
+        G.groups[g].pend = static_cast<uint16_t*>(G.slabs[G.groups[g].pend_slab].p);
+      }
       RP_CUDA(cudaMemcpy(G.groups[g].pend + H.t_off, tmp.data(), H.tn() * 2,
                          cudaMemcpyHostToDevice));
       rt->pend_owner[g] = 0;
@@ -2379,6 +2490,10 @@ RP_API int rp_runtime_stats(rp_runtime_t* p, rp_runtime_stats_t* st) {
     st->iterations_done = rt->iter;
     st->kernels_launched = (int32_t)rt->kernels;
     st->resident_params = rt->resident_params;
+    for (auto& G : rt->gpus) {
+      st->pool_peak_bytes = std::max<int64_t>(st->pool_peak_bytes, (int64_t)G.pool_peak);
+      st->pool_bytes += (int64_t)G.pool_bytes;
+    }
   });
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <array>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -108,6 +109,22 @@ struct DevGroup {
   cudaEvent_t ev_state = nullptr;         // fp32 state written back to host
   bool up_started = false;                // windowed upload: first chunk enqueued
   cudaEvent_t up_xa = nullptr;            // its transfer-timeline start event
+  // pooled workers (N > 1): the buffers above are slabs of the worker's pool,
+  // bound for one version / iteration and returned after their last use
+  int w_slab[2] = {-1, -1}, grad_slab[2] = {-1, -1}, pend_slab = -1;
+};
+
+// A device buffer of a worker's pool (exact-size classes). It is handed out
+// by the controller; its next user's stream waits on free_ev, recorded where
+// the previous user's last access was enqueued. `tag_*` names the action
+// that last released it (for the realised-protocol record).
+struct Slab {
+  void* p = nullptr;
+  std::size_t bytes = 0;
+  cudaEvent_t free_ev = nullptr;
+  bool recorded = false, busy = false;
+  int cat = 0;
+  int tag_kind = -1, tag_group = -1, tag_iter = -1;
 };
 
 // Activations of one decoder layer for one micro-batch.
@@ -128,6 +145,7 @@ struct LayerActs {
 // records `read` after its last read; cross-device waits on either are legal.
 struct Slotbuf {
   void* p = nullptr;
+  int slab = -1;                       // pooled checkpoints: slab of the consumer's pool
   std::vector<cudaEvent_t> ready_dev;  // by producer device
   cudaEvent_t ready = nullptr;         // the one last recorded (what consumers wait on)
   cudaEvent_t read = nullptr;
@@ -196,7 +214,42 @@ struct Gpu {
   cudaEvent_t ev_tokens = nullptr;
   std::vector<std::size_t> allocated;
   std::vector<void*> owned;  // every device allocation of this worker (freed by ~Runtime)
+  std::vector<Slab> slabs;   // pooled buffers (weights, grads, AdamW output, checkpoints)
+  std::size_t pool_bytes = 0, pool_busy = 0, pool_peak = 0;
 };
+
+// ---- memory plan (memory_plan.cpp) ------------------------------------------------
+// Per-worker device bytes that do not scale with the parameter groups.
+struct WorkerBytes {
+  int64_t activations = 0, scratch = 0, handoff = 0, optimizer_ring = 0, workspace = 0;
+  int64_t fixed() const;
+};
+WorkerBytes worker_fixed_bytes(const Shape& s, int T, int seq, int M, int MR, int S, int parities,
+                               int nsets, int logits_rows, int lora_r, int64_t chunk_elems);
+// Peak of a pooled worker's group buffers (the worst worker), by category.
+struct PoolPeak {
+  int worker = 0;
+  int64_t total = 0, weights = 0, grads = 0, pend = 0, checkpoints = 0;
+};
+PoolPeak pooled_peak(const Shape& s, const LayerLayout& LL, const HeadLayout& HL,
+                     const roundpipe::StagePlan& plan,
+                     const std::vector<roundpipe::StageSlot>& slots,
+                     const roundpipe::Schedule& sched, int N, int MR, int T, bool async,
+                     int lora_r, int iters);
+// The stage plan of a configuration: the reference partitioner on the cost
+// table (cfg.costs or the cost model), given cfg.mem_limit_bytes, or else
+// 90 % of the device's HBM minus what a worker holds besides parameters
+// (activation-aware, iterated until the fused stage's activation sets fit).
+struct PlanChoice {
+  std::vector<roundpipe::LayerCost> costs;
+  roundpipe::StagePlan plan;
+  std::vector<roundpipe::StageSlot> slots;
+  int64_t mem_limit = 0;
+  WorkerBytes fixed;
+};
+Shape load_shape(const std::string& model);
+PlanChoice choose_plan(const rp_runtime_config_t& cfg, const Shape& s, const std::string& model,
+                       int64_t hbm_bytes, int logits_rows, int64_t chunk_elems);
 
 struct TaskRecord {
   roundpipe::Task task;

@@ -24,6 +24,7 @@ RP_RT_FUSED_PIPELINE = 4
 RP_RT_UNFUSED_SWIGLU = 8
 RP_RT_RECORD_PROTOCOL = 16
 RP_RT_HOST_PUBLISH = 32
+RP_RT_POOLED = 64
 
 
 class AdamC(C.Structure):
@@ -44,13 +45,43 @@ class StatsC(C.Structure):
     _fields_ = [("num_layers", I32), ("num_slots", I32), ("params_total", I64),
                 ("host_bytes_pinned", I64), ("device_bytes", I64 * 8), ("h2d_bytes", I64),
                 ("d2h_bytes", I64), ("p2p_bytes", I64), ("iterations_done", I32),
-                ("kernels_launched", I32), ("pad_", I32), ("resident_params", I64)]
+                ("kernels_launched", I32), ("pad_", I32), ("resident_params", I64),
+                ("pool_peak_bytes", I64), ("pool_bytes", I64)]
 
 
 LAYER_TENSORS = ["input_norm", "qkv", "q_norm", "k_norm", "o", "post_norm", "gate_up", "down"]
 LORA_TENSORS = ["qkv_lora_A", "qkv_lora_B", "o_lora_A", "o_lora_B", "gate_up_lora_A",
                 "gate_up_lora_B", "down_lora_A", "down_lora_B"]
 HEAD_TENSORS = ["final_norm", "lm_head"]
+
+
+class MemoryPlanC(C.Structure):
+    _fields_ = [("num_slots", I32), ("pooled", I32), ("pool_worker", I32), ("pad_", I32),
+                ("mem_limit_bytes", I64), ("activations", I64), ("scratch", I64),
+                ("handoff", I64), ("optimizer_ring", I64), ("workspace", I64),
+                ("static_groups", I64), ("pool_peak", I64), ("pool_weights", I64),
+                ("pool_grads", I64), ("pool_pend", I64), ("pool_checkpoints", I64),
+                ("total_static", I64), ("total_pooled", I64)]
+
+
+def memory_plan(model="qwen3-8b", seq_len=4096, micro_batch=1, micro_batches=16, num_gpus=1,
+                round_micro_batches=0, async_optimizer=True, hbm_bytes=int(180e9),
+                lora_rank=0, pooled=False, mem_limit_bytes=0) -> dict:
+    """Per-worker device-memory plan of a configuration, on the host (no GPU):
+    rp_memory_plan (include/rp/runtime.h)."""
+    lib = _native.load()
+    name = model.encode()
+    cfg = RuntimeConfigC(name, seq_len, micro_batch, micro_batches, round_micro_batches, num_gpus,
+                         int(async_optimizer), mem_limit_bytes, 2.0, VP(0), 0,
+                         AdamC(1e-4, 0.9, 0.95, 1e-8, 0.0, 1.0), 0, 0.02,
+                         RP_RT_POOLED if pooled else 0, lora_rank, 0.0, -1.0, 0, 0)
+    out = MemoryPlanC()
+    f = lib.rp_memory_plan
+    f.restype = C.c_int
+    code = f(C.byref(cfg), I64(hbm_bytes), C.byref(out))
+    if code != 0:
+        raise _native._ERRORS.get(code, _native.NativeError)(code, "rp_memory_plan failed")
+    return {k: getattr(out, k) for k, _ in MemoryPlanC._fields_ if k != "pad_"}
 
 
 @dataclass
@@ -70,7 +101,8 @@ class RoundPipe:
                  costs=None, mem_limit_bytes=0, residency_factor=2.0, init_seed=0,
                  init_std=0.02, skip_init=False, record_timeline=False, lora_rank=0,
                  lora_alpha=0.0, resident_state_gb=-1.0, logits_rows=0, fused_pipeline=False,
-                 unfused_swiglu=False, record_protocol=False, host_publish=False):
+                 unfused_swiglu=False, record_protocol=False, host_publish=False,
+                 pooled=False):
         """resident_state_gb: fp32 AdamW state placement on a single device —
         < 0 keeps the groups that fit in free HBM resident (default), 0 keeps
         all of it in pinned host memory (host-offloaded Adam, BASELINE
@@ -92,7 +124,8 @@ class RoundPipe:
             | (RP_RT_FUSED_PIPELINE if fused_pipeline else 0)
             | (RP_RT_UNFUSED_SWIGLU if unfused_swiglu else 0)
             | (RP_RT_RECORD_PROTOCOL if record_protocol else 0)
-            | (RP_RT_HOST_PUBLISH if host_publish else 0),
+            | (RP_RT_HOST_PUBLISH if host_publish else 0)
+            | (RP_RT_POOLED if pooled else 0),
             lora_rank, lora_alpha, float(resident_state_gb), int(logits_rows), 0)
         self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.h = VP()
@@ -300,7 +333,8 @@ class RoundPipe:
                 "device_bytes": list(st.device_bytes), "h2d_bytes": st.h2d_bytes,
                 "d2h_bytes": st.d2h_bytes, "p2p_bytes": st.p2p_bytes,
                 "iterations_done": st.iterations_done, "kernels_launched": st.kernels_launched,
-                "resident_params": st.resident_params}
+                "resident_params": st.resident_params, "pool_peak_bytes": st.pool_peak_bytes,
+                "pool_bytes": st.pool_bytes}
 
     # -- profiling ----------------------------------------------------------------
     PROFILE_CATEGORIES = ("gemm", "attention", "hbm_kernels", "adamw")

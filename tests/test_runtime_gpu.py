@@ -125,6 +125,48 @@ def check(mode, losses, grads0, master):
 _GPU_GRADS = {}
 
 
+def test_pooled_workers_hold_their_working_set_only():
+    """Pooled N=4 / S=7 workers allocate less device memory than one buffer
+    per group and worker, give the same losses and grads as the static
+    allocation (same kernels, other addresses), and recycle their slabs
+    (a second run of steps allocates nothing new)."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    params = O.init_params(s, seed=0)
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    out = {}
+    for pooled in (False, True):
+        rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=4,
+                       async_optimizer=True, adam=AdamW(**HP), costs=uniform_costs(5),
+                       skip_init=True, pooled=pooled, resident_state_gb=0.0)
+        rt.load_state({k: v.numpy() for k, v in params.items()}, s.layers)
+        losses = []
+        for it in range(6):
+            losses.append(rt.forward_backward(tok.numpy(), lab.numpy()))
+            if it == 0:
+                g = rt.read_state(s.layers, which=2)
+            rt.step()
+            if it == 2:
+                rt.sync()
+                st2 = rt.stats()
+        rt.sync()
+        st = rt.stats()
+        rt.close()
+        out[pooled] = (losses, g, st, st2)
+    (l0, g0, st0, _), (l1, g1, st1, st1b) = out[False], out[True]
+    for a, b in zip(l0, l1):
+        assert abs(a - b) / abs(a) < 1e-5, (l0, l1)
+    for k in g0:
+        n = np.linalg.norm(g0[k])
+        if n > 1e-6:
+            assert np.linalg.norm(g1[k] - g0[k]) / n < 1e-3, k
+    static = sum(st0["device_bytes"][c] for c in (0, 1, 2, 5))
+    pooled_b = sum(st1["device_bytes"][c] for c in (0, 1, 2, 5))
+    print("static", static, "pooled", pooled_b, "pool peak/worker", st1["pool_peak_bytes"])
+    assert 0 < pooled_b < static
+    assert st1["pool_bytes"] == st1b["pool_bytes"]  # steady state: slabs recycled
+
+
 def test_multi_worker_grads_match_single_fused_stage():
     """The 4-worker / 7-slot execution (hand-offs, checkpoints, recompute)
     computes the same gradients as the single fused stage on the same GPU:
@@ -156,10 +198,15 @@ def test_step_parity_single_fused_stage(mode, variant):
     check(mode, losses, g0, master)
 
 
+@pytest.mark.parametrize("pooled", [False, True])
 @pytest.mark.parametrize("mode", ["sync", "async"])
-def test_step_parity_four_workers_seven_slots(mode):
+def test_step_parity_four_workers_seven_slots(mode, pooled):
+    """pooled: every worker allocates weights / grads / AdamW output /
+    checkpoints on demand from its pool and returns them after their last
+    use (the multi-GPU memory mode, RP_RT_POOLED)."""
     costs = uniform_costs(5)
-    losses, g0, master, tl, (plan, durs) = run_case(mode, 4, costs=costs, timeline=True)
+    losses, g0, master, tl, (plan, durs) = run_case(mode, 4, costs=costs, timeline=True,
+                                                    pooled=pooled)
     assert plan.num_slots() == 7
     assert [(r.first, r.last) for r in plan.fwd_stages] == [(0, 2), (3, 3)]
     assert (plan.fused_stage.first, plan.fused_stage.last) == (4, 4)
@@ -463,3 +510,22 @@ def test_destroy_releases_device_memory(N):
         cycle()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < (64 << 20), (free0, free1)
+
+
+@pytest.mark.parametrize("N", [1, 4])
+def test_memory_plan_matches_the_runtime_allocation(N):
+    """rp_memory_plan (host-only byte formulas) against the runtime's own
+    allocation accounting for the same configuration."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe, memory_plan
+    kw = dict(seq_len=256, micro_batch=1, micro_batches=4, num_gpus=N, async_optimizer=True)
+    rt = RoundPipe("tiny", adam=AdamW(**HP), costs=uniform_costs(5) if N == 4 else None,
+                   resident_state_gb=0.0, **kw)
+    st = rt.stats()
+    S = rt.plan()[0].num_slots()
+    rt.close()
+    mp = memory_plan("tiny", hbm_bytes=torch.cuda.get_device_properties(0).total_memory, **kw)
+    if N == 1:  # (the N=4 case ran on a supplied cost table; the plan uses the cost model)
+        assert mp["num_slots"] == S
+        assert st["device_bytes"][3] == mp["activations"] * N
+    assert st["device_bytes"][6] == mp["optimizer_ring"] * N
+    assert abs(st["device_bytes"][4] - mp["scratch"] * N) <= 0.05 * st["device_bytes"][4]
