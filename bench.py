@@ -51,9 +51,10 @@ MODEL_DIMS = {  # executed FLOPs per token per decoder layer / head (fwd); see D
     "qwen3-1.7b": dict(h=2048, nq=16, nk=8, hd=128, m=6144, L=28, V=151936),
     "tiny": dict(h=256, nq=4, nk=2, hd=64, m=768, L=4, V=32768),
 }
-# pinned host<->device copy rates measured on this pool's B200 boxes
-# (tools/probe_box.sh, capture committed as profiles/r02_pcie_probe.txt)
-PCIE_H2D_GBS, PCIE_D2H_GBS = 55.6, 52.9
+# pinned host<->device copy rates measured on this pool's B200 boxes, CUDA-event
+# timed (tools/transfer_probe.py -> profiles/r02_transfer_probe.json): one
+# direction alone, and both at once (total)
+PCIE_H2D_GBS, PCIE_D2H_GBS, PCIE_BIDIR_GBS = 55.4, 56.4, 96.2
 
 
 def peaks():
@@ -384,6 +385,7 @@ def measure(args, resident, mode, steps, warmup, profile=False, report_dir=None,
         mid = tl[tl["iteration"] == (it_lo + it_hi) // 2]
         bub = pl.idle_in_window(tl, N, int(mid["start_ns"].min()), int(mid["end_ns"].max()))[0] \
             if len(mid) else None
+    whole = pl.timeline_report(tl, N).bubble_ratio  # 1 - busy / (N x span), gaps included
     sched = pl.synthesize("roundpipe" if mode == "async" else "roundpipe-sync", N,
                           args.micro_batches, 0, max(3, steps), durs)
     sim = pl.simulate(sched, mode != "async")
@@ -412,7 +414,8 @@ def measure(args, resident, mode, steps, warmup, profile=False, report_dir=None,
     return {"ms": ms, "wall_s": w1 - w0, "steps": steps, "tokens_step": tokens_step,
             "value": steps * tokens_step / (ms * 1e-3),
             "e2e": steps * tokens_step / (w1 - w0), "st0": st0, "st1": st1, "plan": plan,
-            "bubble": bub, "sim_bubble": sim_bub, "losses": losses, "prof": prof,
+            "bubble": bub, "sim_bubble": sim_bub, "whole_run_idle": whole, "losses": losses,
+            "prof": prof,
             "clocks": clk.summary() if clocks else None, "setup_s": setup_s}
 
 
@@ -436,7 +439,8 @@ def run_ours(args):
     recompute = sum(x.size() for x in plan.bwd_stages)
     flops = step_flops(d, args.seq, r["tokens_step"], recompute, args.lora_rank)
     t_comp = flops / (sustained * 1e12) / args.gpus
-    t_link = max(h2d / (PCIE_H2D_GBS * 1e9), d2h / (PCIE_D2H_GBS * 1e9)) / args.gpus
+    t_link = max(h2d / (PCIE_H2D_GBS * 1e9), d2h / (PCIE_D2H_GBS * 1e9),
+                 (h2d + d2h) / (PCIE_BIDIR_GBS * 1e9)) / args.gpus
     roof_tps = r["tokens_step"] / max(t_comp, t_link)
     traffic = ncu_gemm_traffic()
     line = {
@@ -466,11 +470,13 @@ def run_ours(args):
                           "tokens_per_s_bound": round(roof_tps, 1),
                           "frac": round(r["value"] / roof_tps, 4),
                           "note": "slower of executed FLOPs at sustained bf16 peak and streamed "
-                                  "host-link bytes at measured PCIe H2D/D2H GB/s"},
+                                  "host-link bytes at the measured PCIe H2D / D2H / bidirectional "
+                                  "GB/s (profiles/r02_transfer_probe.json)"},
         "transfers": {"p2p_bytes_per_step": int(p2p), "h2d_gbs_avg": round(h2d / (r["ms"] / steps * 1e-3) / 1e9, 2),
                       "d2h_gbs_avg": round(d2h / (r["ms"] / steps * 1e-3) / 1e9, 2)},
         "bubble": {"measured": round(r["bubble"], 5) if r["bubble"] is not None else None,
                    "simulated": round(r["sim_bubble"], 5), "slots": plan.num_slots(),
+                   "whole_run_idle": round(r["whole_run_idle"], 5),
                    "kind": "interior (async)" if args.mode == "async" else "in-iteration (sync)",
                    "iterations": [args.warmup, args.warmup + steps - 1]},
         "loss": {"first": r["losses"][0], "last": r["losses"][-1]},
@@ -494,6 +500,7 @@ def run_ours(args):
                                   "ms_per_step": round(v["ms"] / vs, 2), "steps": vs,
                                   "bubble": round(v["bubble"], 5) if v["bubble"] is not None else None,
                                   "simulated_bubble": round(v["sim_bubble"], 5),
+                                  "whole_run_idle": round(v["whole_run_idle"], 5),
                                   "config": config_dict(args, res, mode)["workload"]}
             except Exception as e:  # report, never fail the headline
                 variants[name] = {"error": str(e)[:300]}

@@ -2004,19 +2004,28 @@ void Runtime::step() {
   if (!grads_pending) return;
   grads_pending = false;
   const int parity = last_iter & 1;
-  // optimizer lane order = GradWrite order: head first, then layers L-1..0
-  for (int l = s.L; l >= 0; --l) {
-    std::vector<int> gs = l == 0 ? std::vector<int>{1, 0} : std::vector<int>{l + 1};
-    for (int g : gs) {
-      if (!trainable(g)) continue;  // frozen (LoRA base): no grads, no optimizer
-      Gpu& G = gpus[grad_owner[g]];
-      set_dev(G);
-      adam_group(G, g, parity);
-    }
+  // optimizer lane order. async: GradWrite order (head first, then layers
+  // L-1..0) — the result is needed only two iterations later. sync: the
+  // next iteration's forward order (embedding, layers 0..L-1, head): every
+  // GradWrite lands within the last micro-batch's backward, and per-layer
+  // publication then lets iteration t+1's first layers start while the
+  // deeper layers' AdamW still streams
+  std::vector<int> order;
+  if (cfg.async_optimizer) {
+    order.push_back(s.L + 1);
+    for (int l = s.L - 1; l >= 0; --l) order.push_back(l + 1);
+    order.push_back(0);
+  } else {
+    for (int g = 0; g < ngroups(); ++g) order.push_back(g);
   }
-  // sync: uploads of t+1 follow each group's publication; enqueue them in
-  // publication order (head first) so one stalled group cannot block the rest
-  if (!cfg.async_optimizer) prefetch(last_iter + 1, /*reverse=*/true);
+  for (int g : order) {
+    if (!trainable(g)) continue;  // frozen (LoRA base): no grads, no optimizer
+    Gpu& G = gpus[grad_owner[g]];
+    set_dev(G);
+    adam_group(G, g, parity);
+  }
+  // sync: uploads of t+1 follow each group's publication, in the same order
+  if (!cfg.async_optimizer) prefetch(last_iter + 1);
   if (event_pool.size() > 500000) sync_all();
 }
 

@@ -529,3 +529,26 @@ def test_memory_plan_matches_the_runtime_allocation(N):
         assert st["device_bytes"][3] == mp["activations"] * N
     assert st["device_bytes"][6] == mp["optimizer_ring"] * N
     assert abs(st["device_bytes"][4] - mp["scratch"] * N) <= 0.05 * st["device_bytes"][4]
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 visible B200s")
+@pytest.mark.parametrize("pooled", [False, True])
+def test_physical_devices_seven_slots(pooled):
+    """N=4 workers on min(4, visible) physical B200s: hand-offs and
+    checkpoint pushes cross devices over NVLink (cudaMemcpyPeerAsync), ready
+    events are recorded on the producer's device; parity vs the oracle as
+    the logical-worker case, and p2p bytes were moved."""
+    losses, g0, master, tl, (plan, durs) = run_case("async", 4, costs=uniform_costs(5),
+                                                    pooled=pooled)
+    check("async", losses, g0, master)
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    s = O.Shape.from_config("tiny")
+    tok, lab = O.synthetic_batch(s, 4, 1, 256)
+    rt = RoundPipe("tiny", seq_len=256, micro_batch=1, micro_batches=4, num_gpus=4,
+                   async_optimizer=True, adam=AdamW(**HP), costs=uniform_costs(5), pooled=pooled)
+    rt.forward_backward(tok.numpy(), lab.numpy())
+    rt.step()
+    rt.sync()
+    st = rt.stats()
+    rt.close()
+    assert st["p2p_bytes"] > 0

@@ -16,7 +16,7 @@ if [ "$2" != "skip-bench" ]; then
   echo "bench exit $?" >> gpurun_out/${TAG}_bench.err
 fi
 if [ "$3" == "ref" ]; then
-  /usr/bin/time -v timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
+  timeout 1200 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
   echo "ref exit $?" >> gpurun_out/${TAG}_bench_ref.err
 fi
 ls -la gpurun_out | tail -12
