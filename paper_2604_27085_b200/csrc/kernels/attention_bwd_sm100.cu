@@ -517,13 +517,23 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
 // dS^T (bf16) sit in the first 64 TMEM columns of the head's S^T|dP^T block,
 // so the last 64 hold dQ^T = K^T dS^T (M = head_dim, N = 64 queries; K^T is
 // the MN-major view of the resident K tile, dS^T a bf16 copy in shared
-// memory). The softmax warpgroup drains dQ^T (thread = head-dim lane), stages
-// it [dim][query] and adds it into a d-major fp32 dQ^T accumulator with TMA
-// reduce-adds (cp.reduce.async.bulk .add.f32, performed in L2). This removes
-// the dQ kernel's recompute of S and dP (2 of its 3 MMA units) and its exp
-// pass. Tensor-core order per query tile j:
-//   dV,dK,dQ_a(j) | S/dP_a(j+1) | dV,dK,dQ_b(j) | S/dP_b(j+1) | ...
+// memory). This removes the dQ kernel's recompute of S and dP (2 of its 3
+// MMA units) and its exp pass.
+//
+// Four warpgroups (512 threads, registers rebalanced with setmaxnreg):
+//   WG0  w0 TMA producer, w1 MMA issuer (w2, w3 idle)             56 regs
+//   WG1  softmax of head a, WG2 softmax of head b (thread = key)  184 regs
+//   WG3  dQ drain for both heads (thread = head-dim lane): TMEM ->
+//        registers -> swizzled staging -> TMA reduce-add into a d-major
+//        fp32 dQ^T accumulator in L2 (cp.reduce.async.bulk .add.f32)    88 regs
+// The softmax warpgroups never wait for dQ: their loop is S^T/dP^T in,
+// P^T/dS^T out. Tensor-core order per (query tile j, head w):
+//   dQ^T(j,w) | dV,dK(j,w) | S^T(j+1,w) | [dQ^T(j,w) drained] dP^T(j+1,w)
+// so the drain of dQ^T (which shares TMEM columns with dP^T) hides behind
+// ~900 cycles of MMAs instead of stalling the tensor pipe.
 constexpr int A4_NST = 3;
+constexpr int A4_THREADS = 512;
+
 
 template <int HD>
 struct Dkv4Smem {
@@ -534,8 +544,8 @@ struct Dkv4Smem {
   static constexpr int STAGE = 2 * NSUB * SUB64;   // Q + dO of one (tile, head)
   static constexpr int DO_OFF = NSUB * SUB64;
   static constexpr int DST = R0 + A4_NST * STAGE;  // [2] dS^T [128 keys][64 q] bf16, SW128
-  static constexpr int STG = DST + 2 * A_BK * A_BQ * 2;  // [2 wg][4 warps] 4 KB dQ staging
-  static constexpr int LD = STG + 8 * 4096;        // [A4_NST][2][A_BQ] lse, delta
+  static constexpr int STG = DST + 2 * A_BK * A_BQ * 2;  // [4 drain warps][2 halves] 4 KB
+  static constexpr int LD = STG + 8 * 4096;        // [A4_NST][2][A_BQ] -lse*log2e, delta
   static constexpr int BAR = LD + A4_NST * 2 * A_BQ * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
@@ -565,14 +575,15 @@ __device__ __forceinline__ void bulk_wait_done_all() {
 //   2: G = 4, the two CTAs of a group form a cluster: rank 1 ships its fp32
 //      dK/dV rows into rank 0's (then idle) shared memory over DSMEM, rank 0
 //      adds them to its own and writes bf16 — no atomics, memset or cast
+// `nlse2` = -lse * log2(e) per (head, query), written by delta_kernel.
 template <int HD, int CL>
-__global__ void __launch_bounds__(A2_THREADS, 1)
+__global__ void __launch_bounds__(A4_THREADS, 1)
     attn_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_k,
                           const __grid_constant__ CUtensorMap tm_v,
                           const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_dq,
-                          const float* __restrict__ lse, const float* __restrict__ delta,
+                          const float* __restrict__ nlse2, const float* __restrict__ delta,
                           float* __restrict__ dk_acc, float* __restrict__ dv_acc,
                           bf16* __restrict__ dk, long long lddk, bf16* __restrict__ dv,
                           long long lddv, int T, int seq, int nq, int nk, float scale) {
@@ -629,7 +640,16 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
   // softmax pass P^T (bf16 pairs) at w*128 + [0, 32), dS^T at w*128 + [32, 64)
   // and dQ^T (fp32, lane = head dim) at w*128 + [64, 128). dV at 256, dK at 384.
   const uint32_t TM_DV = 256, TM_DK = 384;
+  const bool softmax_wg = warp >= 4 && warp < 12;
 
+  // cluster-wide barrier (CL == 2 epilogue); every thread of both CTAs takes part
+  auto cluster_sync = [] {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+  };
+
+  if (warp < 4) {
+  setmaxnreg_dec<112>();
   if (warp == 0 && lane == 0) {
     mbar_arrive_expect_tx(kv_full, 2 * NSUB * SUB128);
     for (int sub = 0; sub < NSUB; ++sub) {
@@ -647,7 +667,7 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
         tma_load_2d(qd + L::DO_OFF + sub * SUB64, &tm_do, &st_full[s], hq * HD + 64 * sub, qs);
       }
       float* ld = reinterpret_cast<float*>(sm + L::LD) + s * 2 * A_BQ;
-      bulk_load_1d(ld, lse + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
+      bulk_load_1d(ld, nlse2 + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
       bulk_load_1d(ld + A_BQ, delta + (long long)hq * T + qs, A_BQ * 4, &st_full[s]);
     }
   } else if (warp == 1) {  // whole warp: uniform descriptors, elected issue
@@ -656,90 +676,97 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
     constexpr uint32_t idesc_q = umma_idesc_bf16(HD, A_BQ, 1, 1);    // MN-major x MN-major
     const uint32_t k_addr = smem_u32(sm + L::K), v_addr = smem_u32(sm + L::V);
     auto stage = [&](int idx) { return smem_u32(sm + L::R0 + (idx % NS) * L::STAGE); };
-    auto issue_sdp = [&](int j, int w) {
-      const int idx = 2 * j + w;
-      mbar_wait(&st_full[idx % NS], (idx / NS) & 1);
-      tc_fence_after();
-      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+    // S^T = K Q^T into w*128 (ops 0) or dP^T = V dO^T into w*128 + 64 (ops 1)
+    auto issue_sd = [&](int idx, int w, int which) {
+      const uint32_t b_addr = stage(idx) + (which ? L::DO_OFF : 0);
+      const uint32_t a_addr = which ? v_addr : k_addr;
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t ko = (kk >> 2) * SUB128 + (kk & 3) * 32;
           const uint32_t qo = (kk >> 2) * SUB64 + (kk & 3) * 32;
-          umma_f16(tmem + w * 128, umma_desc_sw128(k_addr + ko, 16, 1024),
-                   umma_desc_sw128(q_addr + qo, 16, 1024), idesc_s, kk != 0);
-          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(v_addr + ko, 16, 1024),
-                   umma_desc_sw128(do_addr + qo, 16, 1024), idesc_s, kk != 0);
+          umma_f16(tmem + w * 128 + which * 64, umma_desc_sw128(a_addr + ko, 16, 1024),
+                   umma_desc_sw128(b_addr + qo, 16, 1024), idesc_s, kk != 0);
         }
-        umma_commit(&sd_full[w]);
       }
       __syncwarp();
     };
-    auto issue_gq = [&](int j, int w) {
-      const int idx = 2 * j + w;
-      mbar_wait(&ps_full[w], j & 1);
+    auto wait_stage = [&](int idx) {
+      mbar_wait(&st_full[idx % NS], (idx / NS) & 1);
       tc_fence_after();
-      const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
-      const uint32_t ds_addr = smem_u32(sm + L::DST + w * (A_BK * A_BQ * 2));
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < A_BQ / 16; ++kk) {
-          const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
-          const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
-          umma_f16_ts(tmem + TM_DV, tmem + w * 128 + kk * 8, ob, idesc_g, (idx | kk) != 0);
-          umma_f16_ts(tmem + TM_DK, tmem + w * 128 + 32 + kk * 8, qb, idesc_g, (idx | kk) != 0);
-        }
-        umma_commit(&st_empty[idx % NS]);
-        // dQ^T = K^T dS^T over the 128 keys of this block
-#pragma unroll
-        for (int kk = 0; kk < A_BK / 16; ++kk)
-          umma_f16(tmem + w * 128 + 64, umma_desc_sw128(k_addr + kk * 2048, SUB128, 1024),
-                   umma_desc_sw128(ds_addr + kk * 2048, 8192, 1024), idesc_q, kk != 0);
-        umma_commit(&dq_full[w]);
-      }
-      __syncwarp();
     };
     mbar_wait(kv_full, 0);
-    issue_sdp(0, 0);
-    issue_sdp(0, 1);
-    // gq_a(j) | S/dP_a(j+1) | gq_b(j) | S/dP_b(j+1): each warpgroup's softmax
-    // hides behind the other head's gq + S/dP; the tensor core only waits for
-    // the short dQ^T drain (TMEM -> registers) between a gq and the same
-    // head's next S/dP
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      wait_stage(w);
+      issue_sd(w, w, 0);
+      issue_sd(w, w, 1);
+      if (elect_one()) umma_commit(&sd_full[w]);
+      __syncwarp();
+    }
     for (int j = 0; j < nqt; ++j) {
 #pragma unroll
       for (int w = 0; w < 2; ++w) {
-        issue_gq(j, w);
+        const int idx = 2 * j + w;
+        mbar_wait(&ps_full[w], j & 1);
+        tc_fence_after();
+        const uint32_t q_addr = stage(idx), do_addr = q_addr + L::DO_OFF;
+        const uint32_t ds_addr = smem_u32(sm + L::DST + w * (A_BK * A_BQ * 2));
+        if (elect_one()) {
+          // dQ^T = K^T dS^T over the 128 keys of this block (first, so its
+          // drain overlaps the dV/dK and next S^T MMAs)
+#pragma unroll
+          for (int kk = 0; kk < A_BK / 16; ++kk)
+            umma_f16(tmem + w * 128 + 64, umma_desc_sw128(k_addr + kk * 2048, SUB128, 1024),
+                     umma_desc_sw128(ds_addr + kk * 2048, 8192, 1024), idesc_q, kk != 0);
+          umma_commit(&dq_full[w]);
+#pragma unroll
+          for (int kk = 0; kk < A_BQ / 16; ++kk) {
+            const uint64_t ob = umma_desc_sw128(do_addr + kk * 2048, SUB64, 1024);
+            const uint64_t qb = umma_desc_sw128(q_addr + kk * 2048, SUB64, 1024);
+            umma_f16_ts(tmem + TM_DV, tmem + w * 128 + kk * 8, ob, idesc_g, (idx | kk) != 0);
+            umma_f16_ts(tmem + TM_DK, tmem + w * 128 + 32 + kk * 8, qb, idesc_g, (idx | kk) != 0);
+          }
+          umma_commit(&st_empty[idx % NS]);
+        }
+        __syncwarp();
         if (j + 1 < nqt) {
-          mbar_wait(&dq_free[w], j & 1);  // warpgroup w drained dQ^T_w(j)
+          wait_stage(idx + 2);
+          issue_sd(idx + 2, w, 0);          // S^T(j+1) over P^T/dS^T(j): in order
+          mbar_wait(&dq_free[w], j & 1);    // dQ^T(j) drained from the dP^T columns
           tc_fence_after();
-          issue_sdp(j + 1, w);
+          issue_sd(idx + 2, w, 1);
+          if (elect_one()) umma_commit(&sd_full[w]);
+          __syncwarp();
         }
       }
     }
     if (elect_one()) umma_commit(acc_done);
     __syncwarp();
-  } else if (warp >= 4) {
-    // two softmax warpgroups: w = head slot, thread = key row (softmax) or
-    // head-dim lane (dQ drain)
+  }
+  __syncwarp();
+  if (CL == 2) {  // partner CTA's epilogue exchange (see the softmax branch)
+    cluster_sync();
+    cluster_sync();
+  }
+  } else if (softmax_wg) {
+    setmaxnreg_inc<160>();
+    // softmax warpgroup w (head ha + w), thread = key row
     const int w = (warp - 4) >> 2, quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int key = k0 + r;
-    const int hq = ha + w;
     const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
-    const float sl2 = scale * kLog2e;
+    const float2 sl2 = make_float2(scale * kLog2e, scale * kLog2e);
     uint8_t* dst = sm + L::DST + w * (A_BK * A_BQ * 2);  // this head's dS^T
-    uint8_t* stg0 = sm + L::STG + (w * 4 + quarter) * 4096;
-    uint8_t* stg1 = dst + quarter * 4096;  // this warp's rows of dS^T, free after dQ^T
     for (int j = 0; j < nqt; ++j) {
       const int idx = 2 * j + w, s = idx % NS;
-      const int qs = k0 + j * A_BQ;
-      const float* lse_t = reinterpret_cast<const float*>(sm + L::LD) + s * 2 * A_BQ;
-      const float* del_t = lse_t + A_BQ;
+      const int jq = j * A_BQ;  // query offset of the tile from k0
+      const float4* nl4 = reinterpret_cast<const float4*>(sm + L::LD) + s * 2 * A_BQ / 4;
+      const float4* dl4 = nl4 + A_BQ / 4;
       mbar_wait(&st_full[s], (idx / NS) & 1);  // lse/delta visibility (already complete)
       mbar_wait(&sd_full[w], j & 1);
       tc_fence_after();
-      const bool diag = qs < k0 + A_BK;  // tile overlaps this key block's diagonal
+      const bool diag = jq < A_BK;  // tile overlaps this key block's diagonal
       uint32_t pk[32], dk2[32];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -748,18 +775,31 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
         tmem_ld_32x32b_x32(lane_base + w * 128 + 64 + half * 32, dpv);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
+        for (int i = 0; i < 32; i += 4) {
           const int c = half * 32 + i;
-          float p0 = ex2b(fmaf(__uint_as_float(sv[i]), sl2, -lse_t[c] * kLog2e));
-          float p1 = ex2b(fmaf(__uint_as_float(sv[i + 1]), sl2, -lse_t[c + 1] * kLog2e));
-          if (diag) {
-            if (qs + c < key) p0 = 0.f;
-            if (qs + c + 1 < key) p1 = 0.f;
+          const float4 nl = nl4[c / 4], dl = dl4[c / 4];
+          const float2 a0 = __ffma2_rn(make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])),
+                                       sl2, make_float2(nl.x, nl.y));
+          const float2 a1 = __ffma2_rn(make_float2(__uint_as_float(sv[i + 2]), __uint_as_float(sv[i + 3])),
+                                       sl2, make_float2(nl.z, nl.w));
+          float2 p0 = make_float2(ex2b(a0.x), ex2b(a0.y));
+          float2 p1 = make_float2(ex2b(a1.x), ex2b(a1.y));
+          if (diag) {  // key r sees queries jq + c >= r only
+            if (jq + c < r) p0.x = 0.f;
+            if (jq + c + 1 < r) p0.y = 0.f;
+            if (jq + c + 2 < r) p1.x = 0.f;
+            if (jq + c + 3 < r) p1.y = 0.f;
           }
-          const float d0 = p0 * (__uint_as_float(dpv[i]) - del_t[c]);
-          const float d1 = p1 * (__uint_as_float(dpv[i + 1]) - del_t[c + 1]);
-          pk[c / 2] = pack_bf16x2(p0, p1);
-          dk2[c / 2] = pack_bf16x2(d0, d1);
+          const float2 d0 = __fmul2_rn(p0, __fadd2_rn(make_float2(__uint_as_float(dpv[i]),
+                                                                  __uint_as_float(dpv[i + 1])),
+                                                      make_float2(-dl.x, -dl.y)));
+          const float2 d1 = __fmul2_rn(p1, __fadd2_rn(make_float2(__uint_as_float(dpv[i + 2]),
+                                                                  __uint_as_float(dpv[i + 3])),
+                                                      make_float2(-dl.z, -dl.w)));
+          pk[c / 2] = pack_bf16x2(p0.x, p0.y);
+          pk[c / 2 + 1] = pack_bf16x2(p1.x, p1.y);
+          dk2[c / 2] = pack_bf16x2(d0.x, d0.y);
+          dk2[c / 2 + 1] = pack_bf16x2(d1.x, d1.y);
         }
       }
       // every S^T / dP^T column of this thread has been read: P^T -> [0, 32),
@@ -776,10 +816,7 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
         tmem_st_32x32b_x16(lane_base + w * 128 + 32 + h * 16, b);
       }
       // dS^T (bf16) into shared memory for dQ^T = K^T dS^T: row = key (128 B),
-      // SWIZZLE_128B. These rows were the staging buffer of the previous
-      // tile's second dQ half: its TMA reduce must have read them.
-      if (lane == 0) bulk_wait_read_all();
-      __syncwarp();
+      // SWIZZLE_128B; dQ^T(j-1) read it before S^T/dP^T(j) were committed
 #pragma unroll
       for (int c = 0; c < 8; ++c)
         *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) << 4)) =
@@ -789,40 +826,7 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ps_full[w]);
-      // drain dQ^T (lane = head dim d = r), queries 0-31 and 32-63
-      mbar_wait(&dq_full[w], j & 1);
-      tc_fence_after();
-      uint32_t q0v[32], q1v[32];
-      tmem_ld_32x32b_x32(lane_base + w * 128 + 64, q0v);
-      tmem_ld_32x32b_x32(lane_base + w * 128 + 96, q1v);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_free[w]);
-      // stage [32 dims][32 queries] fp32 (this thread's dim = one SWIZZLE_128B
-      // row) and add into the d-major dQ^T accumulator
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint8_t* buf = half ? stg1 : stg0;
-        if (half == 0) {
-          if (lane == 0) bulk_wait_read_all();  // previous tile's stores from stg0
-          __syncwarp();
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t* v = half ? q1v : q0v;
-          *reinterpret_cast<uint4*>(buf + lane * 128 + ((k ^ (lane & 7)) << 4)) =
-              make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          tma_reduce_add_2d(&tm_dq, buf, qs + half * 32, hq * HD + quarter * 32);
-          bulk_commit_grp();
-        }
-      }
     }
-    if (lane == 0) bulk_wait_done_all();
     // epilogue: warpgroup a -> dK (scaled), warpgroup b -> dV
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -842,27 +846,19 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
                                 __uint_as_float(a[i + 2]) * f, __uint_as_float(a[i + 3]) * f));
       }
     }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (CL >= 1) {
+    if (CL >= 1) {
     // dK / dV rows of this key block: thread = key row, HD fp32 per row; the
     // partner's rows arrive in this CTA's ring + dS^T region (2 x 128 x HD fp32,
     // 16-byte chunks XOR-swizzled by row so 32 rows hit 32 different banks)
     uint32_t rank = 0;
     if (CL == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-    const int w = (warp - 4) >> 2, quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const int key = k0 + r;
-    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
     const uint32_t col = w == 0 ? TM_DK : TM_DV;
     constexpr int CH = HD / 4;  // 16-byte chunks per row
     float* xbuf = reinterpret_cast<float*>(sm + L::R0) + (size_t)w * A_BK * HD + (size_t)r * HD;
     auto chunk = [&](int c4) { return ((c4 ^ (r & (CH - 1))) * 4); };
     if (CL == 2) {
-      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                       : "memory");  // rank 0's ring / dS^T shared memory is free
-      if (rank == 1 && warp >= 4) {
+      cluster_sync();  // rank 0's ring / dS^T shared memory is free
+      if (rank == 1) {
         uint32_t remote;
         asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(xbuf)));
 #pragma unroll 1
@@ -879,10 +875,9 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
                          : "memory");
         }
       }
-      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                       : "memory");
+      cluster_sync();
     }
-    if (warp >= 4 && rank == 0) {
+    if (rank == 0) {
       bf16* dst = (w == 0 ? dk + (long long)key * lddk : dv + (long long)key * lddv) +
                   (long long)kvh * HD;
       const float f = w == 0 ? scale : 1.f;
@@ -910,6 +905,52 @@ __global__ void __launch_bounds__(A2_THREADS, 1)
               make_uint4(pack_bf16x2(o[i] * f, o[i + 1] * f), pack_bf16x2(o[i + 2] * f, o[i + 3] * f),
                          pack_bf16x2(o[i + 4] * f, o[i + 5] * f), pack_bf16x2(o[i + 6] * f, o[i + 7] * f));
       }
+    }
+  }
+  } else {
+    setmaxnreg_dec<80>();
+    // dQ drain warpgroup, thread = head-dim lane d = quarter*32 + lane; per
+    // (tile, head): TMEM -> registers, release the columns, stage two
+    // [32 dims][32 queries] fp32 blocks (one SWIZZLE_128B row per dim) and
+    // reduce-add them into the d-major dQ^T accumulator
+    const int quarter = warp & 3;
+    const uint32_t lane_base = tmem + (uint32_t(quarter * 32) << 16);
+    uint8_t* stg = sm + L::STG + quarter * 8192;
+    for (int idx = 0; idx < 2 * nqt; ++idx) {
+      const int w = idx & 1, j = idx >> 1;
+      const int qs = k0 + j * A_BQ;
+      mbar_wait(&dq_full[w], j & 1);
+      tc_fence_after();
+      uint32_t q0v[32], q1v[32];
+      tmem_ld_32x32b_x32(lane_base + w * 128 + 64, q0v);
+      tmem_ld_32x32b_x32(lane_base + w * 128 + 96, q1v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_free[w]);
+      if (lane == 0) bulk_wait_read_all();  // this warp's previous reduces left the staging
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        *reinterpret_cast<uint4*>(stg + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+            make_uint4(q0v[4 * k], q0v[4 * k + 1], q0v[4 * k + 2], q0v[4 * k + 3]);
+        *reinterpret_cast<uint4*>(stg + 4096 + lane * 128 + ((k ^ (lane & 7)) << 4)) =
+            make_uint4(q1v[4 * k], q1v[4 * k + 1], q1v[4 * k + 2], q1v[4 * k + 3]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        const int hq = ha + w;
+        tma_reduce_add_2d(&tm_dq, stg, qs, hq * HD + quarter * 32);
+        tma_reduce_add_2d(&tm_dq, stg + 4096, qs + 32, hq * HD + quarter * 32);
+        bulk_commit_grp();
+      }
+    }
+    if (lane == 0) bulk_wait_done_all();
+    __syncwarp();
+    if (CL == 2) {
+      cluster_sync();
+      cluster_sync();
     }
   }
   tc_fence_before();
@@ -1142,9 +1183,11 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // delta[h, t] = sum_d dO[t,h,d] * O[t,h,d]; one warp per (t, h), 16-byte loads
+// (and, when nlse2 is given, nlse2[h, t] = -lse[h, t] * log2(e) for the fused kernel)
 template <int HD>
 __global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf16* __restrict__ d,
-                             long long lddo, float* __restrict__ delta, int T, int nq) {
+                             long long lddo, float* __restrict__ delta, int T, int nq,
+                             const float* __restrict__ lse, float* __restrict__ nlse2) {
   const long long w = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (w >= (long long)T * nq) return;
@@ -1160,7 +1203,10 @@ __global__ void delta_kernel(const bf16* __restrict__ o, long long ldo, const bf
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) delta[(long long)h * T + t] = acc;
+  if (lane == 0) {
+    delta[(long long)h * T + t] = acc;
+    if (nlse2) nlse2[(long long)h * T + t] = -lse[(long long)h * T + t] * kLog2e;
+  }
 }
 
 // dk/dv (bf16, strided) = dk_acc/dv_acc (fp32 [T, nk*HD])
@@ -1250,8 +1296,20 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
            long long lddv, float* delta, float* dkv_acc, int T, int seq, int nq, int nk,
            float scale, cudaStream_t s) {
   const long long warps = (long long)T * nq;
+  const int G = nq / nk;
+  const bool fused = HD == 128 && G % 2 == 0;
+  // fused path workspace: fp32 d-major dQ^T accumulator [nq*HD, T], then
+  // -lse*log2(e) [nq, T]
+  const long long qn = (long long)T * nq * HD;
+  float* dq_acc = nullptr;
+  if (fused) {
+    Workspace* w = stream_workspace(s, WS_ATTN_DQ, sizeof(float) * (size_t)(qn + warps));
+    if (!w) return RP_E_CUDA;
+    dq_acc = static_cast<float*>(w->p);
+  }
+  float* nlse2 = fused ? dq_acc + qn : nullptr;
   delta_kernel<HD><<<(int)((warps + 7) / 8), 256, 0, s>>>((const bf16*)o, ldo, (const bf16*)dout,
-                                                         lddo, delta, T, nq);
+                                                         lddo, delta, T, nq, lse, nlse2);
   CUtensorMap mk128, mv128, mq64, mdo64;
   if (!map2d(&mk128, k, T, (long long)nk * HD, ldk, 128) ||
       !map2d(&mv128, v, T, (long long)nk * HD, ldv, 128) ||
@@ -1259,13 +1317,9 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       !map2d(&mdo64, dout, T, (long long)nq * HD, lddo, 64))
     return RP_E_CUDA;
   const long long acc_n = (long long)T * nk * HD;
-  const int G = nq / nk;
-  if (HD == 128 && G % 2 == 0) {  // dK/dV/dQ in one kernel (A4)
-    const long long qn = (long long)T * nq * HD;
-    Workspace* w = stream_workspace(s, WS_ATTN_DQ, sizeof(float) * (size_t)qn);
-    float* dq_acc = w ? static_cast<float*>(w->p) : nullptr;
+  if (fused) {  // dK/dV/dQ in one kernel (A4)
     CUtensorMap mdq;
-    if (!dq_acc || !map_f32(&mdq, dq_acc, (long long)nq * HD, T, T))  // d-major [nq*HD, T]
+    if (!map_f32(&mdq, dq_acc, (long long)nq * HD, T, T))  // d-major [nq*HD, T]
       return RP_E_CUDA;
     if (cudaMemsetAsync(dq_acc, 0, sizeof(float) * qn, s) != cudaSuccess) return RP_E_CUDA;
     // GQA partials of dK/dV: G = 2 both heads share the CTA (bf16 straight
@@ -1275,7 +1329,7 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       if (!set_smem(kern, Dkv4Smem<HD>::BYTES)) return cudaErrorInvalidValue;
       cudaLaunchConfig_t c = {};
       c.gridDim = dim3(nq / 2, T / A_BK, 1);
-      c.blockDim = dim3(A2_THREADS, 1, 1);
+      c.blockDim = dim3(A4_THREADS, 1, 1);
       c.dynamicSmemBytes = Dkv4Smem<HD>::BYTES;
       c.stream = s;
       cudaLaunchAttribute at[1];
@@ -1285,7 +1339,8 @@ int bwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       at[0].val.clusterDim.z = 1;
       c.attrs = at;
       c.numAttrs = 1;
-      return cudaLaunchKernelEx(&c, kern, mk128, mv128, mq64, mdo64, mdq, lse, (const float*)delta,
+      return cudaLaunchKernelEx(&c, kern, mk128, mv128, mq64, mdo64, mdq, (const float*)nlse2,
+                                (const float*)delta,
                                 dkv_acc, dkv_acc + acc_n, (bf16*)dk, (long long)lddk, (bf16*)dv,
                                 (long long)lddv, T, seq, nq, nk, scale);
     };
