@@ -127,6 +127,46 @@ int rp_attn_bwd_tc(const void* q, int64_t ldq, const void* k, int64_t ldk, const
                    int64_t lddv, float* delta, float* dkv_acc, int32_t T, int32_t seq,
                    int32_t nq, int32_t nk, int32_t head_dim, float scale, void* stream);
 
+/* ---- mixture of experts (Qwen3-MoE; csrc/kernels/moe.cu) ----------------
+ * Grouped GEMM: rows [row_off[e], row_off[e+1]) of A (K-major, args->M rows
+ * in all) and D times expert e's B, the e-th block of b_group_rows rows of B
+ * (K-major [groups*N, K]: b_group_rows = N; MN-major [groups*K, N]:
+ * b_group_rows = K). row_off: DEVICE int32[groups+1]. epilogue 0: bf16 D
+ * (+ R); 1: SwiGLU backward (R = gu, D = dgu, B MN-major). */
+int rp_gemm_grouped(const rp_gemm_args_t* args, const int32_t* row_off, int32_t groups,
+                    int32_t b_group_rows, int32_t epilogue, void* stream);
+/* softmax (fp32) over E router logits [T, E] -> top-k experts and weights
+ * (renormalised over the k when norm_topk), per-expert counts [E] (zeroed
+ * here). E <= 256, k <= 32. */
+int rp_moe_route(const float* logits, int32_t T, int32_t E, int32_t k, int32_t norm_topk,
+                 int32_t* topk_idx, float* topk_w, int32_t* counts, void* stream);
+/* counts -> offsets [E+1] (cursor [E] scratch); row pos[t*k+j] of the
+ * expert-sorted buffers for every (token, slot); xs[pos] = x[t] [.., h],
+ * w_s[pos] = topk_w[t, j] */
+int rp_moe_permute(const void* x, int64_t ldx, int32_t T, int32_t h, int32_t k, int32_t E,
+                   const int32_t* topk_idx, const float* topk_w, const int32_t* counts,
+                   int32_t* offsets, int32_t* cursor, int32_t* pos, float* w_s, void* xs,
+                   void* stream);
+/* xs[pos[t*k+j]] = x[t] */
+int rp_moe_gather(const void* x, int64_t ldx, int32_t T, int32_t h, int32_t k,
+                  const int32_t* pos, void* xs, void* stream);
+/* out[t] = res[t] (optional) + sum_j topk_w[t,j] ys[pos[t*k+j]]  (fp32 sum, bf16 out) */
+int rp_moe_combine(const void* ys, const int32_t* pos, const float* topk_w, int32_t T,
+                   int32_t k, int32_t h, const void* res, int64_t ldr, void* out, int64_t ldo,
+                   void* stream);
+/* dh[t] = dh32[t] + sum_j dxs[pos[t*k+j]]  (dh32 fp32 [T, h], dh bf16) */
+int rp_moe_combine_bwd(const void* dxs, const int32_t* pos, int32_t T, int32_t k, int32_t h,
+                       const float* dh32, void* dh, int64_t ldd, void* stream);
+/* per expert-sorted row r: dw_s[r] = <dact[r], silu(g) u>, dgu[r] =
+ * swiglu'(w_s[r] dact[r]) with gu = [g | u] [rows, 2m] */
+int rp_moe_swiglu_bwd(const void* dact, const void* gu, const float* w_s, int64_t rows,
+                      int32_t m, void* dgu, float* dw_s, void* stream);
+/* d(router logits) [T, E] (bf16) from dw through the top-k renormalisation and
+ * the softmax */
+int rp_moe_router_bwd(const float* logits, int32_t T, int32_t E, int32_t k, int32_t norm_topk,
+                      const int32_t* topk_idx, const int32_t* pos, const float* dw_s,
+                      void* dlogits, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

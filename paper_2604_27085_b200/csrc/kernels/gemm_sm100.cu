@@ -71,7 +71,44 @@ struct Params {
   long long ldd2;
   int kb2;                 // k-blocks of the second K segment (0: none)
   int nsplit;              // units beyond `full` are N halves (256 x PBN/2) instead of K halves
+  // grouped (MoE expert) GEMM, single-CTA kernel: rows [g_off[e], g_off[e+1])
+  // of A and D belong to expert e, whose B is the e-th block of g_bstride rows
+  // of the B map (N rows K-major, K rows MN-major); g_off lives on the device
+  const int* g_off;
+  int g_num;
+  int g_bstride;
 };
+constexpr int MAX_GROUPS = 256;
+
+// Tile -> (first row, first column, expert, end row) of the single-CTA kernel.
+// Plain: M fastest. Grouped: expert e owns tiles [tstart[e], tstart[e+1]),
+// M fastest within the expert.
+struct TileCoord {
+  int m0, n0, e, row_end;
+};
+__device__ __forceinline__ TileCoord tile_coord(const Params& p, const int* tstart, int tile,
+                                                int m_tiles, int bm, int bn) {
+  TileCoord t;
+  if (!p.g_off) {
+    t.m0 = (tile % m_tiles) * bm;
+    t.n0 = (tile / m_tiles) * bn;
+    t.e = 0;
+    t.row_end = p.M;
+    return t;
+  }
+  int lo = 0, hi = p.g_num;  // last e with tstart[e] <= tile
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tstart[mid] <= tile) lo = mid; else hi = mid;
+  }
+  const int r0 = p.g_off[lo], r1 = p.g_off[lo + 1];
+  const int mt = (r1 - r0 + bm - 1) / bm, local = tile - tstart[lo];
+  t.m0 = r0 + (local % mt) * bm;
+  t.n0 = (local / mt) * bn;
+  t.e = lo;
+  t.row_end = r1;
+  return t;
+}
 
 // TMA maps of the SwiGLU-backward epilogue: g / u halves of gu and dg / du
 // halves of dgu, each [M, N] bf16 with a {32, 32} SWIZZLE_64B box
@@ -229,8 +266,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m_tiles = (p.M + BM - 1) / BM, n_tiles = (p.N + BN - 1) / BN;
-  const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = (p.K + BK - 1) / BK;
+  __shared__ int tstart[MAX_GROUPS + 1];  // grouped: first tile of each expert
+  int num_tiles = m_tiles * n_tiles;
+  if (p.g_off) {
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int e = 0; e < p.g_num; ++e) {
+        tstart[e] = acc;
+        acc += (p.g_off[e + 1] - p.g_off[e] + BM - 1) / BM * n_tiles;
+      }
+      tstart[p.g_num] = acc;
+    }
+    __syncthreads();
+    num_tiles = tstart[p.g_num];
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tma_a);
@@ -256,7 +306,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      const TileCoord tc = tile_coord(p, tstart, tile, m_tiles, BM, BN);
+      const int m0 = tc.m0, n0 = tc.n0;
+      const int boff = tc.e * p.g_bstride;  // grouped: this expert's block of B
       for (int kb = 0; kb < k_blocks; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -272,9 +324,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (B_MN) {
 #pragma unroll
           for (int j = 0; j < Cfg::B_ROWS / 64; ++j)
-            tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, k0);
+            tma_load_2d(sb + j * 8192, &tma_b, &full[stage], n0 + 64 * j, boff + k0);
         } else {
-          tma_load_2d(sb, &tma_b, &full[stage], k0, n0);
+          tma_load_2d(sb, &tma_b, &full[stage], k0, boff + n0);
         }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -315,11 +367,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile % m_tiles) * BM, n0 = (tile / m_tiles) * BN;
+      const TileCoord tc = tile_coord(p, tstart, tile, m_tiles, BM, BN);
+      const int m0 = tc.m0, n0 = tc.n0;
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
-      const bool row_ok = row < p.M;
+      const bool row_ok = row < tc.row_end;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t v[32];
@@ -972,7 +1025,8 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   const int smem = skinny ? SingleCfg<32, B_MN>::SMEM : SingleCfg<256, B_MN>::SMEM;
   if (!ensure_smem_t(kern, smem)) return cudaErrorInvalidValue;
   const int tbn = skinny ? 32 : BN;
-  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
+  int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
+  if (p.g_off) tiles += p.g_num * ((p.N + tbn - 1) / tbn);  // ragged last m-tile per group (bound)
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, NUM_THREADS, smem, stream>>>(ta, tb, p);
   return cudaGetLastError();
@@ -1194,4 +1248,46 @@ extern "C" __attribute__((visibility("default"))) int rp_gemm_ex(
   s2.ldb2 = ldb2;
   s2.K2 = K2;
   return gemm_entry(g, stream, epilogue, act, ld_act, s2);
+}
+
+// Grouped (MoE expert) GEMM: rows [row_off[e], row_off[e+1]) of A (K-major,
+// args->M rows in all) and D are multiplied by expert e's B — the e-th block
+// of b_group_rows rows of B (K-major: [groups*N, K], b_group_rows = N;
+// MN-major: [groups*K, N], b_group_rows = K). row_off (groups+1 int32) is a
+// DEVICE array, so the routing never syncs the host. epilogue 0: bf16 D
+// (+ R); 1: the SwiGLU-backward epilogue (R = gu [M, 2N], D = dgu, B
+// MN-major). Single-CTA 128 x 256 tiles, persistent over all experts' tiles.
+extern "C" __attribute__((visibility("default"))) int rp_gemm_grouped(
+    const rp_gemm_args_t* g, const int32_t* row_off, int32_t groups, int32_t b_group_rows,
+    int32_t epilogue, void* stream) {
+  if (!g || !row_off || groups <= 0 || groups > MAX_GROUPS || b_group_rows <= 0 ||
+      epilogue < 0 || epilogue > 1 || g->M <= 0 || g->N <= 32 || g->K <= 0 || !g->A || !g->B ||
+      !g->D || g->a_mn_major || g->out_f32 || g->accumulate)
+    return RP_E_INPUT;
+  if (epilogue == 1 && (!g->R || !g->b_mn_major || g->N % 8)) return RP_E_INPUT;
+  if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
+      (reinterpret_cast<uintptr_t>(g->B) & 15))
+    return RP_E_INPUT;
+  CUtensorMap ta, tb, td;
+  std::memset(&td, 0, sizeof(td));
+  const long long brows = (long long)groups * b_group_rows;
+  bool ok = make_map(&ta, g->A, g->M, g->K, g->lda, 64, BM);
+  ok = ok && (g->b_mn_major ? make_map(&tb, g->B, brows, g->N, g->ldb, 64, 64)
+                            : make_map(&tb, g->B, brows, g->K, g->ldb, 64, BN));
+  if (!ok) return RP_E_CUDA;
+  EpiMaps em;
+  std::memset(&em, 0, sizeof(em));
+  const bool vec = (g->ldd * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
+                   (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0));
+  Params p{g->M, g->N, g->K, g->D, g->ldd, reinterpret_cast<const __nv_bfloat16*>(g->R), g->ldr,
+           vec ? 1 : 0, 0, 0, 0, 0, 0, nullptr, nullptr, 0, nullptr, 0, 0, 0,
+           row_off, groups, b_group_rows};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (epilogue == 1)
+    e = launch<0, 1, EPI_SWIGLU_BWD>(ta, tb, td, em, p, false, 0, s);
+  else
+    e = g->b_mn_major ? launch<0, 1, EPI_BF16>(ta, tb, td, em, p, false, 0, s)
+                      : launch<0, 0, EPI_BF16>(ta, tb, td, em, p, false, 0, s);
+  return e == cudaSuccess ? RP_OK : RP_E_CUDA;
 }

@@ -223,3 +223,65 @@ def rope_table(seq, hd, theta=1e6):
     ang = np.arange(seq, dtype=np.float64)[:, None] * inv[None, :]
     tab = np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
     return torch.from_numpy(np.ascontiguousarray(tab))
+
+
+# ---- mixture of experts (include/rp/kernels.h, csrc/kernels/moe.cu) ------------------
+def gemm_grouped(A, B, D, row_off, groups, b_group_rows, *, b_mn_major=False, gu=None,
+                 stream=None):
+    """Rows [row_off[e], row_off[e+1]) of A [M,K] / D [M,N] times expert e's block of B
+    (K-major [groups*N, K] or MN-major [groups*K, N]). gu given: the SwiGLU-backward
+    epilogue (D = dgu [M, 2N], B MN-major)."""
+    M, K = A.shape
+    N = B.shape[1] if b_mn_major else b_group_rows
+    args = GemmArgs(M, N, K, _ptr(A), A.stride(0), 0, _ptr(B), B.stride(0), int(b_mn_major),
+                    _ptr(D), D.stride(0), 0, 0, _ptr(gu), gu.stride(0) if gu is not None else 0)
+    f = _lib().rp_gemm_grouped
+    f.restype = C.c_int
+    _check(f(C.byref(args), _ptr(row_off), I32(groups), I32(b_group_rows),
+             I32(1 if gu is not None else 0), _stream(stream)))
+    return D
+
+
+def moe_route(logits, k, norm_topk, topk_idx, topk_w, counts, stream=None):
+    T, E = logits.shape
+    _call("rp_moe_route", _ptr(logits), I32(T), I32(E), I32(k), I32(int(norm_topk)),
+          _ptr(topk_idx), _ptr(topk_w), _ptr(counts), _stream(stream))
+
+
+def moe_permute(x, k, topk_idx, topk_w, counts, offsets, cursor, pos, w_s, xs, stream=None):
+    T, h = x.shape
+    E = counts.shape[0]
+    _call("rp_moe_permute", _ptr(x), I64(x.stride(0)), I32(T), I32(h), I32(k), I32(E),
+          _ptr(topk_idx), _ptr(topk_w), _ptr(counts), _ptr(offsets), _ptr(cursor), _ptr(pos),
+          _ptr(w_s), _ptr(xs), _stream(stream))
+
+
+def moe_gather(x, k, pos, xs, stream=None):
+    T, h = x.shape
+    _call("rp_moe_gather", _ptr(x), I64(x.stride(0)), I32(T), I32(h), I32(k), _ptr(pos),
+          _ptr(xs), _stream(stream))
+
+
+def moe_combine(ys, pos, topk_w, k, out, res=None, stream=None):
+    T, h = out.shape
+    _call("rp_moe_combine", _ptr(ys), _ptr(pos), _ptr(topk_w), I32(T), I32(k), I32(h),
+          _ptr(res), I64(res.stride(0) if res is not None else 0), _ptr(out),
+          I64(out.stride(0)), _stream(stream))
+
+
+def moe_combine_bwd(dxs, pos, k, dh32, dh, stream=None):
+    T, h = dh.shape
+    _call("rp_moe_combine_bwd", _ptr(dxs), _ptr(pos), I32(T), I32(k), I32(h), _ptr(dh32),
+          _ptr(dh), I64(dh.stride(0)), _stream(stream))
+
+
+def moe_swiglu_bwd(dact, gu, w_s, dgu, dw_s, stream=None):
+    rows, m = dact.shape
+    _call("rp_moe_swiglu_bwd", _ptr(dact), _ptr(gu), _ptr(w_s), I64(rows), I32(m), _ptr(dgu),
+          _ptr(dw_s), _stream(stream))
+
+
+def moe_router_bwd(logits, k, norm_topk, topk_idx, pos, dw_s, dlogits, stream=None):
+    T, E = logits.shape
+    _call("rp_moe_router_bwd", _ptr(logits), I32(T), I32(E), I32(k), I32(int(norm_topk)),
+          _ptr(topk_idx), _ptr(pos), _ptr(dw_s), _ptr(dlogits), _stream(stream))
