@@ -37,6 +37,10 @@ class Value {
     return num_;
   }
   int as_int() const { return static_cast<int>(as_double()); }
+  bool as_bool() const {
+    if (type_ != Type::Bool) throw TypeError("expected a boolean");
+    return b_;
+  }
   const std::string& as_string() const {
     if (type_ != Type::String) throw TypeError("expected a string");
     return str_;

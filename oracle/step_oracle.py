@@ -17,7 +17,13 @@ in fp32 PyTorch on the CPU:
       async — step(t+1) applies grads of t, first visible to iteration t+2
               (staleness 1);
   * loss = sum of token CE over the step / number of valid labels; AdamW =
-    torch.optim.AdamW (decoupled weight decay).
+    torch.optim.AdamW (decoupled weight decay);
+  * Qwen3-MoE layers (BASELINE configs[4]): transformers 5.5.0
+    modeling_qwen3_moe.py — router :254-272 (softmax in fp32, top-k,
+    renormalised when norm_topk_prob), experts :215-251 (SwiGLU per expert,
+    weighted sum), sparse block :275-287; every decoder layer is sparse
+    (decoder_sparse_step 1, no mlp_only_layers). LoRA on a MoE model adapts
+    the attention projections only (experts and router frozen).
 Pinning: tests/golden/make_step_golden.py checks this module's loss and
 gradients against transformers' Qwen3ForCausalLM on identical weights and
 commits the numbers (tests/golden/step_golden.json).
@@ -45,6 +51,13 @@ class Shape:
     vocab: int
     rope_theta: float = 1e6
     eps: float = 1e-6
+    experts: int = 1        # MoE: experts per layer (inter = moe_intermediate_size)
+    active: int = 1         # experts routed per token
+    norm_topk: bool = True  # renormalise the top-k routing weights
+
+    @property
+    def moe(self) -> bool:
+        return self.experts > 1
 
     @staticmethod
     def from_config(name: str) -> "Shape":
@@ -55,26 +68,34 @@ class Shape:
         return Shape(int(j["hidden_dim"]), j["num_heads"], j["num_kv_heads"],
                      j.get("head_dim", int(j["hidden_dim"]) // j["num_heads"]),
                      int(j["intermediate_dim"]), j["num_layers"], j["vocab_size"],
-                     j.get("rope_theta", 1e6), j.get("rms_norm_eps", 1e-6))
+                     j.get("rope_theta", 1e6), j.get("rms_norm_eps", 1e-6),
+                     int(j.get("total_experts", 1)), int(j.get("active_experts", 1)),
+                     bool(j.get("norm_topk_prob", True)))
 
 
 # parameter names and shapes, in the flat per-layer order the runtime uses
 def layer_param_shapes(s: Shape):
     qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
-    return [("input_norm", (s.hidden,)), ("qkv", (qd + 2 * kd, s.hidden)),
+    base = [("input_norm", (s.hidden,)), ("qkv", (qd + 2 * kd, s.hidden)),
             ("q_norm", (s.head_dim,)), ("k_norm", (s.head_dim,)),
-            ("o", (s.hidden, qd)), ("post_norm", (s.hidden,)),
-            ("gate_up", (2 * s.inter, s.hidden)), ("down", (s.hidden, s.inter))]
+            ("o", (s.hidden, qd)), ("post_norm", (s.hidden,))]
+    if s.moe:  # router [E, h]; experts stacked: gate_up [E*2m, h], down [E*h, m]
+        return base + [("router", (s.experts, s.hidden)),
+                       ("gate_up", (s.experts * 2 * s.inter, s.hidden)),
+                       ("down", (s.experts * s.hidden, s.inter))]
+    return base + [("gate_up", (2 * s.inter, s.hidden)), ("down", (s.hidden, s.inter))]
 
 
 def lora_param_shapes(s: Shape, r: int):
     """LoRA adapters of a layer (PEFT semantics): A [r, in],
     B [out, r]; in the runtime's flat order after the base tensors."""
     qd, kd = s.heads * s.head_dim, s.kv_heads * s.head_dim
-    return [("qkv_lora_A", (r, s.hidden)), ("qkv_lora_B", (qd + 2 * kd, r)),
-            ("o_lora_A", (r, qd)), ("o_lora_B", (s.hidden, r)),
-            ("gate_up_lora_A", (r, s.hidden)), ("gate_up_lora_B", (2 * s.inter, r)),
-            ("down_lora_A", (r, s.inter)), ("down_lora_B", (s.hidden, r))]
+    att = [("qkv_lora_A", (r, s.hidden)), ("qkv_lora_B", (qd + 2 * kd, r)),
+           ("o_lora_A", (r, qd)), ("o_lora_B", (s.hidden, r))]
+    if s.moe:  # experts and router frozen
+        return att
+    return att + [("gate_up_lora_A", (r, s.hidden)), ("gate_up_lora_B", (2 * s.inter, r)),
+                  ("down_lora_A", (r, s.inter)), ("down_lora_B", (s.hidden, r))]
 
 
 def init_lora_params(s: Shape, r: int, seed: int = 1, std_a: float = 0.02, std_b: float = 0.0):
@@ -157,9 +178,40 @@ def decoder_layer(x, p, pre, s: Shape, cos, sin, lora_scale: float = 0.0):
     o = (att @ v).transpose(1, 2).reshape(b, S, qd)
     x2 = x + lin(o, "o")
     h2 = rms(x2, p(pre + "post_norm"), s.eps)
+    if s.moe:
+        return x2 + moe_block(h2, p, pre, s)
     gu = lin(h2, "gate_up")
     act = torch.nn.functional.silu(gu[..., :s.inter]) * gu[..., s.inter:]
     return x2 + lin(act, "down")
+
+
+def moe_route(hs, router, s: Shape):
+    """Qwen3MoeTopKRouter (modeling_qwen3_moe.py:263-272): fp32 softmax over
+    the E router logits, top-k, renormalised when norm_topk_prob."""
+    probs = torch.softmax(hs @ router.t(), dim=-1, dtype=torch.float32)
+    topv, topi = torch.topk(probs, s.active, dim=-1)
+    if s.norm_topk:
+        topv = topv / topv.sum(-1, keepdim=True)
+    return topv, topi
+
+
+def moe_block(h2, p, pre, s: Shape):
+    """Qwen3MoeSparseMoeBlock (:275-287) + Qwen3MoeExperts (:215-251) on
+    h2 [b, S, h]: sum over the k routed experts of w * down(silu(g) * u)."""
+    b, S, h = h2.shape
+    hs = h2.reshape(-1, h)
+    topv, topi = moe_route(hs, p(pre + "router"), s)
+    gate_up = p(pre + "gate_up").view(s.experts, 2 * s.inter, h)
+    down = p(pre + "down").view(s.experts, h, s.inter)
+    y = torch.zeros_like(hs)
+    for e in range(s.experts):
+        tok, slot = torch.where(topi == e)
+        if tok.numel() == 0:
+            continue
+        gu = hs[tok] @ gate_up[e].t()
+        act = torch.nn.functional.silu(gu[:, :s.inter]) * gu[:, s.inter:]
+        y = y.index_add(0, tok, (act @ down[e].t()) * topv[tok, slot, None])
+    return y.view(b, S, h)
 
 
 def forward_loss_sum(params, tokens, labels, s: Shape, lora_scale: float = 0.0):

@@ -32,17 +32,25 @@ WorkerBytes worker_fixed_bytes(const Shape& s, int T, int seq, int M, int MR, in
                                int nsets, int logits_rows, int lora_r, int64_t chunk_elems) {
   WorkerBytes b;
   const int64_t Th = (int64_t)T * s.h;
+  const int64_t Tk = (int64_t)T * (s.moe() ? s.ek : 1);  // rows of the MLP buffers
+  const int n_lora = s.moe() ? 2 : 4;                      // adapted linears
+  const int64_t moe_set =
+      s.moe() ? (int64_t)T * s.E * 4 + (int64_t)T * s.ek * 4 * 3 + Tk * 4 + (int64_t)(s.E + 1) * 4 : 0;
   const int64_t act_set = Th * 2 * 4 + (int64_t)T * s.qkvd() * 2 + (int64_t)T * s.qd() * 2 * 2 +
-                          (int64_t)T * s.kd() * 2 + (int64_t)T * 2 * s.m * 2 +
-                          (int64_t)T * s.m * 2 + (int64_t)T * 4 * 2 +
-                          (int64_t)T * s.nq * 4 * 2 + (int64_t)T * s.nk * 4 +
-                          (lora_r ? 4LL * T * lora_r * 2 : 0);
+                          (int64_t)T * s.kd() * 2 + Tk * 2 * s.m * 2 + Tk * s.m * 2 +
+                          (int64_t)T * 4 * 2 + (int64_t)T * s.nq * 4 * 2 + (int64_t)T * s.nk * 4 +
+                          (lora_r ? (int64_t)n_lora * T * lora_r * 2 : 0) + moe_set;
   b.activations = act_set * nsets;
+  const int64_t moe_scratch =
+      s.moe() ? Tk * s.h * 2 * 2 + Tk * s.m * 2 + (int64_t)T * s.E * 2 + (int64_t)s.E * 4 * 2 +
+                    Tk * 4 + Th * 4
+              : 0;
   b.scratch = Th * 4 * 2 + Th * 2 * 2 + (int64_t)T * s.qkvd() * 2 * 2 +
-              3LL * T * 2 * s.m * 2 + Th * 2 + (int64_t)T * s.m * 2 + (int64_t)T * s.qd() * 2 * 2 +
+              3LL * Tk * 2 * s.m * 2 + Th * 2 + (int64_t)T * s.m * 2 + (int64_t)T * s.qd() * 2 * 2 +
               (int64_t)T * s.kd() * 2 + (int64_t)T * s.qd() * 4 + (int64_t)T * s.nq * 4 +
               Th * 2 * 3 + (int64_t)T * 4 + (int64_t)std::min(T, logits_rows) * s.V * 2 +
-              2LL * 2 * M * T * 4 + (int64_t)seq * s.hd * 4 + (lora_r ? (int64_t)T * lora_r * 2 : 0);
+              2LL * 2 * M * T * 4 + (int64_t)seq * s.hd * 4 + (lora_r ? (int64_t)T * lora_r * 2 : 0) +
+              moe_scratch;
   b.handoff = S > 1 ? (int64_t)parities * MR * (Th * 2 + Th * 4) : 0;
   b.optimizer_ring = 2LL * 3 * chunk_elems * 4;
   // per-stream kernel scratch: the fused attention backward's fp32 dQ^T
@@ -195,8 +203,11 @@ Shape load_shape(const std::string& model) {
   s.V = shape.vocab_size;
   s.theta = shape.rope_theta;
   s.eps = shape.rms_norm_eps;
-  if (shape.cfg.total_experts != 1)
-    throw RtError(RP_E_INPUT, "MoE models are not supported by the executor yet");
+  s.E = shape.cfg.total_experts;
+  s.ek = shape.cfg.active_experts;
+  s.norm_topk = shape.norm_topk_prob;
+  if (s.moe() && (s.E > 256 || s.ek > 32 || s.ek > s.E))
+    throw RtError(RP_E_INPUT, "MoE: up to 256 experts and 32 routed per token");
   return s;
 }
 

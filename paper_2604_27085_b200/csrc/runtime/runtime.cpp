@@ -66,8 +66,14 @@ LayerLayout make_layer_layout(const Shape& s, int lora_rank) {
   put(L.k_norm, s.hd, 1);
   put(L.o, s.h, s.qd());
   put(L.post_norm, s.h, 1);
-  put(L.gate_up, 2LL * s.m, s.h);
-  put(L.down, s.h, s.m);
+  if (s.moe()) {
+    put(L.router, s.E, s.h);
+    put(L.gate_up, (int64_t)s.E * 2 * s.m, s.h);
+    put(L.down, (int64_t)s.E * s.h, s.m);
+  } else {
+    put(L.gate_up, 2LL * s.m, s.h);
+    put(L.down, s.h, s.m);
+  }
   L.lora_off = off;
   if (lora_rank > 0) {
     const int r = lora_rank;
@@ -75,10 +81,12 @@ LayerLayout make_layer_layout(const Shape& s, int lora_rank) {
     put(L.qkv_B, s.qkvd(), r);
     put(L.o_A, r, s.qd());
     put(L.o_B, s.h, r);
-    put(L.gu_A, r, s.h);
-    put(L.gu_B, 2LL * s.m, r);
-    put(L.down_A, r, s.m);
-    put(L.down_B, s.h, r);
+    if (!s.moe()) {
+      put(L.gu_A, r, s.h);
+      put(L.gu_B, 2LL * s.m, r);
+      put(L.down_A, r, s.m);
+      put(L.down_B, s.h, r);
+    }
   }
   L.total = off;
   return L;
@@ -494,6 +502,31 @@ struct Runtime {
   void gemm2(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
              bool b_mn, void* D, int64_t ldd, int M_, int N_, int K_, const void* Rz, int64_t ldr,
              const void* A2, int64_t lda2, const void* B2, int64_t ldb2, int K2);
+  // grouped expert GEMM over the expert-sorted rows (row offsets on the device)
+  void grouped(cudaStream_t st, const void* A, int64_t lda, const void* B, int64_t ldb, bool b_mn,
+               void* D, int64_t ldd, int M_, int N_, int K_, const int32_t* off, int brows,
+               const void* gu = nullptr) {
+    rp_gemm_args_t a{};
+    a.M = M_;
+    a.N = N_;
+    a.K = K_;
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.b_mn_major = b_mn;
+    a.D = D;
+    a.ldd = ldd;
+    a.R = gu;
+    a.ldr = gu ? 2LL * N_ : 0;
+    const int pi = prof_begin(st);
+    RP_K(rp_gemm_grouped(&a, off, s.E, brows, gu ? 1 : 0, st));
+    prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)K_);
+    ++kernels;
+  }
+  void moe_mlp_fwd(Gpu& G, cudaStream_t st, const uint16_t* W, LayerActs& A, uint16_t* x_out);
+  void moe_mlp_bwd(Gpu& G, cudaStream_t st, const uint16_t* W, LayerActs& A, const uint16_t* dy,
+                   uint16_t* dgu);
   ~Runtime();
 };
 
@@ -590,6 +623,8 @@ void Runtime::init(const rp_runtime_config_t& c) {
     }
   if (cfg.lora_rank < 0 || cfg.lora_rank > 256 || cfg.lora_rank % 8)
     throw RtError(RP_E_INPUT, "lora_rank must be 0 or a multiple of 8 up to 256");
+  if (s.moe() && cfg.lora_rank == 0)  // BASELINE configs[4]: LoRA of a frozen MoE base
+    throw RtError(RP_E_INPUT, "MoE models: LoRA fine-tune only (experts and router frozen)");
   lora_r = cfg.lora_rank;
   lora_scale = lora_r > 0 ? (cfg.lora_alpha > 0 ? cfg.lora_alpha : (float)lora_r) / lora_r : 0.f;
   LL = make_layer_layout(s, lora_r);
@@ -819,6 +854,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   G.allocated.assign(8, 0);
   auto dalloc = [&](std::size_t bytes, int cat) -> void* { return this->dalloc(G, bytes, cat); };
   const int64_t Th = (int64_t)T * s.h;
+  const int64_t Tk = (int64_t)T * (s.moe() ? s.ek : 1);  // rows of the (expert-sorted) MLP buffers
   G.groups.resize(ngroups());
   for (int g = 0; g < ngroups(); ++g) {
     DevGroup& D = G.groups[g];
@@ -845,8 +881,8 @@ void Runtime::alloc_worker(Gpu& G, int id) {
   // step runs at the 1 kW power cap (the overlap lowers SM clocks instead),
   // while the second activation set costs 20.6 GB of HBM that otherwise holds
   // optimizer state
-  const bool pipe =
-      plan.fused_stage.first == 0 && MR >= 2 && (cfg.flags & RP_RT_FUSED_PIPELINE);
+  const bool pipe = plan.fused_stage.first == 0 && MR >= 2 && !s.moe() &&
+                    (cfg.flags & RP_RT_FUSED_PIPELINE);  // (MoE scratch is single-stream)
   if (pipe) G.acts2.resize(nsets);
   for (auto* set : {&G.acts, &G.acts2})
   for (auto& A : *set) {
@@ -858,8 +894,8 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     A.o = static_cast<uint16_t*>(dalloc((int64_t)T * s.qd() * 2, 3));
     A.x2 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
     A.h2 = static_cast<uint16_t*>(dalloc(Th * 2, 3));
-    A.gu = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 3));
-    A.act = static_cast<uint16_t*>(dalloc((int64_t)T * s.m * 2, 3));
+    A.gu = static_cast<uint16_t*>(dalloc(Tk * 2 * s.m * 2, 3));
+    A.act = static_cast<uint16_t*>(dalloc(Tk * s.m * 2, 3));
     A.rstd1 = static_cast<float*>(dalloc((std::size_t)T * 4, 3));
     A.rstd2 = static_cast<float*>(dalloc((std::size_t)T * 4, 3));
     A.rstd_q = static_cast<float*>(dalloc((int64_t)T * s.nq * 4, 3));
@@ -870,9 +906,29 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     if (lora_r) {
       A.u_qkv = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
       A.u_o = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
-      A.u_gu = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
-      A.u_down = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+      if (!s.moe()) {
+        A.u_gu = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+        A.u_down = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 3));
+      }
     }
+    if (s.moe()) {
+      A.r_logits = static_cast<float*>(dalloc((int64_t)T * s.E * 4, 3));
+      A.r_idx = static_cast<int32_t*>(dalloc((int64_t)T * s.ek * 4, 3));
+      A.r_w = static_cast<float*>(dalloc((int64_t)T * s.ek * 4, 3));
+      A.r_pos = static_cast<int32_t*>(dalloc((int64_t)T * s.ek * 4, 3));
+      A.r_ws = static_cast<float*>(dalloc(Tk * 4, 3));
+      A.r_off = static_cast<int32_t*>(dalloc((int64_t)(s.E + 1) * 4, 3));
+    }
+  }
+  if (s.moe()) {
+    G.m_xs = static_cast<uint16_t*>(dalloc(Tk * s.h * 2, 4));
+    G.m_ys = static_cast<uint16_t*>(dalloc(Tk * s.h * 2, 4));
+    G.m_dact = static_cast<uint16_t*>(dalloc(Tk * s.m * 2, 4));
+    G.m_dlogits = static_cast<uint16_t*>(dalloc((int64_t)T * s.E * 2, 4));
+    G.m_counts = static_cast<int32_t*>(dalloc((int64_t)s.E * 4, 4));
+    G.m_cursor = static_cast<int32_t*>(dalloc((int64_t)s.E * 4, 4));
+    G.m_dws = static_cast<float*>(dalloc(Tk * 4, 4));
+    G.m_dh32 = static_cast<float*>(dalloc(Th * 4, 4));
   }
   if (lora_r) G.du = static_cast<uint16_t*>(dalloc((int64_t)T * lora_r * 2, 4));
   if (pipe) {
@@ -895,7 +951,7 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     G.ev_dqkv_free[b] = new_event(false);
   }
   for (int b = 0; b < G.n_dgu; ++b) {
-    G.dgus[b] = static_cast<uint16_t*>(dalloc((int64_t)T * 2 * s.m * 2, 4));
+    G.dgus[b] = static_cast<uint16_t*>(dalloc(Tk * 2 * s.m * 2, 4));
     G.ev_dgu_free[b] = new_event(false);
   }
   G.ev_wgrad = new_event(false);
@@ -984,7 +1040,7 @@ void Runtime::init_weights() {
               {LL.post_norm.off, s.h}};
       if (lora_r)  // LoRA B starts at zero (the adapted model starts as the base)
         for (const Tensor* t : {&LL.qkv_B, &LL.o_B, &LL.gu_B, &LL.down_B})
-          zeros.emplace_back(t->off, t->numel());
+          if (t->numel() > 0) zeros.emplace_back(t->off, t->numel());
     } else if (g == s.L + 1) {
       ones = {{HL.final_norm.off, s.h}};
     }
@@ -1260,6 +1316,11 @@ void Runtime::layer_fwd(Gpu& G, int l, const uint16_t* x, LayerActs& A, uint16_t
     RP_K(rp_rmsnorm_fwd(A.x2, h, W + LL.post_norm.off, A.h2, h, A.rstd2, T, h, (float)s.eps, st));
     prof_end(pi_, st, 2, 4.0 * T * h);
   }
+  if (s.moe()) {  // routed experts instead of the dense MLP
+    moe_mlp_fwd(G, st, W, A, x_out);
+    kernels += 5;
+    return;
+  }
   const bool unfused = cfg.flags & RP_RT_UNFUSED_SWIGLU;
   if (lora_r && !unfused && T >= 256) {  // LoRA: Us first, then the dual GEMM with [X | Us]
     const int r = lora_r;
@@ -1339,6 +1400,12 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
         RP_CUDA(cudaMemsetAsync(dW + t->off, 0, t->numel() * 4, st));
   }
   // MLP:  x3 = x2 + act(gu(h2)) Wd^T
+  if (s.moe()) {  // routed experts (frozen): dh = d(h2) through experts and router
+    RP_CUDA(cudaStreamWaitEvent(st, G.ev_dgu_free[pg], 0));
+    moe_mlp_bwd(G, st, W, A, dx_a, dgu);
+    RP_CUDA(cudaEventRecord(G.ev_dx16_free[xa], st));
+    RP_CUDA(cudaEventRecord(G.ev_dgu_free[pg], st));
+  } else {
   to_ws();
   if (full) gemm(ws, dx_a, h, true, A.act, m, true, dW + LL.down.off, m, true, !first, h, m, T);
   // full fine-tune: the SwiGLU backward runs in the dgrad GEMM's epilogue
@@ -1394,6 +1461,7 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
     lin_dgrad(G, st, W, LL.gate_up, &LL.gu_A, &LL.gu_B, dgu, 2 * m, 2 * m, G.dh, h, h);
     lora_wgrad(G, st, dW, LL.gu_A, LL.gu_B, A.h2, h, h, A.u_gu, dgu, 2 * m, 2 * m, first);
   }
+  }  // dense MLP
   RP_CUDA(cudaStreamWaitEvent(st, G.ev_dx16_free[xb], 0));
   {
     const int pi_ = prof_begin(st);
@@ -1448,6 +1516,49 @@ void Runtime::layer_bwd(Gpu& G, int l, LayerActs& A, bool first) {
   }
   RP_CUDA(cudaEventRecord(A.ev_chain_free, st));
   kernels += 8;
+}
+
+// MoE MLP forward (Qwen3-MoE sparse block, modeling_qwen3_moe.py:254-287):
+// router logits (fp32) -> softmax / top-k -> expert-sorted rows -> grouped
+// gate/up GEMM -> SwiGLU -> grouped down GEMM -> weighted sum + residual.
+// A.gu / A.act keep the T*ek sorted rows for the backward.
+void Runtime::moe_mlp_fwd(Gpu& G, cudaStream_t st, const uint16_t* W, LayerActs& A,
+                          uint16_t* x_out) {
+  const int h = s.h, m = s.m, E = s.E, k = s.ek, Tk = T * k;
+  gemm(st, A.h2, h, false, W + LL.router.off, h, false, A.r_logits, E, true, false, T, E, h);
+  RP_K(rp_moe_route(A.r_logits, T, E, k, s.norm_topk ? 1 : 0, A.r_idx, A.r_w, G.m_counts, st));
+  RP_K(rp_moe_permute(A.h2, h, T, h, k, E, A.r_idx, A.r_w, G.m_counts, A.r_off, G.m_cursor,
+                      A.r_pos, A.r_ws, G.m_xs, st));
+  grouped(st, G.m_xs, h, W + LL.gate_up.off, h, false, A.gu, 2 * m, Tk, 2 * m, h, A.r_off, 2 * m);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_swiglu_fwd(A.gu, A.act, Tk, m, st));
+    prof_end(pi_, st, 2, 6.0 * Tk * m);
+  }
+  grouped(st, A.act, m, W + LL.down.off, m, false, G.m_ys, h, Tk, h, m, A.r_off, h);
+  RP_K(rp_moe_combine(G.m_ys, A.r_pos, A.r_w, T, k, h, A.x2, h, x_out, h, st));
+}
+
+// MoE MLP backward with frozen experts and router: G.dh = dL/dh2 from dy =
+// dL/d(MLP output) through the weighted expert sum (dw per routed row), the
+// experts (grouped dgrad GEMMs, SwiGLU backward) and the router (top-k
+// renormalisation + softmax backward, router dgrad GEMM).
+void Runtime::moe_mlp_bwd(Gpu& G, cudaStream_t st, const uint16_t* W, LayerActs& A,
+                          const uint16_t* dy, uint16_t* dgu) {
+  const int h = s.h, m = s.m, E = s.E, k = s.ek, Tk = T * k;
+  RP_K(rp_moe_gather(dy, h, T, h, k, A.r_pos, G.m_xs, st));
+  grouped(st, G.m_xs, h, W + LL.down.off, m, true, G.m_dact, m, Tk, m, h, A.r_off, h);
+  {
+    const int pi_ = prof_begin(st);
+    RP_K(rp_moe_swiglu_bwd(G.m_dact, A.gu, A.r_ws, Tk, m, dgu, G.m_dws, st));
+    prof_end(pi_, st, 2, 10.0 * Tk * m);
+  }
+  grouped(st, dgu, 2 * m, W + LL.gate_up.off, h, true, G.m_ys, h, Tk, h, 2 * m, A.r_off, 2 * m);
+  RP_K(rp_moe_router_bwd(A.r_logits, T, E, k, s.norm_topk ? 1 : 0, A.r_idx, A.r_pos, G.m_dws,
+                         G.m_dlogits, st));
+  gemm(st, G.m_dlogits, E, false, W + LL.router.off, h, true, G.m_dh32, h, true, false, T, h, E);
+  RP_K(rp_moe_combine_bwd(G.m_ys, A.r_pos, T, k, h, G.m_dh32, G.dh, h, st));
+  kernels += 5;
 }
 
 // Head pseudo-layer: final RMSNorm + LM head + CE forward and backward,
@@ -2176,7 +2287,7 @@ RP_API int rp_param_count(rp_runtime_t* p, int32_t group, int64_t* n) {
 }
 
 // Flat layout of a group: (offset, rows, cols) per tensor, in the order
-// embed | in_norm qkv q_norm k_norm o post_norm gate_up down | final_norm lm_head.
+// embed | in_norm qkv q_norm k_norm o post_norm [router] gate_up down | final_norm lm_head.
 RP_API int rp_param_layout(rp_runtime_t* p, int32_t group, int64_t* offs, int64_t* rows,
                            int64_t* cols, int32_t cap, int32_t* n) {
   return rt_guard([&] {
@@ -2187,11 +2298,14 @@ RP_API int rp_param_layout(rp_runtime_t* p, int32_t group, int64_t* offs, int64_
     else if (g == rt->s.L + 1) ts = {rt->HL.final_norm, rt->HL.lm_head};
     else {
       const auto& L = rt->LL;
-      ts = {L.in_norm, L.qkv, L.q_norm, L.k_norm, L.o, L.post_norm, L.gate_up, L.down};
-      if (rt->lora_r)  // adapters after the base tensors
+      ts = {L.in_norm, L.qkv, L.q_norm, L.k_norm, L.o, L.post_norm};
+      if (rt->s.moe()) ts.push_back(L.router);
+      ts.push_back(L.gate_up);
+      ts.push_back(L.down);
+      if (rt->lora_r)  // adapters after the base tensors (MoE: attention only)
         for (const auto* t : {&L.qkv_A, &L.qkv_B, &L.o_A, &L.o_B, &L.gu_A, &L.gu_B, &L.down_A,
                               &L.down_B})
-          ts.push_back(*t);
+          if (t->numel() > 0) ts.push_back(*t);
     }
     *n = (int32_t)ts.size();
     if (*n > cap) throw RtError(RP_E_TOOSMALL, "layout capacity");

@@ -39,6 +39,11 @@ struct RtError : std::runtime_error {
 // Decoder shape (Qwen3 family).
 struct Shape {
   int h = 0, nq = 0, nk = 0, hd = 0, m = 0, L = 0, V = 0;
+  // mixture of experts (Qwen3-MoE): E experts of intermediate size m, ek
+  // routed per token, top-k weights renormalised when norm_topk
+  int E = 1, ek = 1;
+  bool norm_topk = true;
+  bool moe() const { return E > 1; }
   double theta = 1e6, eps = 1e-6;
   int qd() const { return nq * hd; }
   int kd() const { return nk * hd; }
@@ -52,8 +57,11 @@ struct Tensor {
   int64_t numel() const { return rows * cols; }
 };
 struct LayerLayout {
-  Tensor in_norm, qkv, q_norm, k_norm, o, post_norm, gate_up, down;
+  // dense: gate_up [2m x h], down [h x m]; MoE: router [E x h], gate_up
+  // [E*2m x h] (per expert gate rows then up rows), down [E*h x m]
+  Tensor in_norm, qkv, q_norm, k_norm, o, post_norm, router, gate_up, down;
   // LoRA adapters (rank r > 0), after the base tensors: A [r x in], B [out x r]
+  // (MoE layers: attention projections only — experts and router frozen)
   Tensor qkv_A, qkv_B, o_A, o_B, gu_A, gu_B, down_A, down_B;
   int64_t lora_off = 0;  // start of the adapters (= total without LoRA)
   int64_t total = 0;
@@ -132,6 +140,12 @@ struct LayerActs {
   uint16_t *x, *h1, *qkv, *q, *k, *o, *x2, *h2, *gu, *act;
   float *rstd1, *rstd_q, *rstd_k, *lse, *rstd2;
   uint16_t *u_qkv = nullptr, *u_o = nullptr, *u_gu = nullptr, *u_down = nullptr;  // LoRA: s X A^T
+  // MoE: router logits [T, E] (fp32), top-k experts / weights / expert-sorted
+  // rows [T, ek], routing weight per sorted row, expert row offsets [E+1];
+  // gu / act then hold the T*ek expert-sorted rows
+  float* r_logits = nullptr;
+  int32_t *r_idx = nullptr, *r_pos = nullptr, *r_off = nullptr;
+  float *r_w = nullptr, *r_ws = nullptr;
   const uint16_t* xin = nullptr;  // the input actually used by layer_fwd
   cudaEvent_t ev_free = nullptr;        // weight-gradient GEMMs done reading act/h2/o/h1
   cudaEvent_t ev_chain_free = nullptr;  // the dgrad chain done with this layer's activations
@@ -191,6 +205,11 @@ struct Gpu {
   uint16_t *dx16 = nullptr, *dh = nullptr, *dact = nullptr, *dgu = nullptr, *dattn = nullptr;
   uint16_t *dqkv = nullptr, *dq_t = nullptr, *dk_t = nullptr;
   uint16_t* du = nullptr;  // LoRA: s dY B of the linear being back-propagated (T x r)
+  // MoE scratch: expert-sorted rows (gathered inputs / dY, expert outputs /
+  // input grads), counts and cursors, dact', dL/dw per row, router grads
+  uint16_t *m_xs = nullptr, *m_ys = nullptr, *m_dact = nullptr, *m_dlogits = nullptr;
+  int32_t *m_counts = nullptr, *m_cursor = nullptr;
+  float *m_dws = nullptr, *m_dh32 = nullptr;
   float *dq_acc = nullptr, *delta = nullptr;
   uint16_t* xbuf[2] = {nullptr, nullptr};
   uint16_t *hN = nullptr, *logits = nullptr;

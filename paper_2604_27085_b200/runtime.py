@@ -50,6 +50,9 @@ class StatsC(C.Structure):
 
 
 LAYER_TENSORS = ["input_norm", "qkv", "q_norm", "k_norm", "o", "post_norm", "gate_up", "down"]
+# Qwen3-MoE layers: router [E, h], experts stacked gate_up [E*2m, h], down [E*h, m]
+MOE_LAYER_TENSORS = ["input_norm", "qkv", "q_norm", "k_norm", "o", "post_norm", "router",
+                     "gate_up", "down"]
 LORA_TENSORS = ["qkv_lora_A", "qkv_lora_B", "o_lora_A", "o_lora_B", "gate_up_lora_A",
                 "gate_up_lora_B", "down_lora_A", "down_lora_B"]
 HEAD_TENSORS = ["final_norm", "lm_head"]
@@ -127,9 +130,14 @@ class RoundPipe:
             | (RP_RT_HOST_PUBLISH if host_publish else 0)
             | (RP_RT_POOLED if pooled else 0),
             lora_rank, lora_alpha, float(resident_state_gb), int(logits_rows), 0)
-        self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.h = VP()
         self._call("rp_runtime_create", C.byref(cfg), C.byref(self.h))
+        # MoE layers carry a router and adapt the attention projections only
+        self.moe = len(self.layout(0)) in (len(MOE_LAYER_TENSORS), len(MOE_LAYER_TENSORS) + 4)
+        if self.moe:
+            self.layer_tensors = MOE_LAYER_TENSORS + (LORA_TENSORS[:4] if lora_rank else [])
+        else:
+            self.layer_tensors = LAYER_TENSORS + (LORA_TENSORS if lora_rank else [])
         self.seq_len, self.micro_batch, self.micro_batches = seq_len, micro_batch, micro_batches
         self.num_gpus = num_gpus
 
