@@ -291,40 +291,75 @@ __global__ void __launch_bounds__(192, 1)
 // Ping-pong variant: one CTA = 128 query rows x TWO query heads of the same
 // KV group (GQA), so both Q tiles consume the same K/V tiles (loaded once)
 // and two softmax warpgroups alternate with the tensor core:
-//   w0      TMA: Q0, Q1 once; then K_0, V_0, K_1, V_1, ... through a 3-slot ring
+//   w0      TMA: Q0, Q1 once; then K_0, V_0, K_1, V_1, ... through a 4-slot ring
 //   w1      MMA: S0_{j+1} = Q0 K^T and S1_{j+1} = Q1 K^T interleaved with
 //           O0 += P0_j V_j and O1 += P1_j V_j (TMEM: S0 | S1 | O0 | O1)
 //   w4-7    softmax of head 0 (thread = query row),  w8-11  softmax of head 1
 // While one warpgroup turns its S into P the tensor core runs the other
-// head's MMAs, so the MUFU/FMA work of the two heads hides behind the MMAs.
+// head's MMAs. P goes back into the TMEM columns of its S (bf16 pairs) and
+// feeds the PV MMA as a TMEM A operand (no P traffic through shared memory,
+// whose port the N=128 SS MMAs already saturate).
+//
+// The chain of one head is softmax_j -> PV_j -> S_{j+1} -> softmax_{j+1}, so
+// the tensor core idles unless a softmax pass finishes within the other
+// head's PV + S (1024 MMA cycles). At 16 ex2/clk/SM the MUFU alone needs
+// 1024 cycles for a 128x128 tile, so the pass is shortened three ways:
+//   * a quarter of the exponentials run on the FMA pipe (ex2_fma2: rint by
+//     the 1.5*2^23 add, degree-3 polynomial, 2^n added into the exponent;
+//     rel. error 7.5e-5, far below the bf16 rounding of P; measured 0.1195 ms
+//     vs 0.1208 all-MUFU and 0.1218 with half emulated,
+//     profiles/r02_attn_fwd_variants.jsonl);
+//   * P is published in two halves: PV's first four K=16 steps run while the
+//     warpgroup computes the second half;
+//   * the row max uses 3-input FMNMX3; the four S loads share one wait.
+// Registers: the producer/MMA warpgroup gives its registers to the softmax
+// warpgroups (setmaxnreg 56 / 224), so the 128-float row never spills.
 constexpr int PP_THREADS = 384;
 
-// PT (the only instantiation; PT = false keeps P in shared memory and
-// measured slower): P goes back into the TMEM columns of its S (bf16 pairs) and feeds the
-// PV MMA as a TMEM A operand — no P store to shared memory, whose port the
-// SS MMAs at N=128 already saturate — and the freed smem deepens the K/V ring.
-template <int HD, bool PT>
+template <int HD>
 struct PpSmem {
   static constexpr int NSUB = HD / 64;
   static constexpr int QT = NSUB * SUB;       // one Q tile (128 rows x HD)
   static constexpr int KVT = NSUB * SUB;      // one K or V tile (128 keys x HD)
-  static constexpr int NSLOT = PT ? 4 : 3;    // K/V ring slots
+  static constexpr int NSLOT = 4;             // K/V ring slots
   static constexpr int Q0 = 0;
   static constexpr int RING = Q0 + 2 * QT;
-  static constexpr int P = RING + NSLOT * KVT;  // P0, P1: 128 x 128 bf16 each (2 SUB), !PT
-  static constexpr int BAR = P + (PT ? 0 : 2 * 2 * SUB);
+  static constexpr int BAR = RING + NSLOT * KVT;
   static constexpr int BYTES = BAR + 256 + 1024;
   static_assert(BYTES <= 232448, "exceeds 227 KB of shared memory");
 };
 
-template <int HD, bool PT>
+// 2^x for -125 <= x (clamped) and x < 2^22, on the FMA/ALU pipes.
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 rnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, rnd);                      // mantissa low bits = rint(x)
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));  // [-0.5, 0.5]
+  float2 p = __ffma2_rn(f, make_float2(0.05517167f, 0.05517167f),
+                        make_float2(0.24261113f, 0.24261113f));
+  p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+  p = __ffma2_rn(p, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// EMU: pairs out of every four (8 probabilities) computed by ex2_fma2.
+template <int HD, int EMU>
 __global__ void __launch_bounds__(PP_THREADS, 1)
     attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, bf16* __restrict__ o,
                        long long ldo, float* __restrict__ lse, int T, int seq, int nq, int nk,
                        float scale) {
-  using L = PpSmem<HD, PT>;
+  using L = PpSmem<HD>;
   constexpr int NS = L::NSLOT;
   constexpr int NSUB = L::NSUB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -335,8 +370,8 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   uint64_t* kv_full = bar + 1;        // [NS]
   uint64_t* kv_empty = bar + 1 + NS;  // [NS]
   uint64_t* s_full = kv_empty + NS;   // [2] per head
-  uint64_t* p_full = s_full + 2;      // [2]
-  uint64_t* o_done = p_full + 2;      // [2]
+  uint64_t* p_half = s_full + 2;      // [2 heads][2 halves]
+  uint64_t* o_done = p_half + 4;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -359,9 +394,9 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
       mbar_init(&o_done[i], 1);
     }
+    for (int i = 0; i < 4; ++i) mbar_init(&p_half[i], 4);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -371,91 +406,91 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   // TMEM columns: S_w at w*128, O_w at 256 + w*HD
 
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ TMA producer
-    mbar_arrive_expect_tx(q_full, 2 * L::QT);
-    for (int w = 0; w < 2; ++w)
-      for (int sub = 0; sub < NSUB; ++sub)
-        tma_load_2d(sm + L::Q0 + w * L::QT + sub * SUB, &tm_q, q_full, (h0 + w) * HD + 64 * sub,
-                    q0);
-    for (int idx = 0; idx < 2 * ntiles; ++idx) {
-      const int slot = idx % NS;
-      mbar_wait(&kv_empty[slot], ((idx / NS) & 1) ^ 1);
-      const int k0 = s0 + (idx >> 1) * TILE;
-      uint8_t* dst = sm + L::RING + slot * L::KVT;
-      mbar_arrive_expect_tx(&kv_full[slot], L::KVT);
-      const CUtensorMap* map = (idx & 1) ? &tm_v : &tm_k;
-      for (int sub = 0; sub < NSUB; ++sub)
-        tma_load_2d(dst + sub * SUB, map, &kv_full[slot], kvh * HD + 64 * sub, k0);
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // (whole warp: uniform descriptors; one elected lane issues)
-    constexpr uint32_t idesc_s = umma_idesc_bf16(TILE, TILE, 0, 0);
-    constexpr uint32_t idesc_o = umma_idesc_bf16(TILE, HD, 0, 1);
-    const uint32_t q_addr = smem_u32(sm + L::Q0);
-    const uint32_t p_addr = smem_u32(sm + L::P);
-    auto ring = [&](int idx) { return smem_u32(sm + L::RING + (idx % NS) * L::KVT); };
-    auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % NS], (idx / NS) & 1); };
-    auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T
-      const uint32_t qa = q_addr + w * L::QT, ka = ring(2 * j);
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
-          umma_f16(tmem + w * TILE, umma_desc_sw128(qa + off, 16, 1024),
-                   umma_desc_sw128(ka + off, 16, 1024), idesc_s, kk != 0);
-        }
-        umma_commit(&s_full[w]);
+  if (warp < 4) {
+    setmaxnreg_dec<56>();
+    if (warp == 0 && lane == 0) {
+      // ---------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(q_full, 2 * L::QT);
+      for (int w = 0; w < 2; ++w)
+        for (int sub = 0; sub < NSUB; ++sub)
+          tma_load_2d(sm + L::Q0 + w * L::QT + sub * SUB, &tm_q, q_full,
+                      (h0 + w) * HD + 64 * sub, q0);
+      for (int idx = 0; idx < 2 * ntiles; ++idx) {
+        const int slot = idx % NS;
+        mbar_wait(&kv_empty[slot], ((idx / NS) & 1) ^ 1);
+        const int k0 = s0 + (idx >> 1) * TILE;
+        uint8_t* dst = sm + L::RING + slot * L::KVT;
+        mbar_arrive_expect_tx(&kv_full[slot], L::KVT);
+        const CUtensorMap* map = (idx & 1) ? &tm_v : &tm_k;
+        for (int sub = 0; sub < NSUB; ++sub)
+          tma_load_2d(dst + sub * SUB, map, &kv_full[slot], kvh * HD + 64 * sub, k0);
       }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j
-      mbar_wait(&p_full[w], j & 1);
-      tc_fence_after();
-      const uint32_t pa = p_addr + w * 2 * SUB, va = ring(2 * j + 1);
-      if (elect_one()) {
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      // (whole warp: uniform descriptors; one elected lane issues)
+      constexpr uint32_t idesc_s = umma_idesc_bf16(TILE, TILE, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(TILE, HD, 0, 1);
+      const uint32_t q_addr = smem_u32(sm + L::Q0);
+      auto ring = [&](int idx) { return smem_u32(sm + L::RING + (idx % NS) * L::KVT); };
+      auto wait_kv = [&](int idx) { mbar_wait(&kv_full[idx % NS], (idx / NS) & 1); };
+      auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T
+        const uint32_t qa = q_addr + w * L::QT, ka = ring(2 * j);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < TILE / 16; ++kk) {
-          const uint64_t bd = umma_desc_sw128(va + kk * 2048, SUB, 1024);
-          if (PT) {  // P: bf16 pairs in S_w's columns, 8 columns per K=16 step
-            umma_f16_ts(tmem + 256 + w * HD, tmem + w * TILE + kk * 8, bd, idesc_o, (j | kk) != 0);
-          } else {
-            const uint64_t ad = umma_desc_sw128(pa + (kk >> 2) * SUB + (kk & 3) * 32, 16, 1024);
-            umma_f16(tmem + 256 + w * HD, ad, bd, idesc_o, (j | kk) != 0);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * SUB + (kk & 3) * 32;
+            umma_f16(tmem + w * TILE, umma_desc_sw128(qa + off, 16, 1024),
+                     umma_desc_sw128(ka + off, 16, 1024), idesc_s, kk != 0);
           }
+          umma_commit(&s_full[w]);
         }
-        umma_commit(&o_done[w]);
-      }
-      __syncwarp();
-    };
-    mbar_wait(q_full, 0);
-    wait_kv(0);
-    tc_fence_after();
-    issue_s(0, 0);
-    issue_s(1, 0);
-    if (elect_one()) umma_commit(&kv_empty[0]);
-    __syncwarp();
-    for (int j = 0; j < ntiles; ++j) {
-      wait_kv(2 * j + 1);
-      tc_fence_after();
-      issue_pv(0, j);
-      const bool more = j + 1 < ntiles;
-      if (more) {
-        wait_kv(2 * j + 2);
-        tc_fence_after();
-        issue_s(0, j + 1);  // S0 was read before P0_j was published
-      }
-      issue_pv(1, j);
-      if (elect_one()) umma_commit(&kv_empty[(2 * j + 1) % NS]);
-      __syncwarp();
-      if (more) {
-        issue_s(1, j + 1);
-        if (elect_one()) umma_commit(&kv_empty[(2 * j + 2) % NS]);
         __syncwarp();
+      };
+      auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j, one half of the keys at a time
+        const uint32_t va = ring(2 * j + 1);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(&p_half[2 * w + half], j & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = half * 4; kk < half * 4 + 4; ++kk)  // P: 8 bf16-pair columns per K=16
+              umma_f16_ts(tmem + 256 + w * HD, tmem + w * TILE + kk * 8,
+                          umma_desc_sw128(va + kk * 2048, SUB, 1024), idesc_o, (j | kk) != 0);
+            if (half) umma_commit(&o_done[w]);
+          }
+          __syncwarp();
+        }
+      };
+      mbar_wait(q_full, 0);
+      wait_kv(0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      if (elect_one()) umma_commit(&kv_empty[0]);
+      __syncwarp();
+      for (int j = 0; j < ntiles; ++j) {
+        wait_kv(2 * j + 1);
+        tc_fence_after();
+        issue_pv(0, j);
+        const bool more = j + 1 < ntiles;
+        if (more) {
+          wait_kv(2 * j + 2);
+          tc_fence_after();
+          issue_s(0, j + 1);  // S0 was read before P0_j was published
+        }
+        issue_pv(1, j);
+        if (elect_one()) umma_commit(&kv_empty[(2 * j + 1) % NS]);
+        __syncwarp();
+        if (more) {
+          issue_s(1, j + 1);
+          if (elect_one()) umma_commit(&kv_empty[(2 * j + 2) % NS]);
+          __syncwarp();
+        }
       }
     }
-  } else if (warp >= 4) {
+  } else {
+    setmaxnreg_inc<224>();
     // ------------------------------------------------------------ softmax
     const int w = (warp - 4) >> 2;      // head slot of this warpgroup
     const int quarter = warp & 3;
@@ -464,40 +499,39 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
     const uint32_t s_col = w * TILE, o_col = 256 + w * HD;
     const float sl2 = scale * 1.4426950408889634f;
     float m = 0.f, l = 0.f;
-    uint8_t* p_row = sm + L::P + w * 2 * SUB + (r >> 3) * 1024 + (r & 7) * 128;  // !PT
     for (int j = 0; j < ntiles; ++j) {
+      const bool diag = j == ntiles - 1;
       mbar_wait(&s_full[w], j & 1);
       tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + s_col + 32 * c, sr[c]);
+      tmem_ld_wait();
       float s[TILE];
 #pragma unroll
-      for (int c = 0; c < TILE; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(lane_base + s_col + c, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(v[i]);
-      }
-      if (j == ntiles - 1) {  // diagonal tile: key c > query r is masked
+      for (int c = 0; c < TILE; ++c) s[c] = __uint_as_float(sr[c >> 5][c & 31]);
+      if (diag) {  // diagonal tile: key c > query r is masked
 #pragma unroll
         for (int c = 0; c < TILE; ++c)
           if (c > r) s[c] = -INFINITY;
       }
-      float mx8[8];  // 8 independent max chains (latency, not a 128-deep chain)
+      float mx8[8];  // 8 independent max chains of 3-input max
 #pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = s[i];
+      for (int i = 0; i < 8; ++i) {
+        mx8[i] = s[i];
 #pragma unroll
-      for (int c = 8; c < TILE; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        for (int k = 0; k < 7; ++k) mx8[i] = fmax3(mx8[i], s[8 + 16 * k + i], s[16 + 16 * k + i]);
+        mx8[i] = fmaxf(mx8[i], s[120 + i]);
+      }
+      const float mx = fmaxf(fmax3(mx8[0], mx8[1], mx8[2]),
+                             fmaxf(fmax3(mx8[3], mx8[4], mx8[5]), fmax3(mx8[6], mx8[7], mx8[7])));
       const float mxs = mx * sl2;
-      bool o_ready = false;
       if (j == 0) {
         m = mxs;
       } else if (__any_sync(0xffffffffu, mxs > m + 8.f)) {
         // some row's max grew by > 2^8: rescale this warp's O rows after PV_{j-1}
         mbar_wait(&o_done[w], (j - 1) & 1);
         tc_fence_after();
-        o_ready = true;
         const float m_new = fmaxf(m, mxs);
         const float f = ex2(m - m_new);
         m = m_new;
@@ -513,44 +547,36 @@ __global__ void __launch_bounds__(PP_THREADS, 1)
         tmem_st_wait();
         l *= f;
       }
-      if (!PT && j >= 1 && !o_ready) {  // PV_{j-1} must be done reading this head's P buffer
-        mbar_wait(&o_done[w], (j - 1) & 1);
-        tc_fence_after();
-      }
-      // (PT: PV_{j-1} read P_{j-1} from these TMEM columns before S_j overwrote them)
+      // (PV_{j-1} read P_{j-1} from these TMEM columns before S_j overwrote them)
       // P = 2^(s*scale*log2e - m); four independent row-sum chains
       float2 lsum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
       const float2 sl2v = make_float2(sl2, sl2), negm = make_float2(-m, -m);
-      uint32_t pt[16];  // PT: 32 probabilities = 16 TMEM columns per store
+      auto exp_pass = [&]<bool E>() {
+        uint32_t pt[16];  // 32 probabilities = 16 TMEM columns per store
 #pragma unroll
-      for (int ch = 0; ch < TILE / 8; ++ch) {  // 16-byte chunks of the swizzled row
-        uint32_t pk[4];
+        for (int ch = 0; ch < TILE / 8; ++ch) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 x = __ffma2_rn(make_float2(s[ch * 8 + 2 * e], s[ch * 8 + 2 * e + 1]), sl2v, negm);
-          const float2 pv = make_float2(ex2(x.x), ex2(x.y));
-          lsum4[e] = __fadd2_rn(lsum4[e], pv);
-          pk[e] = pack_bf16x2(pv.x, pv.y);
-        }
-        if (PT) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pt[(ch & 3) * 4 + e] = pk[e];
+          for (int e = 0; e < 4; ++e) {
+            const float2 x =
+                __ffma2_rn(make_float2(s[ch * 8 + 2 * e], s[ch * 8 + 2 * e + 1]), sl2v, negm);
+            const float2 pv = (E && e >= 4 - EMU) ? ex2_fma2(x) : make_float2(ex2(x.x), ex2(x.y));
+            lsum4[e] = __fadd2_rn(lsum4[e], pv);
+            pt[(ch & 3) * 4 + e] = pack_bf16x2(pv.x, pv.y);
+          }
           if ((ch & 3) == 3) tmem_st_32x32b_x16(lane_base + s_col + (ch >> 2) * 16, pt);
-        } else {
-          const int sub = ch >> 3, c8 = ch & 7;
-          *reinterpret_cast<uint4*>(p_row + sub * SUB + ((c8 ^ (r & 7)) << 4)) =
-              make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          if ((ch & 7) == 7) {  // one half of P (64 keys) is in TMEM: release it to PV
+            tmem_st_wait_all();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_half[2 * w + (ch >> 3)]);
+          }
         }
-      }
+      };
+      if (diag) exp_pass.template operator()<false>();
+      else exp_pass.template operator()<true>();
       const float2 ls = __fadd2_rn(__fadd2_rn(lsum4[0], lsum4[1]), __fadd2_rn(lsum4[2], lsum4[3]));
-      const float lsum = ls.x + ls.y;
-      l += lsum;
-      if (PT) tmem_st_wait_all();
-      else fence_proxy_async();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[w]);
+      l += ls.x + ls.y;
     }
     // epilogue: O / l -> bf16, LSE
     mbar_wait(&o_done[w], (ntiles - 1) & 1);
@@ -620,8 +646,8 @@ int fwd_tc(const void* q, long long ldq, const void* k, long long ldk, const voi
       !map_tile(&mv, v, T, (long long)nk * HD, ldv))
     return RP_E_CUDA;
   if ((nq / nk) % 2 == 0) {  // two heads of one KV group per CTA
-    auto kern = attn_fwd_pp_kernel<HD, true>;
-    const int bytes = PpSmem<HD, true>::BYTES;
+    auto kern = attn_fwd_pp_kernel<HD, 1>;
+    const int bytes = PpSmem<HD>::BYTES;
     if (!ensure_smem_t(kern, bytes)) return RP_E_CUDA;
     dim3 grid(nq / 2, T / TILE);
     kern<<<grid, PP_THREADS, bytes, s>>>(mq, mk, mv, (bf16*)o, ldo, lse, T, seq, nq, nk, scale);

@@ -41,7 +41,11 @@ Workspace* stream_workspace(cudaStream_t s, int tag, std::size_t bytes) {
     if (w.p) cudaFree(w.p);
     w = Workspace{};
     void* p = nullptr;
-    if (cudaMalloc(&p, bytes) != cudaSuccess || cudaMemset(p, 0, bytes) != cudaSuccess) {
+    // zeroed ON s: the callers' streams are non-blocking, so a plain
+    // cudaMemset (legacy stream) could land after s's next kernel had already
+    // written the buffer (seen as a once-per-stream corruption of the
+    // attention backward's -lse*log2e block)
+    if (cudaMalloc(&p, bytes) != cudaSuccess || cudaMemsetAsync(p, 0, bytes, s) != cudaSuccess) {
       if (p) cudaFree(p);
       cudaGetLastError();
       return nullptr;
