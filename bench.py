@@ -46,11 +46,22 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-MODEL_DIMS = {  # executed FLOPs per token per decoder layer / head (fwd); see DESIGN.md
-    "qwen3-8b": dict(h=4096, nq=32, nk=8, hd=128, m=12288, L=36, V=151936),
-    "qwen3-1.7b": dict(h=2048, nq=16, nk=8, hd=128, m=6144, L=28, V=151936),
-    "tiny": dict(h=256, nq=4, nk=2, hd=64, m=768, L=4, V=32768),
-}
+def model_dims(model):
+    """Shape of a model config (configs/models/<model>.json)."""
+    with open(os.path.join(ROOT, "configs", "models", f"{model}.json")) as f:
+        c = json.load(f)
+    return dict(h=c["hidden_dim"], nq=c["num_heads"], nk=c["num_kv_heads"], hd=c["head_dim"],
+                m=c["intermediate_dim"], L=c["num_layers"], V=c["vocab_size"],
+                E=c.get("total_experts", 1), k=c.get("active_experts", 1))
+
+
+class _Dims(dict):
+    def __missing__(self, model):
+        self[model] = model_dims(model)
+        return self[model]
+
+
+MODEL_DIMS = _Dims()  # executed FLOPs per token per decoder layer / head (fwd); see DESIGN.md
 # pinned host<->device copy rates measured on this pool's B200 boxes, CUDA-event
 # timed (tools/transfer_probe.py -> profiles/r02_transfer_probe.json): one
 # direction alone, and both at once (total)
@@ -86,16 +97,22 @@ def ncu_gemm_traffic():
 
 def step_flops(d, seq, tokens, recompute_layers, lora_rank=0):
     """Executed FLOPs of one step: 3x fwd per layer (+1 fwd for recomputed
-    layers), causal attention, head fwd+dgrad+wgrad. LoRA: no base wgrad
-    (frozen), plus the rank-r adapter GEMMs (2 fwd + 4 bwd per linear)."""
+    layers), causal attention, head fwd+dgrad+wgrad. MoE layers: router +
+    k of E experts per token. LoRA: no base wgrad (frozen), plus the rank-r
+    adapter GEMMs (2 fwd + 4 bwd per adapted linear: the four linears of a
+    dense layer, the attention projections of an MoE layer)."""
     qkvd = (d["nq"] + 2 * d["nk"]) * d["hd"]
-    lin = 2 * tokens * (d["h"] * qkvd + d["nq"] * d["hd"] * d["h"] + 3 * d["h"] * d["m"])
+    moe = d.get("E", 1) > 1
+    mlp = d["k"] * 3 * d["h"] * d["m"] + d["h"] * d["E"] if moe else 3 * d["h"] * d["m"]
+    lin = 2 * tokens * (d["h"] * qkvd + d["nq"] * d["hd"] * d["h"] + mlp)
     attn = 2 * d["nq"] * d["hd"] * tokens * seq  # causal fwd (QK^T + PV)
     layer_fwd = lin + attn
     head = 2 * tokens * d["h"] * d["V"]
     if lora_rank:
-        io = (d["h"] + qkvd) + (d["nq"] * d["hd"] + d["h"]) + (d["h"] + 2 * d["m"]) + (d["m"] + d["h"])
-        adapters = 2 * tokens * lora_rank * io  # one pass of X A^T + U B^T over the 4 linears
+        io = (d["h"] + qkvd) + (d["nq"] * d["hd"] + d["h"])
+        if not moe:
+            io += (d["h"] + 2 * d["m"]) + (d["m"] + d["h"])
+        adapters = 2 * tokens * lora_rank * io  # one pass of X A^T + U B^T over the adapted linears
         per_layer = 2 * lin + 3.5 * attn + 3 * adapters
         return d["L"] * per_layer + recompute_layers * (layer_fwd + adapters) + 2 * head
     return d["L"] * 3 * layer_fwd + recompute_layers * layer_fwd + 3 * head
@@ -290,7 +307,20 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------- GPU side
-MODEL_NAMES = {"qwen3-8b": "Qwen3-8B", "qwen3-1.7b": "Qwen3-1.7B", "tiny": "tiny Qwen3"}
+MODEL_NAMES = {"qwen3-8b": "Qwen3-8B", "qwen3-1.7b": "Qwen3-1.7B", "tiny": "tiny Qwen3",
+               "qwen3-235b-a22b-l8": "Qwen3-235B-A22B (8 of 94 layers)",
+               "qwen3-235b-a22b-l6": "Qwen3-235B-A22B (6 of 94 layers)"}
+
+
+def baseline_config(args):
+    """Which BASELINE.json config the run measures."""
+    if args.model.startswith("qwen3-235b-a22b"):
+        return "BASELINE configs[4] at reduced depth: MoE LoRA, weights streamed from pinned host"
+    if args.model == "qwen3-1.7b":
+        return "BASELINE configs[1]"
+    if args.model == "qwen3-8b" and not args.lora_rank:
+        return "BASELINE configs[2]"
+    return "not a BASELINE config"
 
 
 def metric_name(args):
@@ -302,7 +332,8 @@ def metric_name(args):
 def weight_gb(model):
     d = MODEL_DIMS[model]
     qkvd = (d["nq"] + 2 * d["nk"]) * d["hd"]
-    layer = d["h"] * qkvd + d["nq"] * d["hd"] * d["h"] + 3 * d["h"] * d["m"]
+    mlp = 3 * d["h"] * d["m"] * d.get("E", 1) + (d["h"] * d["E"] if d.get("E", 1) > 1 else 0)
+    layer = d["h"] * qkvd + d["nq"] * d["hd"] * d["h"] + mlp
     return 2 * (d["L"] * layer + 2 * d["V"] * d["h"]) / 1e9
 
 
@@ -315,7 +346,7 @@ def config_dict(args, resident=None, mode=None):
                          f"{'K' if args.seq >= 1024 else ''} with "
                          + ("fp32 AdamW states HBM-resident for the groups that fit (rest "
                             "host-offloaded)" if resident else "host-offloaded Adam states")
-                         + " and activation recompute (BASELINE configs[2]): b=1, "
+                         + f" and activation recompute ({baseline_config(args)}): b=1, "
                          f"M={args.micro_batches} micro-batches/step, "
                          f"RoundPipe-{'async' if mode == 'async' else 'sync'}, N={args.gpus}"),
             "model": args.model, "global_batch": args.micro_batches, "seq_len": args.seq,

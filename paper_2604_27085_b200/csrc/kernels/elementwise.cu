@@ -209,10 +209,17 @@ __global__ void __launch_bounds__(RN_THREADS)
 // A head of HD elements is handled by TPH = HD/8 consecutive lanes, 8
 // elements (16 bytes) each; the per-head RMS reduces over those lanes and the
 // rotate_half partner (element e +- HD/2) lives in lane ^ TPH/2. A 128-thread
-// block covers 128/TPH heads of one token at a time and walks heads then
-// tokens (grid-stride); a thread's (cos, sin) pairs depend only on its lane
-// slot and the token, so they are loaded once per token.
+// block covers HPB = 128/TPH heads of one token per pass and walks passes
+// then tokens (grid-stride over one wave of resident blocks); a thread's
+// (cos, sin) pairs depend only on its lane slot and the token, so they are
+// loaded once per token. The loads of QK_NB passes are issued together
+// before any of them is used (occupancy is register-limited to 5-8 blocks of
+// 128 threads per SM, profiles/r02g_ncu_full.json): backward 52.2 -> 48.1 us,
+// forward unchanged at 25.6 us (profiles/r02h_qk_ab.jsonl) — its remaining
+// limit is the serial per-token chain (2 load rounds per token for 40 heads,
+// ~5.5 tokens per block), not the loads in flight of one round.
 constexpr int QK_THREADS = 128;
+constexpr int QK_NB = 4;
 
 template <int HD>
 __global__ void __launch_bounds__(QK_THREADS)
@@ -236,40 +243,50 @@ __global__ void __launch_bounds__(QK_THREADS)
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[i] = c4[i];
     const __nv_bfloat16* row = qkv + (long long)t * ld;
-    // every lane runs every pass (the shuffles below are warp-wide); lanes
-    // whose head is past the end compute on zeros and store nothing
-    for (int base = 0; base < heads; base += HPB) {
-      const int hh = base + hl;
-      const bool act = hh < heads;
-      const bool is_q = hh < nq;
-      float v[8];
-      if (act) load8(row + hh * HD + sub * 8, v);
-      else for (int i = 0; i < 8; ++i) v[i] = 0.f;
-      float ss = 0.f;
+    for (int base0 = 0; base0 < heads; base0 += QK_NB * HPB) {
+      uint4 raw[QK_NB];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
-#pragma unroll
-      for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      const float r = rsqrtf(ss / HD + eps);
-      float n[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf((is_q ? wq[i] : wk[i]) * (v[i] * r)));
-      float out[8];
-#pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        const float4 cc = c[i / 2];  // (cos, sin) of elements i, i+1
-        const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
-        const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
-        out[i] = lo ? n[i] * cc.x - p0 * cc.y : n[i] * cc.x + p0 * cc.y;
-        out[i + 1] = lo ? n[i + 1] * cc.z - p1 * cc.w : n[i + 1] * cc.z + p1 * cc.w;
+      for (int b = 0; b < QK_NB; ++b) {
+        const int hh = base0 + b * HPB + hl;
+        raw[b] = hh < heads ? *reinterpret_cast<const uint4*>(row + hh * HD + sub * 8)
+                            : make_uint4(0, 0, 0, 0);
       }
-      if (!act) continue;
-      __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD
-                                : ko + ((long long)t * nk + (hh - nq)) * HD;
-      store8(dst + sub * 8, out);
-      if (sub == 0) {
-        if (is_q) rstd_q[(long long)t * nq + hh] = r;
-        else rstd_k[(long long)t * nk + (hh - nq)] = r;
+      // every lane runs every pass (the shuffles below are warp-wide); lanes
+      // whose head is past the end compute on zeros and store nothing
+#pragma unroll
+      for (int b = 0; b < QK_NB; ++b) {
+        if (base0 + b * HPB >= heads) break;  // block-uniform
+        const int hh = base0 + b * HPB + hl;
+        const bool act = hh < heads;
+        const bool is_q = hh < nq;
+        float v[8];
+        unpack8(raw[b], v);
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
+#pragma unroll
+        for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        const float r = rsqrtf(ss / HD + eps);
+        float n[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf((is_q ? wq[i] : wk[i]) * (v[i] * r)));
+        float out[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float4 cc = c[i / 2];  // (cos, sin) of elements i, i+1
+          const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
+          const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
+          out[i] = lo ? n[i] * cc.x - p0 * cc.y : n[i] * cc.x + p0 * cc.y;
+          out[i + 1] = lo ? n[i + 1] * cc.z - p1 * cc.w : n[i + 1] * cc.z + p1 * cc.w;
+        }
+        if (!act) continue;
+        __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD
+                                  : ko + ((long long)t * nk + (hh - nq)) * HD;
+        store8(dst + sub * 8, out);
+        if (sub == 0) {
+          if (is_q) rstd_q[(long long)t * nq + hh] = r;
+          else rstd_k[(long long)t * nk + (hh - nq)] = r;
+        }
       }
     }
   }
@@ -277,7 +294,8 @@ __global__ void __launch_bounds__(QK_THREADS)
 
 // Backward: undo the rotation (R^T), then per-head RMSNorm backward;
 // dqkv[:, q/k slots] = dx; dqw/dkw[HD] += sum(dn * xhat) (registers -> smem
-// -> one atomic per column per block).
+// -> one atomic per column per block). Loads batched over QK_NB passes as in
+// the forward.
 template <int HD>
 __global__ void __launch_bounds__(QK_THREADS)
     qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
@@ -305,43 +323,58 @@ __global__ void __launch_bounds__(QK_THREADS)
     float4 c[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) c[i] = c4[i];
-    for (int base = 0; base < heads; base += HPB) {  // warp-uniform passes (shuffles)
-      const int hh = base + hl;
-      const bool act = hh < heads;
-      const bool is_q = hh < nq;
-      float r = 0.f, gv[8], xv[8];
-      if (act) {
-        r = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
-        load8((is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) +
-                  sub * 8, gv);
-        load8(qkv + (long long)t * ld + hh * HD + sub * 8, xv);
-      } else {
-        for (int i = 0; i < 8; ++i) gv[i] = xv[i] = 0.f;
-      }
-      float dn[8];
+    for (int base0 = 0; base0 < heads; base0 += QK_NB * HPB) {  // warp-uniform passes (shuffles)
+      uint4 graw[QK_NB], xraw[QK_NB];
+      float rr[QK_NB];
 #pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        const float4 cc = c[i / 2];
-        const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
-        const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
-        dn[i] = lo ? gv[i] * cc.x + p0 * cc.y : gv[i] * cc.x - p0 * cc.y;
-        dn[i + 1] = lo ? gv[i + 1] * cc.z + p1 * cc.w : gv[i + 1] * cc.z - p1 * cc.w;
-      }
-      float dot = 0.f, gx[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        xv[i] *= r;  // xhat
-        gx[i] = dn[i] * (is_q ? wq[i] : wk[i]);
-        dot += gx[i] * xv[i];
-        if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
+      for (int b = 0; b < QK_NB; ++b) {
+        const int hh = base0 + b * HPB + hl;
+        graw[b] = xraw[b] = make_uint4(0, 0, 0, 0);
+        rr[b] = 0.f;
+        if (hh < heads) {
+          const bool is_q = hh < nq;
+          rr[b] = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
+          graw[b] = *reinterpret_cast<const uint4*>(
+              (is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) +
+              sub * 8);
+          xraw[b] = *reinterpret_cast<const uint4*>(qkv + (long long)t * ld + hh * HD + sub * 8);
+        }
       }
 #pragma unroll
-      for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      const float mean = dot / HD;
-      float out[8];
+      for (int b = 0; b < QK_NB; ++b) {
+        if (base0 + b * HPB >= heads) break;  // block-uniform
+        const int hh = base0 + b * HPB + hl;
+        const bool act = hh < heads;
+        const bool is_q = hh < nq;
+        const float r = rr[b];
+        float gv[8], xv[8];
+        unpack8(graw[b], gv);
+        unpack8(xraw[b], xv);
+        float dn[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
-      if (act) store8(dqkv + (long long)t * ldd + hh * HD + sub * 8, out);
+        for (int i = 0; i < 8; i += 2) {
+          const float4 cc = c[i / 2];
+          const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
+          const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
+          dn[i] = lo ? gv[i] * cc.x + p0 * cc.y : gv[i] * cc.x - p0 * cc.y;
+          dn[i + 1] = lo ? gv[i + 1] * cc.z + p1 * cc.w : gv[i + 1] * cc.z - p1 * cc.w;
+        }
+        float dot = 0.f, gx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          xv[i] *= r;  // xhat
+          gx[i] = dn[i] * (is_q ? wq[i] : wk[i]);
+          dot += gx[i] * xv[i];
+          if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
+        }
+#pragma unroll
+        for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const float mean = dot / HD;
+        float out[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
+        if (act) store8(dqkv + (long long)t * ldd + hh * HD + sub * 8, out);
+      }
     }
   }
 #pragma unroll
@@ -572,6 +605,23 @@ int grid_for(long long work, int threads, int max_blocks = 148 * 8) {
 
 int status() { return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA; }
 
+// one wave of resident QK_THREADS blocks (occupancy per device, cached), at
+// most one block per token
+template <auto Kern>
+int wave_grid(int T) {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& g = cached[dev & 63];
+  if (!g) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, Kern, QK_THREADS, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
+  }
+  return T < g ? T : g;
+}
+
 }  // namespace
 }  // namespace rp
 
@@ -649,15 +699,14 @@ RP_API int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t 
                                float* rstd_q, float* rstd_k, int32_t T, float eps,
                                void* stream) {
   if (ld % 8 || T % 128 || T <= 0) return RP_E_INPUT;
-  const int grid = T < 148 * 16 ? T : 148 * 16;
   auto s = (cudaStream_t)stream;
   if (head_dim == 128)
-    qk_norm_rope_fwd_kernel<128><<<grid, QK_THREADS, 0, s>>>(
+    qk_norm_rope_fwd_kernel<128><<<wave_grid<qk_norm_rope_fwd_kernel<128>>(T), QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
   else if (head_dim == 64)
-    qk_norm_rope_fwd_kernel<64><<<grid, QK_THREADS, 0, s>>>(
+    qk_norm_rope_fwd_kernel<64><<<wave_grid<qk_norm_rope_fwd_kernel<64>>(T), QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
         (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
         T, eps);
@@ -673,14 +722,13 @@ RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, 
                                float* dqw, float* dkw, int32_t T, void* stream) {
   if (ld % 8 || ldd % 8 || T % 128 || T <= 0) return RP_E_INPUT;
   auto s = (cudaStream_t)stream;
-  const int grid = T < 148 * 8 ? T : 148 * 8;
   if (head_dim == 128)
-    qk_norm_rope_bwd_kernel<128><<<grid, QK_THREADS, 0, s>>>(
+    qk_norm_rope_bwd_kernel<128><<<wave_grid<qk_norm_rope_bwd_kernel<128>>(T), QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
   else if (head_dim == 64)
-    qk_norm_rope_bwd_kernel<64><<<grid, QK_THREADS, 0, s>>>(
+    qk_norm_rope_bwd_kernel<64><<<wave_grid<qk_norm_rope_bwd_kernel<64>>(T), QK_THREADS, 0, s>>>(
         (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
         (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
         seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);

@@ -186,7 +186,7 @@ def _attn_ref(q, k, v, seq, nq, nk, hd):
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
                                             (2048, 1024, 16, 4, 128), (768, 256, 6, 2, 128),
-                                            (1024, 1024, 16, 2, 128)])
+                                            (1024, 1024, 16, 2, 128), (2048, 2048, 32, 2, 128)])
 def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K
     qkv = rnd(T, (nq + 2 * nk) * hd, seed=30, scale=2.0)
@@ -205,7 +205,7 @@ def test_flash_attention_fwd_tcgen05(T, seq, nq, nk, hd):
 @pytest.mark.parametrize("T,seq,nq,nk,hd", [(256, 256, 4, 2, 64), (1024, 512, 8, 2, 128),
                                             (4096, 4096, 32, 8, 128), (512, 128, 4, 4, 64),
                                             (2048, 1024, 16, 4, 128), (768, 256, 6, 2, 128),
-                                            (1024, 1024, 16, 2, 128)])
+                                            (1024, 1024, 16, 2, 128), (2048, 2048, 32, 2, 128)])
 def test_flash_attention_bwd_tcgen05(T, seq, nq, nk, hd):
     from paper_2604_27085_b200 import kernels as K
     qkv = rnd(T, (nq + 2 * nk) * hd, seed=40, scale=1.5)
