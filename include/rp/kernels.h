@@ -26,6 +26,9 @@ typedef struct {
   const void* R; int64_t ldr;
 } rp_gemm_args_t;
 int rp_gemm_bf16(const rp_gemm_args_t* args, void* stream);
+/* Why the last rp_gemm_* call of this thread failed ("" after a success):
+ * the precondition, tensor-map encode or launch step that refused it. */
+const char* rp_gemm_last_error(void);
 /* D = A . B^T + A2 . B2^T (+ R / accumulate as in rp_gemm_bf16): a second K
  * segment of K2 columns with the same majors as A and B (A2 [M,K2] or [K2,M],
  * B2 [N,K2] or [K2,N]). Used for LoRA: X W^T + U B^T and dY W + dU A in one

@@ -979,6 +979,14 @@ SplitWs split_ws(cudaStream_t st, std::size_t elems, std::size_t flags) {
 // B200: half-size MMAs double the per-k-block pipeline overhead).
 constexpr int PBN = 256;
 
+// why the last rp_gemm_* call on this thread failed (rp_gemm_last_error)
+thread_local const char* g_gemm_why = "";
+inline cudaError_t launch_status(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) g_gemm_why = what;
+  return e;
+}
+
 template <int A_MN, int B_MN, int EPI>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                    const EpiMaps& em, const Params& p, bool pair, int n_fastest,
@@ -986,7 +994,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   if (pair) {
     auto kern = gemm_pair_kernel<A_MN, B_MN, EPI, PBN>;
     const int smem = PairCfg<PBN, EPI>::SMEM;
-    if (!ensure_smem_t(kern, smem)) return cudaErrorInvalidValue;
+    if (!ensure_smem_t(kern, smem)) return g_gemm_why = "pair kernel: shared-memory attribute", cudaErrorInvalidValue;
     const int pbn = PBN;
     const int tn = EPI == EPI_SWIGLU_FWD ? pbn / 2 : pbn;  // output columns per tile
     const int tiles = ((p.M + 255) / 256) * ((p.N + tn - 1) / tn);
@@ -1018,18 +1026,18 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
     }
     const int pairs = q.units < npairs ? q.units : npairs;
     kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, em, q, n_fastest);
-    return cudaGetLastError();
+    return launch_status("pair kernel launch");
   }
   const bool skinny = p.N <= 32;
   auto kern = skinny ? gemm_kernel<A_MN, B_MN, EPI, 32> : gemm_kernel<A_MN, B_MN, EPI, 256>;
   const int smem = skinny ? SingleCfg<32, B_MN>::SMEM : SingleCfg<256, B_MN>::SMEM;
-  if (!ensure_smem_t(kern, smem)) return cudaErrorInvalidValue;
+  if (!ensure_smem_t(kern, smem)) return g_gemm_why = "single kernel: shared-memory attribute", cudaErrorInvalidValue;
   const int tbn = skinny ? 32 : BN;
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
   if (p.g_off) tiles += p.g_num * ((p.N + tbn - 1) / tbn);  // ragged last m-tile per group (bound)
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, NUM_THREADS, smem, stream>>>(ta, tb, p);
-  return cudaGetLastError();
+  return launch_status("single kernel launch");
 }
 
 template <int A_MN, int B_MN>
@@ -1041,16 +1049,16 @@ cudaError_t dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
     case EPI_F32: return launch<A_MN, B_MN, EPI_F32>(ta, tb, td, em, p, pair, n_fastest, s);
     case EPI_SWIGLU_FWD:  // pair kernel, gate/up forward layout only
       if constexpr (A_MN == 0 && B_MN == 0) {
-        if (!pair) return cudaErrorInvalidValue;
+        if (!pair) return g_gemm_why = "SwiGLU forward epilogue needs pair tiles", cudaErrorInvalidValue;
         return launch<A_MN, B_MN, EPI_SWIGLU_FWD>(ta, tb, td, em, p, pair, n_fastest, s);
       } else {
-        return cudaErrorInvalidValue;
+        return g_gemm_why = "SwiGLU forward epilogue: K-major operands only", cudaErrorInvalidValue;
       }
     case EPI_SWIGLU_BWD:  // only the down-projection dgrad layout is instantiated
       if constexpr (A_MN == 0 && B_MN == 1)
         return launch<A_MN, B_MN, EPI_SWIGLU_BWD>(ta, tb, td, em, p, pair, n_fastest, s);
       else
-        return cudaErrorInvalidValue;
+        return g_gemm_why = "SwiGLU backward epilogue: A K-major, B MN-major only", cudaErrorInvalidValue;
     default: return launch<A_MN, B_MN, EPI_F32_ACC>(ta, tb, td, em, p, pair, n_fastest, s);
   }
 }
@@ -1091,7 +1099,9 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
     g = &sw;
     trans = true;
   }
-  if (!g || g->M <= 0 || g->N <= 0 || g->K <= 0 || !g->A || !g->B || !g->D) return RP_E_INPUT;
+  g_gemm_why = "";
+  if (!g || g->M <= 0 || g->N <= 0 || g->K <= 0 || !g->A || !g->B || !g->D)
+    return g_gemm_why = "bad shape or null operand", RP_E_INPUT;
   if ((g->lda * 2) % 16 || (g->ldb * 2) % 16 || (reinterpret_cast<uintptr_t>(g->A) & 15) ||
       (reinterpret_cast<uintptr_t>(g->B) & 15))
     return RP_E_INPUT;
@@ -1109,7 +1119,7 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                                             : g->N <= 32 ? 32 : BN));  // = launch()'s tile
   // raster: keep the larger operand's tile hot (walk the other dimension fastest)
   const int n_fastest = (double)g->M > (double)g->N ? 1 : 0;
-  if (!ok) return RP_E_CUDA;
+  if (!ok) return g_gemm_why = "A/B tensor map encode", RP_E_CUDA;
   const int esz = g->out_f32 ? 4 : 2;
   const bool vec = (g->ldd * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                    (!g->R || ((g->ldr * 2) % 16 == 0 && (reinterpret_cast<uintptr_t>(g->R) & 15) == 0)) &&
@@ -1118,7 +1128,10 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
   // fp32 outputs of the pair kernel go through a TMA map (store / L2 reduce-add)
   CUtensorMap td;
   std::memset(&td, 0, sizeof(td));
-  const bool tma_out = pair && g->out_f32 && (g->ldd * 4) % 16 == 0 &&
+  // (not for a swapped skinny GEMM: its D is stored transposed, element by
+  // element in epi_chunk — a TMA map over the swapped shape would write rows
+  // of the untransposed layout past the end of D)
+  const bool tma_out = pair && !trans && g->out_f32 && (g->ldd * 4) % 16 == 0 &&
                        (reinterpret_cast<uintptr_t>(g->D) & 15) == 0 &&
                        make_map_f32(&td, g->D, g->M, g->N, g->ldd);
   EpiMaps em;
@@ -1132,7 +1145,7 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
                           make_map_sw64(&em.du, D16 + g->N, g->M, g->N, g->ldd);
   if (pair && !g->b_mn_major && !dual &&
       !make_map(&em.bh, g->B, g->N, g->K, g->ldb, 64, PBN / 4))
-    return RP_E_CUDA;
+    return g_gemm_why = "N-half B tensor map encode", RP_E_CUDA;
   if (s2.K2 > 0) {  // second K segment: same majors and boxes as A / B
     if (!pair) return RP_E_INPUT;
     const bool ok2 =
@@ -1141,7 +1154,7 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
         (g->b_mn_major ? make_map(&em.b2, s2.B2, s2.K2, g->N, s2.ldb2, 64, 64)
                        : make_map(&em.b2, s2.B2, dual ? 2LL * g->N : g->N, s2.K2, s2.ldb2, 64,
                                   PBN / 2));
-    if (!ok2) return RP_E_CUDA;
+    if (!ok2) return g_gemm_why = "second-segment tensor map encode", RP_E_CUDA;
   }
   Params p{g->M, g->N, g->K, g->D, g->ldd, R16, g->ldr, vec ? 1 : 0, tma_out ? 1 : 0,
            tma_swiglu ? 1 : 0, trans ? 1 : 0, 0, 0,
@@ -1158,6 +1171,10 @@ static int gemm_entry(const rp_gemm_args_t* g, void* stream, int mode, void* act
     e = g->b_mn_major ? dispatch_epi<0, 1>(epi, ta, tb, td, em, p, pair, n_fastest, s)
                       : dispatch_epi<0, 0>(epi, ta, tb, td, em, p, pair, n_fastest, s);
   return e == cudaSuccess ? RP_OK : RP_E_CUDA;
+}
+
+extern "C" __attribute__((visibility("default"))) const char* rp_gemm_last_error(void) {
+  return rp::g_gemm_why;
 }
 
 extern "C" __attribute__((visibility("default"))) int rp_gemm_bf16(const rp_gemm_args_t* g,

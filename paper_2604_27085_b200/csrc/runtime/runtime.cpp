@@ -567,7 +567,16 @@ void Runtime::gemm(cudaStream_t st, const void* A, int64_t lda, bool a_mn, const
   a.R = Rz;
   a.ldr = ldr;
   const int pi = prof_begin(st);
-  RP_K(swiglu_bwd ? rp_gemm_swiglu_bwd(&a, st) : rp_gemm_bf16(&a, st));
+  const int rc = swiglu_bwd ? rp_gemm_swiglu_bwd(&a, st) : rp_gemm_bf16(&a, st);
+  if (rc != RP_OK)
+    throw RtError(rc, "gemm failed: M " + std::to_string(M_) + " N " + std::to_string(N_) + " K " +
+                          std::to_string(K_) + " lda " + std::to_string(lda) + " ldb " +
+                          std::to_string(ldb) + " ldd " + std::to_string(ldd) + " a_mn " +
+                          std::to_string(a_mn) + " b_mn " + std::to_string(b_mn) + " f32 " +
+                          std::to_string(f32) + " acc " + std::to_string(acc) + " R " +
+                          std::to_string(Rz != nullptr) + " swiglu_bwd " +
+                          std::to_string(swiglu_bwd) + " -> " + rp_gemm_last_error() + " / " +
+                          cudaGetErrorString(cudaGetLastError()));
   prof_end(pi, st, 0, 2.0 * M_ * N_ * (double)K_);
   ++kernels;
 }

@@ -64,7 +64,12 @@ def gemm(A: torch.Tensor, B: torch.Tensor, D: torch.Tensor, *, a_mn_major=False,
                     _ptr(residual), residual.stride(0) if residual is not None else 0)
     f = _lib().rp_gemm_bf16
     f.restype = C.c_int
-    _check(f(C.byref(args), _stream(stream)))
+    rc = f(C.byref(args), _stream(stream))
+    if rc:
+        why = _lib().rp_gemm_last_error
+        why.restype = C.c_char_p
+        raise _native._ERRORS.get(rc, _native.NativeError)(
+            rc, f"rp_gemm_bf16 M={M} N={N} K={K}: {why().decode()}")
     return D
 
 

@@ -64,6 +64,31 @@ def test_gemm_f32_and_accumulate(M, N, K, a_mn, b_mn):
     assert _rel(D, 2 * ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [
+    # LoRA adapter gradients at long sequences (K = tokens > 8192): dA = dU^T X
+    # (M = rank <= 32: swapped roles, transposed fp32 store through the pair
+    # kernel) and dB = dY^T U (N = rank) — the shapes of the C5 MoE LoRA run
+    (32, 4096, 16384, 1, 1), (32, 9216, 16384, 1, 1), (9216, 32, 16384, 1, 1),
+    (4096, 32, 31744, 1, 1), (32, 4096, 4096, 1, 1)])
+def test_gemm_long_k_skinny_f32_accumulate(M, N, K, a_mn, b_mn):
+    from paper_2604_27085_b200 import kernels
+    A, B = _mk(M, K, 5), _mk(N, K, 6)
+    Aop = A.t().contiguous() if a_mn else A
+    Bop = B.t().contiguous() if b_mn else B
+    pad = torch.full((1 << 20,), 7.0, device="cuda")  # guard: nothing past D may change
+    D = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    guard = torch.full((1 << 20,), 7.0, device="cuda")
+    kernels.gemm(Aop, Bop, D, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn))
+    ref = A.float() @ B.float().t()
+    torch.cuda.synchronize()
+    tol = 1e-5 * max(1.0, K / 8192)  # fp32 summation-order error grows with K
+    assert _rel(D, ref) < tol
+    kernels.gemm(Aop, Bop, D, a_mn_major=bool(a_mn), b_mn_major=bool(b_mn), accumulate=True)
+    torch.cuda.synchronize()
+    assert _rel(D, 2 * ref) < tol
+    assert bool((pad == 7.0).all()) and bool((guard == 7.0).all())
+
+
 def test_gemm_residual_epilogue():
     from paper_2604_27085_b200 import kernels
     M, N, K = 512, 768, 256
