@@ -517,8 +517,9 @@ def run_ours(args):
         # the runtime's device allocations by category (all workers), GB
         "hbm_gb": {k: round(v / 1e9, 2) for k, v in zip(
             ("weights_2_versions", "grads", "pending_adamw_out", "activations",
-             "scratch", "resident_optimizer_state", "optimizer_chunk_ring"),
-            st1["device_bytes"][:7])},
+             "scratch", "checkpoints_handoffs", "optimizer_chunk_ring",
+             "resident_optimizer_state"),
+            st1["device_bytes"][:8])},
     }
     if not args.no_variants:
         variants = {}

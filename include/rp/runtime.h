@@ -87,6 +87,10 @@ typedef struct {
   int32_t num_slots;           /* S of the plan */
   int64_t params_total;
   int64_t host_bytes_pinned;
+  /* device allocations by category, all workers: 0 weights (bf16, both
+   * versions), 1 fp32 grads, 2 pending AdamW output, 3 activations, 4
+   * scratch, 5 checkpoints + hand-offs, 6 optimizer chunk ring, 7
+   * HBM-resident fp32 AdamW state; pooled slabs count under their use */
   int64_t device_bytes[8];
   int64_t h2d_bytes, d2h_bytes, p2p_bytes; /* cumulative */
   int32_t iterations_done;

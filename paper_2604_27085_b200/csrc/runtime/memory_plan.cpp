@@ -119,7 +119,7 @@ PoolPeak pooled_peak(const Shape& s, const LayerLayout& LL, const HeadLayout& HL
   };
   for (int t = 0; t < iters; ++t) {
     if (async) {
-      for (auto& [wg, w] : pend_owner) add(w, 2, -n_of(wg.second) * 2);  // p_copy
+      for (auto& [wg, w] : pend_owner) add(w, 2, -tn_of(wg.second) * 2);  // p_copy
       pend_owner.clear();
       reserve(t + 1);  // LPT-windowed uploads of the next iteration
     }
@@ -167,12 +167,12 @@ PoolPeak pooled_peak(const Shape& s, const LayerLayout& LL, const HeadLayout& HL
         continue;
       }
       const int g = it->first.first, w = it->second;
-      add(w, 2, n_of(g) * 2);
+      add(w, 2, tn_of(g) * 2);  // AdamW output: the trainable region
       add(w, 1, -tn_of(g) * 4);
       if (async)
         pend_owner[{w, g}] = w;
       else
-        add(w, 2, -n_of(g) * 2);  // sync: p_copy at once
+        add(w, 2, -tn_of(g) * 2);  // sync: p_copy at once
       it = grad_owner.erase(it);
     }
     if (!async) reserve(t + 1);  // sync prefetch after the step
@@ -316,7 +316,7 @@ RP_API int rp_memory_plan(const rp_runtime_config_t* cfg, int64_t hbm_bytes,
     for (int g = 0; g < s.L + 2; ++g) {
       const int64_t n = g == 0 ? (int64_t)s.V * s.h : g == s.L + 1 ? HL.total : LL.total;
       const int64_t tn = cfg->lora_rank ? (g >= 1 && g <= s.L ? LL.total - LL.lora_off : 0) : n;
-      groups += n * 2 * 3 + tn * 4 * 2;
+      groups += n * 2 * 2 + tn * 2 + tn * 4 * 2;  // 2 weight versions, AdamW output, 2 grads
     }
     const int lck = std::max(0, pc.plan.fused_stage.first);
     if (pc.slots.size() > 1) groups += (int64_t)(N > 1 ? 2 : 1) * lck * MR * T * s.h * 2;

@@ -743,9 +743,9 @@ void Runtime::place_resident_state() {
       D.grad[1] = D.grad[0];
       G.allocated[1] -= (std::size_t)n * 4;
       if (direct) {
-        dfree(G, D.pend);
+        dfree(G, D.pend + host[g].t_off);
         D.pend = nullptr;
-        G.allocated[2] -= (std::size_t)host[g].n * 2;
+        G.allocated[2] -= (std::size_t)host[g].tn() * 2;
       }
     }
     host[g].direct = direct;
@@ -756,7 +756,8 @@ void Runtime::place_resident_state() {
       for (Gpu& G : gpus) {  // undo: back to two buffers (and a pend buffer)
         DevGroup& D = G.groups[g];
         D.grad[1] = static_cast<float*>(dalloc(G, (std::size_t)n * 4, 1)) - o;
-        if (!D.pend) D.pend = static_cast<uint16_t*>(dalloc(G, (std::size_t)host[g].n * 2, 2));
+        if (!D.pend)
+          D.pend = static_cast<uint16_t*>(dalloc(G, (std::size_t)host[g].tn() * 2, 2)) - host[g].t_off;
       }
       host[g].direct = false;
       break;
@@ -765,7 +766,7 @@ void Runtime::place_resident_state() {
     budget -= n * 12;
     placed += n * 12;
     resident_params += n;
-    gpus[0].allocated[5] += (std::size_t)(n * 12);
+    gpus[0].allocated[7] += (std::size_t)(n * 12);
     push_resident(g);
   }
 }
@@ -877,7 +878,8 @@ void Runtime::alloc_worker(Gpu& G, int id) {
     if (!pooled) {
       D.grad[0] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
       D.grad[1] = tn > 0 ? static_cast<float*>(dalloc(tn * 4, 1)) - to : nullptr;
-      D.pend = static_cast<uint16_t*>(dalloc(n * 2, 2));
+      // AdamW output: the trainable region only (indexed from t_off like grads)
+      D.pend = static_cast<uint16_t*>(dalloc(tn * 2, 2)) - to;
     }
     D.ev_gradwrite = new_event(false);
     D.ev_adam[0] = new_event(false);
@@ -2077,8 +2079,8 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     return;
   }
   if (pooled && !D.pend) {  // AdamW output slab until p_copy publishes it
-    D.pend_slab = slab_acquire(G, (std::size_t)H.n * 2, 2, G.opt_comp);
-    D.pend = static_cast<uint16_t*>(G.slabs[D.pend_slab].p);
+    D.pend_slab = slab_acquire(G, (std::size_t)H.tn() * 2, 2, G.opt_comp);
+    D.pend = static_cast<uint16_t*>(G.slabs[D.pend_slab].p) - H.t_off;
   }
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
   cudaEvent_t xa = xfer_begin(G.opt_h2d);
@@ -2520,8 +2522,8 @@ RP_API int rp_runtime_load(rp_runtime_t* p, const char* path) {
         continue;
       }
       if (rt->pooled && !G.groups[g].pend) {
-        G.groups[g].pend_slab = rt->slab_acquire(G, (std::size_t)H.n * 2, 2, G.opt_d2h);
-        G.groups[g].pend = static_cast<uint16_t*>(G.slabs[G.groups[g].pend_slab].p);
+        G.groups[g].pend_slab = rt->slab_acquire(G, (std::size_t)H.tn() * 2, 2, G.opt_d2h);
+        G.groups[g].pend = static_cast<uint16_t*>(G.slabs[G.groups[g].pend_slab].p) - H.t_off;
       }
       RP_CUDA(cudaMemcpy(G.groups[g].pend + H.t_off, tmp.data(), H.tn() * 2,
                          cudaMemcpyHostToDevice));
