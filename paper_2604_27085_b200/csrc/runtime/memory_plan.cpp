@@ -52,7 +52,7 @@ WorkerBytes worker_fixed_bytes(const Shape& s, int T, int seq, int M, int MR, in
               2LL * 2 * M * T * 4 + (int64_t)seq * s.hd * 4 + (lora_r ? (int64_t)T * lora_r * 2 : 0) +
               moe_scratch;
   b.handoff = S > 1 ? (int64_t)parities * MR * (Th * 2 + Th * 4) : 0;
-  b.optimizer_ring = 2LL * 3 * chunk_elems * 4;
+  b.optimizer_ring = (int64_t)Gpu::kOptSlots * 3 * chunk_elems * 4;
   // per-stream kernel scratch: the fused attention backward's fp32 dQ^T
   // accumulator and split-K partials on the compute / weight-gradient streams
   b.workspace = (int64_t)T * s.qd() * 4 + 2LL * (37 * 2 * 128 * 256 * 4 + 37 * 8 * 4);
@@ -313,10 +313,13 @@ RP_API int rp_memory_plan(const rp_runtime_config_t* cfg, int64_t hbm_bytes,
     out->optimizer_ring = pc.fixed.optimizer_ring;
     out->workspace = pc.fixed.workspace;
     int64_t groups = 0;
+    // one worker publishes AdamW results into the device weights in place
+    // (Runtime::publish_in_place): no AdamW output buffer
+    const bool in_place = N == 1 && !(cfg->flags & RP_RT_HOST_PUBLISH);
     for (int g = 0; g < s.L + 2; ++g) {
       const int64_t n = g == 0 ? (int64_t)s.V * s.h : g == s.L + 1 ? HL.total : LL.total;
       const int64_t tn = cfg->lora_rank ? (g >= 1 && g <= s.L ? LL.total - LL.lora_off : 0) : n;
-      groups += n * 2 * 2 + tn * 2 + tn * 4 * 2;  // 2 weight versions, AdamW output, 2 grads
+      groups += n * 2 * 2 + (in_place ? 0 : tn * 2) + tn * 4 * 2;  // 2 weight versions, AdamW output, 2 grads
     }
     const int lck = std::max(0, pc.plan.fused_stage.first);
     if (pc.slots.size() > 1) groups += (int64_t)(N > 1 ? 2 : 1) * lck * MR * T * s.h * 2;

@@ -430,6 +430,7 @@ struct Runtime {
   void step();
   void adam_group(Gpu& G, int g, int parity);
   void place_resident_state();      // choose groups whose fp32 state lives in HBM
+  void publish_in_place();          // one worker: streamed groups publish into w[] too
   void push_resident(int g);        // host master/m/v -> device state
   void pull_resident(int g);        // device state -> host master/m/v (if stale)
   void pull_w16(int g);             // direct groups: device bf16 of the next iteration -> host
@@ -703,6 +704,32 @@ void Runtime::init(const rp_runtime_config_t& c) {
   if (!(cfg.flags & RP_RT_SKIP_INIT)) init_weights();
   sync_all();
   place_resident_state();
+  publish_in_place();
+}
+
+// One worker on one device: the streamed (host-offloaded) groups' AdamW
+// writes its bf16 result straight into the device buffer of the version that
+// will use it, as the HBM-resident groups do — the fp32 master/m/v still
+// stream through the GPU every step (BASELINE configs[2]), but the bf16
+// weights no longer round-trip through the pinned master (p_copy D2H +
+// upload H2D: 2 x 16.4 GB of PCIe per Qwen3-8B step). Same versions, same
+// staleness; the host bf16 copy is refreshed on demand (pull_w16).
+// RP_RT_HOST_PUBLISH keeps the paper's p_copy / upload path.
+void Runtime::publish_in_place() {
+  if (N != 1 || ndev != 1 || pooled || (cfg.flags & RP_RT_HOST_PUBLISH)) return;
+  Gpu& G = gpus[0];
+  set_dev(G);
+  for (int g = 0; g < ngroups(); ++g) {
+    HostGroup& H = host[g];
+    if (H.direct || H.tn() == 0) continue;
+    DevGroup& D = G.groups[g];
+    if (D.pend) {
+      dfree(G, D.pend + H.t_off);
+      D.pend = nullptr;
+      G.allocated[2] -= (std::size_t)H.tn() * 2;
+    }
+    H.direct = true;
+  }
 }
 
 // Optimizer state in free HBM (single device only: with N devices a group's
@@ -1021,11 +1048,11 @@ void Runtime::alloc_worker(Gpu& G, int id) {
         for (int mb = 0; mb < MR; ++mb)
           G.ckpt[((std::size_t)p * s.L + l) * MR + mb] = mkbuf(Th * 2, pooled ? -1 : 5);
   }
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < Gpu::kOptSlots; ++b) {
     for (int j = 0; j < 3; ++j)
       G.opt_buf[b][j] = static_cast<float*>(dalloc((std::size_t)chunk_elems * 4, 6));
-  G.opt_free[0] = new_event(false);
-  G.opt_free[1] = new_event(false);
+    G.opt_free[b] = new_event(false);
+  }
   G.anchor = new_event(true);
   RP_CUDA(cudaEventRecord(G.anchor, G.compute));
 }
@@ -2083,11 +2110,22 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     D.pend = static_cast<uint16_t*>(G.slabs[D.pend_slab].p) - H.t_off;
   }
   if (state_ev[g]) RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, state_ev[g], 0));  // prev. write-back
+  // in-place publication (one worker): version `ver` overwrites w[b] once
+  // iteration ver-2's (sync: ver-1's) last compute read of it is done
+  const int ver = last_iter + (cfg.async_optimizer ? 2 : 1), vb = ver & 1;
+  uint16_t* out = D.pend;
+  if (H.direct) {
+    RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_lastuse[vb], 0));  // WAR on w[vb]
+    RP_CUDA(cudaStreamWaitEvent(G.opt_comp, D.ev_upload[vb], 0));
+    out = D.w[vb];
+    if (H.t_off > 0 && D.loaded[vb] < 0)  // frozen part (LoRA base) never written to w[vb] yet
+      RP_CUDA(cudaMemcpyAsync(D.w[vb], H.w16, H.t_off * 2, cudaMemcpyHostToDevice, G.opt_comp));
+  }
   cudaEvent_t xa = xfer_begin(G.opt_h2d);
   for (int64_t off = H.t_off; off < H.n; off += chunk_elems) {  // trainable region
     const int64_t n = std::min<int64_t>(chunk_elems, H.n - off);
     const int sl = G.opt_slot;
-    G.opt_slot ^= 1;
+    G.opt_slot = (G.opt_slot + 1) % Gpu::kOptSlots;
     float** buf = G.opt_buf[sl];
     RP_CUDA(cudaStreamWaitEvent(G.opt_h2d, G.opt_free[sl], 0));
     RP_CUDA(cudaMemcpyAsync(buf[0], H.master + off, n * 4, cudaMemcpyHostToDevice, G.opt_h2d));
@@ -2096,7 +2134,7 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
     h2d_bytes += n * 12;
     join(G, G.opt_h2d, G.opt_comp);
     const int pi_ = prof_begin(G.opt_comp);
-    RP_K(rp_adamw(buf[0], buf[1], buf[2], D.grad[parity] + off, D.pend + off, n, &cfg.adam,
+    RP_K(rp_adamw(buf[0], buf[1], buf[2], D.grad[parity] + off, out + off, n, &cfg.adam,
                   step_no, G.opt_comp));
     prof_end(pi_, G.opt_comp, 3, 30.0 * n);
     ++kernels;
@@ -2118,6 +2156,13 @@ void Runtime::adam_group(Gpu& G, int g, int parity) {
   RP_CUDA(cudaEventRecord(D.ev_state, G.opt_d2h));
   xfer_end(xa, G.opt_d2h, 2, g - 1, last_iter, G.id);
   state_ev[g] = D.ev_state;
+  if (H.direct) {  // published in place: no p_copy, no upload
+    RP_CUDA(cudaEventRecord(D.ev_upload[vb], G.opt_comp));
+    flags.set(G.opt_comp, flag_pub(g), (uint32_t)ver);  // = the ParamCopy index (ver - 1) + 1
+    D.loaded[vb] = ver;
+    H.w16_stale = true;
+    return;
+  }
   pend_owner[g] = G.id;
   if (!cfg.async_optimizer) p_copy(g);  // sync: iteration t+1 sees grads of t
 }

@@ -222,8 +222,12 @@ struct Gpu {
   cudaEvent_t ev_iter_done[2] = {nullptr, nullptr};  // last read of parity set (compute)
   cudaEvent_t ev_loss_par[2] = {nullptr, nullptr};
   float* cos_sin = nullptr;
-  float* opt_buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-  cudaEvent_t opt_free[2] = {nullptr, nullptr};
+  // streamed-AdamW chunk ring: kOptSlots x (master, m, v) chunks (3 slots
+  // measured 2-4 % slower than 2 on the C3 headline, profiles/r02q_ab.jsonl:
+  // more DMA in flight delays the weight uploads sharing the H2D lane)
+  static constexpr int kOptSlots = 2;
+  float* opt_buf[kOptSlots][3] = {};
+  cudaEvent_t opt_free[kOptSlots] = {};
   int opt_slot = 0;
   // hand-offs by round parity and micro-batch: activations (bf16) into a
   // forward/fused slot, gradients (fp32) into a backward slot

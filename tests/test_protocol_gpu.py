@@ -13,7 +13,8 @@ layer l -> l, head -> L, so the model is build_protocol(L+1, T).
   EventPerLayer set (minus ParamCopy(., 0): nothing is published before the
   first step, so the runtime issues no copy), and the reference checker
   proves that set safe in every interleaving.
-* Host-offloaded state (two fp32 grad buffers by iteration parity) and N=4
+* Host-offloaded state (two fp32 grad buffers by iteration parity; at N=1
+  through the pinned master as well, host_publish) and N=4
   logical workers (grads stay on the worker that produced them): edges
   (1)-(3) are the reference's exactly; edge (4) protects each PHYSICAL grad
   buffer — GradCopy of the last iteration that wrote the same (worker,
@@ -136,7 +137,9 @@ def test_single_buffer_edges_equal_reference_event_per_layer():
 @pytest.mark.parametrize("N,resident", [(1, False), (4, True), (4, False)])
 def test_per_buffer_edges(N, resident):
     L = O.Shape.from_config("tiny").layers
-    got, plan, durs, st, pub = realised(N, resident)
+    # (N=1 publishes in place by default — no p_copy / upload at all — so the
+    # paper's publication path is requested explicitly there)
+    got, plan, durs, st, pub = realised(N, resident, host_publish=N == 1)
     ref = reference_edges(L + 1)
     for pair in ((UP, PC), (PC, UP), (GW, GC)):  # (1), (2), (3): global, exactly the reference's
         assert by_kind(got, pair) == by_kind(ref, pair), pair
