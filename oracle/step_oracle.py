@@ -252,32 +252,40 @@ class StepOracle:
         self.mode = mode
         self.lora_scale = lora_scale
         self.master = {k: v.clone().float().requires_grad_(False) for k, v in params.items()}
-        self.opt_params = {k: torch.nn.Parameter(v.clone()) for k, v in self.master.items()}
-        train = [v for k, v in self.opt_params.items() if not lora_scale or "_lora_" in k]
-        self.opt = torch.optim.AdamW(train, lr=lr, betas=betas, eps=eps,
-                                     weight_decay=weight_decay)
+        # LoRA: frozen base weights are bf16-representable (init_params) and
+        # never change, so they are shared rather than copied (and get no
+        # grads) — the oracle then fits full-width MoE layers in host memory
+        self.trainable = {k for k in params if not lora_scale or "_lora_" in k}
+        self.opt_params = {k: torch.nn.Parameter(v.clone()) for k, v in self.master.items()
+                           if k in self.trainable}
+        self.opt = torch.optim.AdamW(list(self.opt_params.values()), lr=lr, betas=betas,
+                                     eps=eps, weight_decay=weight_decay)
         # weights the next iteration computes with (bf16 master copy)
-        self.used = {k: bf16_round(v) for k, v in self.master.items()}
+        self.used = {k: (bf16_round(v) if k in self.trainable else v)
+                     for k, v in self.master.items()}
         self.pending = None  # async: result of the last optimizer step
         self.last_grads = None
 
     def _fwd_bwd(self, tokens, labels):
-        w = {k: v.clone().requires_grad_(True) for k, v in self.used.items()}
+        w = {k: (v.clone().requires_grad_(True) if k in self.trainable else v)
+             for k, v in self.used.items()}
         n_valid = int((labels >= 0).sum())
         total = 0.0
         for mb in range(tokens.shape[0]):
             loss = forward_loss_sum(w, tokens[mb], labels[mb], self.s, self.lora_scale) / n_valid
             loss.backward()
             total += loss.item()
-        return total, {k: v.grad if v.grad is not None else torch.zeros_like(v)
-                       for k, v in w.items()}
+        return total, {k: (v.grad if v.grad is not None else torch.zeros_like(v))
+                       if k in self.trainable else None for k, v in w.items()}
 
     def _apply(self, grads):
         for k, prm in self.opt_params.items():
             prm.grad = grads[k].clone()
         self.opt.step()
         self.opt.zero_grad(set_to_none=True)
-        return {k: bf16_round(p.detach()) for k, p in self.opt_params.items()}
+        out = dict(self.used)  # frozen: unchanged
+        out.update({k: bf16_round(p.detach()) for k, p in self.opt_params.items()})
+        return out
 
     def step(self, tokens, labels):
         """tokens, labels: [M, b, S] int. Returns the step's mean loss."""
@@ -293,7 +301,9 @@ class StepOracle:
         return loss
 
     def master_fp32(self):
-        return {k: p.detach().clone() for k, p in self.opt_params.items()}
+        out = {k: v for k, v in self.master.items() if k not in self.trainable}
+        out.update({k: p.detach().clone() for k, p in self.opt_params.items()})
+        return out
 
 
 def synthetic_batch(s: Shape, M: int, b: int, S: int, seed: int = 1234):
