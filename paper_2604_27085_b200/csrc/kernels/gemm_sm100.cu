@@ -253,6 +253,7 @@ template <int A_MN, int B_MN, int EPI, int TBN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                 const __grid_constant__ CUtensorMap tma_b, Params p) {
+  griddep_wait();  // PDL: p.g_off (grouped GEMM) is written by the previous kernel
   using Cfg = SingleCfg<TBN, B_MN>;
   constexpr int BN = TBN, STAGES = Cfg::STAGES, STAGE_BYTES = Cfg::STAGE, TMEM_COLS = Cfg::TMEM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  griddep_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
@@ -575,6 +577,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  // PDL: the prologue above overlapped the previous kernel's tail; nothing of
+  // its output is read before this
+  griddep_wait();
+  griddep_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer (both CTAs; each loads its halves) ----------------
@@ -979,6 +985,26 @@ SplitWs split_ws(cudaStream_t st, std::size_t elems, std::size_t flags) {
 // B200: half-size MMAs double the per-k-block pipeline overhead).
 constexpr int PBN = 256;
 
+// Launch with programmatic stream serialization (PDL): the grid may be
+// scheduled while the stream's previous kernel drains, its CTAs run their
+// prologue (barriers, TMEM allocation, tensor-map prefetch) and then block in
+// griddep_wait() until that kernel has completed. The GEMMs trigger their own
+// dependents right after their prologue.
+template <class K, class... Args>
+cudaError_t launch_pdl(K kern, dim3 grid, int smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = grid;
+  c.blockDim = dim3(NUM_THREADS, 1, 1);
+  c.dynamicSmemBytes = smem;
+  c.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = at;
+  c.numAttrs = 1;
+  return cudaLaunchKernelEx(&c, kern, args...);
+}
+
 // why the last rp_gemm_* call on this thread failed (rp_gemm_last_error)
 thread_local const char* g_gemm_why = "";
 inline cudaError_t launch_status(const char* what) {
@@ -1025,8 +1051,9 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
       }
     }
     const int pairs = q.units < npairs ? q.units : npairs;
-    kern<<<2 * pairs, NUM_THREADS, smem, stream>>>(ta, tb, td, em, q, n_fastest);
-    return launch_status("pair kernel launch");
+    return launch_pdl(kern, dim3(2 * pairs), smem, stream, ta, tb, td, em, q, n_fastest) == cudaSuccess
+               ? cudaSuccess
+               : launch_status("pair kernel launch");
   }
   const bool skinny = p.N <= 32;
   auto kern = skinny ? gemm_kernel<A_MN, B_MN, EPI, 32> : gemm_kernel<A_MN, B_MN, EPI, 256>;
@@ -1036,8 +1063,9 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorM
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + tbn - 1) / tbn);
   if (p.g_off) tiles += p.g_num * ((p.N + tbn - 1) / tbn);  // ragged last m-tile per group (bound)
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NUM_THREADS, smem, stream>>>(ta, tb, p);
-  return launch_status("single kernel launch");
+  return launch_pdl(kern, dim3(grid), smem, stream, ta, tb, p) == cudaSuccess
+             ? cudaSuccess
+             : launch_status("single kernel launch");
 }
 
 template <int A_MN, int B_MN>
