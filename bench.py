@@ -349,6 +349,7 @@ def config_dict(args, resident=None, mode=None):
                          + f" and activation recompute ({baseline_config(args)}): b=1, "
                          f"M={args.micro_batches} micro-batches/step, "
                          f"RoundPipe-{'async' if mode == 'async' else 'sync'}, N={args.gpus}"),
+            "partitioner_residency_factor": args.residency_factor,
             "weights": ("published through the pinned bf16 master and re-uploaded every "
                         "iteration" if args.host_publish or args.gpus > 1 else
                         "AdamW results published into the device weights in place (one GPU)"),
@@ -371,7 +372,7 @@ def measure(args, resident, mode, steps, warmup, profile=False, report_dir=None,
     rt = RoundPipe(args.model, seq_len=args.seq, micro_batch=1, micro_batches=args.micro_batches,
                    num_gpus=args.gpus, async_optimizer=mode == "async", adam=AdamW(lr=1e-5),
                    record_timeline=True, lora_rank=args.lora_rank, lora_alpha=args.lora_alpha,
-                   host_publish=args.host_publish,
+                   host_publish=args.host_publish, residency_factor=args.residency_factor,
                    resident_state_gb=-1.0 if resident else 0.0)
     setup_s = time.time() - t_setup
     d = MODEL_DIMS[args.model]
@@ -574,6 +575,11 @@ def main():
     ap.add_argument("--lora-rank", type=int, default=0,
                     help="LoRA fine-tune (base frozen, rank-r adapters); 0 = full fine-tune")
     ap.add_argument("--lora-alpha", type=float, default=0.0)
+    ap.add_argument("--residency-factor", type=float, default=2.0,
+                    help="the partitioner's residency factor (reference default 2.0: two "
+                         "weight versions; its backward/fused stages add same-size gradients). "
+                         "LoRA runs have no base-weight gradients, so 1.0 models their "
+                         "backward/fused stages exactly (2 x weights)")
     ap.add_argument("--host-publish", action="store_true",
                     help="one GPU: publish every AdamW result through the pinned bf16 master "
                          "and re-upload it (the paper's path; C5's weights streamed from pinned "
