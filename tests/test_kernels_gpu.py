@@ -166,7 +166,9 @@ def test_adamw_chunk():
     pr = pr - lr * upd
     torch.cuda.synchronize()
     assert rel(m, mr) < 1e-6 and rel(v, vr) < 1e-6 and rel(p, pr) < 1e-6
-    assert torch.equal(w16, pr.to(torch.bfloat16))
+    # the bf16 weights are the kernel's own fp32 master rounded (torch's fp32
+    # result may differ in the last bit, which can flip a bf16 rounding)
+    assert torch.equal(w16, p.to(torch.bfloat16))
 
 
 def _attn_ref(q, k, v, seq, nq, nk, hd):
