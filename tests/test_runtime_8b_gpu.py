@@ -158,3 +158,68 @@ def test_8b_width_n2_four_slots(mode):
     losses, g0, master, plan, st = run(mode, 2, costs=uniform_costs(shape().layers + 1))
     assert plan.num_slots() == 4 and [(r.first, r.last) for r in plan.bwd_stages] == [(1, 1), (0, 0)]
     compare("n2-S4", mode, losses, g0, master)
+
+
+def test_8b_width_lora_r32():
+    """LoRA r=32 / alpha 64 on the four linears at full Qwen3-8B width, N=1,
+    async, host-offloaded adapter state: the adapter GEMMs at real shapes —
+    the rank-side pair-kernel path of dU = dY B over K = 24576 (gate/up),
+    the 128x32 skinny tiles, the swapped M <= 32 adapter gradients — plus the
+    second-K-segment base GEMMs. Loss rel <= 2e-3 every step, adapter grads
+    rel-L2 <= 2e-2 and cosine >= 0.999, adapter update cosine >= 0.98,
+    frozen base bit-unchanged."""
+    from paper_2604_27085_b200.runtime import AdamW, RoundPipe
+    r, alpha, mode = 32, 64.0, "async"
+    s = shape()
+    p = dict(params())
+    p.update(O.init_lora_params(s, r, seed=1, std_b=0.02))
+    tok, lab = batch()
+    rt = RoundPipe(MODEL, seq_len=SEQ, micro_batch=1, micro_batches=M, num_gpus=1,
+                   async_optimizer=True,
+                   adam=AdamW(HP["lr"], HP["betas"], HP["eps"], HP["weight_decay"]),
+                   skip_init=True, lora_rank=r, lora_alpha=alpha, resident_state_gb=0.0)
+    rt.load_state({k: v.numpy() for k, v in p.items()}, s.layers)
+    keys = [f"layers.{l}.{n}" for l in range(s.layers)
+            for n in ("qkv_lora_A", "qkv_lora_B", "o_lora_A", "o_lora_B", "gate_up_lora_A",
+                      "gate_up_lora_B", "down_lora_A", "down_lora_B")]
+    losses = []
+    for it in range(STEPS):
+        losses.append(rt.forward_backward(tok.numpy(), lab.numpy()))
+        if it == 0:
+            g0 = rt.read_state(s.layers, which=2)
+            g0 = {k: np.asarray(g0[k]).copy() for k in keys}
+        rt.step()
+    rt.sync()
+    w = rt.read_state(s.layers, which=1)
+    w = {k: np.asarray(w[k]).copy() for k in ("layers.0.qkv", "layers.1.down", "head.lm_head")}
+    m = rt.read_state(s.layers, which=0)
+    m = {k: np.asarray(m[k]).copy() for k in keys}
+    rt.close()
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    o = O.StepOracle(s, p, mode=mode, lora_scale=alpha / r, **HP)
+    ol = []
+    for it in range(STEPS):
+        ol.append(o.step(tok, lab))
+        if it == 0:
+            og = {k: o.last_grads[k] for k in keys}
+    om = o.master_fp32()
+    loss_rel = max(abs(a - b) / abs(b) for a, b in zip(losses, ol))
+    grel, gcos, ucos = {}, {}, {}
+    for k in keys:
+        g = torch.from_numpy(g0[k]).reshape(og[k].shape)
+        grel[k] = ((g - og[k]).norm() / og[k].norm()).item()
+        gcos[k] = torch.nn.functional.cosine_similarity(g.flatten(), og[k].flatten(), dim=0).item()
+        du = torch.from_numpy(m[k]).reshape(om[k].shape) - p[k]
+        dr = om[k] - p[k]
+        ucos[k] = float((du * dr).sum() / (du.norm() * dr.norm()))
+    wg = max(grel.items(), key=lambda kv: kv[1])
+    wc = min(gcos.items(), key=lambda kv: kv[1])
+    wu = min(ucos.items(), key=lambda kv: kv[1])
+    print(f"MARGINS lora-r32 {mode}: losses {losses} oracle {ol} max loss rel {loss_rel:.2e}; "
+          f"worst adapter grad rel-L2 {wg[0]} {wg[1]:.3e}; worst grad cos {wc[0]} {wc[1]:.6f}; "
+          f"worst update cos {wu[0]} {wu[1]:.5f}")
+    assert loss_rel < 2e-3, (losses, ol)
+    assert wg[1] < 2e-2 and wc[1] > 0.999, (wg, wc)
+    assert wu[1] > 0.98, wu
+    for k, v in w.items():  # frozen base
+        assert np.array_equal(v.reshape(-1), p[k].numpy().reshape(-1)), k
