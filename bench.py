@@ -309,13 +309,17 @@ def run_reference(args):
 # ---------------------------------------------------------------------------- GPU side
 MODEL_NAMES = {"qwen3-8b": "Qwen3-8B", "qwen3-1.7b": "Qwen3-1.7B", "tiny": "tiny Qwen3",
                "qwen3-235b-a22b-l8": "Qwen3-235B-A22B (8 of 94 layers)",
-               "qwen3-235b-a22b-l6": "Qwen3-235B-A22B (6 of 94 layers)"}
+               "qwen3-235b-a22b-l6": "Qwen3-235B-A22B (6 of 94 layers)",
+               "qwen3-32b-l12": "Qwen3-32B (12 of 64 layers)"}
 
 
 def baseline_config(args):
     """Which BASELINE.json config the run measures."""
     if args.model.startswith("qwen3-235b-a22b"):
         return "BASELINE configs[4] at reduced depth: MoE LoRA, weights streamed from pinned host"
+    if args.model.startswith("qwen3-32b"):
+        return ("BASELINE configs[3]" + ("" if args.model == "qwen3-32b" else " at reduced depth")
+                + ": auto layer partitioning")
     if args.model == "qwen3-1.7b":
         return "BASELINE configs[1]"
     if args.model == "qwen3-8b" and not args.lora_rank:
