@@ -592,6 +592,9 @@ def main():
                     help="write the measured timeline (report JSON + SVG Gantt) here")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1:  # the CPU baseline is an N=1 figure; the variants are single-device
+        args.no_cpu_baseline = True
+        args.no_variants = True
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
