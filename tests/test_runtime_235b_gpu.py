@@ -35,6 +35,15 @@ import torch
 from oracle import step_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _free_module_caches():
+    """The driver runs every GPU file in one pytest process: drop this
+    module's multi-GB parameter / oracle caches once its tests are done."""
+    yield
+    _P.clear()
+    _ORACLE.clear()
 MODEL = "qwen3-235b-a22b-l1"
 HP = dict(lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0)
 R, ALPHA, M, SEQ, STEPS = 16, 32.0, 2, 2048, 3

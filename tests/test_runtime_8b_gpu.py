@@ -33,6 +33,15 @@ import torch
 from oracle import step_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _free_module_caches():
+    """The driver runs every GPU file in one pytest process: drop this
+    module's multi-GB parameter / oracle caches once its tests are done."""
+    yield
+    _PARAMS.clear()
+    _ORACLE.clear()
 MODEL = "qwen3-8b-l2"
 HP = dict(lr=1e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0)
 M, SEQ, STEPS = 2, 4096, 3
