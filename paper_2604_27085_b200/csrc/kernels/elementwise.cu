@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+
+#include "kernels/launch_util.h"
+#include "kernels/sm100.cuh"
 #include "kernels/swiglu.cuh"
 #include "rp/kernels.h"
 
@@ -67,6 +71,18 @@ __device__ __forceinline__ float rn_block_sum(float v, float* red) {
   return t;
 }
 
+__device__ __forceinline__ void unpack4(const uint2& u, float (&f)[4]) {
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) f[i] = bf2f(b[i]);
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* p, const float (&f)[4]) {
+  uint2 u;
+  __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = f2bf(f[i]);
+  *reinterpret_cast<uint2*>(p) = u;
+}
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
@@ -205,188 +221,400 @@ __global__ void __launch_bounds__(RN_THREADS)
   }
 }
 
+// The same backward with the row's operands staged by the copy engine: one
+// wave of persistent blocks, each with a ring of RN_ST rows in shared memory
+// ([dy bf16 | x bf16 | dres fp32 | the 16-byte rstd group of the row]) filled
+// by 1-D bulk copies on an mbarrier per slot, so the bytes in flight are not
+// bounded by the registers that hold them (the register version keeps one
+// row per block in flight, profiles/r02n_step_breakdown_8b.txt: 3.7 TB/s in
+// step). The per-thread column assignment, the dot-product order and the
+// output arithmetic are the register version's, so dx is bit-identical.
+constexpr int RN_ST = 2;
+#ifndef RN_STAGED  // -DRN_STAGED=0: register version only (same-box A/B builds)
+#define RN_STAGED 1
+#endif
+template <int RN_THREADS, int VPT>
+__global__ void __launch_bounds__(RN_THREADS)
+    rmsnorm_bwd_staged_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                              const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                              const float* __restrict__ dres, float* __restrict__ dx32,
+                              __nv_bfloat16* __restrict__ dx16, float* __restrict__ dw, int rows,
+                              int h) {
+  using namespace sm100;
+  extern __shared__ __align__(128) uint8_t rsm[];
+  __shared__ float red[2][RN_THREADS / 32];
+  const int slot_bytes = h * (dres ? 8 : 4) + 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(rsm + RN_ST * slot_bytes);
+  auto issue = [&](int row, int s) {
+    uint8_t* slot = rsm + s * slot_bytes;
+    const long long off = (long long)row * h;
+    mbar_arrive_expect_tx(&full[s], slot_bytes);
+    bulk_load_1d(slot, dy + off, h * 2, &full[s]);
+    bulk_load_1d(slot + h * 2, x + off, h * 2, &full[s]);
+    if (dres) bulk_load_1d(slot + h * 4, dres + off, h * 4, &full[s]);
+    bulk_load_1d(slot + slot_bytes - 16, rstd + (row & ~3), 16, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RN_ST; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < RN_ST; ++s)
+      if (blockIdx.x + s * gridDim.x < rows) issue(blockIdx.x + s * gridDim.x, s);
+  }
+  uint4 wv[VPT];
+  float dwa[VPT][8];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int c = (threadIdx.x + j * RN_THREADS) * 8;
+    wv[j] = c < h ? *reinterpret_cast<const uint4*>(w + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dwa[j][i] = 0.f;
+  }
+  __syncthreads();
+  int par = 0, it = 0;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x, par ^= 1, ++it) {
+    const int s = it % RN_ST;
+    mbar_wait(&full[s], (it / RN_ST) & 1);
+    const uint8_t* slot = rsm + s * slot_bytes;
+    const __nv_bfloat16* dys = reinterpret_cast<const __nv_bfloat16*>(slot);
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(slot + h * 2);
+    const float* ds = reinterpret_cast<const float*>(slot + h * 4);
+    const long long off = (long long)row * h;
+    const float r = reinterpret_cast<const float*>(slot + slot_bytes - 16)[row & 3];
+    // dy / x are read from the slot twice (before and after the row
+    // reduction) instead of being held in registers across it
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      float a[8], b[8], g[8];
+      unpack8(c < h ? *reinterpret_cast<const uint4*>(dys + c) : make_uint4(0, 0, 0, 0), a);
+      unpack8(c < h ? *reinterpret_cast<const uint4*>(xs + c) : make_uint4(0, 0, 0, 0), b);
+      unpack8(wv[j], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dot += a[i] * g[i] * (b[i] * r);
+    }
+    dot = warp_sum(dot);
+    if (threadIdx.x % 32 == 0) red[par][threadIdx.x / 32] = dot;
+    __syncthreads();  // red[par] is rewritten two rows later, after another barrier
+    float tot = 0.f;
+#pragma unroll
+    for (int i = 0; i < RN_THREADS / 32; ++i) tot += red[par][i];
+    const float mean = tot / h;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      if (c >= h) continue;
+      float a[8], b[8], g[8], o[8];
+      unpack8(*reinterpret_cast<const uint4*>(dys + c), a);
+      unpack8(*reinterpret_cast<const uint4*>(xs + c), b);
+      unpack8(wv[j], g);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float xh = b[i] * r;
+        o[i] = r * (a[i] * g[i] - xh * mean);
+        dwa[j][i] += a[i] * xh;
+      }
+      if (dres) {
+        const float4 d0 = *reinterpret_cast<const float4*>(ds + c);
+        const float4 d1 = *reinterpret_cast<const float4*>(ds + c + 4);
+        o[0] += d0.x; o[1] += d0.y; o[2] += d0.z; o[3] += d0.w;
+        o[4] += d1.x; o[5] += d1.y; o[6] += d1.z; o[7] += d1.w;
+      }
+      if (dx32) {
+        *reinterpret_cast<float4*>(dx32 + off + c) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(dx32 + off + c + 4) = make_float4(o[4], o[5], o[6], o[7]);
+      }
+      if (dx16) store8(dx16 + off + c, o);
+    }
+    __syncthreads();  // slot s consumed
+    if (threadIdx.x == 0 && row + RN_ST * gridDim.x < rows) issue(row + RN_ST * gridDim.x, s);
+  }
+  if (dw && (int)blockIdx.x < rows) {
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int c = (threadIdx.x + j * RN_THREADS) * 8;
+      if (c < h) {
+        atomicAdd(reinterpret_cast<float4*>(dw + c),
+                  make_float4(dwa[j][0], dwa[j][1], dwa[j][2], dwa[j][3]));
+        atomicAdd(reinterpret_cast<float4*>(dw + c + 4),
+                  make_float4(dwa[j][4], dwa[j][5], dwa[j][6], dwa[j][7]));
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------- QK-norm + RoPE
-// A head of HD elements is handled by TPH = HD/8 consecutive lanes, 8
-// elements (16 bytes) each; the per-head RMS reduces over those lanes and the
-// rotate_half partner (element e +- HD/2) lives in lane ^ TPH/2. A 128-thread
-// block covers HPB = 128/TPH heads of one token per pass and walks passes
-// then tokens (grid-stride over one wave of resident blocks); a thread's
-// (cos, sin) pairs depend only on its lane slot and the token, so they are
-// loaded once per token. The loads of QK_NB passes are issued together
-// before any of them is used (occupancy is register-limited to 5-8 blocks of
-// 128 threads per SM, profiles/r02g_ncu_full.json): backward 52.2 -> 48.1 us,
-// forward unchanged at 25.6 us (profiles/r02h_qk_ab.jsonl) — its remaining
-// limit is the serial per-token chain (2 load rounds per token for 40 heads,
-// ~5.5 tokens per block), not the loads in flight of one round.
-constexpr int QK_THREADS = 128;
-constexpr int QK_NB = 4;
+// A head of HD elements is handled by TPH = HD/8 consecutive lanes; lane
+// `sub` owns the rotate_half PAIRS (e, e + HD/2) for e in [4 sub, 4 sub + 4),
+// so the rotation needs no shuffles (only the per-head RMS reduces over the
+// TPH lanes) and a lane's (cos, sin) are 4 float2 kept in registers for the
+// token.
+//
+// Bytes in flight come from the copy engine, not from registers: one wave of
+// persistent blocks walks tokens, and one thread per block keeps a ring of
+// QK_STAGES tokens in shared memory filled with 1-D bulk copies
+// (cp.async.bulk, an mbarrier per slot): a token's q|k head slice of the qkv
+// row (contiguous), its (cos, sin) row and, backward, the dq / dk rows and
+// the per-head rstd. The block's threads (qk_block_threads: QK_NB passes
+// cover a token's heads) compute from the slot, store straight to global,
+// and a __syncthreads hands the slot back to the producer for the token
+// QK_STAGES steps ahead. The round-1/2 kernels held QK_NB 16-byte loads per
+// thread in registers (8 contiguous elements, partner via lane ^ TPH/2):
+// register-limited occupancy, 12 shuffles per 8 elements, one memory round
+// trip per token (profiles/r02g_ncu_full.json, profiles/r02_qk_ab.jsonl).
+#ifndef QK_NB
+#define QK_NB 4
+#endif
+constexpr int QK_MAX_THREADS = 512;
+#ifndef QK_STAGES_FWD
+#define QK_STAGES_FWD 2
+#endif
+#ifndef QK_STAGES_BWD
+#define QK_STAGES_BWD 2
+#endif
 
 template <int HD>
-__global__ void __launch_bounds__(QK_THREADS)
+__host__ __device__ constexpr int qk_tph() { return HD / 8; }
+
+template <int HD>
+int qk_block_threads(int heads, int nb) {
+  const int slots = heads * qk_tph<HD>();
+  int bt = (slots + nb - 1) / nb;
+  bt = (bt + 31) / 32 * 32;
+  return bt < QK_MAX_THREADS ? bt : QK_MAX_THREADS;
+}
+
+__host__ __device__ constexpr int qk_align16(int b) { return (b + 15) / 16 * 16; }
+
+// shared-memory slot of one token: [x: heads*HD bf16 | cs: HD/2 float2] (fwd),
+// [g: heads*HD bf16 (dq row, dk row) | x | cs | rstd: heads fp32] (bwd)
+struct QkSlot {
+  int x, cs, g, rstd, bytes;
+};
+template <int HD>
+__host__ __device__ QkSlot qk_slot(int heads, bool bwd) {
+  QkSlot q;
+  const int row = heads * HD * 2;
+  q.g = 0;
+  q.x = bwd ? row : 0;
+  q.cs = q.x + row;
+  q.rstd = q.cs + qk_align16(HD / 2 * 8);
+  q.bytes = (q.rstd + (bwd ? qk_align16(heads * 4) : 0) + 127) / 128 * 128;
+  return q;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(QK_MAX_THREADS)
     qk_norm_rope_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
                             const __nv_bfloat16* __restrict__ qw,
                             const __nv_bfloat16* __restrict__ kw, const float2* __restrict__ cs,
                             int seq, __nv_bfloat16* __restrict__ qo, __nv_bfloat16* __restrict__ ko,
                             float* __restrict__ rstd_q, float* __restrict__ rstd_k, int T,
                             float eps) {
-  constexpr int TPH = HD / 8, HALF = HD / 2, HPB = QK_THREADS / TPH;
+  using namespace sm100;
+  constexpr int TPH = qk_tph<HD>(), HALF = HD / 2, ST = QK_STAGES_FWD;
+  extern __shared__ __align__(128) uint8_t qsm[];
   const int heads = nq + nk;
-  const int sub = threadIdx.x % TPH, hl = threadIdx.x / TPH;
+  const QkSlot L = qk_slot<HD>(heads, false);
+  uint64_t* full = reinterpret_cast<uint64_t*>(qsm + ST * L.bytes);
+  const int sub = threadIdx.x % TPH, h0 = threadIdx.x / TPH, hstep = blockDim.x / TPH;
   const bool lo = sub < TPH / 2;
-  float wq[8], wk[8];
-  load8(qw + sub * 8, wq);
-  load8(kw + sub * 8, wk);
-  for (int t = blockIdx.x; t < T; t += gridDim.x) {
-    const int pos = t % seq;
-    const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
-    float4 c[4];
+  auto issue = [&](int t, int s) {
+    uint8_t* slot = qsm + s * L.bytes;
+    mbar_arrive_expect_tx(&full[s], heads * HD * 2 + HALF * 8);
+    bulk_load_1d(slot + L.x, qkv + (long long)t * ld, heads * HD * 2, &full[s]);
+    bulk_load_1d(slot + L.cs, cs + (long long)(t % seq) * HALF, HALF * 8, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < ST; ++s)
+      if (blockIdx.x + s * gridDim.x < T) issue(blockIdx.x + s * gridDim.x, s);
+  }
+  __syncthreads();
+  const int e0 = sub * 4;  // this lane's pairs (e0 + k, e0 + k + HALF), k < 4
+  float wql[4], wqh[4], wkl[4], wkh[4];  // norm weights, converted once
+  unpack4(*reinterpret_cast<const uint2*>(qw + e0), wql);
+  unpack4(*reinterpret_cast<const uint2*>(qw + HALF + e0), wqh);
+  unpack4(*reinterpret_cast<const uint2*>(kw + e0), wkl);
+  unpack4(*reinterpret_cast<const uint2*>(kw + HALF + e0), wkh);
+  int i = 0;
+  for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
+    const int s = i % ST;
+    mbar_wait(&full[s], (i / ST) & 1);
+    const uint8_t* slot = qsm + s * L.bytes;
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(slot + L.x);
+    const float4* c4 = reinterpret_cast<const float4*>(slot + L.cs) + e0 / 2;
+    const float4 ca = c4[0], cb = c4[1];  // (cos, sin) of pairs e0 .. e0+3
+    const float cosv[4] = {ca.x, ca.z, cb.x, cb.z}, sinv[4] = {ca.y, ca.w, cb.y, cb.w};
+    __nv_bfloat16* qrow = qo + (long long)t * nq * HD;
+    __nv_bfloat16* krow = ko + (long long)t * nk * HD;
+    float* rq_row = rstd_q + (long long)t * nq;
+    float* rk_row = rstd_k + (long long)t * nk;
+    // every lane runs every pass (the RMS shuffles are warp-wide); lanes
+    // whose head is past the end compute on zeros and store nothing
+    for (int hb = 0; hb < heads; hb += hstep) {  // block-uniform
+      const int hh = hb + h0;
+      const bool act = hh < heads;
+      const bool is_q = hh < nq;
+      const uint2 z = make_uint2(0, 0);
+      float lo[4], hi[4], wl[4], wh[4];
+      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + e0) : z, lo);
+      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + HALF + e0) : z, hi);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c[i] = c4[i];
-    const __nv_bfloat16* row = qkv + (long long)t * ld;
-    for (int base0 = 0; base0 < heads; base0 += QK_NB * HPB) {
-      uint4 raw[QK_NB];
+      for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
+      float ss = 0.f;
 #pragma unroll
-      for (int b = 0; b < QK_NB; ++b) {
-        const int hh = base0 + b * HPB + hl;
-        raw[b] = hh < heads ? *reinterpret_cast<const uint4*>(row + hh * HD + sub * 8)
-                            : make_uint4(0, 0, 0, 0);
+      for (int k = 0; k < 4; ++k) ss += lo[k] * lo[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ss += hi[k] * hi[k];
+#pragma unroll
+      for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float r = rsqrtf(ss / HD + eps);
+      float ol[4], oh[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float nl = bf2f(f2bf(wl[k] * (lo[k] * r))), nh = bf2f(f2bf(wh[k] * (hi[k] * r)));
+        ol[k] = nl * cosv[k] - nh * sinv[k];  // x1 cos - x2 sin
+        oh[k] = nh * cosv[k] + nl * sinv[k];  // x2 cos + x1 sin
       }
-      // every lane runs every pass (the shuffles below are warp-wide); lanes
-      // whose head is past the end compute on zeros and store nothing
-#pragma unroll
-      for (int b = 0; b < QK_NB; ++b) {
-        if (base0 + b * HPB >= heads) break;  // block-uniform
-        const int hh = base0 + b * HPB + hl;
-        const bool act = hh < heads;
-        const bool is_q = hh < nq;
-        float v[8];
-        unpack8(raw[b], v);
-        float ss = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) ss += v[i] * v[i];
-#pragma unroll
-        for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        const float r = rsqrtf(ss / HD + eps);
-        float n[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) n[i] = bf2f(f2bf((is_q ? wq[i] : wk[i]) * (v[i] * r)));
-        float out[8];
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          const float4 cc = c[i / 2];  // (cos, sin) of elements i, i+1
-          const float p0 = __shfl_xor_sync(0xffffffffu, n[i], TPH / 2);
-          const float p1 = __shfl_xor_sync(0xffffffffu, n[i + 1], TPH / 2);
-          out[i] = lo ? n[i] * cc.x - p0 * cc.y : n[i] * cc.x + p0 * cc.y;
-          out[i + 1] = lo ? n[i + 1] * cc.z - p1 * cc.w : n[i + 1] * cc.z + p1 * cc.w;
-        }
-        if (!act) continue;
-        __nv_bfloat16* dst = is_q ? qo + ((long long)t * nq + hh) * HD
-                                  : ko + ((long long)t * nk + (hh - nq)) * HD;
-        store8(dst + sub * 8, out);
-        if (sub == 0) {
-          if (is_q) rstd_q[(long long)t * nq + hh] = r;
-          else rstd_k[(long long)t * nk + (hh - nq)] = r;
-        }
-      }
+      if (!act) continue;
+      __nv_bfloat16* dst = is_q ? qrow + hh * HD : krow + (hh - nq) * HD;
+      store4(dst + e0, ol);
+      store4(dst + HALF + e0, oh);
+      if (sub == 0) (is_q ? rq_row[hh] : rk_row[hh - nq]) = r;
     }
+    __syncthreads();  // slot s consumed
+    if (threadIdx.x == 0 && t + ST * gridDim.x < T) issue(t + ST * gridDim.x, s);
   }
 }
 
 // Backward: undo the rotation (R^T), then per-head RMSNorm backward;
 // dqkv[:, q/k slots] = dx; dqw/dkw[HD] += sum(dn * xhat) (registers -> smem
-// -> one atomic per column per block). Loads batched over QK_NB passes as in
-// the forward.
+// -> one atomic per column per block). rstd_bulk: nq, nk multiples of 4 (the
+// rstd rows are bulk-copied); otherwise rstd is read from global.
 template <int HD>
-__global__ void __launch_bounds__(QK_THREADS)
+__global__ void __launch_bounds__(QK_MAX_THREADS)
     qk_norm_rope_bwd_kernel(const __nv_bfloat16* __restrict__ dq, const __nv_bfloat16* __restrict__ dk,
                             const __nv_bfloat16* __restrict__ qkv, long long ld, int nq, int nk,
                             const __nv_bfloat16* __restrict__ qw,
                             const __nv_bfloat16* __restrict__ kw, const float* __restrict__ rstd_q,
                             const float* __restrict__ rstd_k, const float2* __restrict__ cs, int seq,
                             __nv_bfloat16* __restrict__ dqkv, long long ldd, float* __restrict__ dqw,
-                            float* __restrict__ dkw, int T) {
-  constexpr int TPH = HD / 8, HALF = HD / 2, HPB = QK_THREADS / TPH;
+                            float* __restrict__ dkw, int T, int rstd_bulk) {
+  using namespace sm100;
+  constexpr int TPH = qk_tph<HD>(), HALF = HD / 2, ST = QK_STAGES_BWD;
+  extern __shared__ __align__(128) uint8_t qsm[];
   __shared__ float sq[HD], sk[HD];
-  for (int i = threadIdx.x; i < HD; i += blockDim.x) sq[i] = sk[i] = 0.f;
-  __syncthreads();
   const int heads = nq + nk;
-  const int sub = threadIdx.x % TPH, hl = threadIdx.x / TPH;
+  const QkSlot L = qk_slot<HD>(heads, true);
+  uint64_t* full = reinterpret_cast<uint64_t*>(qsm + ST * L.bytes);
+  const int sub = threadIdx.x % TPH, h0 = threadIdx.x / TPH, hstep = blockDim.x / TPH;
   const bool lo = sub < TPH / 2;
-  float wq[8], wk[8], aq[8], ak[8];
-  load8(qw + sub * 8, wq);
-  load8(kw + sub * 8, wk);
+  auto issue = [&](int t, int s) {
+    uint8_t* slot = qsm + s * L.bytes;
+    mbar_arrive_expect_tx(&full[s], 2 * heads * HD * 2 + HALF * 8 + (rstd_bulk ? heads * 4 : 0));
+    bulk_load_1d(slot + L.g, dq + (long long)t * nq * HD, nq * HD * 2, &full[s]);
+    bulk_load_1d(slot + L.g + nq * HD * 2, dk + (long long)t * nk * HD, nk * HD * 2, &full[s]);
+    bulk_load_1d(slot + L.x, qkv + (long long)t * ld, heads * HD * 2, &full[s]);
+    bulk_load_1d(slot + L.cs, cs + (long long)(t % seq) * HALF, HALF * 8, &full[s]);
+    if (rstd_bulk) {
+      bulk_load_1d(slot + L.rstd, rstd_q + (long long)t * nq, nq * 4, &full[s]);
+      bulk_load_1d(slot + L.rstd + nq * 4, rstd_k + (long long)t * nk, nk * 4, &full[s]);
+    }
+  };
+  for (int k = threadIdx.x; k < HD; k += blockDim.x) sq[k] = sk[k] = 0.f;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    for (int s = 0; s < ST; ++s)
+      if (blockIdx.x + s * gridDim.x < T) issue(blockIdx.x + s * gridDim.x, s);
+  }
+  __syncthreads();
+  const int e0 = sub * 4;  // this lane's pairs (e0 + k, e0 + k + HALF), k < 4
+  float wql[4], wqh[4], wkl[4], wkh[4];  // norm weights, converted once
+  unpack4(*reinterpret_cast<const uint2*>(qw + e0), wql);
+  unpack4(*reinterpret_cast<const uint2*>(qw + HALF + e0), wqh);
+  unpack4(*reinterpret_cast<const uint2*>(kw + e0), wkl);
+  unpack4(*reinterpret_cast<const uint2*>(kw + HALF + e0), wkh);
+  float aq[8], ak[8];  // [0, 4): elements e0 + k, [4, 8): e0 + HALF + k
 #pragma unroll
-  for (int i = 0; i < 8; ++i) aq[i] = ak[i] = 0.f;
-  for (int t = blockIdx.x; t < T; t += gridDim.x) {
-    const int pos = t % seq;
-    const float4* c4 = reinterpret_cast<const float4*>(cs + (long long)pos * HALF + (sub * 8) % HALF);
-    float4 c[4];
+  for (int k = 0; k < 8; ++k) aq[k] = ak[k] = 0.f;
+  int i = 0;
+  for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
+    const int s = i % ST;
+    mbar_wait(&full[s], (i / ST) & 1);
+    const uint8_t* slot = qsm + s * L.bytes;
+    const __nv_bfloat16* gs = reinterpret_cast<const __nv_bfloat16*>(slot + L.g);
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(slot + L.x);
+    const float* rs = reinterpret_cast<const float*>(slot + L.rstd);
+    const float4* c4 = reinterpret_cast<const float4*>(slot + L.cs) + e0 / 2;
+    const float4 ca = c4[0], cb = c4[1];
+    const float cosv[4] = {ca.x, ca.z, cb.x, cb.z}, sinv[4] = {ca.y, ca.w, cb.y, cb.w};
+    __nv_bfloat16* drow = dqkv + (long long)t * ldd;
+    for (int hb = 0; hb < heads; hb += hstep) {  // block-uniform (shuffles)
+      const int hh = hb + h0;
+      const bool act = hh < heads;
+      const bool is_q = hh < nq;
+      float r = 0.f;
+      if (act)
+        r = rstd_bulk ? rs[hh] : is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
+      const uint2 z = make_uint2(0, 0);
+      float gl[4], gh[4], xl[4], xh[4], wl[4], wh[4];
+      unpack4(act ? *reinterpret_cast<const uint2*>(gs + hh * HD + e0) : z, gl);
+      unpack4(act ? *reinterpret_cast<const uint2*>(gs + hh * HD + HALF + e0) : z, gh);
+      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + e0) : z, xl);
+      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + HALF + e0) : z, xh);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c[i] = c4[i];
-    for (int base0 = 0; base0 < heads; base0 += QK_NB * HPB) {  // warp-uniform passes (shuffles)
-      uint4 graw[QK_NB], xraw[QK_NB];
-      float rr[QK_NB];
+      for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
+      float dot = 0.f, gxl[4], gxh[4];
 #pragma unroll
-      for (int b = 0; b < QK_NB; ++b) {
-        const int hh = base0 + b * HPB + hl;
-        graw[b] = xraw[b] = make_uint4(0, 0, 0, 0);
-        rr[b] = 0.f;
-        if (hh < heads) {
-          const bool is_q = hh < nq;
-          rr[b] = is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
-          graw[b] = *reinterpret_cast<const uint4*>(
-              (is_q ? dq + ((long long)t * nq + hh) * HD : dk + ((long long)t * nk + (hh - nq)) * HD) +
-              sub * 8);
-          xraw[b] = *reinterpret_cast<const uint4*>(qkv + (long long)t * ld + hh * HD + sub * 8);
+      for (int k = 0; k < 4; ++k) {
+        const float dnl = gl[k] * cosv[k] + gh[k] * sinv[k];  // R^T
+        const float dnh = gh[k] * cosv[k] - gl[k] * sinv[k];
+        xl[k] *= r;  // xhat
+        xh[k] *= r;
+        gxl[k] = dnl * wl[k];
+        gxh[k] = dnh * wh[k];
+        dot += gxl[k] * xl[k] + gxh[k] * xh[k];
+        if (is_q) {
+          aq[k] += dnl * xl[k];
+          aq[4 + k] += dnh * xh[k];
+        } else {
+          ak[k] += dnl * xl[k];
+          ak[4 + k] += dnh * xh[k];
         }
       }
 #pragma unroll
-      for (int b = 0; b < QK_NB; ++b) {
-        if (base0 + b * HPB >= heads) break;  // block-uniform
-        const int hh = base0 + b * HPB + hl;
-        const bool act = hh < heads;
-        const bool is_q = hh < nq;
-        const float r = rr[b];
-        float gv[8], xv[8];
-        unpack8(graw[b], gv);
-        unpack8(xraw[b], xv);
-        float dn[8];
+      for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const float mean = dot / HD;
+      float ol[4], oh[4];
 #pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          const float4 cc = c[i / 2];
-          const float p0 = __shfl_xor_sync(0xffffffffu, gv[i], TPH / 2);
-          const float p1 = __shfl_xor_sync(0xffffffffu, gv[i + 1], TPH / 2);
-          dn[i] = lo ? gv[i] * cc.x + p0 * cc.y : gv[i] * cc.x - p0 * cc.y;
-          dn[i + 1] = lo ? gv[i + 1] * cc.z + p1 * cc.w : gv[i + 1] * cc.z - p1 * cc.w;
-        }
-        float dot = 0.f, gx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          xv[i] *= r;  // xhat
-          gx[i] = dn[i] * (is_q ? wq[i] : wk[i]);
-          dot += gx[i] * xv[i];
-          if (is_q) aq[i] += dn[i] * xv[i]; else ak[i] += dn[i] * xv[i];
-        }
-#pragma unroll
-        for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        const float mean = dot / HD;
-        float out[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) out[i] = r * (gx[i] - xv[i] * mean);
-        if (act) store8(dqkv + (long long)t * ldd + hh * HD + sub * 8, out);
+      for (int k = 0; k < 4; ++k) {
+        ol[k] = r * (gxl[k] - xl[k] * mean);
+        oh[k] = r * (gxh[k] - xh[k] * mean);
+      }
+      if (act) {
+        __nv_bfloat16* dst = drow + hh * HD;
+        store4(dst + e0, ol);
+        store4(dst + HALF + e0, oh);
       }
     }
+    __syncthreads();  // slot s consumed
+    if (threadIdx.x == 0 && t + ST * gridDim.x < T) issue(t + ST * gridDim.x, s);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    atomicAdd(&sq[sub * 8 + i], aq[i]);
-    atomicAdd(&sk[sub * 8 + i], ak[i]);
+  for (int k = 0; k < 4; ++k) {
+    atomicAdd(&sq[e0 + k], aq[k]);
+    atomicAdd(&sq[HALF + e0 + k], aq[4 + k]);
+    atomicAdd(&sk[e0 + k], ak[k]);
+    atomicAdd(&sk[HALF + e0 + k], ak[4 + k]);
   }
   __syncthreads();
   if (dqw && dkw)  // null: frozen norm weights (LoRA)
-    for (int i = threadIdx.x; i < HD; i += blockDim.x) {
-      atomicAdd(dqw + i, sq[i]);
-      atomicAdd(dkw + i, sk[i]);
+    for (int k = threadIdx.x; k < HD; k += blockDim.x) {
+      atomicAdd(dqw + k, sq[k]);
+      atomicAdd(dkw + k, sk[k]);
     }
 }
 
@@ -603,23 +831,35 @@ int grid_for(long long work, int threads, int max_blocks = 148 * 8) {
   return (int)(b < max_blocks ? b : max_blocks);
 }
 
-int status() { return cudaGetLastError() == cudaSuccess ? RP_OK : RP_E_CUDA; }
+// a failed launch names its CUDA error on stderr (the caller only sees RP_E_CUDA)
+int status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return RP_OK;
+  std::fprintf(stderr, "rp elementwise kernel launch: %s\n", cudaGetErrorString(e));
+  return RP_E_CUDA;
+}
 
-// one wave of resident QK_THREADS blocks (occupancy per device, cached), at
-// most one block per token
-template <auto Kern>
-int wave_grid(int T) {
-  static int cached[64] = {0};
+// one wave of resident bt-thread blocks of kern with `smem` dynamic shared
+// memory (occupancy per (device, kernel, bt, smem), the last configuration
+// asked per device and kernel type cached), at most one block per token
+template <class K>
+int qk_wave_grid(K* kern, int bt, int smem, int T) {
+  struct Entry {
+    const void* kern = nullptr;
+    int bt = 0, smem = -1, grid = 0;
+  };
+  static thread_local Entry cached[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  int& g = cached[dev & 63];
-  if (!g) {
+  Entry& e = cached[dev & 63];
+  if (e.kern != reinterpret_cast<const void*>(kern) || e.bt != bt || e.smem != smem) {
     int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, Kern, QK_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, bt, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
+    e.grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 1);
+    e.kern = reinterpret_cast<const void*>(kern), e.bt = bt, e.smem = smem;
   }
-  return T < g ? T : g;
+  return T < e.grid ? T : e.grid;
 }
 
 }  // namespace
@@ -666,53 +906,86 @@ RP_API int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const fl
   auto st = (cudaStream_t)stream;
   // exactly the resident blocks (one wave); each walks rows grid-stride,
   // keeping dw in registers
-  auto go = [&](auto kern, int th) {
+  auto go = [&](auto kern, int th, int smem) {
     int per_sm = 0, dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, th, smem) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
     const int grid = rows < sms * per_sm ? rows : sms * per_sm;
-    kern<<<grid, th, 0, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                              (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
-                              dw, rows, h);
+    kern<<<grid, th, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                 (const __nv_bfloat16*)w, rstd, dres, dx32, (__nv_bfloat16*)dx16,
+                                 dw, rows, h);
   };
+  // staged (bulk-copy ring) when the operands allow 16-byte bulk copies:
+  // 16-byte aligned bases, rstd readable in 16-byte groups (rows % 4 == 0)
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool staged = RN_STAGED && h >= 1024 && rows % 4 == 0 && al(dy) && al(x) && al(rstd) && (!dres || al(dres));
+  if (staged) {
+    const int smem = RN_ST * (h * (dres ? 8 : 4) + 16) + RN_ST * 8;
+    auto sgo = [&](auto kern, int th) {
+      if (!ensure_smem_t(kern, smem)) return false;
+      go(kern, th, smem);
+      return true;
+    };
+    bool ok;
+    if (h <= 2048)
+      ok = sgo(rmsnorm_bwd_staged_kernel<256, 1>, 256);
+    else if (h <= 4096)
+      ok = sgo(rmsnorm_bwd_staged_kernel<256, 2>, 256);
+    else if (h <= 6144)
+      ok = sgo(rmsnorm_bwd_staged_kernel<256, 3>, 256);
+    else
+      ok = sgo(rmsnorm_bwd_staged_kernel<256, 4>, 256);
+    if (!ok) return RP_E_INPUT;
+    return status();
+  }
   // 256 threads above h = 1024: the row's dy / x / dres and the dw partials
   // live in registers, so fewer columns per thread keep occupancy up
   if (h <= 1024)
-    go(rmsnorm_bwd_kernel<128, 1>, 128);
+    go(rmsnorm_bwd_kernel<128, 1>, 128, 0);
   else if (h <= 2048)
-    go(rmsnorm_bwd_kernel<256, 1>, 256);
+    go(rmsnorm_bwd_kernel<256, 1>, 256, 0);
   else if (h <= 4096)
-    go(rmsnorm_bwd_kernel<256, 2>, 256);
+    go(rmsnorm_bwd_kernel<256, 2>, 256, 0);
   else if (h <= 6144)
-    go(rmsnorm_bwd_kernel<256, 3>, 256);
+    go(rmsnorm_bwd_kernel<256, 3>, 256, 0);
   else
-    go(rmsnorm_bwd_kernel<256, 4>, 256);
+    go(rmsnorm_bwd_kernel<256, 4>, 256, 0);
   return status();
 }
+
+// bulk copies need 16-byte aligned sources: ld % 8 (bf16), 16-byte aligned
+// base pointers (row strides nq*HD, nk*HD are multiples of 8 elements)
+static bool qk_aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 RP_API int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t nk,
                                int32_t head_dim, const void* qw, const void* kw,
                                const float* cos_sin, int32_t seq, void* q_out, void* k_out,
                                float* rstd_q, float* rstd_k, int32_t T, float eps,
                                void* stream) {
-  if (ld % 8 || T % 128 || T <= 0) return RP_E_INPUT;
-  auto s = (cudaStream_t)stream;
-  if (head_dim == 128)
-    qk_norm_rope_fwd_kernel<128><<<wave_grid<qk_norm_rope_fwd_kernel<128>>(T), QK_THREADS, 0, s>>>(
-        (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
-        (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
-        T, eps);
-  else if (head_dim == 64)
-    qk_norm_rope_fwd_kernel<64><<<wave_grid<qk_norm_rope_fwd_kernel<64>>(T), QK_THREADS, 0, s>>>(
-        (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
-        (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k,
-        T, eps);
-  else
+  if (ld % 8 || T % 128 || T <= 0 || nq <= 0 || nk <= 0 || seq <= 0) return RP_E_INPUT;
+  if (!qk_aligned(qkv) || !qk_aligned(cos_sin) || !qk_aligned(qw) || !qk_aligned(kw) ||
+      !qk_aligned(q_out) || !qk_aligned(k_out))
     return RP_E_INPUT;
-  return status();
+  auto s = (cudaStream_t)stream;
+  auto go = [&](auto kern, int bt, QkSlot L) -> int {
+    const int smem = QK_STAGES_FWD * L.bytes + QK_STAGES_FWD * 8;
+    if (!ensure_smem_t(kern, smem)) return RP_E_INPUT;
+    kern<<<qk_wave_grid(kern, bt, smem, T), bt, smem, s>>>(
+        (const __nv_bfloat16*)qkv, ld, nq, nk, (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw,
+        (const float2*)cos_sin, seq, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_out, rstd_q, rstd_k, T,
+        eps);
+    return status();
+  };
+  if (head_dim == 128)
+    return go(qk_norm_rope_fwd_kernel<128>, qk_block_threads<128>(nq + nk, QK_NB),
+              qk_slot<128>(nq + nk, false));
+  if (head_dim == 64)
+    return go(qk_norm_rope_fwd_kernel<64>, qk_block_threads<64>(nq + nk, QK_NB),
+              qk_slot<64>(nq + nk, false));
+  return RP_E_INPUT;
 }
 
 RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, int64_t ld,
@@ -720,21 +993,28 @@ RP_API int rp_qk_norm_rope_bwd(const void* dq, const void* dk, const void* qkv, 
                                const void* kw, const float* rstd_q, const float* rstd_k,
                                const float* cos_sin, int32_t seq, void* dqkv, int64_t ldd,
                                float* dqw, float* dkw, int32_t T, void* stream) {
-  if (ld % 8 || ldd % 8 || T % 128 || T <= 0) return RP_E_INPUT;
-  auto s = (cudaStream_t)stream;
-  if (head_dim == 128)
-    qk_norm_rope_bwd_kernel<128><<<wave_grid<qk_norm_rope_bwd_kernel<128>>(T), QK_THREADS, 0, s>>>(
-        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
-        (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
-        seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
-  else if (head_dim == 64)
-    qk_norm_rope_bwd_kernel<64><<<wave_grid<qk_norm_rope_bwd_kernel<64>>(T), QK_THREADS, 0, s>>>(
-        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
-        (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
-        seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T);
-  else
+  if (ld % 8 || ldd % 8 || T % 128 || T <= 0 || nq <= 0 || nk <= 0 || seq <= 0) return RP_E_INPUT;
+  if (!qk_aligned(dq) || !qk_aligned(dk) || !qk_aligned(qkv) || !qk_aligned(cos_sin) ||
+      !qk_aligned(qw) || !qk_aligned(kw) || !qk_aligned(dqkv))
     return RP_E_INPUT;
-  return status();
+  const int rstd_bulk = nq % 4 == 0 && nk % 4 == 0 && qk_aligned(rstd_q) && qk_aligned(rstd_k);
+  auto s = (cudaStream_t)stream;
+  auto go = [&](auto kern, int bt, QkSlot L) -> int {
+    const int smem = QK_STAGES_BWD * L.bytes + QK_STAGES_BWD * 8;
+    if (!ensure_smem_t(kern, smem)) return RP_E_INPUT;
+    kern<<<qk_wave_grid(kern, bt, smem, T), bt, smem, s>>>(
+        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)qkv, ld, nq, nk,
+        (const __nv_bfloat16*)qw, (const __nv_bfloat16*)kw, rstd_q, rstd_k, (const float2*)cos_sin,
+        seq, (__nv_bfloat16*)dqkv, ldd, dqw, dkw, T, rstd_bulk);
+    return status();
+  };
+  if (head_dim == 128)
+    return go(qk_norm_rope_bwd_kernel<128>, qk_block_threads<128>(nq + nk, QK_NB),
+              qk_slot<128>(nq + nk, true));
+  if (head_dim == 64)
+    return go(qk_norm_rope_bwd_kernel<64>, qk_block_threads<64>(nq + nk, QK_NB),
+              qk_slot<64>(nq + nk, true));
+  return RP_E_INPUT;
 }
 
 RP_API int rp_swiglu_fwd(const void* gu, void* act, int64_t T, int32_t m, void* stream) {

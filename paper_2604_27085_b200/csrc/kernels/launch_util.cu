@@ -9,7 +9,11 @@
 namespace rp {
 namespace {
 std::mutex g_mu;
-std::set<std::tuple<const void*, int, int>> g_smem_done;  // (kernel, device, bytes)
+// (kernel, device) -> the MaxDynamicSharedMemorySize set so far. The attribute
+// is an upper bound for every later launch, so it only ever grows: setting it
+// to a smaller size for one launch would make a later, larger launch of the
+// same kernel fail with "invalid argument".
+std::map<std::pair<const void*, int>, int> g_smem_max;
 struct WsKey {
   cudaStream_t s;
   int dev, tag;
@@ -22,11 +26,12 @@ bool ensure_smem(const void* kern, int bytes) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   std::lock_guard<std::mutex> g(g_mu);
-  const auto key = std::make_tuple(kern, dev, bytes);
-  if (g_smem_done.count(key)) return true;
+  constexpr int kDefault = 48 * 1024;  // allowed without opting in
+  int& cur = g_smem_max[std::make_pair(kern, dev)];
+  if (bytes <= (cur > kDefault ? cur : kDefault)) return true;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess)
     return false;
-  g_smem_done.insert(key);
+  cur = bytes;
   return true;
 }
 

@@ -45,6 +45,26 @@ def test_rmsnorm_fwd_bwd(T, h):
     assert rel(dw, wf.grad) < 1e-4
 
 
+@pytest.mark.parametrize("T,h", [(512, 4096), (128, 2048)])
+def test_rmsnorm_bwd_staged_no_residual(T, h):
+    """The bulk-copy-staged backward without a residual gradient and bf16-only
+    output (slot = dy | x | rstd group), against the register version's math."""
+    from paper_2604_27085_b200 import kernels as K
+    x, w, dy = rnd(T, h, seed=21), rnd(h, seed=22, scale=0.5) + 1, rnd(T, h, seed=23)
+    y = torch.empty_like(x)
+    rstd = torch.empty(T, device="cuda")
+    K.rmsnorm_fwd(x, w, y, rstd)
+    xf = x.float().requires_grad_(True)
+    wf = w.float().requires_grad_(True)
+    ref = wf * (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6))
+    ref.backward(dy.float())
+    dx16 = torch.empty(T, h, device="cuda", dtype=torch.bfloat16)
+    dw = torch.zeros(h, device="cuda")
+    K.rmsnorm_bwd(dy, x, w, rstd, dx16=dx16, dw=dw)
+    assert rel(dx16, xf.grad) < 1e-2
+    assert rel(dw, wf.grad) < 1e-4
+
+
 def _rope_ref(x, cs):  # x [T, H, hd] fp32; cs [T, hd/2, 2]
     hd = x.shape[-1]
     cos = torch.cat([cs[..., 0], cs[..., 0]], -1)[:, None, :]
@@ -53,7 +73,7 @@ def _rope_ref(x, cs):  # x [T, H, hd] fp32; cs [T, hd/2, 2]
     return x * cos + torch.cat([-x2, x1], -1) * sin
 
 
-@pytest.mark.parametrize("hd,nq,nk", [(128, 32, 8), (64, 4, 2)])
+@pytest.mark.parametrize("hd,nq,nk", [(128, 32, 8), (64, 4, 2), (128, 16, 8), (128, 64, 8), (128, 64, 4), (128, 6, 2)])
 def test_qk_norm_rope_fwd_bwd(hd, nq, nk):
     from paper_2604_27085_b200 import kernels as K
     seq, T = 256, 512
