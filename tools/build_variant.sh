@@ -11,7 +11,10 @@ OBJ=ab_libs/obj_$NAME/$(basename $UNIT).o
   -Xcompiler -fPIC,-fvisibility=hidden,-fvisibility-inlines-hidden -Iinclude -I$PKG/csrc \
   --expt-relaxed-constexpr -DROUNDPIPE_CONFIG_DIR=\"$(pwd)/configs\" -Xptxas -v "$@" \
   -c $PKG/csrc/kernels/$UNIT -o $OBJ 2> ab_libs/obj_$NAME/ptxas.log
-OTHERS=$(find build -name '*.o' ! -name "$(basename $UNIT).o")
+# REPLACES: the built unit this variant stands in for (default: UNIT itself;
+# e.g. REPLACES=elementwise.cu for a copy of an older elementwise.cu)
+REPLACES=${REPLACES:-$UNIT}
+OTHERS=$(find build -name '*.o' ! -name "$(basename $REPLACES).o")
 /usr/local/cuda/bin/nvcc -shared -gencode arch=compute_100a,code=sm_100a -Xlinker -Bsymbolic \
   -o ab_libs/$NAME.so $OBJ $OTHERS -lpthread -ldl
 grep -A2 "qk_norm" ab_libs/obj_$NAME/ptxas.log | grep -E "Used|spill" | sed 's/ptxas info    ://' | paste - - | head
