@@ -452,15 +452,17 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
     float* rq_row = rstd_q + (long long)t * nq;
     float* rk_row = rstd_k + (long long)t * nk;
     // every lane runs every pass (the RMS shuffles are warp-wide); lanes
-    // whose head is past the end compute on zeros and store nothing
+    // whose head is past the end store nothing
     for (int hb = 0; hb < heads; hb += hstep) {  // block-uniform
       const int hh = hb + h0;
       const bool act = hh < heads;
       const bool is_q = hh < nq;
-      const uint2 z = make_uint2(0, 0);
+      // lanes past the last head recompute the last head (no zero paths;
+      // their 16-lane reductions never mix with a stored head's)
+      const int hr = act ? hh : heads - 1;
       float lo[4], hi[4], wl[4], wh[4];
-      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + e0) : z, lo);
-      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + HALF + e0) : z, hi);
+      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + e0), lo);
+      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0), hi);
 #pragma unroll
       for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
       float ss = 0.f;
@@ -556,15 +558,16 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
       const int hh = hb + h0;
       const bool act = hh < heads;
       const bool is_q = hh < nq;
-      float r = 0.f;
-      if (act)
-        r = rstd_bulk ? rs[hh] : is_q ? rstd_q[(long long)t * nq + hh] : rstd_k[(long long)t * nk + (hh - nq)];
-      const uint2 z = make_uint2(0, 0);
+      // lanes past the last head recompute the last head and store nothing
+      // (their dw contributions are masked below)
+      const int hr = act ? hh : heads - 1;
+      const bool rq = hr < nq;
+      const float r = rstd_bulk ? rs[hr] : rq ? rstd_q[(long long)t * nq + hr] : rstd_k[(long long)t * nk + (hr - nq)];
       float gl[4], gh[4], xl[4], xh[4], wl[4], wh[4];
-      unpack4(act ? *reinterpret_cast<const uint2*>(gs + hh * HD + e0) : z, gl);
-      unpack4(act ? *reinterpret_cast<const uint2*>(gs + hh * HD + HALF + e0) : z, gh);
-      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + e0) : z, xl);
-      unpack4(act ? *reinterpret_cast<const uint2*>(xs + hh * HD + HALF + e0) : z, xh);
+      unpack4(*reinterpret_cast<const uint2*>(gs + hr * HD + e0), gl);
+      unpack4(*reinterpret_cast<const uint2*>(gs + hr * HD + HALF + e0), gh);
+      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + e0), xl);
+      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0), xh);
 #pragma unroll
       for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
       float dot = 0.f, gxl[4], gxh[4];
@@ -577,10 +580,10 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
         gxl[k] = dnl * wl[k];
         gxh[k] = dnh * wh[k];
         dot += gxl[k] * xl[k] + gxh[k] * xh[k];
-        if (is_q) {
+        if (act && is_q) {
           aq[k] += dnl * xl[k];
           aq[4 + k] += dnh * xh[k];
-        } else {
+        } else if (act) {
           ak[k] += dnl * xl[k];
           ak[4 + k] += dnh * xh[k];
         }
