@@ -64,12 +64,20 @@ typedef struct {
 int rp_rmsnorm_fwd(const void* x, int64_t ldx, const void* w, void* y, int64_t ldy,
                    float* rstd, int32_t rows, int32_t h, float eps, void* stream);
 /* dx = rstd*(dy*w - xhat*mean(dy*w*xhat)) [+ dres]; dx32 (fp32) and/or dx16
- * (bf16) outputs; dw[h] += sum_rows dy*xhat (fp32, atomics). Rows dense. */
+ * (bf16) outputs; dw[h] += sum_rows dy*xhat (fp32, atomics). Rows dense.
+ * dy | x | dres rows are staged through a bulk-copy ring when h >= 1024,
+ * rows % 4 == 0 and dy, x, rstd, dres are 16-byte aligned; otherwise a
+ * register version runs (same math; fp32 contraction may differ in the last
+ * bit). */
 int rp_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
                    const float* dres, float* dx32, void* dx16, float* dw, int32_t rows,
                    int32_t h, void* stream);
 /* Per-head RMSNorm of q and k slots of the fused qkv row + RoPE (rotate_half,
- * cos_sin = float2 (cos, sin) table [seq, head_dim/2]); position = t % seq. */
+ * cos_sin = float2 (cos, sin) table [seq, head_dim/2]); position = t % seq.
+ * head_dim 64 or 128, T % 128 == 0, ld % 8 == 0; every pointer 16-byte
+ * aligned (operands are staged by 1-D bulk copies) -> RP_E_INPUT otherwise.
+ * The backward bulk-copies rstd when nq % 4 == 0 and nk % 4 == 0 and reads
+ * it from global memory otherwise. */
 int rp_qk_norm_rope_fwd(const void* qkv, int64_t ld, int32_t nq, int32_t nk,
                         int32_t head_dim, const void* qw, const void* kw,
                         const float* cos_sin, int32_t seq, void* q_out, void* k_out,

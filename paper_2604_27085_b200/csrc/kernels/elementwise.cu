@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(RN_THREADS)
 // bounded by the registers that hold them (the register version keeps one
 // row per block in flight, profiles/r02n_step_breakdown_8b.txt: 3.7 TB/s in
 // step). The per-thread column assignment, the dot-product order and the
-// output arithmetic are the register version's, so dx is bit-identical.
+// output arithmetic are the register version's (the compiler's fp32
+// contraction can still differ in the last bit).
 constexpr int RN_ST = 2;
 #ifndef RN_STAGED  // -DRN_STAGED=0: register version only (same-box A/B builds)
 #define RN_STAGED 1
