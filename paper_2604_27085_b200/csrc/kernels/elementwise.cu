@@ -71,6 +71,14 @@ __device__ __forceinline__ float rn_block_sum(float v, float* red) {
   return t;
 }
 
+// bf16x2 word <-> float2 (low half = .x)
+__device__ __forceinline__ float2 bf2x2(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2_rn(float2 v) {
+  const __nv_bfloat162 b = __floats2bfloat162_rn(v.x, v.y);
+  return *reinterpret_cast<const uint32_t*>(&b);
+}
 __device__ __forceinline__ void unpack4(const uint2& u, float (&f)[4]) {
   const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
@@ -434,11 +442,13 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
   }
   __syncthreads();
   const int e0 = sub * 4;  // this lane's pairs (e0 + k, e0 + k + HALF), k < 4
-  float wql[4], wqh[4], wkl[4], wkh[4];  // norm weights, converted once
-  unpack4(*reinterpret_cast<const uint2*>(qw + e0), wql);
-  unpack4(*reinterpret_cast<const uint2*>(qw + HALF + e0), wqh);
-  unpack4(*reinterpret_cast<const uint2*>(kw + e0), wkl);
-  unpack4(*reinterpret_cast<const uint2*>(kw + HALF + e0), wkh);
+  float2 wq2l[2], wq2h[2], wk2l[2], wk2h[2];  // norm weights, converted once
+  {
+    const uint2 a = *reinterpret_cast<const uint2*>(qw + e0), b = *reinterpret_cast<const uint2*>(qw + HALF + e0);
+    const uint2 c = *reinterpret_cast<const uint2*>(kw + e0), d = *reinterpret_cast<const uint2*>(kw + HALF + e0);
+    wq2l[0] = bf2x2(a.x), wq2l[1] = bf2x2(a.y), wq2h[0] = bf2x2(b.x), wq2h[1] = bf2x2(b.y);
+    wk2l[0] = bf2x2(c.x), wk2l[1] = bf2x2(c.y), wk2h[0] = bf2x2(d.x), wk2h[1] = bf2x2(d.y);
+  }
   int i = 0;
   for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
     const int s = i % ST;
@@ -447,7 +457,9 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
     const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(slot + L.x);
     const float4* c4 = reinterpret_cast<const float4*>(slot + L.cs) + e0 / 2;
     const float4 ca = c4[0], cb = c4[1];  // (cos, sin) of pairs e0 .. e0+3
-    const float cosv[4] = {ca.x, ca.z, cb.x, cb.z}, sinv[4] = {ca.y, ca.w, cb.y, cb.w};
+    const float2 cos2[2] = {make_float2(ca.x, ca.z), make_float2(cb.x, cb.z)};
+    const float2 sin2[2] = {make_float2(ca.y, ca.w), make_float2(cb.y, cb.w)};
+    const float2 nsin2[2] = {make_float2(-ca.y, -ca.w), make_float2(-cb.y, -cb.w)};
     __nv_bfloat16* qrow = qo + (long long)t * nq * HD;
     __nv_bfloat16* krow = ko + (long long)t * nk * HD;
     float* rq_row = rstd_q + (long long)t * nq;
@@ -461,25 +473,30 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
       // lanes past the last head recompute the last head (no zero paths;
       // their 16-lane reductions never mix with a stored head's)
       const int hr = act ? hh : heads - 1;
-      float lo[4], hi[4], wl[4], wh[4];
-      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + e0), lo);
-      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0), hi);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
-      float ss = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ss += lo[k] * lo[k];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ss += hi[k] * hi[k];
+      // packed fp32x2 math (FFMA2 / FMUL2): element pairs (e0+2j, e0+2j+1)
+      const uint2 xl = *reinterpret_cast<const uint2*>(xs + hr * HD + e0);
+      const uint2 xh = *reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0);
+      const float2 lo[2] = {bf2x2(xl.x), bf2x2(xl.y)}, hi[2] = {bf2x2(xh.x), bf2x2(xh.y)};
+      float2 acc = __fmul2_rn(lo[0], lo[0]);
+      acc = __ffma2_rn(lo[1], lo[1], acc);
+      acc = __ffma2_rn(hi[0], hi[0], acc);
+      acc = __ffma2_rn(hi[1], hi[1], acc);
+      float ss = acc.x + acc.y;
 #pragma unroll
       for (int o = TPH / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
       const float r = rsqrtf(ss / HD + eps);
+      const float2 r2 = make_float2(r, r);
       float ol[4], oh[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float nl = bf2f(f2bf(wl[k] * (lo[k] * r))), nh = bf2f(f2bf(wh[k] * (hi[k] * r)));
-        ol[k] = nl * cosv[k] - nh * sinv[k];  // x1 cos - x2 sin
-        oh[k] = nh * cosv[k] + nl * sinv[k];  // x2 cos + x1 sin
+      for (int j = 0; j < 2; ++j) {
+        const float2 wl = is_q ? wq2l[j] : wk2l[j], wh = is_q ? wq2h[j] : wk2h[j];
+        // the normalised value rounded to bf16 (HF computes the norm in bf16)
+        const float2 nl = bf2x2(pack_bf16x2_rn(__fmul2_rn(wl, __fmul2_rn(lo[j], r2))));
+        const float2 nh = bf2x2(pack_bf16x2_rn(__fmul2_rn(wh, __fmul2_rn(hi[j], r2))));
+        const float2 l2 = __ffma2_rn(nl, cos2[j], __fmul2_rn(nh, nsin2[j]));  // x1 cos - x2 sin
+        const float2 h2 = __ffma2_rn(nh, cos2[j], __fmul2_rn(nl, sin2[j]));   // x2 cos + x1 sin
+        ol[2 * j] = l2.x, ol[2 * j + 1] = l2.y;
+        oh[2 * j] = h2.x, oh[2 * j + 1] = h2.y;
       }
       if (!act) continue;
       __nv_bfloat16* dst = is_q ? qrow + hh * HD : krow + (hh - nq) * HD;
@@ -535,14 +552,17 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
   }
   __syncthreads();
   const int e0 = sub * 4;  // this lane's pairs (e0 + k, e0 + k + HALF), k < 4
-  float wql[4], wqh[4], wkl[4], wkh[4];  // norm weights, converted once
-  unpack4(*reinterpret_cast<const uint2*>(qw + e0), wql);
-  unpack4(*reinterpret_cast<const uint2*>(qw + HALF + e0), wqh);
-  unpack4(*reinterpret_cast<const uint2*>(kw + e0), wkl);
-  unpack4(*reinterpret_cast<const uint2*>(kw + HALF + e0), wkh);
-  float aq[8], ak[8];  // [0, 4): elements e0 + k, [4, 8): e0 + HALF + k
+  float2 wq2l[2], wq2h[2], wk2l[2], wk2h[2];  // norm weights, converted once
+  {
+    const uint2 a = *reinterpret_cast<const uint2*>(qw + e0), b = *reinterpret_cast<const uint2*>(qw + HALF + e0);
+    const uint2 c = *reinterpret_cast<const uint2*>(kw + e0), d = *reinterpret_cast<const uint2*>(kw + HALF + e0);
+    wq2l[0] = bf2x2(a.x), wq2l[1] = bf2x2(a.y), wq2h[0] = bf2x2(b.x), wq2h[1] = bf2x2(b.y);
+    wk2l[0] = bf2x2(c.x), wk2l[1] = bf2x2(c.y), wk2h[0] = bf2x2(d.x), wk2h[1] = bf2x2(d.y);
+  }
+  // dw partials, element pairs: [0, 2) = lo pairs (e0 + 2j, +1), [2, 4) = hi pairs
+  float2 aq[4], ak[4];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) aq[k] = ak[k] = 0.f;
+  for (int k = 0; k < 4; ++k) aq[k] = ak[k] = make_float2(0.f, 0.f);
   int i = 0;
   for (int t = blockIdx.x; t < T; t += gridDim.x, ++i) {
     const int s = i % ST;
@@ -553,7 +573,9 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
     const float* rs = reinterpret_cast<const float*>(slot + L.rstd);
     const float4* c4 = reinterpret_cast<const float4*>(slot + L.cs) + e0 / 2;
     const float4 ca = c4[0], cb = c4[1];
-    const float cosv[4] = {ca.x, ca.z, cb.x, cb.z}, sinv[4] = {ca.y, ca.w, cb.y, cb.w};
+    const float2 cos2[2] = {make_float2(ca.x, ca.z), make_float2(cb.x, cb.z)};
+    const float2 sin2[2] = {make_float2(ca.y, ca.w), make_float2(cb.y, cb.w)};
+    const float2 nsin2[2] = {make_float2(-ca.y, -ca.w), make_float2(-cb.y, -cb.w)};
     __nv_bfloat16* drow = dqkv + (long long)t * ldd;
     for (int hb = 0; hb < heads; hb += hstep) {  // block-uniform (shuffles)
       const int hh = hb + h0;
@@ -564,55 +586,62 @@ __global__ void __launch_bounds__(QK_MAX_THREADS)
       const int hr = act ? hh : heads - 1;
       const bool rq = hr < nq;
       const float r = rstd_bulk ? rs[hr] : rq ? rstd_q[(long long)t * nq + hr] : rstd_k[(long long)t * nk + (hr - nq)];
-      float gl[4], gh[4], xl[4], xh[4], wl[4], wh[4];
-      unpack4(*reinterpret_cast<const uint2*>(gs + hr * HD + e0), gl);
-      unpack4(*reinterpret_cast<const uint2*>(gs + hr * HD + HALF + e0), gh);
-      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + e0), xl);
-      unpack4(*reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0), xh);
+      // packed fp32x2 math (FFMA2 / FMUL2) over element pairs (e0+2j, e0+2j+1)
+      const uint2 ugl = *reinterpret_cast<const uint2*>(gs + hr * HD + e0);
+      const uint2 ugh = *reinterpret_cast<const uint2*>(gs + hr * HD + HALF + e0);
+      const uint2 uxl = *reinterpret_cast<const uint2*>(xs + hr * HD + e0);
+      const uint2 uxh = *reinterpret_cast<const uint2*>(xs + hr * HD + HALF + e0);
+      const float2 gl[2] = {bf2x2(ugl.x), bf2x2(ugl.y)}, gh[2] = {bf2x2(ugh.x), bf2x2(ugh.y)};
+      const float2 r2 = make_float2(r, r);
+      float2 xl[2] = {__fmul2_rn(bf2x2(uxl.x), r2), __fmul2_rn(bf2x2(uxl.y), r2)};  // xhat
+      float2 xh[2] = {__fmul2_rn(bf2x2(uxh.x), r2), __fmul2_rn(bf2x2(uxh.y), r2)};
+      float2 gxl[2], gxh[2], dnl[2], dnh[2];
+      float2 dacc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) wl[k] = is_q ? wql[k] : wkl[k], wh[k] = is_q ? wqh[k] : wkh[k];
-      float dot = 0.f, gxl[4], gxh[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float dnl = gl[k] * cosv[k] + gh[k] * sinv[k];  // R^T
-        const float dnh = gh[k] * cosv[k] - gl[k] * sinv[k];
-        xl[k] *= r;  // xhat
-        xh[k] *= r;
-        gxl[k] = dnl * wl[k];
-        gxh[k] = dnh * wh[k];
-        dot += gxl[k] * xl[k] + gxh[k] * xh[k];
-        if (act && is_q) {
-          aq[k] += dnl * xl[k];
-          aq[4 + k] += dnh * xh[k];
-        } else if (act) {
-          ak[k] += dnl * xl[k];
-          ak[4 + k] += dnh * xh[k];
-        }
-      }
-#pragma unroll
-      for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      const float mean = dot / HD;
-      float ol[4], oh[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        ol[k] = r * (gxl[k] - xl[k] * mean);
-        oh[k] = r * (gxh[k] - xh[k] * mean);
+      for (int j = 0; j < 2; ++j) {
+        dnl[j] = __ffma2_rn(gl[j], cos2[j], __fmul2_rn(gh[j], sin2[j]));   // R^T
+        dnh[j] = __ffma2_rn(gh[j], cos2[j], __fmul2_rn(gl[j], nsin2[j]));
+        gxl[j] = __fmul2_rn(dnl[j], is_q ? wq2l[j] : wk2l[j]);
+        gxh[j] = __fmul2_rn(dnh[j], is_q ? wq2h[j] : wk2h[j]);
+        dacc = __ffma2_rn(gxl[j], xl[j], dacc);
+        dacc = __ffma2_rn(gxh[j], xh[j], dacc);
       }
       if (act) {
+        float2* acc = is_q ? aq : ak;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          acc[j] = __ffma2_rn(dnl[j], xl[j], acc[j]);
+          acc[2 + j] = __ffma2_rn(dnh[j], xh[j], acc[2 + j]);
+        }
+      }
+      float dot = dacc.x + dacc.y;
+#pragma unroll
+      for (int o = TPH / 2; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const float2 nmean = make_float2(-dot / HD, -dot / HD);
+      if (act) {
+        uint2 ol, oh;
+        ol.x = pack_bf16x2_rn(__fmul2_rn(r2, __ffma2_rn(xl[0], nmean, gxl[0])));
+        ol.y = pack_bf16x2_rn(__fmul2_rn(r2, __ffma2_rn(xl[1], nmean, gxl[1])));
+        oh.x = pack_bf16x2_rn(__fmul2_rn(r2, __ffma2_rn(xh[0], nmean, gxh[0])));
+        oh.y = pack_bf16x2_rn(__fmul2_rn(r2, __ffma2_rn(xh[1], nmean, gxh[1])));
         __nv_bfloat16* dst = drow + hh * HD;
-        store4(dst + e0, ol);
-        store4(dst + HALF + e0, oh);
+        *reinterpret_cast<uint2*>(dst + e0) = ol;
+        *reinterpret_cast<uint2*>(dst + HALF + e0) = oh;
       }
     }
     __syncthreads();  // slot s consumed
     if (threadIdx.x == 0 && t + ST * gridDim.x < T) issue(t + ST * gridDim.x, s);
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    atomicAdd(&sq[e0 + k], aq[k]);
-    atomicAdd(&sq[HALF + e0 + k], aq[4 + k]);
-    atomicAdd(&sk[e0 + k], ak[k]);
-    atomicAdd(&sk[HALF + e0 + k], ak[4 + k]);
+  for (int j = 0; j < 2; ++j) {
+    atomicAdd(&sq[e0 + 2 * j], aq[j].x);
+    atomicAdd(&sq[e0 + 2 * j + 1], aq[j].y);
+    atomicAdd(&sq[HALF + e0 + 2 * j], aq[2 + j].x);
+    atomicAdd(&sq[HALF + e0 + 2 * j + 1], aq[2 + j].y);
+    atomicAdd(&sk[e0 + 2 * j], ak[j].x);
+    atomicAdd(&sk[e0 + 2 * j + 1], ak[j].y);
+    atomicAdd(&sk[HALF + e0 + 2 * j], ak[2 + j].x);
+    atomicAdd(&sk[HALF + e0 + 2 * j + 1], ak[2 + j].y);
   }
   __syncthreads();
   if (dqw && dkw)  // null: frozen norm weights (LoRA)
